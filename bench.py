@@ -1,0 +1,313 @@
+#!/usr/bin/env python
+"""Benchmark: docked ligands/s of the B200 pose-search path (BASELINE config 1).
+
+One step = one pass of the hot path over one batch: every ligand of the
+rank's shard goes through the rigid sweep, top-K selection, K restart
+chains of fragment optimisation, and the final ordering (E1-E8).
+
+* ``value``: device-resident throughput -- descriptors already in HBM, CUDA
+  events around the two kernels of each step, L2 flushed between steps.
+* ``e2e``: the same metric through the public C-ABI call (gd_dock_batch)
+  with host buffers: host preprocessing, pinned H2D, kernels, D2H.
+* ``--impl reference``: the reference's own CPU path (oracle/_ref: the
+  reference headers compiled from /root/reference, PocketIndex, all host
+  threads) on a bounded sample of the same workload.
+
+Multi-GPU (torchrun): ligands are sharded by id (weak scaling: every rank
+docks its own 10,000); per-ligand top-K results are all-gathered over NCCL.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "docked ligands/sec and poses scored/sec at 1/2/4/8 B200 vs host-core CPU ref"
+# Algorithmic fp64 FLOPs per unit of counted work.
+FLOPS = {"pairs": 9, "rotated": 36, "bump_pairs": 11, "queries": 0, "sum_terms": 2,
+         "evaluations": 2, "xform": 18}
+CPU_SAMPLE = 256  # ligands of the shard timed on the host cores
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--ligands", type=int, default=0, help="override ligands per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (median SM clock, reasons)."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.rows = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "100", "-i", str(device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower() in ("active", "1")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def flops_of(work: dict) -> float:
+    return float(sum(FLOPS[k] * v for k, v in work.items()))
+
+
+def cpu_reference(batch, pocket, knobs, n: int):
+    """The reference CPU path on the first n ligands: (ligands/s, dict)."""
+    from oracle import oracle_py as O
+    sub = batch.subset(range(min(n, batch.n_ligands)))
+    threads = O.threads()
+    kind = "reference" if O.have_ref() else "port"
+    impl = "ref" if kind == "reference" else "oracle"
+    t0 = time.perf_counter()
+    res = O.dock_batch(sub, pocket, knobs, nthreads=threads, keep_poses=False, impl=impl,
+                       use_index=True)
+    dt = time.perf_counter() - t0
+    return sub.n_ligands / dt, {
+        "kind": kind, "cores": threads,
+        "sample": (f"first {sub.n_ligands} ligands of the workload, "
+                   + ("reference headers (oracle/_ref) with PocketIndex"
+                      if kind == "reference" else "C oracle, brute force")
+                   + f", {threads} threads"),
+        "poses_scored_per_s": float(res.poses_scored.sum()) / dt, "seconds": dt}
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1901_06363_b200 import workloads as W
+    w = W.config(a.config)
+    pocket = w.pocket()
+    n = a.ligands or CPU_SAMPLE
+    batch = w.ligands(range(n), pocket.mean(axis=0))
+    for _ in range(a.warmup):
+        cpu_reference(batch, pocket, w.knobs, n)
+    rates, info = [], None
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        r, info = cpu_reference(batch, pocket, w.knobs, n)
+        rates.append(r)
+    wall = time.perf_counter() - t0
+    value = n * a.steps / wall
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "ligands/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * wall / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "ligands_per_step": n},
+        "cpu_baseline": {"value": value, "unit": "ligands/s", "cores": info["cores"],
+                         "kind": info["kind"], "sample": info["sample"]},
+        "e2e": {"value": value, "unit": "ligands/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(a):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1901_06363_b200 import Docker, Knobs, workloads as W
+    from paper_1901_06363_b200.native import DockResult, GD_FLAG_COUNT_WORK
+
+    w = W.config(a.config)
+    pocket = w.pocket()
+    n_per = a.ligands or w.n_ligands
+    ids = range(rank * n_per, (rank + 1) * n_per)
+    batch = w.ligands(ids, pocket.mean(axis=0))
+    knobs = w.knobs
+    K = knobs.slots
+
+    stream = torch.cuda.current_stream()
+    d = Docker(local)
+    d.set_stream(stream.cuda_stream)
+    d.set_pocket(pocket)
+    info = d.pocket_info()
+    d.upload(batch)
+
+    # One counted, untimed step: exact executed work per launch.
+    d.dock_resident(Knobs(**{**knobs.__dict__, "flags": GD_FLAG_COUNT_WORK}))
+    work = d.work_counters()
+    fp64_peak = d.fp64_peak_tflops()
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    res = DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False)
+    gather_bufs = None
+
+    def gather_results():
+        # Top-K gather: every rank's (final score, orientation) to every rank.
+        nonlocal gather_bufs
+        if world == 1:
+            return
+        import torch.distributed as dist
+        d.download(res)
+        fs = torch.from_numpy(res.final_score.reshape(-1)).cuda()
+        if gather_bufs is None:
+            gather_bufs = torch.empty(world * fs.numel(), dtype=fs.dtype, device="cuda")
+        dist.all_gather_into_tensor(gather_bufs, fs)
+
+    for _ in range(a.warmup):
+        d.dock_resident(knobs)
+    rigid_ms, flex_ms, step_ms = [], [], []
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    for _ in range(a.steps):
+        flush.zero_()  # untimed: evicts the 126 MB L2 between steps
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d.dock_resident(knobs)
+        e1.record(stream)
+        e1.synchronize()
+        t = d.timing()
+        rigid_ms.append(t["rigid_ms"])
+        flex_ms.append(t["flex_ms"])
+        step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+        gather_results()
+        dist.barrier()
+    ms_per_step = total_ms / a.steps
+    value = world * batch.n_ligands / (ms_per_step / 1e3)
+
+    d.download(DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False))
+    res_scored = DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False)
+    d.download(res_scored)
+    poses_per_step = float(res_scored.poses_scored.sum()) * world
+    poses_per_s = poses_per_step / (ms_per_step / 1e3)
+
+    # e2e: host buffers through gd_dock_batch (prep + pinned H2D + kernels + D2H).
+    e2e = None
+    if not a.no_e2e:
+        e2e_steps = max(1, min(a.steps, 5))
+        d.dock(batch, knobs)  # warm
+        tms = []
+        for _ in range(e2e_steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            d.dock(batch, knobs)
+            tms.append(time.perf_counter() - t0)
+        tt = float(np.mean(tms))
+        if world > 1:
+            import torch.distributed as dist
+            x = torch.tensor([tt], device="cuda", dtype=torch.float64)
+            dist.all_reduce(x, op=dist.ReduceOp.MAX)
+            tt = float(x.item())
+        tim = d.timing()
+        e2e = {"value": world * batch.n_ligands / tt, "unit": "ligands/s",
+               "h2d_bytes_per_step": int(tim["h2d_bytes"]),
+               "d2h_bytes_per_step": int(tim["d2h_bytes"]), "ms_per_step": 1e3 * tt,
+               "steps": e2e_steps, "timer": "host wall clock around gd_dock_batch"}
+
+    if rank != 0:
+        return
+    # Roofline of the dominant kernel: fp64 FLOPs it executed / its time.
+    r_ms, f_ms = float(np.mean(rigid_ms)), float(np.mean(flex_ms))
+    dom = "flex_kernel" if f_ms >= r_ms else "rigid_topk_kernel"
+    dom_work = work["flex" if dom == "flex_kernel" else "rigid"]
+    dom_ms = max(r_ms, f_ms)
+    achieved = flops_of(dom_work) / (dom_ms / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "ligands/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generators, DESIGN.md §5)",
+        "config": {"workload": w.name, "ligands_per_gpu": batch.n_ligands,
+                   "pocket_points": len(pocket), "rigid_step": knobs.rigid_step,
+                   "fragment_step": knobs.high_precision_step, "restarts": knobs.repetitions,
+                   "top_k": knobs.top_k, "parallelism": f"ligand-sharded x{world}",
+                   "l2": "flushed between steps (256 MiB write, untimed)",
+                   "voxel_index": {k: (v.tolist() if hasattr(v, "tolist") else v)
+                                   for k, v in info.items()}},
+        "poses_scored_per_s": poses_per_s,
+        "kernel_ms": {"rigid_topk_kernel": r_ms, "flex_kernel": f_ms},
+        "gpu_launches": 2 * a.steps,
+        "roofline": {"kernel": dom, "bound": "fp64", "achieved": achieved, "peak": fp64_peak,
+                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
+                     "peak_source": "measured fp64 DADD/DMUL probe (gd_fp64_peak) on this GPU",
+                     "work_per_launch": dom_work},
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not a.no_cpu_baseline:
+        v, inf = cpu_reference(batch, pocket, knobs, CPU_SAMPLE)
+        line["cpu_baseline"] = {"value": v, "unit": "ligands/s", "cores": inf["cores"],
+                                "kind": inf["kind"], "sample": inf["sample"]}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    a = args_()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,189 @@
+/*
+ * geodock_b200.h -- C-ABI of the B200-native GeoDock-MA pose-search hot path.
+ *
+ * This is the drop-in boundary: plain pointers and sizes, integer return
+ * codes, no exceptions and no torch types.  Every entry point names the
+ * reference interface (under /root/reference/proj/include/geodock/) it
+ * replaces.  The C++ drop-in header <geodock_b200/geodock.hpp> maps these
+ * calls back onto the reference's own C++ API (geodock::match_probes_shape,
+ * geodock::screen, geodock::overlap_score, ...), including its exception
+ * messages; bindings for other hosts (ctypes, cgo, JNI) bind this file.
+ *
+ * Numerics: every score, coordinate and decision is computed in fp64 with
+ * the reference's exact expression trees (no FMA contraction, atom-order
+ * sums, host-built trig tables), so results are bit-identical to the
+ * reference CPU path.  See DESIGN.md.
+ *
+ * Threading: one gd_ctx per device, not thread-safe per context.
+ */
+#ifndef GEODOCK_B200_H
+#define GEODOCK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Return codes.  GD_ERR_INVALID/GD_ERR_DEGENERATE map onto geodock::Error
+ * (reference error.hpp:14-17); the message is in gd_last_error(). */
+#define GD_OK 0
+#define GD_ERR_INVALID 1    /* argument / validation failure            */
+#define GD_ERR_CUDA 2       /* CUDA runtime failure (device, OOM, ...)  */
+#define GD_ERR_DEGENERATE 3 /* degenerate rotation axis (geometry.hpp:168) */
+#define GD_ERR_NO_POCKET 4  /* gd_set_pocket not called                 */
+
+/* Per-ligand status codes written to gd_result.status. */
+#define GD_LIG_OK 0
+#define GD_LIG_INVALID 1    /* Ligand ctor validation failed (molecule.hpp:66-115) */
+#define GD_LIG_DEGENERATE 3 /* rotate_fragment threw "degenerate rotation axis"   */
+
+/* gd_knobs.flags */
+#define GD_FLAG_BRUTE_FORCE 1u /* scan every pocket point instead of the voxel index */
+#define GD_FLAG_KEEP_POSES 2u  /* gd_dock_resident: keep final poses for gd_download */
+#define GD_FLAG_COUNT_WORK 4u  /* count executed work (gd_work_counters) */
+
+typedef struct gd_ctx gd_ctx;
+
+/* A batch of ligands, SoA, caller-owned; copied in by the call.
+ * Mirrors geodock::Ligand(id, atoms, bonds) (molecule.hpp:45-50) and the
+ * initial pose make_initial_pose (geometry.hpp:23-28). */
+typedef struct {
+  int32_t n_ligands;
+  const int32_t* atom_offsets;   /* [n_ligands+1] prefix sums of atom counts      */
+  const double* xyz;             /* [total_atoms*3] initial pose, Angstrom         */
+  const double* radii;           /* [total_atoms] Angstrom, > 0                    */
+  const int32_t* bond_offsets;   /* [n_ligands+1] prefix sums of bond counts       */
+  const int32_t* bonds;          /* [total_bonds*2] ligand-local atom indices a,b  */
+  const uint8_t* bond_rotatable; /* [total_bonds] Bond::rotatable                  */
+} gd_ligand_batch;
+
+/* The five reference knobs (KnobConfig, kernel.hpp:21-26) plus the three
+ * north-star knobs of the batch path. */
+typedef struct {
+  int32_t high_precision_step; /* KnobConfig::high_precision_step */
+  int32_t low_precision_step;  /* KnobConfig::low_precision_step  */
+  double threshold;            /* KnobConfig::threshold           */
+  int32_t repetitions;         /* KnobConfig::repetitions (restarts) */
+  int32_t enable_refinement;   /* KnobConfig::enable_refinement   */
+  int32_t rigid_step;          /* degrees of the rigid Euler grid; 0 = no sweep:
+                                  dock the given pose (reference screen semantics) */
+  int32_t top_k;               /* poses kept per ligand (>= 1)    */
+  uint32_t flags;              /* GD_FLAG_*                       */
+} gd_knobs;
+
+/* Caller-allocated results, ligand-major, top_k slots per ligand.  Slot
+ * (l, e) lives at index l*top_k + e, sorted by (final score desc, seed rank
+ * asc); slots e >= k_eff[l] are zero with orientation = -2. */
+typedef struct {
+  int32_t* orientation;          /* [L*K] Euler-grid linear index, -1 = given pose  */
+  int32_t* seed_rank;            /* [L*K] rank of the seed in the rigid top-K        */
+  double* rigid_score;           /* [L*K] overlap score of the rigid seed pose       */
+  double* final_score;           /* [L*K] PoseResult::score                          */
+  int64_t* evaluations;          /* [L*K] PoseResult::evaluations                    */
+  int64_t* feasibility_checks;   /* [L*K] PoseResult::feasibility_checks             */
+  double* final_pose;            /* optional (NULL): [K*total_atoms*3]; ligand l,
+                                    slot e at (K*atom_offsets[l] + e*n_l)*3         */
+  int32_t* k_eff;                /* [L] min(top_k, distinct orientations) (1 if no sweep) */
+  int64_t* poses_scored;         /* [L] rigid orientations scored + sum evaluations  */
+  int32_t* status;               /* [L] GD_LIG_*                                     */
+} gd_result;
+
+/* Device-side timing of the last gd_dock_* call (CUDA events on the
+ * context stream). */
+typedef struct {
+  float upload_ms;     /* H2D of descriptors (0 for gd_dock_resident)  */
+  float rigid_ms;      /* rigid sweep + top-K kernel                   */
+  float flex_ms;       /* fragment-optimisation/restart kernel         */
+  float download_ms;   /* D2H of results                               */
+  float total_ms;      /* first to last event                          */
+  int64_t rigid_atom_queries; /* atoms x orientations scored in the sweep */
+  int64_t flex_atom_queries;  /* fragment-atom nearest-point queries      */
+  int64_t launches;    /* kernels launched by the call                 */
+  int64_t h2d_bytes;   /* bytes copied host->device by the last upload */
+  int64_t d2h_bytes;   /* bytes copied device->host by the last download */
+} gd_timing;
+
+/* ---- context ------------------------------------------------------------ */
+int gd_create(int device, gd_ctx** out);
+int gd_destroy(gd_ctx* ctx);
+/* Message of the last failed call on ctx (or of gd_create when ctx is NULL). */
+const char* gd_last_error(const gd_ctx* ctx);
+/* Run kernels on this cudaStream_t (NULL = the context's own stream). */
+int gd_set_stream(gd_ctx* ctx, void* cuda_stream);
+const char* gd_version(void);
+
+/* ---- pocket ------------------------------------------------------------- */
+/* Stages the pocket in HBM and builds the exact voxel nearest-point index.
+ * Replaces geodock::Pocket(id, points) validation (molecule.hpp:152-157)
+ * and PocketIndex(pocket) (geometry.hpp:49-65).  Also fixes the rigid-sweep
+ * centre c = (sum_j P_j)/P, summed in index order (E1). */
+int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n_points);
+/* Centre and index statistics of the staged pocket. */
+int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[3], double* voxel,
+                   int64_t* n_candidates, int32_t* max_candidates);
+
+/* ---- batch docking (the hot path) --------------------------------------- */
+/* Host buffers in, host buffers out: validate + preprocess (Ligand ctor,
+ * find_rotamers, grow_fragments; molecule.hpp:45-301), H2D, rigid sweep,
+ * top-K, K x match_probes_shape (kernel.hpp:205-248), final ordering, D2H.
+ * With rigid_step == 0 and top_k == 1 this is geodock::screen
+ * (screening.hpp:96-178) without the thread pool. */
+int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd_knobs* knobs,
+                  gd_result* result);
+
+/* Split form used to time the device-resident path: gd_upload preprocesses
+ * and copies a batch into HBM (kept in the context, replacing any previous
+ * one); gd_dock_resident runs the kernels on it; gd_download copies the
+ * results of the last gd_dock_resident into `result`. */
+int gd_upload(gd_ctx* ctx, const gd_ligand_batch* batch);
+int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs);
+int gd_download(gd_ctx* ctx, gd_result* result);
+int gd_last_timing(const gd_ctx* ctx, gd_timing* out);
+/* Exact work executed by the last call made with GD_FLAG_COUNT_WORK:
+ * out[0..6] rigid kernel, out[8..14] flex kernel, each {point pairs, rotated
+ * atoms, bump pairs, nearest-point queries, score-sum terms, candidate
+ * evaluations, rigid-transformed atoms}.  DESIGN.md §4 turns them into FLOPs. */
+int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]);
+/* Measures this device's fp64 DADD/DMUL issue rate (TFLOP/s, no FMA) with
+ * a probe kernel; the denominator of the fp64 roofline. */
+int gd_fp64_peak(gd_ctx* ctx, double* tflops);
+
+/* ---- fine-grained kernels ------------------------------------------------ */
+/* overlap_score (geometry.hpp:140-155) of n_poses poses of n_atoms atoms
+ * each, xyz pose-major [n_poses*n_atoms*3]. */
+int gd_overlap_score_batch(gd_ctx* ctx, const double* xyz, int32_t n_atoms, int32_t n_poses,
+                           uint32_t flags, double* out_scores);
+
+/* ---- host helpers (no device work) --------------------------------------- */
+/* optimal_tile_size (kernel.hpp:62-75); returns -1 when step < 1. */
+int32_t gd_optimal_tile_size(int32_t high_precision_step);
+/* KnobConfig::validate (kernel.hpp:28-38) + batch-knob checks.  Returns
+ * GD_OK or GD_ERR_INVALID with the reference message copied to msg. */
+int gd_validate_knobs(const gd_knobs* knobs, char* msg, size_t msg_len);
+/* Distinct orientations of the rigid Euler grid (E2): writes up
+ * to cap linear indices (ascending) and, if R != NULL, their row-major 3x3
+ * matrices; returns the count or -1 when step does not divide 360. */
+int32_t gd_orientations(int32_t rigid_step, int32_t* indices, double* R, int32_t cap);
+
+/* ---- synthetic BASELINE data (tools; not the hot path) ------------------ */
+/* Lattice ellipsoid pocket, points in (i,j,k) lexicographic order, centred
+ * at the origin; rough_max > 0 removes a seeded U(0, rough_max) fraction of
+ * the outermost points.  Returns the point count (writes at most cap). */
+int32_t gd_synth_pocket(double a, double b, double c, double spacing, double rough_max,
+                        uint64_t seed, double* xyz, int32_t cap);
+/* Sizes of ligand `id` of the seeded random-walk-tree family: n ~ U{n_lo..n_hi}
+ * (or fixed_n > 0), rotatable bonds R ~ U{0..min(r_cap, n/4)} (or fixed_r >= 0). */
+int gd_synth_ligand_size(uint64_t base_seed, int64_t id, int32_t n_lo, int32_t n_hi,
+                         int32_t fixed_n, int32_t* n_atoms);
+/* Ligand `id`: writes n atoms (xyz, radii) and n-1 bonds; centroid moved to
+ * `centre`.  Returns the number of rotatable bonds. */
+int gd_synth_ligand(uint64_t base_seed, int64_t id, int32_t n_lo, int32_t n_hi, int32_t fixed_n,
+                    int32_t r_cap, int32_t fixed_r, const double centre[3], double* xyz,
+                    double* radii, int32_t* bonds, uint8_t* rotatable);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEODOCK_B200_H */

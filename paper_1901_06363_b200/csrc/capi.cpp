@@ -1,0 +1,763 @@
+// C-ABI of the B200 pose-search path (include/geodock_b200.h).
+//
+// Host runtime: validation and preprocessing (prep.cpp), pinned staging,
+// one CUDA stream per context, the voxel index build, and the two hot-path
+// launches (rigid_topk_kernel, flex_kernel).  No CPU fallback exists: every
+// score comes from the kernels in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "geodock_b200.h"
+#include "kernels.h"
+#include "orient.hpp"
+#include "prep.hpp"
+
+using namespace gdb200;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes && ptr) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    const cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 256));
+    if (e == cudaSuccess) bytes = std::max<size_t>(n, 256);
+    return e;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(ptr);
+  }
+};
+
+struct PinnedBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  ~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes && ptr) return cudaSuccess;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    const cudaError_t e = cudaHostAlloc(&ptr, std::max<size_t>(n, 256), cudaHostAllocDefault);
+    if (e == cudaSuccess) bytes = std::max<size_t>(n, 256);
+    return e;
+  }
+};
+
+double env_double(const char* name, double dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atof(v) : dflt;
+}
+
+}  // namespace
+
+struct gd_ctx {
+  int device = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  cudaEvent_t ev[5] = {};
+
+  // Pocket.
+  int32_t P = 0;
+  double centre[3] = {0, 0, 0};
+  DevBuf pts, vox_off, vox_pts;
+  VoxelGrid grid{};
+  int64_t n_cand = 0;
+  int32_t max_cand = 0;
+  PocketView view{};
+
+  DevBuf cos_t, sin_t;
+  int orient_step = -1;
+  int32_t n_orient = 0;
+  std::vector<int32_t> orient_idx_host;
+  DevBuf orient_idx, orient_R;
+
+  // Resident batch.
+  int32_t n_lig = 0;
+  int32_t total_atoms = 0;
+  int32_t max_n = 0;
+  int max_nfrag = 0;
+  std::vector<int32_t> atom_off;
+  std::vector<int32_t> status_host;
+  std::vector<std::string> errors;
+  DevBuf meta, xyz, radii, far, fmask, fax, fan, frel, order;
+  PinnedBuf staging;
+
+  // Outputs of the last gd_dock_resident.
+  int32_t last_topk = 0;
+  bool last_rigid = false;
+  bool last_pose = false;
+  bool have_result = false;
+  DevBuf counters;
+  bool counted = false;
+  DevBuf seed_slot, seed_score, k_eff, o_orient, o_rank, o_rigid, o_final, o_evals, o_checks,
+      o_pose, stage_pose, o_scored, o_status;
+  std::vector<double> initial_score;  // given-pose mode: rigid_score column
+
+  gd_timing timing{};
+
+  int fail(int code, std::string msg) {
+    err = std::move(msg);
+    return code;
+  }
+  int cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return GD_OK;
+    return fail(GD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+};
+
+#define GD_CUDA(ctx, expr)                          \
+  do {                                              \
+    const int _rc = (ctx)->cuda((expr), #expr);     \
+    if (_rc != GD_OK) return _rc;                   \
+  } while (0)
+
+extern "C" const char* gd_version(void) { return "geodock_b200 0.1 (sm_100a, fp64 exact)"; }
+
+extern "C" int gd_create(int device, gd_ctx** out) {
+  if (out == nullptr) {
+    g_create_error = "gd_create: null output pointer";
+    return GD_ERR_INVALID;
+  }
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    g_create_error = std::string("gd_create: no CUDA device: ") + cudaGetErrorString(e);
+    return GD_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) {
+    g_create_error = "gd_create: device index out of range";
+    return GD_ERR_INVALID;
+  }
+  auto* ctx = new gd_ctx();
+  ctx->device = device;
+  e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking);
+  for (int i = 0; i < 5 && e == cudaSuccess; ++i) e = cudaEventCreate(&ctx->ev[i]);
+  if (e != cudaSuccess) {
+    g_create_error = std::string("gd_create: ") + cudaGetErrorString(e);
+    delete ctx;
+    return GD_ERR_CUDA;
+  }
+  ctx->stream = ctx->own_stream;
+  std::vector<double> c, s;
+  trig_tables(c, s);
+  if (ctx->cos_t.ensure(360 * sizeof(double)) != cudaSuccess ||
+      ctx->sin_t.ensure(360 * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(ctx->cos_t.ptr, c.data(), 360 * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(ctx->sin_t.ptr, s.data(), 360 * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess) {
+    g_create_error = "gd_create: trig table upload failed";
+    delete ctx;
+    return GD_ERR_CUDA;
+  }
+  *out = ctx;
+  return GD_OK;
+}
+
+extern "C" int gd_destroy(gd_ctx* ctx) {
+  if (ctx == nullptr) return GD_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (cudaEvent_t ev : ctx->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+  return GD_OK;
+}
+
+extern "C" const char* gd_last_error(const gd_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+extern "C" int gd_set_stream(gd_ctx* ctx, void* cuda_stream) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+  return GD_OK;
+}
+
+extern "C" int32_t gd_optimal_tile_size(int32_t step) {
+  // kernel.hpp:62-75: argmin over divisors x of step*(360/x) + x, smaller x on ties.
+  if (step < 1) return -1;
+  long best = -1;
+  int32_t tile = 360;
+  for (int x = 1; x <= 360; ++x) {
+    if (360 % x) continue;
+    const long v = static_cast<long>(step) * (360 / x) + x;
+    if (best < 0 || v < best) {
+      best = v;
+      tile = x;
+    }
+  }
+  return tile;
+}
+
+extern "C" int gd_validate_knobs(const gd_knobs* k, char* msg, size_t msg_len) {
+  const char* m = nullptr;
+  if (k == nullptr) m = "knob config: null";
+  // KnobConfig::validate (kernel.hpp:28-38), same order and messages.
+  else if (k->high_precision_step < 1 || 360 % k->high_precision_step != 0)
+    m = "knob config: high-precision step must be a divisor of 360";
+  else if (k->low_precision_step < 1 || 360 % k->low_precision_step != 0)
+    m = "knob config: low-precision step must be a divisor of 360";
+  else if (k->low_precision_step < k->high_precision_step)
+    m = "knob config: low-precision step must be >= high-precision step";
+  else if (!(k->threshold >= 0.0 && k->threshold <= 1.0))
+    m = "knob config: threshold must be in [0,1]";
+  else if (k->repetitions < 1)
+    m = "knob config: repetitions must be >= 1";
+  else if (k->rigid_step < 0 || (k->rigid_step > 0 && 360 % k->rigid_step != 0))
+    m = "knob config: rigid step must be 0 or a divisor of 360";
+  else if (k->top_k < 1 || k->top_k > 256)
+    m = "knob config: top_k must be in [1,256]";
+  if (m == nullptr) return GD_OK;
+  if (msg && msg_len) {
+    std::strncpy(msg, m, msg_len - 1);
+    msg[msg_len - 1] = 0;
+  }
+  return GD_ERR_INVALID;
+}
+
+extern "C" int32_t gd_orientations(int32_t step, int32_t* indices, double* R, int32_t cap) {
+  if (step < 1 || 360 % step != 0) return -1;
+  std::vector<int32_t> idx;
+  std::vector<double> mats;
+  rigid_orientations(step, idx, mats);
+  const int32_t n = static_cast<int32_t>(idx.size());
+  for (int32_t i = 0; i < std::min(n, cap); ++i) {
+    if (indices) indices[i] = idx[i];
+    if (R) std::memcpy(R + 9 * i, mats.data() + 9 * i, 9 * sizeof(double));
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// Pocket staging and the voxel index.
+// ---------------------------------------------------------------------------
+extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  // Pocket ctor validation (molecule.hpp:152-157).
+  if (n < 1 || xyz == nullptr) return ctx->fail(GD_ERR_INVALID, "pocket: needs at least 1 point");
+  for (int32_t j = 0; j < 3 * n; ++j)
+    if (!std::isfinite(xyz[j])) return ctx->fail(GD_ERR_INVALID, "pocket: non-finite point");
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  // E1: centre = (sum_j P_j) / P, summed in index order.
+  double sx = 0.0, sy = 0.0, sz = 0.0, lo[3], hi[3];
+  for (int k = 0; k < 3; ++k) lo[k] = hi[k] = xyz[k];
+  for (int32_t j = 0; j < n; ++j) {
+    sx += xyz[3 * j];
+    sy += xyz[3 * j + 1];
+    sz += xyz[3 * j + 2];
+    for (int k = 0; k < 3; ++k) {
+      lo[k] = std::min(lo[k], xyz[3 * j + k]);
+      hi[k] = std::max(hi[k], xyz[3 * j + k]);
+    }
+  }
+  ctx->centre[0] = sx / n;
+  ctx->centre[1] = sy / n;
+  ctx->centre[2] = sz / n;
+  ctx->P = n;
+
+  std::vector<double> padded(4 * static_cast<size_t>(n), 0.0);
+  for (int32_t j = 0; j < n; ++j)
+    for (int k = 0; k < 3; ++k) padded[4 * j + k] = xyz[3 * j + k];
+  GD_CUDA(ctx, ctx->pts.ensure(padded.size() * sizeof(double)));
+  GD_CUDA(ctx, cudaMemcpy(ctx->pts.ptr, padded.data(), padded.size() * sizeof(double),
+                          cudaMemcpyHostToDevice));
+
+  // Grid: pocket bounding box plus a margin; voxel edge h (0.5 A default).
+  double h = env_double("GD_VOXEL_H", 0.5);
+  const double margin = env_double("GD_VOXEL_MARGIN", 8.0);
+  VoxelGrid g{};
+  for (;;) {
+    int dims[3];
+    long total = 1;
+    for (int k = 0; k < 3; ++k) {
+      dims[k] = static_cast<int>(std::floor((hi[k] - lo[k] + 2 * margin) / h)) + 1;
+      total *= dims[k];
+    }
+    if (total <= (1l << 23)) {
+      g = VoxelGrid{lo[0] - margin, lo[1] - margin, lo[2] - margin, h, dims[0], dims[1], dims[2]};
+      break;
+    }
+    h *= 1.25;
+  }
+  const int nv = g.dim_x * g.dim_y * g.dim_z;
+  DevBuf counts;
+  GD_CUDA(ctx, counts.ensure(sizeof(int32_t) * nv));
+  GD_CUDA(ctx, static_cast<cudaError_t>(
+                   launch_voxel_count(ctx->pts.as<double>(), n, g, counts.as<int32_t>(), ctx->stream)));
+  std::vector<int32_t> cnt(nv);
+  GD_CUDA(ctx, cudaMemcpyAsync(cnt.data(), counts.ptr, sizeof(int32_t) * nv, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  std::vector<int32_t> off(nv + 1, 0);
+  int64_t total = 0;
+  int32_t mx = 0;
+  for (int v = 0; v < nv; ++v) {
+    off[v] = static_cast<int32_t>(total);
+    total += cnt[v];
+    mx = std::max(mx, cnt[v]);
+    if (total > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
+  }
+  off[nv] = static_cast<int32_t>(total);
+  GD_CUDA(ctx, ctx->vox_off.ensure(sizeof(int32_t) * (nv + 1)));
+  GD_CUDA(ctx, ctx->vox_pts.ensure(sizeof(double) * 4 * std::max<int64_t>(total, 1)));
+  GD_CUDA(ctx, cudaMemcpyAsync(ctx->vox_off.ptr, off.data(), sizeof(int32_t) * (nv + 1),
+                               cudaMemcpyHostToDevice, ctx->stream));
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_voxel_fill(ctx->pts.as<double>(), n, g,
+                                                          ctx->vox_off.as<int32_t>(),
+                                                          ctx->vox_pts.as<double>(), ctx->stream)));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->grid = g;
+  ctx->n_cand = total;
+  ctx->max_cand = mx;
+  PocketView& v = ctx->view;
+  v.pts = ctx->pts.as<double>();
+  v.P = n;
+  v.use_index = 1;
+  v.vox_off = ctx->vox_off.as<int32_t>();
+  v.vox_pts = ctx->vox_pts.as<double>();
+  v.lo_x = g.lo_x;
+  v.lo_y = g.lo_y;
+  v.lo_z = g.lo_z;
+  v.inv_h = 1.0 / g.h;
+  v.dim_x = g.dim_x;
+  v.dim_y = g.dim_y;
+  v.dim_z = g.dim_z;
+  return GD_OK;
+}
+
+extern "C" int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[3], double* voxel,
+                              int64_t* n_candidates, int32_t* max_candidates) {
+  if (ctx == nullptr || ctx->P == 0) return GD_ERR_NO_POCKET;
+  if (centre)
+    for (int k = 0; k < 3; ++k) centre[k] = ctx->centre[k];
+  if (dims) {
+    dims[0] = ctx->grid.dim_x;
+    dims[1] = ctx->grid.dim_y;
+    dims[2] = ctx->grid.dim_z;
+  }
+  if (voxel) *voxel = ctx->grid.h;
+  if (n_candidates) *n_candidates = ctx->n_cand;
+  if (max_candidates) *max_candidates = ctx->max_cand;
+  return GD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Batch upload: validate + preprocess on the host, pack, one H2D per array.
+// ---------------------------------------------------------------------------
+extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  if (b == nullptr || b->n_ligands < 0 || (b->n_ligands > 0 &&
+      (!b->atom_offsets || !b->xyz || !b->radii || !b->bond_offsets ||
+       (b->bond_offsets[b->n_ligands] > 0 && (!b->bonds || !b->bond_rotatable)))))
+    return ctx->fail(GD_ERR_INVALID, "gd_upload: invalid ligand batch");
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int L = b->n_ligands;
+  std::vector<PreparedLigand> prep(L);
+  ctx->errors.assign(L, std::string());
+  ctx->status_host.assign(L, 0);
+  ctx->atom_off.assign(b->atom_offsets, b->atom_offsets + L + 1);
+  int32_t max_n = 1;
+  int max_nfrag = 0;
+  size_t far_words = 0, fmask_words = 0, nfrag_total = 0;
+  for (int l = 0; l < L; ++l) {
+    const int a0 = b->atom_offsets[l], n = b->atom_offsets[l + 1] - a0;
+    const int b0 = b->bond_offsets[l], nb = b->bond_offsets[l + 1] - b0;
+    if (n < 0 || nb < 0) return ctx->fail(GD_ERR_INVALID, "gd_upload: offsets not ascending");
+    prep[l] = prepare_ligand(std::to_string(l), n, b->xyz + 3 * a0, b->radii + a0, nb,
+                             b->bonds + 2 * b0, b->bond_rotatable + b0);
+    ctx->status_host[l] = prep[l].status;
+    ctx->errors[l] = prep[l].error;
+    if (prep[l].status != 0) continue;
+    max_n = std::max(max_n, n);
+    max_nfrag = std::max(max_nfrag, prep[l].nfrag());
+    far_words += prep[l].far_mask.size();
+    fmask_words += prep[l].frag_mask.size();
+    nfrag_total += prep[l].nfrag();
+  }
+  const int32_t total_atoms = b->atom_offsets[L];
+
+  // Pinned arena layout.
+  const size_t sz_meta = sizeof(LigMeta) * std::max(L, 1);
+  const size_t sz_xyz = sizeof(double) * 3 * std::max(total_atoms, 1);
+  const size_t sz_rad = sizeof(double) * std::max(total_atoms, 1);
+  const size_t sz_far = sizeof(uint64_t) * std::max<size_t>(far_words, 1);
+  const size_t sz_fm = sizeof(uint64_t) * std::max<size_t>(fmask_words, 1);
+  const size_t sz_fi = sizeof(int32_t) * std::max<size_t>(nfrag_total, 1);
+  const size_t sz_fr = sizeof(double) * std::max<size_t>(nfrag_total, 1);
+  const size_t sz_ord = sizeof(int32_t) * std::max(L, 1);
+  const size_t sizes[] = {sz_meta, sz_xyz, sz_rad, sz_far, sz_fm, sz_fi, sz_fi, sz_fr, sz_ord};
+  size_t arena = 0;
+  for (size_t s : sizes) arena += (s + 255) & ~size_t(255);
+  GD_CUDA(ctx, ctx->staging.ensure(arena));
+  unsigned char* base = static_cast<unsigned char*>(ctx->staging.ptr);
+  unsigned char* ptrs[9];
+  {
+    size_t o = 0;
+    for (int i = 0; i < 9; ++i) {
+      ptrs[i] = base + o;
+      o += (sizes[i] + 255) & ~size_t(255);
+    }
+  }
+  auto* meta = reinterpret_cast<LigMeta*>(ptrs[0]);
+  auto* hxyz = reinterpret_cast<double*>(ptrs[1]);
+  auto* hrad = reinterpret_cast<double*>(ptrs[2]);
+  auto* hfar = reinterpret_cast<uint64_t*>(ptrs[3]);
+  auto* hfm = reinterpret_cast<uint64_t*>(ptrs[4]);
+  auto* hax = reinterpret_cast<int32_t*>(ptrs[5]);
+  auto* han = reinterpret_cast<int32_t*>(ptrs[6]);
+  auto* hrel = reinterpret_cast<double*>(ptrs[7]);
+  auto* hord = reinterpret_cast<int32_t*>(ptrs[8]);
+  std::memcpy(hxyz, b->xyz, sizeof(double) * 3 * total_atoms);
+  std::memcpy(hrad, b->radii, sizeof(double) * total_atoms);
+  size_t fo = 0, wo = 0, mo = 0;
+  std::vector<double> cost(L, 0.0);
+  for (int l = 0; l < L; ++l) {
+    const PreparedLigand& p = prep[l];
+    LigMeta& m = meta[l];
+    m.atom_off = b->atom_offsets[l];
+    m.n = b->atom_offsets[l + 1] - b->atom_offsets[l];
+    m.status = p.status;
+    m.frag_off = static_cast<int32_t>(fo);
+    m.nfrag = p.status == 0 ? p.nfrag() : 0;
+    m.far_off = static_cast<int32_t>(wo);
+    m.fmask_off = static_cast<int32_t>(mo);
+    m.words = p.words;
+    if (p.status != 0) continue;
+    std::copy(p.far_mask.begin(), p.far_mask.end(), hfar + wo);
+    std::copy(p.frag_mask.begin(), p.frag_mask.end(), hfm + mo);
+    for (int f = 0; f < p.nfrag(); ++f) {
+      hax[fo + f] = p.frag_axis[f];
+      han[fo + f] = p.frag_anchor[f];
+      hrel[fo + f] = p.frag_rel[f];
+    }
+    wo += p.far_mask.size();
+    mo += p.frag_mask.size();
+    fo += p.nfrag();
+    cost[l] = static_cast<double>(m.n) * (4.0 + m.nfrag);
+  }
+  // Longest-processing-time-first CTA order (ties by ligand index).
+  std::iota(hord, hord + L, 0);
+  std::stable_sort(hord, hord + L, [&](int32_t a, int32_t c) { return cost[a] > cost[c]; });
+
+  DevBuf* dev[9] = {&ctx->meta, &ctx->xyz, &ctx->radii, &ctx->far, &ctx->fmask,
+                    &ctx->fax,  &ctx->fan, &ctx->frel,  &ctx->order};
+  cudaEventRecord(ctx->ev[0], ctx->stream);
+  for (int i = 0; i < 9; ++i) {
+    GD_CUDA(ctx, dev[i]->ensure(sizes[i]));
+    GD_CUDA(ctx, cudaMemcpyAsync(dev[i]->ptr, ptrs[i], sizes[i], cudaMemcpyHostToDevice, ctx->stream));
+  }
+  cudaEventRecord(ctx->ev[1], ctx->stream);
+  ctx->n_lig = L;
+  ctx->total_atoms = total_atoms;
+  ctx->max_n = max_n;
+  ctx->max_nfrag = max_nfrag;
+  ctx->have_result = false;
+  ctx->timing = gd_timing{};
+  for (size_t s : sizes) ctx->timing.h2d_bytes += static_cast<int64_t>(s);
+  return GD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// The hot path on the resident batch.
+// ---------------------------------------------------------------------------
+static int ensure_orientations(gd_ctx* ctx, int step) {
+  if (ctx->orient_step == step) return GD_OK;
+  std::vector<int32_t> idx;
+  std::vector<double> R;
+  rigid_orientations(step, idx, R);
+  GD_CUDA(ctx, ctx->orient_idx.ensure(sizeof(int32_t) * idx.size()));
+  GD_CUDA(ctx, ctx->orient_R.ensure(sizeof(double) * R.size()));
+  GD_CUDA(ctx, cudaMemcpy(ctx->orient_idx.ptr, idx.data(), sizeof(int32_t) * idx.size(),
+                          cudaMemcpyHostToDevice));
+  GD_CUDA(ctx, cudaMemcpy(ctx->orient_R.ptr, R.data(), sizeof(double) * R.size(),
+                          cudaMemcpyHostToDevice));
+  ctx->orient_step = step;
+  ctx->n_orient = static_cast<int32_t>(idx.size());
+  ctx->orient_idx_host = idx;
+  return GD_OK;
+}
+
+static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
+  char msg[128];
+  if (gd_validate_knobs(k, msg, sizeof msg) != GD_OK) return ctx->fail(GD_ERR_INVALID, msg);
+  if (ctx->P == 0) return ctx->fail(GD_ERR_NO_POCKET, "gd_dock: no pocket staged (gd_set_pocket)");
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  const bool rigid = k->rigid_step > 0;
+  if (rigid) {
+    const int rc = ensure_orientations(ctx, k->rigid_step);
+    if (rc != GD_OK) return rc;
+  }
+  const int L = ctx->n_lig;
+  const int K = rigid ? k->top_k : 1;
+  const size_t slots = static_cast<size_t>(L) * K;
+  GD_CUDA(ctx, ctx->seed_slot.ensure(sizeof(int32_t) * slots));
+  GD_CUDA(ctx, ctx->seed_score.ensure(sizeof(double) * slots));
+  GD_CUDA(ctx, ctx->k_eff.ensure(sizeof(int32_t) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->o_orient.ensure(sizeof(int32_t) * slots));
+  GD_CUDA(ctx, ctx->o_rank.ensure(sizeof(int32_t) * slots));
+  GD_CUDA(ctx, ctx->o_rigid.ensure(sizeof(double) * slots));
+  GD_CUDA(ctx, ctx->o_final.ensure(sizeof(double) * slots));
+  GD_CUDA(ctx, ctx->o_evals.ensure(sizeof(int64_t) * slots));
+  GD_CUDA(ctx, ctx->o_checks.ensure(sizeof(int64_t) * slots));
+  GD_CUDA(ctx, ctx->o_scored.ensure(sizeof(int64_t) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->o_status.ensure(sizeof(int32_t) * std::max(L, 1)));
+  if (keep_pose) {
+    const size_t pose_bytes = sizeof(double) * 3 * static_cast<size_t>(ctx->total_atoms) * K;
+    GD_CUDA(ctx, ctx->o_pose.ensure(pose_bytes));
+    GD_CUDA(ctx, ctx->stage_pose.ensure(pose_bytes));
+  }
+  GD_CUDA(ctx, cudaMemcpyAsync(ctx->o_status.ptr, ctx->status_host.data(), sizeof(int32_t) * L,
+                               cudaMemcpyHostToDevice, ctx->stream));
+
+  DockParams p{};
+  p.n_lig = L;
+  p.order = ctx->order.as<int32_t>();
+  p.meta = ctx->meta.as<LigMeta>();
+  p.xyz = ctx->xyz.as<double>();
+  p.radii = ctx->radii.as<double>();
+  p.far_mask = ctx->far.as<uint64_t>();
+  p.frag_mask = ctx->fmask.as<uint64_t>();
+  p.frag_axis = ctx->fax.as<int32_t>();
+  p.frag_anchor = ctx->fan.as<int32_t>();
+  p.frag_rel = ctx->frel.as<double>();
+  p.pocket = ctx->view;
+  p.pocket.use_index = (k->flags & GD_FLAG_BRUTE_FORCE) ? 0 : 1;
+  p.cx = ctx->centre[0];
+  p.cy = ctx->centre[1];
+  p.cz = ctx->centre[2];
+  p.n_orient = rigid ? ctx->n_orient : 0;
+  p.orient_idx = ctx->orient_idx.as<int32_t>();
+  p.orient_R = ctx->orient_R.as<double>();
+  p.cos_deg = ctx->cos_t.as<double>();
+  p.sin_deg = ctx->sin_t.as<double>();
+  p.hp = k->high_precision_step;
+  p.lp = k->low_precision_step;
+  p.reps = k->repetitions;
+  p.refine = k->enable_refinement ? 1 : 0;
+  p.tile = gd_optimal_tile_size(k->high_precision_step);
+  p.threshold = k->threshold;
+  p.top_k = K;
+  p.rigid = rigid ? 1 : 0;
+  p.max_n = ctx->max_n;
+  int amax = std::max(360 / p.hp - 1, 360 / p.lp - 1);
+  if (p.refine) amax = std::max({amax, 360 / p.tile, p.tile / p.hp});
+  p.amax = std::max(amax, 1);
+  p.seed_slot = ctx->seed_slot.as<int32_t>();
+  p.seed_score = ctx->seed_score.as<double>();
+  p.k_eff = ctx->k_eff.as<int32_t>();
+  p.out_orient = ctx->o_orient.as<int32_t>();
+  p.out_rank = ctx->o_rank.as<int32_t>();
+  p.out_rigid = ctx->o_rigid.as<double>();
+  p.out_final = ctx->o_final.as<double>();
+  p.out_evals = ctx->o_evals.as<int64_t>();
+  p.out_checks = ctx->o_checks.as<int64_t>();
+  p.out_pose = keep_pose ? ctx->o_pose.as<double>() : nullptr;
+  p.stage_pose = keep_pose ? ctx->stage_pose.as<double>() : nullptr;
+  p.poses_scored = ctx->o_scored.as<int64_t>();
+  p.status = ctx->o_status.as<int32_t>();
+  p.counters = nullptr;
+  if (k->flags & GD_FLAG_COUNT_WORK) {
+    GD_CUDA(ctx, ctx->counters.ensure(sizeof(unsigned long long) * 16));
+    GD_CUDA(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * 16, ctx->stream));
+    p.counters = ctx->counters.as<unsigned long long>();
+  }
+  ctx->counted = p.counters != nullptr;
+  // Chains resident per CTA: as many as fit a ~100 KB shared-memory budget.
+  const size_t budget = static_cast<size_t>(env_double("GD_FLEX_SMEM", 100 * 1024));
+  p.chains_per_cta = std::min(K, 32);
+  while (p.chains_per_cta > 1 && flex_smem_bytes(p) > budget) --p.chains_per_cta;
+
+  int launches = 0;
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  if (L > 0 && rigid) {
+    int sort_slots = 2;
+    while (sort_slots < std::min(ctx->n_orient, 2048)) sort_slots <<= 1;
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_rigid_topk(p, sort_slots, ctx->stream)));
+    ++launches;
+  }
+  cudaEventRecord(ctx->ev[3], ctx->stream);
+  if (L > 0) {
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_flex(p, ctx->stream)));
+    ++launches;
+  }
+  cudaEventRecord(ctx->ev[4], ctx->stream);
+  ctx->last_topk = K;
+  ctx->last_rigid = rigid;
+  ctx->last_pose = keep_pose;
+  ctx->have_result = true;
+  ctx->timing.launches = launches;
+  return GD_OK;
+}
+
+extern "C" int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  const int rc = run_kernels(ctx, knobs, knobs && (knobs->flags & GD_FLAG_KEEP_POSES));
+  if (rc != GD_OK) return rc;
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  cudaEventElapsedTime(&ctx->timing.rigid_ms, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&ctx->timing.flex_ms, ctx->ev[3], ctx->ev[4]);
+  ctx->timing.total_ms = ctx->timing.rigid_ms + ctx->timing.flex_ms;
+  return GD_OK;
+}
+
+static int download(gd_ctx* ctx, gd_result* r) {
+  if (!ctx->have_result) return ctx->fail(GD_ERR_INVALID, "gd_download: nothing docked yet");
+  const int L = ctx->n_lig, K = ctx->last_topk;
+  const size_t slots = static_cast<size_t>(L) * K;
+  cudaStream_t s = ctx->stream;
+  ctx->timing.d2h_bytes = 0;
+  auto cp = [&](void* dst, const DevBuf& src, size_t bytes) -> int {
+    if (dst == nullptr || bytes == 0) return GD_OK;
+    ctx->timing.d2h_bytes += static_cast<int64_t>(bytes);
+    return ctx->cuda(cudaMemcpyAsync(dst, src.ptr, bytes, cudaMemcpyDeviceToHost, s), "download");
+  };
+  int rc = GD_OK;
+  if ((rc = cp(r->orientation, ctx->o_orient, sizeof(int32_t) * slots))) return rc;
+  if ((rc = cp(r->seed_rank, ctx->o_rank, sizeof(int32_t) * slots))) return rc;
+  if ((rc = cp(r->rigid_score, ctx->o_rigid, sizeof(double) * slots))) return rc;
+  if ((rc = cp(r->final_score, ctx->o_final, sizeof(double) * slots))) return rc;
+  if ((rc = cp(r->evaluations, ctx->o_evals, sizeof(int64_t) * slots))) return rc;
+  if ((rc = cp(r->feasibility_checks, ctx->o_checks, sizeof(int64_t) * slots))) return rc;
+  if ((rc = cp(r->k_eff, ctx->k_eff, sizeof(int32_t) * L))) return rc;
+  if ((rc = cp(r->poses_scored, ctx->o_scored, sizeof(int64_t) * L))) return rc;
+  if ((rc = cp(r->status, ctx->o_status, sizeof(int32_t) * L))) return rc;
+  if (r->final_pose != nullptr) {
+    if (!ctx->last_pose) return ctx->fail(GD_ERR_INVALID, "gd_download: poses were not kept");
+    if ((rc = cp(r->final_pose, ctx->o_pose, sizeof(double) * 3 * size_t(ctx->total_atoms) * K)))
+      return rc;
+  }
+  GD_CUDA(ctx, cudaStreamSynchronize(s));
+  // Empty slots (ligands that failed, or slots past k_eff) read as
+  // orientation -2 and zeros.
+  std::vector<int32_t> keff(L), stat(L);
+  GD_CUDA(ctx, cudaMemcpy(keff.data(), ctx->k_eff.ptr, sizeof(int32_t) * L, cudaMemcpyDeviceToHost));
+  GD_CUDA(ctx, cudaMemcpy(stat.data(), ctx->o_status.ptr, sizeof(int32_t) * L, cudaMemcpyDeviceToHost));
+  for (int l = 0; l < L; ++l) {
+    const int kk = stat[l] != 0 ? 0 : (ctx->last_rigid ? keff[l] : 1);
+    if (r->k_eff) r->k_eff[l] = kk;
+    if (stat[l] != 0 && r->poses_scored) r->poses_scored[l] = 0;
+    const int n = ctx->atom_off[l + 1] - ctx->atom_off[l];
+    for (int e = kk; e < K; ++e) {
+      const size_t d = static_cast<size_t>(l) * K + e;
+      if (r->orientation) r->orientation[d] = -2;
+      if (r->seed_rank) r->seed_rank[d] = 0;
+      if (r->rigid_score) r->rigid_score[d] = 0.0;
+      if (r->final_score) r->final_score[d] = 0.0;
+      if (r->evaluations) r->evaluations[d] = 0;
+      if (r->feasibility_checks) r->feasibility_checks[d] = 0;
+      if (r->final_pose)
+        std::memset(r->final_pose + 3 * (static_cast<size_t>(K) * ctx->atom_off[l] + size_t(e) * n), 0,
+                    sizeof(double) * 3 * n);
+    }
+  }
+  return GD_OK;
+}
+
+extern "C" int gd_download(gd_ctx* ctx, gd_result* r) {
+  if (ctx == nullptr || r == nullptr) return GD_ERR_INVALID;
+  return download(ctx, r);
+}
+
+extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd_knobs* knobs,
+                             gd_result* result) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  if (result == nullptr) return ctx->fail(GD_ERR_INVALID, "gd_dock_batch: null result");
+  char msg[128];
+  if (gd_validate_knobs(knobs, msg, sizeof msg) != GD_OK) return ctx->fail(GD_ERR_INVALID, msg);
+  int rc = gd_upload(ctx, batch);
+  if (rc != GD_OK) return rc;
+  rc = run_kernels(ctx, knobs, result->final_pose != nullptr);
+  if (rc != GD_OK) return rc;
+  rc = download(ctx, result);
+  if (rc != GD_OK) return rc;
+  cudaEventElapsedTime(&ctx->timing.upload_ms, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&ctx->timing.rigid_ms, ctx->ev[2], ctx->ev[3]);
+  cudaEventElapsedTime(&ctx->timing.flex_ms, ctx->ev[3], ctx->ev[4]);
+  cudaEventElapsedTime(&ctx->timing.total_ms, ctx->ev[0], ctx->ev[4]);
+  return GD_OK;
+}
+
+extern "C" int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]) {
+  if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
+  if (!ctx->counted) return GD_ERR_INVALID;
+  if (cudaMemcpy(out, ctx->counters.ptr, sizeof(uint64_t) * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return GD_ERR_CUDA;
+  return GD_OK;
+}
+
+extern "C" int gd_fp64_peak(gd_ctx* ctx, double* tflops) {
+  if (ctx == nullptr || tflops == nullptr) return GD_ERR_INVALID;
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  int sms = 0;
+  GD_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  DevBuf sink;
+  GD_CUDA(ctx, sink.ensure(64));
+  const int blocks = sms * 8, threads = 256, iters = 1 << 14;
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    GD_CUDA(ctx, cudaEventRecord(ctx->ev[0], ctx->stream));
+    GD_CUDA(ctx, static_cast<cudaError_t>(
+                     launch_fp64_probe(sink.as<double>(), blocks, threads, iters, ctx->stream)));
+    GD_CUDA(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
+    GD_CUDA(ctx, cudaEventSynchronize(ctx->ev[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  const double ops = 2.0 * 8.0 * static_cast<double>(blocks) * threads * iters;
+  *tflops = ops / (best * 1e-3) / 1e12;
+  return GD_OK;
+}
+
+extern "C" int gd_last_timing(const gd_ctx* ctx, gd_timing* out) {
+  if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
+  *out = ctx->timing;
+  return GD_OK;
+}
+
+extern "C" int gd_overlap_score_batch(gd_ctx* ctx, const double* xyz, int32_t n_atoms,
+                                      int32_t n_poses, uint32_t flags, double* out) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  if (ctx->P == 0) return ctx->fail(GD_ERR_NO_POCKET, "overlap_score: no pocket staged");
+  if (n_atoms < 1) return ctx->fail(GD_ERR_INVALID, "overlap_score: empty pose");
+  if (n_poses < 0 || (n_poses > 0 && (xyz == nullptr || out == nullptr)))
+    return ctx->fail(GD_ERR_INVALID, "overlap_score: invalid arguments");
+  if (n_poses == 0) return GD_OK;
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  DevBuf dx, dout;
+  const size_t bytes = sizeof(double) * 3 * static_cast<size_t>(n_atoms) * n_poses;
+  GD_CUDA(ctx, dx.ensure(bytes));
+  GD_CUDA(ctx, dout.ensure(sizeof(double) * n_poses));
+  GD_CUDA(ctx, cudaMemcpyAsync(dx.ptr, xyz, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  PocketView v = ctx->view;
+  v.use_index = (flags & GD_FLAG_BRUTE_FORCE) ? 0 : 1;
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_score_poses(v, dx.as<double>(), n_atoms, n_poses,
+                                                           dout.as<double>(), ctx->stream)));
+  GD_CUDA(ctx, cudaMemcpyAsync(out, dout.ptr, sizeof(double) * n_poses, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}

@@ -1,0 +1,108 @@
+// Device data layout and kernel launchers shared by capi.cpp (host, g++)
+// and kernels.cu (device, nvcc -fmad=false).  No CUDA headers needed here.
+#pragma once
+
+#include <cstdint>
+
+namespace gdb200 {
+
+// One record per ligand; offsets index the flat SoA arrays below.
+struct LigMeta {
+  int32_t atom_off;   // into xyz (x3) and radii
+  int32_t n;          // atoms
+  int32_t frag_off;   // into frag_* arrays
+  int32_t nfrag;      // 2 x rotamers, reference order (kernel.hpp:221-227)
+  int32_t far_off;    // into far_mask (words)
+  int32_t fmask_off;  // into frag_mask (words)
+  int32_t words;      // ceil(n/64)
+  int32_t status;     // GD_LIG_*
+};
+
+// Exact nearest-pocket-point structure staged in HBM.
+struct PocketView {
+  const double* pts;       // [P*4] x,y,z,pad (32-B records)
+  int32_t P;
+  int32_t use_index;       // 0 = brute force only
+  const int32_t* vox_off;  // [nvox+1] candidate-list offsets
+  const double* vox_pts;   // [ncand*4] candidate coordinates, voxel-major
+  double lo_x, lo_y, lo_z; // grid origin
+  double inv_h;            // 1 / voxel edge
+  int32_t dim_x, dim_y, dim_z;
+};
+
+struct DockParams {
+  int32_t n_lig;
+  const int32_t* order;  // CTA b docks ligand order[b] (cost-descending)
+  const LigMeta* meta;
+  const double* xyz;       // [3*atoms] initial pose
+  const double* radii;     // [atoms]
+  const uint64_t* far_mask;
+  const uint64_t* frag_mask;
+  const int32_t* frag_axis;
+  const int32_t* frag_anchor;
+  const double* frag_rel;
+
+  PocketView pocket;
+  double cx, cy, cz;       // rigid-sweep centre (E1)
+
+  // Rigid Euler grid (E2): distinct orientations, ascending linear index.
+  int32_t n_orient;
+  const int32_t* orient_idx;
+  const double* orient_R;  // [n_orient*9] row-major
+  const double* cos_deg;   // [360] std::cos(a * (pi/180)) from the host libm
+  const double* sin_deg;   // [360]
+
+  // Knobs (kernel.hpp:21-26) + batch knobs.
+  int32_t hp, lp, reps, refine, tile;
+  double threshold;
+  int32_t top_k;           // slots per ligand in the outputs
+  int32_t rigid;           // 1 = rigid sweep + top-K seeds, 0 = dock given pose
+  int32_t chains_per_cta;  // G: chains resident in shared memory at once
+  int32_t max_n;           // largest ligand in the batch (smem sizing)
+  int32_t amax;            // largest candidate count of one sub-step
+
+  // Rigid -> flex hand-off (rank order).
+  int32_t* seed_slot;      // [L*K] position in the orientation list
+  double* seed_score;      // [L*K]
+  int32_t* k_eff;          // [L]
+
+  // Outputs, final order (E7).
+  int32_t* out_orient;
+  int32_t* out_rank;
+  double* out_rigid;
+  double* out_final;
+  int64_t* out_evals;
+  int64_t* out_checks;
+  double* out_pose;        // nullable; [K*atoms*3]
+  double* stage_pose;      // nullable; rank-order staging, same shape
+  int64_t* poses_scored;   // [L]
+  int32_t* status;         // [L]
+  // Optional exact work counters: [0..6] rigid kernel, [8..14] flex kernel,
+  // each {pairs, rotated atoms, bump pairs, queries, sum terms, candidate
+  // evaluations, rigid-transformed atoms}.
+  unsigned long long* counters;
+};
+
+// FP64 pipe probe: independent DADD/DMUL chains, returns fp64 ops executed.
+int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* stream);
+
+// Bytes of dynamic shared memory the kernels need for these params.
+size_t rigid_smem_bytes(const DockParams& p, int sort_slots);
+size_t flex_smem_bytes(const DockParams& p);
+
+// Launchers; return cudaError_t as int.  `stream` is a cudaStream_t.
+int launch_rigid_topk(const DockParams& p, int sort_slots, void* stream);
+int launch_flex(const DockParams& p, void* stream);
+int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int n_poses,
+                       double* out, void* stream);
+
+// Voxel index build (two passes: count, then fill after a host scan).
+struct VoxelGrid {
+  double lo_x, lo_y, lo_z, h;
+  int32_t dim_x, dim_y, dim_z;
+};
+int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, void* stream);
+int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets,
+                      double* vox_pts, void* stream);
+
+}  // namespace gdb200

@@ -1,0 +1,401 @@
+"""ctypes binding of the C-ABI in include/geodock_b200.h.
+
+This is plumbing for the tests and the benchmark; the product is the
+native library.  Loading fails loudly if ``libgeodock_b200.so`` is missing:
+there is no Python or CPU fallback for any hot-path call.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libgeodock_b200.so"
+
+GD_OK = 0
+GD_ERR_INVALID = 1
+GD_ERR_CUDA = 2
+GD_ERR_DEGENERATE = 3
+GD_ERR_NO_POCKET = 4
+GD_LIG_OK = 0
+GD_LIG_INVALID = 1
+GD_LIG_DEGENERATE = 3
+GD_FLAG_BRUTE_FORCE = 1
+GD_FLAG_KEEP_POSES = 2
+GD_FLAG_COUNT_WORK = 4
+WORK_FIELDS = ["pairs", "rotated", "bump_pairs", "queries", "sum_terms", "evaluations", "xform"]
+
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+_u8p = C.POINTER(C.c_uint8)
+
+
+class gd_ligand_batch(C.Structure):
+    _fields_ = [("n_ligands", C.c_int32), ("atom_offsets", _i32p), ("xyz", _f64p),
+                ("radii", _f64p), ("bond_offsets", _i32p), ("bonds", _i32p),
+                ("bond_rotatable", _u8p)]
+
+
+class gd_knobs(C.Structure):
+    _fields_ = [("high_precision_step", C.c_int32), ("low_precision_step", C.c_int32),
+                ("threshold", C.c_double), ("repetitions", C.c_int32),
+                ("enable_refinement", C.c_int32), ("rigid_step", C.c_int32),
+                ("top_k", C.c_int32), ("flags", C.c_uint32)]
+
+
+class gd_result(C.Structure):
+    _fields_ = [("orientation", _i32p), ("seed_rank", _i32p), ("rigid_score", _f64p),
+                ("final_score", _f64p), ("evaluations", _i64p),
+                ("feasibility_checks", _i64p), ("final_pose", _f64p), ("k_eff", _i32p),
+                ("poses_scored", _i64p), ("status", _i32p)]
+
+
+class gd_timing(C.Structure):
+    _fields_ = [("upload_ms", C.c_float), ("rigid_ms", C.c_float), ("flex_ms", C.c_float),
+                ("download_ms", C.c_float), ("total_ms", C.c_float),
+                ("rigid_atom_queries", C.c_int64), ("flex_atom_queries", C.c_int64),
+                ("launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+
+
+# Every symbol include/geodock_b200.h declares, with its ctypes signature.
+SIGNATURES = {
+    "gd_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),
+    "gd_destroy": (C.c_int, [C.c_void_p]),
+    "gd_last_error": (C.c_char_p, [C.c_void_p]),
+    "gd_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "gd_version": (C.c_char_p, []),
+    "gd_set_pocket": (C.c_int, [C.c_void_p, _f64p, C.c_int32]),
+    "gd_pocket_info": (C.c_int, [C.c_void_p, _f64p, _i32p, _f64p, _i64p, _i32p]),
+    "gd_dock_batch": (C.c_int, [C.c_void_p, C.POINTER(gd_ligand_batch), C.POINTER(gd_knobs),
+                                C.POINTER(gd_result)]),
+    "gd_upload": (C.c_int, [C.c_void_p, C.POINTER(gd_ligand_batch)]),
+    "gd_dock_resident": (C.c_int, [C.c_void_p, C.POINTER(gd_knobs)]),
+    "gd_download": (C.c_int, [C.c_void_p, C.POINTER(gd_result)]),
+    "gd_last_timing": (C.c_int, [C.c_void_p, C.POINTER(gd_timing)]),
+    "gd_work_counters": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "gd_fp64_peak": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
+    "gd_overlap_score_batch": (C.c_int, [C.c_void_p, _f64p, C.c_int32, C.c_int32, C.c_uint32,
+                                         _f64p]),
+    "gd_optimal_tile_size": (C.c_int32, [C.c_int32]),
+    "gd_validate_knobs": (C.c_int, [C.POINTER(gd_knobs), C.c_char_p, C.c_size_t]),
+    "gd_orientations": (C.c_int32, [C.c_int32, _i32p, _f64p, C.c_int32]),
+    "gd_synth_pocket": (C.c_int32, [C.c_double, C.c_double, C.c_double, C.c_double,
+                                    C.c_double, C.c_uint64, _f64p, C.c_int32]),
+    "gd_synth_ligand_size": (C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                       _i32p]),
+    "gd_synth_ligand": (C.c_int, [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_int32, _f64p, _f64p, _f64p, _i32p, _u8p]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """The loaded native library (raises if it was never built)."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1901_06363_b200.build` "
+                "(there is no CPU fallback)")
+        h = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(h, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = h
+    return _lib
+
+
+def _p(a: np.ndarray, t):
+    return a.ctypes.data_as(t) if a is not None else None
+
+
+class GeoDockError(RuntimeError):
+    """geodock::Error raised through the C-ABI (reference error.hpp:14-17)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+# ---------------------------------------------------------------------------
+# Inputs
+# ---------------------------------------------------------------------------
+@dataclass
+class LigandBatch:
+    """SoA ligand batch (gd_ligand_batch)."""
+    atom_offsets: np.ndarray   # int32 [L+1]
+    xyz: np.ndarray            # float64 [A, 3]
+    radii: np.ndarray          # float64 [A]
+    bond_offsets: np.ndarray   # int32 [L+1]
+    bonds: np.ndarray          # int32 [B, 2]
+    rotatable: np.ndarray      # uint8 [B]
+
+    def __post_init__(self):
+        self.atom_offsets = np.ascontiguousarray(self.atom_offsets, dtype=np.int32)
+        self.xyz = np.ascontiguousarray(self.xyz, dtype=np.float64).reshape(-1, 3)
+        self.radii = np.ascontiguousarray(self.radii, dtype=np.float64)
+        self.bond_offsets = np.ascontiguousarray(self.bond_offsets, dtype=np.int32)
+        self.bonds = np.ascontiguousarray(self.bonds, dtype=np.int32).reshape(-1, 2)
+        self.rotatable = np.ascontiguousarray(self.rotatable, dtype=np.uint8)
+
+    @property
+    def n_ligands(self) -> int:
+        return len(self.atom_offsets) - 1
+
+    @property
+    def sizes(self) -> np.ndarray:
+        return np.diff(self.atom_offsets)
+
+    def c_struct(self) -> gd_ligand_batch:
+        return gd_ligand_batch(self.n_ligands, _p(self.atom_offsets, _i32p), _p(self.xyz, _f64p),
+                               _p(self.radii, _f64p), _p(self.bond_offsets, _i32p),
+                               _p(self.bonds, _i32p), _p(self.rotatable, _u8p))
+
+    def ligand(self, l: int):
+        a0, a1 = self.atom_offsets[l], self.atom_offsets[l + 1]
+        b0, b1 = self.bond_offsets[l], self.bond_offsets[l + 1]
+        return self.xyz[a0:a1], self.radii[a0:a1], self.bonds[b0:b1], self.rotatable[b0:b1]
+
+    def subset(self, idx) -> "LigandBatch":
+        parts = [self.ligand(int(l)) for l in idx]
+        return LigandBatch.from_parts(parts)
+
+    @staticmethod
+    def from_parts(parts) -> "LigandBatch":
+        ao = np.zeros(len(parts) + 1, np.int32)
+        bo = np.zeros(len(parts) + 1, np.int32)
+        for i, (x, _, b, _) in enumerate(parts):
+            ao[i + 1] = ao[i] + len(x)
+            bo[i + 1] = bo[i] + len(b)
+        cat = lambda k, shape, dt: (np.concatenate([p[k] for p in parts]) if parts
+                                    else np.zeros(shape, dt))
+        return LigandBatch(ao, cat(0, (0, 3), np.float64), cat(1, (0,), np.float64), bo,
+                           cat(2, (0, 2), np.int32), cat(3, (0,), np.uint8))
+
+
+@dataclass
+class Knobs:
+    """KnobConfig (kernel.hpp:21-26) + the batch knobs."""
+    high_precision_step: int = 1
+    low_precision_step: int = 45
+    threshold: float = 0.0
+    repetitions: int = 3
+    enable_refinement: bool = False
+    rigid_step: int = 0
+    top_k: int = 1
+    flags: int = 0
+
+    @staticmethod
+    def baseline(rigid_step: int, frag_step: int, restarts: int, top_k: int) -> "Knobs":
+        """BASELINE.json knob mapping: lp = max(45, step), threshold 0, no refinement."""
+        return Knobs(frag_step, max(45, frag_step), 0.0, restarts, False, rigid_step, top_k)
+
+    def c_struct(self) -> gd_knobs:
+        return gd_knobs(self.high_precision_step, self.low_precision_step, self.threshold,
+                        self.repetitions, int(bool(self.enable_refinement)), self.rigid_step,
+                        self.top_k, self.flags)
+
+    def validate(self) -> None:
+        buf = C.create_string_buffer(256)
+        k = self.c_struct()
+        if lib().gd_validate_knobs(C.byref(k), buf, 256) != GD_OK:
+            raise GeoDockError(GD_ERR_INVALID, buf.value.decode())
+
+    @property
+    def slots(self) -> int:
+        return self.top_k if self.rigid_step > 0 else 1
+
+
+@dataclass
+class DockResult:
+    """gd_result as [L, K] numpy arrays (final order: score desc, seed rank asc)."""
+    orientation: np.ndarray
+    seed_rank: np.ndarray
+    rigid_score: np.ndarray
+    final_score: np.ndarray
+    evaluations: np.ndarray
+    feasibility_checks: np.ndarray
+    k_eff: np.ndarray
+    poses_scored: np.ndarray
+    status: np.ndarray
+    final_pose: np.ndarray | None = None  # flat [K*A*3] (see header for layout)
+
+    @staticmethod
+    def empty(L: int, K: int, total_atoms: int, poses: bool) -> "DockResult":
+        return DockResult(np.zeros((L, K), np.int32), np.zeros((L, K), np.int32),
+                          np.zeros((L, K)), np.zeros((L, K)), np.zeros((L, K), np.int64),
+                          np.zeros((L, K), np.int64), np.zeros(L, np.int32),
+                          np.zeros(L, np.int64), np.zeros(L, np.int32),
+                          np.zeros(K * total_atoms * 3) if poses else None)
+
+    def c_struct(self) -> gd_result:
+        return gd_result(_p(self.orientation, _i32p), _p(self.seed_rank, _i32p),
+                         _p(self.rigid_score, _f64p), _p(self.final_score, _f64p),
+                         _p(self.evaluations, _i64p), _p(self.feasibility_checks, _i64p),
+                         _p(self.final_pose, _f64p), _p(self.k_eff, _i32p),
+                         _p(self.poses_scored, _i64p), _p(self.status, _i32p))
+
+    def pose(self, batch: LigandBatch, l: int, e: int) -> np.ndarray:
+        K = self.orientation.shape[1]
+        a0 = int(batch.atom_offsets[l])
+        n = int(batch.atom_offsets[l + 1]) - a0
+        off = 3 * (K * a0 + e * n)
+        return self.final_pose[off:off + 3 * n].reshape(n, 3)
+
+
+# ---------------------------------------------------------------------------
+# Device context
+# ---------------------------------------------------------------------------
+class Docker:
+    """One gd_ctx: a pocket staged on one GPU plus the resident batch."""
+
+    def __init__(self, device: int = 0):
+        self._lib = lib()
+        h = C.c_void_p()
+        rc = self._lib.gd_create(device, C.byref(h))
+        if rc != GD_OK:
+            raise GeoDockError(rc, self._lib.gd_last_error(None).decode())
+        self._h = h
+        self._batch = None
+        self._K = 1
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.gd_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _check(self, rc: int):
+        if rc != GD_OK:
+            raise GeoDockError(rc, self._lib.gd_last_error(self._h).decode())
+
+    def set_stream(self, stream_ptr: int | None):
+        self._check(self._lib.gd_set_stream(self._h, C.c_void_p(stream_ptr or 0)))
+
+    def set_pocket(self, xyz: np.ndarray):
+        pts = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+        self._check(self._lib.gd_set_pocket(self._h, _p(pts, _f64p), len(pts)))
+
+    def pocket_info(self) -> dict:
+        c = np.zeros(3)
+        d = np.zeros(3, np.int32)
+        h = C.c_double()
+        n = C.c_int64()
+        m = C.c_int32()
+        self._check(self._lib.gd_pocket_info(self._h, _p(c, _f64p), _p(d, _i32p), C.byref(h),
+                                             C.byref(n), C.byref(m)))
+        return {"centre": c, "dims": d, "voxel": h.value, "n_candidates": n.value,
+                "max_candidates": m.value}
+
+    def dock(self, batch: LigandBatch, knobs: Knobs, keep_poses: bool = False) -> DockResult:
+        """gd_dock_batch: host buffers in, host buffers out."""
+        K = knobs.slots
+        res = DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), keep_poses)
+        b, k, r = batch.c_struct(), knobs.c_struct(), res.c_struct()
+        self._check(self._lib.gd_dock_batch(self._h, C.byref(b), C.byref(k), C.byref(r)))
+        return res
+
+    def upload(self, batch: LigandBatch):
+        b = batch.c_struct()
+        self._check(self._lib.gd_upload(self._h, C.byref(b)))
+        self._batch = batch
+
+    def dock_resident(self, knobs: Knobs, keep_poses: bool = False):
+        k = knobs.c_struct()
+        if keep_poses:
+            k.flags |= GD_FLAG_KEEP_POSES
+        self._check(self._lib.gd_dock_resident(self._h, C.byref(k)))
+        self._K = knobs.slots
+
+    def download(self, result: DockResult):
+        r = result.c_struct()
+        self._check(self._lib.gd_download(self._h, C.byref(r)))
+        return result
+
+    def work_counters(self) -> dict:
+        """Executed work of the last call made with GD_FLAG_COUNT_WORK."""
+        out = (C.c_uint64 * 16)()
+        self._check(self._lib.gd_work_counters(self._h, out))
+        return {"rigid": dict(zip(WORK_FIELDS, out[0:7])), "flex": dict(zip(WORK_FIELDS, out[8:15]))}
+
+    def fp64_peak_tflops(self) -> float:
+        t = C.c_double()
+        self._check(self._lib.gd_fp64_peak(self._h, C.byref(t)))
+        return t.value
+
+    def timing(self) -> dict:
+        t = gd_timing()
+        self._check(self._lib.gd_last_timing(self._h, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in gd_timing._fields_}
+
+    def overlap_scores(self, poses: np.ndarray, brute: bool = False) -> np.ndarray:
+        """overlap_score (geometry.hpp:140) of poses shaped [n_poses, n_atoms, 3]."""
+        p = np.ascontiguousarray(poses, dtype=np.float64)
+        if p.ndim == 2:
+            p = p[None]
+        out = np.zeros(p.shape[0])
+        self._check(self._lib.gd_overlap_score_batch(
+            self._h, _p(p, _f64p), p.shape[1], p.shape[0],
+            GD_FLAG_BRUTE_FORCE if brute else 0, _p(out, _f64p)))
+        return out
+
+
+# ---------------------------------------------------------------------------
+# Host helpers
+# ---------------------------------------------------------------------------
+def optimal_tile_size(step: int) -> int:
+    return int(lib().gd_optimal_tile_size(step))
+
+
+def orientations(step: int):
+    n = lib().gd_orientations(step, None, None, 0)
+    if n < 0:
+        raise GeoDockError(GD_ERR_INVALID, "rigid step must divide 360")
+    idx = np.zeros(n, np.int32)
+    R = np.zeros((n, 9))
+    lib().gd_orientations(step, _p(idx, _i32p), _p(R, _f64p), n)
+    return idx, R.reshape(n, 3, 3)
+
+
+def synth_pocket(a: float, b: float, c: float, spacing: float, rough_max: float = 0.0,
+                 seed: int = 0) -> np.ndarray:
+    n = lib().gd_synth_pocket(a, b, c, spacing, rough_max, seed, None, 0)
+    out = np.zeros((n, 3))
+    lib().gd_synth_pocket(a, b, c, spacing, rough_max, seed, _p(out, _f64p), n)
+    return out
+
+
+def synth_ligands(base_seed: int, ids, n_lo: int = 20, n_hi: int = 60, fixed_n: int = 0,
+                  r_cap: int = 12, fixed_r: int = -1, centre=(0.0, 0.0, 0.0)) -> LigandBatch:
+    """BASELINE random-walk-tree ligands `ids` of the family `base_seed`."""
+    L = lib()
+    ids = list(ids)
+    sizes = np.zeros(len(ids), np.int32)
+    tmp = C.c_int32()
+    for i, lid in enumerate(ids):
+        if L.gd_synth_ligand_size(base_seed, lid, n_lo, n_hi, fixed_n, C.byref(tmp)) != GD_OK:
+            raise GeoDockError(GD_ERR_INVALID, "bad ligand size range")
+        sizes[i] = tmp.value
+    ao = np.zeros(len(ids) + 1, np.int32)
+    ao[1:] = np.cumsum(sizes)
+    bo = np.zeros(len(ids) + 1, np.int32)
+    bo[1:] = np.cumsum(sizes - 1)
+    xyz = np.zeros((ao[-1], 3))
+    radii = np.zeros(ao[-1])
+    bonds = np.zeros((bo[-1], 2), np.int32)
+    rot = np.zeros(bo[-1], np.uint8)
+    cen = np.ascontiguousarray(centre, dtype=np.float64)
+    for i, lid in enumerate(ids):
+        a0, b0 = ao[i], bo[i]
+        rc = L.gd_synth_ligand(base_seed, lid, n_lo, n_hi, fixed_n, r_cap, fixed_r, _p(cen, _f64p),
+                               _p(xyz[a0:], _f64p), _p(radii[a0:], _f64p), _p(bonds[b0:], _i32p),
+                               _p(rot[b0:], _u8p))
+        if rc < 0:
+            raise GeoDockError(GD_ERR_INVALID, "ligand synthesis failed")
+    return LigandBatch(ao, xyz, radii, bo, bonds, rot)

@@ -1,0 +1,124 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle.
+
+Bar: bit-exact.  Every score is fp64 computed with the reference's
+expression trees, so top-K orientation indices, ordering, scores, counters
+and final coordinates must be identical -- stricter than BASELINE's 1e-4
+relative tolerance on scores/coordinates, which we therefore also meet.
+"""
+import numpy as np
+import pytest
+
+from paper_1901_06363_b200 import Knobs, workloads as W
+from tests.helpers import assert_same_result
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-4  # BASELINE.json north_star tolerance (we require bit-exact)
+
+
+def _oracle():
+    from oracle import oracle_py
+    return oracle_py
+
+
+def _cpu(batch, pocket, knobs):
+    """The reference itself (oracle/_ref, PocketIndex) when built, else the C oracle."""
+    O = _oracle()
+    if O.have_ref():
+        return O.dock_batch(batch, pocket, knobs, nthreads=O.threads(), impl="ref")
+    return O.dock_batch(batch, pocket, knobs, nthreads=O.threads())
+
+
+def test_config0_full_parity(docker):
+    w = W.config(0)
+    pocket = w.pocket()
+    batch = w.ligands()
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, w.knobs, keep_poses=True)
+    want = _oracle().dock_batch(batch, pocket, w.knobs, nthreads=1)
+    assert got.k_eff[0] == 30
+    assert_same_result(got, want)
+    np.testing.assert_allclose(got.final_score, want.final_score, rtol=REL_TOL)
+
+
+def test_config0_brute_force_equals_index(docker):
+    w = W.config(0)
+    docker.set_pocket(w.pocket())
+    batch = w.ligands()
+    a = docker.dock(batch, w.knobs, keep_poses=True)
+    k = Knobs(**{**w.knobs.__dict__, "flags": 1})
+    b = docker.dock(batch, k, keep_poses=True)
+    assert_same_result(a, b)
+
+
+@pytest.mark.parametrize("n_lig", [48])
+def test_config1_subset_parity(docker, n_lig):
+    w = W.config(1)
+    pocket = w.pocket()
+    batch = w.ligands(range(n_lig))
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, w.knobs, keep_poses=True)
+    want = _cpu(batch, pocket, w.knobs)
+    assert_same_result(got, want)
+
+
+def test_config2_knobs_parity(docker):
+    """c2 knobs (rigid 10, frag 10, 3 restarts, K=100) on two c1-distribution ligands."""
+    w = W.config(2)
+    pocket = w.pocket()
+    batch = w.ligands([3, 11])
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, w.knobs, keep_poses=True)
+    want = _cpu(batch, pocket, w.knobs)
+    assert (got.k_eff == 100).all()
+    assert_same_result(got, want)
+
+
+@pytest.mark.parametrize("knobs", [
+    Knobs(1, 45, 0.0, 1, False),    # Algorithm-1 baseline (test_kernel.cpp:241-250)
+    Knobs(2, 90, 0.3, 2, True),     # determinism test config (test_kernel.cpp:205-220)
+    Knobs(5, 90, 0.3, 1, False),    # screening invariance config (test_screening.cpp:45)
+    Knobs(3, 45, 0.2, 1, True),     # spatial-index config (test_kernel.cpp:252-263)
+    Knobs(10, 90, 0.5, 1, False),   # bookkeeping config (test_screening.cpp:62)
+    Knobs(1, 90, 1.0, 1, False),    # threshold 1: every fragment at the low step
+    Knobs(360, 360, 0.0, 3, False), # step 360: only the current pose
+])
+def test_given_pose_match_probes_shape(docker, knobs):
+    """rigid_step 0 = the reference's screen path: match_probes_shape on the input pose."""
+    O = _oracle()
+    pocket, batch = None, None
+    if O.have_ref():
+        pocket, batch = O.ref_generate_synthetic(24, 4242)
+    else:
+        w = W.config(1)
+        pocket = w.pocket()
+        batch = w.ligands(range(24))
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, knobs, keep_poses=True)
+    want = O.dock_batch(batch, pocket, knobs, nthreads=O.threads())
+    assert_same_result(got, want)
+
+
+def test_overlap_score_kats(docker):
+    """test_geometry.cpp:45-56 hand values through the GPU scoring kernel."""
+    docker.set_pocket(np.array([[0.0, 0.0, 1.0]]))
+    assert docker.overlap_scores(np.array([[0.0, 0.0, 0.0]]))[0] == 1.0
+    docker.set_pocket(np.array([[0.0, 0.0, 0.0]]))
+    assert docker.overlap_scores(np.array([[0.0, 0.0, 0.0], [0.0, 0.0, 3.0]]))[0] == 2.0 / (1e-12 + 9.0)
+    docker.set_pocket(np.array([[0.0, 0.0, 1.0], [0.0, 0.0, 4.0]]))
+    assert docker.overlap_scores(np.array([[0.0, 0.0, 2.0]]))[0] == 1.0
+
+
+def test_overlap_scores_random_poses_exact(docker):
+    """Index vs brute vs oracle on random poses, including far-away atoms."""
+    O = _oracle()
+    pocket = W.config(1).pocket()
+    docker.set_pocket(pocket)
+    rng = np.random.default_rng(7)
+    poses = rng.uniform(-16, 16, size=(64, 40, 3))
+    poses[0, 0] = [500.0, -300.0, 200.0]  # outside the grid: brute fallback
+    idx = docker.overlap_scores(poses)
+    brute = docker.overlap_scores(poses, brute=True)
+    want = np.array([O.overlap_score(p, pocket) for p in poses])
+    assert np.array_equal(idx, want)
+    assert np.array_equal(brute, want)
