@@ -266,6 +266,7 @@ typedef struct {
   double* scratch;
   long long evals, checks;
   int err;
+  int last_angle; /* committed angle of the last flat/refined search */
 } osearch;
 
 /* CandidateEvaluator::evaluate; returns 0 if infeasible (score untouched). */
@@ -307,6 +308,7 @@ static double flat(osearch* S, double* pose, int f, int step) {
       have = 1;
     }
   }
+  S->last_angle = best_a;
   commit(S, pose, f, best_a);
   return best;
 }
@@ -351,6 +353,7 @@ static double refined(osearch* S, double* pose, int f, int hp, double entry_scor
     best = entry_score;
     best_a = 0;
   }
+  S->last_angle = best_a;
   commit(S, pose, f, best_a);
   return best;
 }
@@ -359,7 +362,7 @@ static double refined(osearch* S, double* pose, int f, int hp, double entry_scor
  * GD_LIG_* error. */
 static int mps(const olig* L, const double* pocket, int P, const gd_knobs* k, double* pose,
                double* score, long long* evals, long long* checks) {
-  osearch S = {L, pocket, P, (double*)malloc(sizeof(double) * 3 * L->n), 1, 1, 0};
+  osearch S = {L, pocket, P, (double*)malloc(sizeof(double) * 3 * L->n), 1, 1, 0, 0};
   double cur = gdo_overlap_score(pose, L->n, pocket, P);
   for (int rep = 0; rep < k->repetitions && !S.err; ++rep)
     for (int f = 0; f < L->nfrag && !S.err; ++f) {
@@ -628,6 +631,34 @@ int gdo_match_probes_shape(int n, const double* xyz, const double* radii, int nb
   if (rc == 0) {
     memcpy(pose_out, xyz, sizeof(double) * 3 * n);
     rc = mps(&L, pocket, P, k, pose_out, score, evals, checks);
+  }
+  olig_free(&L);
+  free(rad);
+  return rc;
+}
+
+/* optimize_fragment_flat (mode 0) / optimize_fragment_refined (mode 1) on
+ * fragment f of the given pose (kernel.hpp:125-198); entry_score < 0 means
+ * "not known" (the refined search then scores the entry pose itself). */
+int gdo_optimize_fragment(int n, const double* xyz, const double* radii, int nb, const int32_t* bonds,
+                          const uint8_t* rot, const double* pocket, int P, const double* pose, int f,
+                          int mode, int step, double entry_score, double* pose_out, int* best_angle,
+                          double* best_score, long long* evals, long long* checks) {
+  olig L;
+  double* rad = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+  if (n > 0) memcpy(rad, radii, sizeof(double) * n);
+  int rc = olig_build(&L, n, xyz, rad, nb, bonds, rot);
+  if (rc == 0 && (f < 0 || f >= L.nfrag || step < 1 || 360 % step)) rc = GD_LIG_INVALID;
+  if (rc == 0) {
+    osearch S = {&L, pocket, P, (double*)malloc(sizeof(double) * 3 * n), 0, 0, 0, 0};
+    memcpy(pose_out, pose, sizeof(double) * 3 * n);
+    const double entry = entry_score >= 0.0 ? entry_score : gdo_overlap_score(pose, n, pocket, P);
+    *best_score = mode == 0 ? flat(&S, pose_out, f, step) : refined(&S, pose_out, f, step, entry);
+    *best_angle = S.last_angle;
+    *evals = S.evals;
+    *checks = S.checks;
+    rc = S.err;
+    free(S.scratch);
   }
   olig_free(&L);
   free(rad);

@@ -157,6 +157,31 @@ def match_probes_shape(xyz, radii, bonds, rot, pocket, knobs: Knobs, impl: str =
     return sc.value, ev.value, ck.value, out
 
 
+def optimize_fragment(xyz, radii, bonds, rot, pocket, f: int, step: int, refined: bool = False,
+                      pose=None, entry_score: float = -1.0):
+    """optimize_fragment_flat / _refined on fragment f: (best_angle, best_score, evals,
+    checks, committed pose)."""
+    h = oracle()
+    h.gdo_optimize_fragment.argtypes = [C.c_int, _f64p, _f64p, C.c_int, _i32p, _u8p, _f64p,
+                                        C.c_int, _f64p, C.c_int, C.c_int, C.c_int, C.c_double,
+                                        _f64p, C.POINTER(C.c_int), _f64p, _i64p, _i64p]
+    x = np.ascontiguousarray(xyz, dtype=np.float64)
+    r = np.ascontiguousarray(radii, dtype=np.float64)
+    b = np.ascontiguousarray(bonds, dtype=np.int32).reshape(-1, 2)
+    ro = np.ascontiguousarray(rot, dtype=np.uint8)
+    pk = np.ascontiguousarray(pocket, dtype=np.float64)
+    p = x if pose is None else np.ascontiguousarray(pose, dtype=np.float64)
+    out = np.zeros_like(x)
+    ang, sc, ev, ck = C.c_int(), C.c_double(), C.c_longlong(), C.c_longlong()
+    rc = h.gdo_optimize_fragment(len(x), _p(x, _f64p), _p(r, _f64p), len(b), _p(b, _i32p),
+                                 _p(ro, _u8p), _p(pk, _f64p), len(pk), _p(p, _f64p), f,
+                                 int(refined), step, entry_score, _p(out, _f64p), C.byref(ang),
+                                 C.byref(sc), C.byref(ev), C.byref(ck))
+    if rc:
+        raise RuntimeError(f"oracle error {rc}")
+    return ang.value, sc.value, ev.value, ck.value, out
+
+
 def rotate_fragment(xyz, radii, bonds, rot, pose, f: int, angle: float, impl: str = "oracle"):
     """(rotated pose, feasible) for fragment f (rotamer f//2; left if f even)."""
     x = np.ascontiguousarray(xyz, dtype=np.float64)

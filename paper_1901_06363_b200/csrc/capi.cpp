@@ -80,8 +80,8 @@ struct gd_ctx {
   // Pocket.
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, vox_off, vox_pts;
-  VoxelGrid grid{};
+  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels];
+  VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
   PocketView view{};
@@ -285,66 +285,76 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   GD_CUDA(ctx, cudaMemcpy(ctx->pts.ptr, padded.data(), padded.size() * sizeof(double),
                           cudaMemcpyHostToDevice));
 
-  // Grid: pocket bounding box plus a margin; voxel edge h (0.5 A default).
-  double h = env_double("GD_VOXEL_H", 0.5);
-  const double margin = env_double("GD_VOXEL_MARGIN", 8.0);
-  VoxelGrid g{};
-  for (;;) {
-    int dims[3];
-    long total = 1;
-    for (int k = 0; k < 3; ++k) {
-      dims[k] = static_cast<int>(std::floor((hi[k] - lo[k] + 2 * margin) / h)) + 1;
-      total *= dims[k];
-    }
-    if (total <= (1l << 23)) {
-      g = VoxelGrid{lo[0] - margin, lo[1] - margin, lo[2] - margin, h, dims[0], dims[1], dims[2]};
-      break;
-    }
-    h *= 1.25;
-  }
-  const int nv = g.dim_x * g.dim_y * g.dim_z;
-  DevBuf counts;
-  GD_CUDA(ctx, counts.ensure(sizeof(int32_t) * nv));
-  GD_CUDA(ctx, static_cast<cudaError_t>(
-                   launch_voxel_count(ctx->pts.as<double>(), n, g, counts.as<int32_t>(), ctx->stream)));
-  std::vector<int32_t> cnt(nv);
-  GD_CUDA(ctx, cudaMemcpyAsync(cnt.data(), counts.ptr, sizeof(int32_t) * nv, cudaMemcpyDeviceToHost,
-                               ctx->stream));
-  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  std::vector<int32_t> off(nv + 1, 0);
-  int64_t total = 0;
-  int32_t mx = 0;
-  for (int v = 0; v < nv; ++v) {
-    off[v] = static_cast<int32_t>(total);
-    total += cnt[v];
-    mx = std::max(mx, cnt[v]);
-    if (total > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
-  }
-  off[nv] = static_cast<int32_t>(total);
-  GD_CUDA(ctx, ctx->vox_off.ensure(sizeof(int32_t) * (nv + 1)));
-  GD_CUDA(ctx, ctx->vox_pts.ensure(sizeof(double) * 4 * std::max<int64_t>(total, 1)));
-  GD_CUDA(ctx, cudaMemcpyAsync(ctx->vox_off.ptr, off.data(), sizeof(int32_t) * (nv + 1),
-                               cudaMemcpyHostToDevice, ctx->stream));
-  GD_CUDA(ctx, static_cast<cudaError_t>(launch_voxel_fill(ctx->pts.as<double>(), n, g,
-                                                          ctx->vox_off.as<int32_t>(),
-                                                          ctx->vox_pts.as<double>(), ctx->stream)));
-  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  ctx->grid = g;
-  ctx->n_cand = total;
-  ctx->max_cand = mx;
+  // Two grid levels over the pocket bounding box: a fine near field (voxel
+  // 0.5 A, margin 4 A) and a coarse far field (2 A, margin 32 A); queries
+  // beyond both fall back to the exact full scan.
   PocketView& v = ctx->view;
   v.pts = ctx->pts.as<double>();
   v.P = n;
   v.use_index = 1;
-  v.vox_off = ctx->vox_off.as<int32_t>();
-  v.vox_pts = ctx->vox_pts.as<double>();
-  v.lo_x = g.lo_x;
-  v.lo_y = g.lo_y;
-  v.lo_z = g.lo_z;
-  v.inv_h = 1.0 / g.h;
-  v.dim_x = g.dim_x;
-  v.dim_y = g.dim_y;
-  v.dim_z = g.dim_z;
+  ctx->n_cand = 0;
+  ctx->max_cand = 0;
+  const double hs[kGridLevels] = {env_double("GD_VOXEL_H", 0.5), env_double("GD_VOXEL_H2", 2.0)};
+  const double ms[kGridLevels] = {env_double("GD_VOXEL_MARGIN", 4.0),
+                                  env_double("GD_VOXEL_MARGIN2", 32.0)};
+  for (int L = 0; L < kGridLevels; ++L) {
+    double h = hs[L];
+    const double margin = ms[L];
+    VoxelGrid g{};
+    for (;;) {
+      int dims[3];
+      long total = 1;
+      for (int k = 0; k < 3; ++k) {
+        dims[k] = static_cast<int>(std::floor((hi[k] - lo[k] + 2 * margin) / h)) + 1;
+        total *= dims[k];
+      }
+      if (total <= (1l << 22)) {
+        g = VoxelGrid{lo[0] - margin, lo[1] - margin, lo[2] - margin, h, dims[0], dims[1], dims[2]};
+        break;
+      }
+      h *= 1.25;
+    }
+    const int nv = g.dim_x * g.dim_y * g.dim_z;
+    DevBuf counts;
+    GD_CUDA(ctx, counts.ensure(sizeof(int32_t) * nv));
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_voxel_count(ctx->pts.as<double>(), n, g,
+                                                             counts.as<int32_t>(), ctx->stream)));
+    std::vector<int32_t> cnt(nv);
+    GD_CUDA(ctx, cudaMemcpyAsync(cnt.data(), counts.ptr, sizeof(int32_t) * nv,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    std::vector<int32_t> off(nv + 1, 0);
+    int64_t total = 0;
+    int32_t mx = 0;
+    for (int c = 0; c < nv; ++c) {
+      off[c] = static_cast<int32_t>(total);
+      total += cnt[c];
+      mx = std::max(mx, cnt[c]);
+      if (total > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
+    }
+    off[nv] = static_cast<int32_t>(total);
+    GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(int32_t) * (nv + 1)));
+    GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(total, 1)));
+    GD_CUDA(ctx, cudaMemcpyAsync(ctx->vox_off[L].ptr, off.data(), sizeof(int32_t) * (nv + 1),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    GD_CUDA(ctx, static_cast<cudaError_t>(
+                     launch_voxel_fill(ctx->pts.as<double>(), n, g, ctx->vox_off[L].as<int32_t>(),
+                                       ctx->vox_pts[L].as<double>(), ctx->stream)));
+    GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    ctx->grid[L] = g;
+    ctx->n_cand += total;
+    ctx->max_cand = std::max(ctx->max_cand, mx);
+    GridLevel& gl = v.lv[L];
+    gl.off = ctx->vox_off[L].as<int32_t>();
+    gl.pts = ctx->vox_pts[L].as<double>();
+    gl.lo_x = g.lo_x;
+    gl.lo_y = g.lo_y;
+    gl.lo_z = g.lo_z;
+    gl.inv_h = 1.0 / g.h;
+    gl.dim_x = g.dim_x;
+    gl.dim_y = g.dim_y;
+    gl.dim_z = g.dim_z;
+  }
   return GD_OK;
 }
 
@@ -354,11 +364,11 @@ extern "C" int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[
   if (centre)
     for (int k = 0; k < 3; ++k) centre[k] = ctx->centre[k];
   if (dims) {
-    dims[0] = ctx->grid.dim_x;
-    dims[1] = ctx->grid.dim_y;
-    dims[2] = ctx->grid.dim_z;
+    dims[0] = ctx->grid[0].dim_x;
+    dims[1] = ctx->grid[0].dim_y;
+    dims[2] = ctx->grid[0].dim_z;
   }
-  if (voxel) *voxel = ctx->grid.h;
+  if (voxel) *voxel = ctx->grid[0].h;
   if (n_candidates) *n_candidates = ctx->n_cand;
   if (max_candidates) *max_candidates = ctx->max_cand;
   return GD_OK;

@@ -87,20 +87,24 @@ __device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, do
                                               Work& w) {
   ++w.query;
   if (pk.use_index) {
-    const double fx = (x - pk.lo_x) * pk.inv_h;
-    const double fy = (y - pk.lo_y) * pk.inv_h;
-    const double fz = (z - pk.lo_z) * pk.inv_h;
-    if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < pk.dim_x && fy < pk.dim_y && fz < pk.dim_z) {
-      const int v = (static_cast<int>(fx) * pk.dim_y + static_cast<int>(fy)) * pk.dim_z +
-                    static_cast<int>(fz);
-      const int s = __ldg(pk.vox_off + v), e = __ldg(pk.vox_off + v + 1);
-      w.pairs += e - s;
-      double m = __longlong_as_double(0x7ff0000000000000ll);
-      for (int k = s; k < e; ++k) {
-        const P3 p = ldp(pk.vox_pts, k);
-        m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+#pragma unroll
+    for (int L = 0; L < kGridLevels; ++L) {
+      const GridLevel& g = pk.lv[L];
+      const double fx = (x - g.lo_x) * g.inv_h;
+      const double fy = (y - g.lo_y) * g.inv_h;
+      const double fz = (z - g.lo_z) * g.inv_h;
+      if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
+        const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
+                      static_cast<int>(fz);
+        const int s = __ldg(g.off + v), e = __ldg(g.off + v + 1);
+        w.pairs += e - s;
+        double m = __longlong_as_double(0x7ff0000000000000ll);
+        for (int k = s; k < e; ++k) {
+          const P3 p = ldp(g.pts, k);
+          m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+        }
+        return m;
       }
-      return m;
     }
   }
   w.pairs += pk.P;
@@ -678,6 +682,20 @@ constexpr double kVoxEps = 1e-6;
 constexpr double kVoxMargin = 1e-9;
 constexpr int kVoxMaxCand = 1024;
 
+// Does point b beat point a by more than the margin everywhere in box
+// [bl, bh]?  d^2(q,b) - d^2(q,a) is affine in q, so the 8 corners decide.
+__device__ bool dominates(const P3& b, const P3& a, const double* bl, const double* bh) {
+  for (int corner = 0; corner < 8; ++corner) {
+    const double qx = (corner & 1) ? bh[0] : bl[0];
+    const double qy = (corner & 2) ? bh[1] : bl[1];
+    const double qz = (corner & 4) ? bh[2] : bl[2];
+    const double da = (qx - a.x) * (qx - a.x) + (qy - a.y) * (qy - a.y) + (qz - a.z) * (qz - a.z);
+    const double db = (qx - b.x) * (qx - b.x) + (qy - b.y) * (qy - b.y) + (qz - b.z) * (qz - b.z);
+    if (!(db < da - kVoxMargin)) return false;
+  }
+  return true;
+}
+
 __device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, int* cand) {
   const int iz = v % g.dim_z;
   const int iy = (v / g.dim_z) % g.dim_y;
@@ -686,46 +704,46 @@ __device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, i
                         g.lo_z + iz * g.h - kVoxEps};
   const double bh[3] = {bl[0] + g.h + 2 * kVoxEps, bl[1] + g.h + 2 * kVoxEps,
                         bl[2] + g.h + 2 * kVoxEps};
-  double U = 1e300;
+  const double cx = 0.5 * (bl[0] + bh[0]), cy = 0.5 * (bl[1] + bh[1]), cz = 0.5 * (bl[2] + bh[2]);
+  // Pass 1: U (upper bound on the NN distance^2 anywhere in B) and the point
+  // nearest the box centre, a strong dominator for pass 2's pre-filter.
+  double U = 1e300, dc = 1e300;
+  int jc = 0;
   for (int j = 0; j < P; ++j) {
     const P3 q = ldp(pts, j);
     const double fx = fmax(fabs(q.x - bl[0]), fabs(q.x - bh[0]));
     const double fy = fmax(fabs(q.y - bl[1]), fabs(q.y - bh[1]));
     const double fz = fmax(fabs(q.z - bl[2]), fabs(q.z - bh[2]));
     U = fmin(U, fx * fx + fy * fy + fz * fz);
+    const double d = (q.x - cx) * (q.x - cx) + (q.y - cy) * (q.y - cy) + (q.z - cz) * (q.z - cz);
+    if (d < dc) {
+      dc = d;
+      jc = j;
+    }
   }
   const double lim = U * (1.0 + 1e-12) + kVoxMargin;
+  const P3 C = ldp(pts, jc);
+  // Pass 2: points that can be nearest somewhere in B and that jc does not
+  // dominate (a point dominated by anything is dominated by a kept point,
+  // by transitivity, so the final set does not depend on this filter).
   int k = 0;
   for (int j = 0; j < P; ++j) {
     const P3 q = ldp(pts, j);
     const double nx = fmax(0.0, fmax(bl[0] - q.x, q.x - bh[0]));
     const double ny = fmax(0.0, fmax(bl[1] - q.y, q.y - bh[1]));
     const double nz = fmax(0.0, fmax(bl[2] - q.z, q.z - bh[2]));
-    if (nx * nx + ny * ny + nz * nz <= lim) {
+    if (nx * nx + ny * ny + nz * nz <= lim && !dominates(C, q, bl, bh)) {
       if (k >= kVoxMaxCand) return -1;
       cand[k++] = j;
     }
   }
-  // Dominance pruning; transitivity makes the kept set order-independent.
+  // Pass 3: full dominance pruning among the survivors.
   int kept = 0;
   for (int a = 0; a < k; ++a) {
     const P3 A = ldp(pts, cand[a]);
     bool dominated = false;
-    for (int b = 0; b < k && !dominated; ++b) {
-      if (b == a) continue;
-      const P3 Bp = ldp(pts, cand[b]);
-      bool all = true;
-      for (int corner = 0; corner < 8 && all; ++corner) {
-        const double qx = (corner & 1) ? bh[0] : bl[0];
-        const double qy = (corner & 2) ? bh[1] : bl[1];
-        const double qz = (corner & 4) ? bh[2] : bl[2];
-        const double da = (qx - A.x) * (qx - A.x) + (qy - A.y) * (qy - A.y) + (qz - A.z) * (qz - A.z);
-        const double db =
-            (qx - Bp.x) * (qx - Bp.x) + (qy - Bp.y) * (qy - Bp.y) + (qz - Bp.z) * (qz - Bp.z);
-        all = db < da - kVoxMargin;
-      }
-      dominated = all;
-    }
+    for (int b = 0; b < k && !dominated; ++b)
+      if (b != a) dominated = dominates(ldp(pts, cand[b]), A, bl, bh);
     if (!dominated) cand[kept++] = cand[a];
   }
   return kept;

@@ -18,16 +18,24 @@ struct LigMeta {
   int32_t status;     // GD_LIG_*
 };
 
+// One level of the exact voxel candidate-list index.
+struct GridLevel {
+  const int32_t* off;      // [nvox+1] candidate-list offsets
+  const double* pts;       // [ncand*4] candidate coordinates, voxel-major
+  double lo_x, lo_y, lo_z; // grid origin
+  double inv_h;            // 1 / voxel edge
+  int32_t dim_x, dim_y, dim_z;
+  int32_t pad;
+};
+
+constexpr int kGridLevels = 2;  // fine (near field) + coarse (far field)
+
 // Exact nearest-pocket-point structure staged in HBM.
 struct PocketView {
   const double* pts;       // [P*4] x,y,z,pad (32-B records)
   int32_t P;
   int32_t use_index;       // 0 = brute force only
-  const int32_t* vox_off;  // [nvox+1] candidate-list offsets
-  const double* vox_pts;   // [ncand*4] candidate coordinates, voxel-major
-  double lo_x, lo_y, lo_z; // grid origin
-  double inv_h;            // 1 / voxel edge
-  int32_t dim_x, dim_y, dim_z;
+  GridLevel lv[kGridLevels];
 };
 
 struct DockParams {

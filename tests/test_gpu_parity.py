@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from paper_1901_06363_b200 import Knobs, workloads as W
-from tests.helpers import assert_same_result
+from gd_test_helpers import assert_same_result
 
 pytestmark = pytest.mark.gpu
 
