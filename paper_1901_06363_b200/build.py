@@ -21,8 +21,8 @@ BUILD = PKG / "_build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_SRCS = ["capi.cpp", "prep.cpp", "orient.cpp", "synth.cpp"]
-CUDA_SRCS = ["kernels.cu"]
-HEADERS = ["kernels.h", "prep.hpp", "orient.hpp"]
+CUDA_SRCS = ["rigid.cu", "flex.cu", "pocket_index.cu"]
+HEADERS = ["kernels.h", "device_common.cuh", "prep.hpp", "orient.hpp"]
 
 
 def _run(cmd: list[str]) -> None:
@@ -48,6 +48,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = BUILD / (src + ".o")
         if force or _stale(obj, [CSRC / src] + hdrs):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
+                  *os.environ.get("GD_NVCC_EXTRA", "").split(),
                   "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *inc,
                   "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)

@@ -110,6 +110,7 @@ struct gd_ctx {
   bool have_result = false;
   DevBuf counters;
   bool counted = false;
+  DevBuf st_final, st_evals, st_checks;
   DevBuf seed_slot, seed_score, k_eff, o_orient, o_rank, o_rigid, o_final, o_evals, o_checks,
       o_pose, stage_pose, o_scored, o_status;
   std::vector<double> initial_score;  // given-pose mode: rigid_score column
@@ -532,6 +533,9 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   GD_CUDA(ctx, ctx->o_final.ensure(sizeof(double) * slots));
   GD_CUDA(ctx, ctx->o_evals.ensure(sizeof(int64_t) * slots));
   GD_CUDA(ctx, ctx->o_checks.ensure(sizeof(int64_t) * slots));
+  GD_CUDA(ctx, ctx->st_final.ensure(sizeof(double) * slots));
+  GD_CUDA(ctx, ctx->st_evals.ensure(sizeof(int64_t) * slots));
+  GD_CUDA(ctx, ctx->st_checks.ensure(sizeof(int64_t) * slots));
   GD_CUDA(ctx, ctx->o_scored.ensure(sizeof(int64_t) * std::max(L, 1)));
   GD_CUDA(ctx, ctx->o_status.ensure(sizeof(int32_t) * std::max(L, 1)));
   if (keep_pose) {
@@ -572,9 +576,11 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   p.top_k = K;
   p.rigid = rigid ? 1 : 0;
   p.max_n = ctx->max_n;
-  int amax = std::max(360 / p.hp - 1, 360 / p.lp - 1);
-  if (p.refine) amax = std::max({amax, 360 / p.tile, p.tile / p.hp});
-  p.amax = std::max(amax, 1);
+  p.max_pairs = std::max(1, ctx->max_n * ctx->max_n / 4);
+  p.k_slots = rigid ? std::min(K, ctx->n_orient) : 1;
+  p.st_final = ctx->st_final.as<double>();
+  p.st_evals = ctx->st_evals.as<int64_t>();
+  p.st_checks = ctx->st_checks.as<int64_t>();
   p.seed_slot = ctx->seed_slot.as<int32_t>();
   p.seed_score = ctx->seed_score.as<double>();
   p.k_eff = ctx->k_eff.as<int32_t>();
@@ -595,10 +601,6 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
     p.counters = ctx->counters.as<unsigned long long>();
   }
   ctx->counted = p.counters != nullptr;
-  // Chains resident per CTA: as many as fit a ~100 KB shared-memory budget.
-  const size_t budget = static_cast<size_t>(env_double("GD_FLEX_SMEM", 100 * 1024));
-  p.chains_per_cta = std::min(K, 32);
-  while (p.chains_per_cta > 1 && flex_smem_bytes(p) > budget) --p.chains_per_cta;
 
   int launches = 0;
   cudaEventRecord(ctx->ev[2], ctx->stream);
@@ -611,7 +613,8 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   cudaEventRecord(ctx->ev[3], ctx->stream);
   if (L > 0) {
     GD_CUDA(ctx, static_cast<cudaError_t>(launch_flex(p, ctx->stream)));
-    ++launches;
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_finalize(p, ctx->stream)));
+    launches += 2;
   }
   cudaEventRecord(ctx->ev[4], ctx->stream);
   ctx->last_topk = K;

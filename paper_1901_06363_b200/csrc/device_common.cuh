@@ -1,0 +1,237 @@
+// Device helpers shared by the sm_100a kernels (rigid.cu, flex.cu,
+// pocket_index.cu).
+//
+// Numerics: every decision-critical value is computed in fp64 with
+// __dadd_rn/__dsub_rn/__dmul_rn/__ddiv_rn/__dsqrt_rn in the reference's
+// expression order (vec3.hpp:19-44, geometry.hpp:140-213), so no FMA
+// contraction can change a bit; the TUs are also built with -fmad=false.
+// Scores, committed poses and all argmax/top-K decisions are therefore
+// bit-identical to the reference CPU path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace gdb200 {
+namespace {
+
+constexpr double kMinDistanceSq = 1e-12;  // geometry.hpp:33
+constexpr double kBumpScale = 0.8;        // geometry.hpp:37
+constexpr double kMinAxisLength = 1e-9;   // geometry.hpp:43
+constexpr double kInfeasible = -1.0;      // scores are > 0
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// distance_sq (vec3.hpp:44): d = a - b; (d.x*d.x + d.y*d.y) + d.z*d.z.
+__device__ __forceinline__ double dist_sq(double ax, double ay, double az, double bx, double by,
+                                          double bz) {
+  const double dx = dsub(ax, bx), dy = dsub(ay, by), dz = dsub(az, bz);
+  return dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
+}
+
+// 32-byte point record (x, y, z, pad) through the read-only path.
+struct P3 {
+  double x, y, z;
+};
+__device__ __forceinline__ P3 ldp(const double* base, int j) {
+  const double2 a = __ldg(reinterpret_cast<const double2*>(base) + 2 * j);
+  const double b = __ldg(base + 4 * j + 2);
+  return P3{a.x, a.y, b};
+}
+
+// Executed-work counters (exact; DESIGN.md §4 turns them into fp64 FLOPs).
+// Kernels are instantiated twice: Work<true> counts (GD_FLAG_COUNT_WORK),
+// Work<false> compiles every increment away so the timed kernels carry no
+// counter registers.
+enum WorkKind { kPairs, kRot, kBump, kQuery, kTerms, kEvals, kXform, kWorkKinds };
+template <bool On>
+struct Work {
+  unsigned c[kWorkKinds];
+  __device__ Work() {
+    if constexpr (On)
+      for (int k = 0; k < kWorkKinds; ++k) c[k] = 0;
+  }
+  __device__ __forceinline__ void add(int k, unsigned v) {
+    if constexpr (On) c[k] += v;
+  }
+};
+
+// Per-thread publish (rigid kernel: all threads reach it).
+template <bool On>
+__device__ void publish(const Work<On>& w, unsigned long long* out, int base) {
+  if constexpr (On) {
+    if (out == nullptr) return;
+    for (int k = 0; k < kWorkKinds; ++k) atomicAdd(out + base + k, static_cast<unsigned long long>(w.c[k]));
+  }
+}
+
+// min_j distance_sq(q, P_j) over every pocket point (geometry.hpp:149-150).
+__device__ __noinline__ double min_dist_sq_brute(const PocketView& pk, double x, double y,
+                                                 double z) {
+  double m = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+  for (int j = 0; j < pk.P; ++j) {
+    const P3 p = ldp(pk.pts, j);
+    m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+  }
+  return m;
+}
+
+// Exact nearest-point query: the voxel's candidate list holds every point
+// that can attain the fp64 minimum anywhere in the (slightly expanded)
+// voxel, so the minimum is bit-identical to the brute-force scan (the
+// reference's PocketIndex makes the same exactness argument,
+// geometry.hpp:45-46).  Fine level first, then the coarse far-field level;
+// queries beyond both fall back to the full scan.
+template <bool On>
+__device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, double y, double z,
+                                              Work<On>& w) {
+  w.add(kQuery, 1);
+  if (pk.use_index) {
+#pragma unroll
+    for (int L = 0; L < kGridLevels; ++L) {
+      const GridLevel& g = pk.lv[L];
+      const double fx = (x - g.lo_x) * g.inv_h;
+      const double fy = (y - g.lo_y) * g.inv_h;
+      const double fz = (z - g.lo_z) * g.inv_h;
+      if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
+        const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
+                      static_cast<int>(fz);
+        const int s = __ldg(g.off + v), e = __ldg(g.off + v + 1);
+        w.add(kPairs, e - s);
+        double m = __longlong_as_double(0x7ff0000000000000ll);
+        for (int k = s; k < e; ++k) {
+          const P3 p = ldp(g.pts, k);
+          m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+        }
+        return m;
+      }
+    }
+  }
+  w.add(kPairs, pk.P);
+  return min_dist_sq_brute(pk, x, y, z);
+}
+
+// Voxel lookup half of a query: the candidate list of the first grid level
+// containing q, or (nullptr, 0, 0) for the full-scan fallback.
+struct Loc {
+  const double* pts;
+  int s, e;
+};
+__device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, double z) {
+  if (pk.use_index) {
+#pragma unroll
+    for (int L = 0; L < kGridLevels; ++L) {
+      const GridLevel& g = pk.lv[L];
+      const double fx = (x - g.lo_x) * g.inv_h;
+      const double fy = (y - g.lo_y) * g.inv_h;
+      const double fz = (z - g.lo_z) * g.inv_h;
+      if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
+        const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
+                      static_cast<int>(fz);
+        return Loc{g.pts, __ldg(g.off + v), __ldg(g.off + v + 1)};
+      }
+    }
+  }
+  return Loc{nullptr, 0, 0};
+}
+
+// Two independent queries with both lookups issued before either scan and
+// the two candidate scans interleaved (memory-level parallelism 2).
+template <bool On>
+__device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, double y0, double z0,
+                                             double x1, double y1, double z1, double& m0,
+                                             double& m1, Work<On>& w) {
+  w.add(kQuery, 2);
+  const Loc a = locate(pk, x0, y0, z0);
+  const Loc b = locate(pk, x1, y1, z1);
+  const double inf = __longlong_as_double(0x7ff0000000000000ll);
+  m0 = inf;
+  m1 = inf;
+  const int na = a.pts ? a.e - a.s : 0, nb = b.pts ? b.e - b.s : 0;
+  w.add(kPairs, na + nb);
+  const int nmax = max(na, nb);
+  for (int k = 0; k < nmax; ++k) {
+    if (k < na) {
+      const P3 p = ldp(a.pts, a.s + k);
+      m0 = fmin(m0, dist_sq(x0, y0, z0, p.x, p.y, p.z));
+    }
+    if (k < nb) {
+      const P3 p = ldp(b.pts, b.s + k);
+      m1 = fmin(m1, dist_sq(x1, y1, z1, p.x, p.y, p.z));
+    }
+  }
+  if (a.pts == nullptr) {
+    w.add(kPairs, pk.P);
+    m0 = min_dist_sq_brute(pk, x0, y0, z0);
+  }
+  if (b.pts == nullptr) {
+    w.add(kPairs, pk.P);
+    m1 = min_dist_sq_brute(pk, x1, y1, z1);
+  }
+}
+
+// Rodrigues rotation of one atom (geometry.hpp:182-184):
+// ((o + v*c) + cross(k,v)*s) + k*(dot(k,v)*(1-c)), v = p - o.
+struct Axis {
+  double ox, oy, oz, kx, ky, kz;
+};
+__device__ __forceinline__ void rodrigues(const Axis& a, double c, double s, double omc, double px,
+                                          double py, double pz, double& qx, double& qy,
+                                          double& qz) {
+  const double vx = dsub(px, a.ox), vy = dsub(py, a.oy), vz = dsub(pz, a.oz);
+  const double crx = dsub(dmul(a.ky, vz), dmul(a.kz, vy));
+  const double cry = dsub(dmul(a.kz, vx), dmul(a.kx, vz));
+  const double crz = dsub(dmul(a.kx, vy), dmul(a.ky, vx));
+  const double d = dadd(dadd(dmul(a.kx, vx), dmul(a.ky, vy)), dmul(a.kz, vz));
+  const double w = dmul(d, omc);
+  qx = dadd(dadd(dadd(a.ox, dmul(vx, c)), dmul(crx, s)), dmul(a.kx, w));
+  qy = dadd(dadd(dadd(a.oy, dmul(vy, c)), dmul(cry, s)), dmul(a.ky, w));
+  qz = dadd(dadd(dadd(a.oz, dmul(vz, c)), dmul(crz, s)), dmul(a.kz, w));
+}
+
+// Rigid pose (E3): p' = c + R (p - c), rows summed left to right.
+__device__ __forceinline__ void rigid_apply(const double* R, double cx, double cy, double cz,
+                                            double vx, double vy, double vz, double& x, double& y,
+                                            double& z) {
+  x = dadd(cx, dadd(dadd(dmul(R[0], vx), dmul(R[1], vy)), dmul(R[2], vz)));
+  y = dadd(cy, dadd(dadd(dmul(R[3], vx), dmul(R[4], vy)), dmul(R[5], vz)));
+  z = dadd(cz, dadd(dadd(dmul(R[6], vx), dmul(R[7], vy)), dmul(R[8], vz)));
+}
+
+// (score desc, slot asc): does (ka, ia) precede (kb, ib)?
+__device__ __forceinline__ bool precede(double ka, int ia, double kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+template <int BT>
+__device__ void bitonic_sort(double* key, int* idx, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += BT) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const bool up = (i & k) == 0;
+          const double ki = key[i], kj = key[ixj];
+          const int ii = idx[i], ij = idx[ixj];
+          const bool sw = up ? precede(kj, ij, ki, ii) : precede(ki, ii, kj, ij);
+          if (sw) {
+            key[i] = kj;
+            key[ixj] = ki;
+            idx[i] = ij;
+            idx[ixj] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+}  // namespace
+}  // namespace gdb200

@@ -1,0 +1,481 @@
+// (2) fragment optimisation + (3) bump check + (4) scoring + (5a) restarts,
+// and (E7) the final ordering.
+//
+// flex_chain_kernel: one WARP per (ligand, seed rank) chain, i.e. one
+// match_probes_shape call (reference kernel.hpp:205-248).  Chains are
+// independent, so warps never wait for each other: a CTA is just four
+// chains (usually of the same ligand, in longest-ligand-first order) with
+// private shared-memory state.  Within a chain the greedy dependency
+// (rep -> rotamer -> left/right fragment, kernel.hpp:225-242) is sequential;
+// each fragment search evaluates its candidate angles in batches of kBatch:
+//
+//   * bump phase  -- lanes over (candidate, surviving bump pair): Rodrigues
+//                    rotation (geometry.hpp:182-184) + the clash rule
+//                    (geometry.hpp:199-213); warp OR-reduce per candidate;
+//   * query phase -- lanes over (feasible candidate, fragment atom): rotation
+//                    + exact nearest-pocket-point query (voxel index);
+//   * fold phase  -- lane c folds candidate c's overlap score in atom order
+//                    (geometry.hpp:143-154), reusing the committed pose's
+//                    terms for atoms outside the fragment and a per-step
+//                    prefix for the atoms before the first fragment atom.
+//
+// The bump-pair list is rebuilt once per fragment step and pruned exactly:
+// a pair (i in F, j not in F) whose distance from j to the whole circle
+// that atom i sweeps stays above the cutoff (1e-6 relative margin) cannot
+// bump at any angle, so dropping it changes no decision.
+//
+// All decisions reproduce the reference: strict '>' with first-encountered
+// ties (kernel.hpp:136, :169, :173, :185, :194), angle 0 = committed pose,
+// feasibility_checks / evaluations counted as CandidateEvaluator does.
+#include "device_common.cuh"
+
+namespace gdb200 {
+namespace {
+
+#ifndef GD_FLEX_MINB
+#define GD_FLEX_MINB 6       // resident CTAs per SM the register budget targets
+#endif
+constexpr int kWarps = 4;    // chains per CTA
+constexpr int kBatch = 4;    // candidates evaluated together by one warp
+constexpr unsigned kFull = 0xffffffffu;
+
+__host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pairs) {
+  return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * kBatch * n) +
+         a16(2ull * max_pairs) + a16(n) + a16(32);
+}
+
+struct WarpMem {
+  double* radius;        // [n]
+  uint64_t* far;         // [n*W]  bit j of row i: capped graph distance >= 4
+  double *px, *py, *pz;  // [n]    committed pose of the chain
+  double* term;          // [n]    max(1e-12, min_j d^2) of the committed pose
+  double* v;             // [kBatch*n] candidate terms of fragment atoms
+  uint16_t* pairs;       // [max_pairs] surviving bump pairs: F-slot | j << 8
+  uint8_t* fidx;         // [n] fragment atoms, ascending
+  uint64_t* fm;          // [4] fragment membership bits
+};
+
+__device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
+  WarpMem s;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    unsigned char* q = base + o;
+    o += a16(bytes);
+    return q;
+  };
+  s.radius = reinterpret_cast<double*>(take(8ull * n));
+  s.far = reinterpret_cast<uint64_t*>(take(8ull * n * W));
+  s.px = reinterpret_cast<double*>(take(8ull * n));
+  s.py = reinterpret_cast<double*>(take(8ull * n));
+  s.pz = reinterpret_cast<double*>(take(8ull * n));
+  s.term = reinterpret_cast<double*>(take(8ull * n));
+  s.v = reinterpret_cast<double*>(take(8ull * kBatch * n));
+  s.pairs = reinterpret_cast<uint16_t*>(take(2ull * max_pairs));
+  s.fidx = reinterpret_cast<uint8_t*>(take(n));
+  s.fm = reinterpret_cast<uint64_t*>(take(32));
+  return s;
+}
+
+__device__ __forceinline__ bool in_frag(const uint64_t* fm, int i) {
+  return (fm[i >> 6] >> (i & 63)) & 1ull;
+}
+
+// Evaluates candidates angle(c) = a0 + c*da, c < nb, of the current fragment
+// (CandidateEvaluator::evaluate, kernel.hpp:100-112).  Returns, in lane c,
+// candidate c's overlap score (cur for angle 0), and warp-uniformly the
+// mask of candidates that bumped.
+template <bool On>
+__device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X, int n, int nf,
+                           int np, int first, double pre, double cur, int a0, int da, int nb,
+                           int lane, double& score_out, unsigned& bumped_out, Work<On>& wk) {
+  const unsigned zero = (a0 == 0) ? 1u : 0u;  // only c = 0 can be angle 0
+  // Bump phase.
+  unsigned bl = 0;
+  const int total = nb * np;
+  for (int t = lane; t < total; t += 32) {
+    const int c = t / np;
+    if (((bl | zero) >> c) & 1u) continue;
+    const int pr = s.pairs[t - c * np];
+    const int i = s.fidx[pr & 0xff], j = pr >> 8;
+    const int a = a0 + c * da;
+    const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
+    double qx, qy, qz;
+    rodrigues(X, cs, sn, dsub(1.0, cs), s.px[i], s.py[i], s.pz[i], qx, qy, qz);
+    wk.add(kRot, 1);
+    wk.add(kBump, 1);
+    const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
+    if (dist_sq(qx, qy, qz, s.px[j], s.py[j], s.pz[j]) < dmul(cut, cut)) bl |= 1u << c;
+  }
+  const unsigned bumped = __reduce_or_sync(kFull, bl);
+  const unsigned live = ((1u << nb) - 1u) & ~bumped & ~zero;
+  // Query phase.
+  // Two items per lane per iteration (t, t+32): both lookups in flight.
+  const int tq = nb * nf;
+  for (int t = lane; t < tq; t += 64) {
+    const int c0 = t / nf;
+    const int t1 = t + 32 < tq ? t + 32 : t;
+    const int c1 = t1 / nf;
+    const bool l0 = (live >> c0) & 1u, l1 = t1 != t && ((live >> c1) & 1u);
+    if (!l0 && !l1) continue;
+    const int i0 = s.fidx[t - c0 * nf], i1 = s.fidx[t1 - c1 * nf];
+    const int a0c = a0 + c0 * da, a1c = a0 + c1 * da;
+    const double cs0 = __ldg(p.cos_deg + a0c), sn0 = __ldg(p.sin_deg + a0c);
+    const double cs1 = __ldg(p.cos_deg + a1c), sn1 = __ldg(p.sin_deg + a1c);
+    double x0, y0, z0, x1, y1, z1, m0, m1;
+    rodrigues(X, cs0, sn0, dsub(1.0, cs0), s.px[i0], s.py[i0], s.pz[i0], x0, y0, z0);
+    rodrigues(X, cs1, sn1, dsub(1.0, cs1), s.px[i1], s.py[i1], s.pz[i1], x1, y1, z1);
+    wk.add(kRot, 2);
+    min_dist_sq2(p.pocket, x0, y0, z0, x1, y1, z1, m0, m1, wk);
+    if (l0) s.v[c0 * n + i0] = fmax(kMinDistanceSq, m0);
+    if (l1) s.v[c1 * n + i1] = fmax(kMinDistanceSq, m1);
+  }
+  __syncwarp();
+  // Fold phase: lane c, atom order.
+  double score = cur;
+  if (lane < nb && ((live >> lane) & 1u)) {
+    double sum = pre;
+    const double* vc = s.v + lane * n;
+#pragma unroll 4
+    for (int i = first; i < n; ++i) sum = dadd(sum, vc[i]);
+    score = __ddiv_rn(static_cast<double>(n), sum);
+    wk.add(kTerms, n);
+    wk.add(kEvals, 1);
+  }
+  __syncwarp();
+  score_out = score;
+  bumped_out = bumped;
+}
+
+template <bool On>
+__device__ void publish_warp(const Work<On>& w, unsigned long long* c, int base, int lane) {
+  if constexpr (On) {
+    if (c == nullptr) return;
+#pragma unroll
+    for (int k = 0; k < kWorkKinds; ++k) {
+      const unsigned s = __reduce_add_sync(kFull, w.c[k]);
+      if (lane == 0) atomicAdd(c + base + k, static_cast<unsigned long long>(s));
+    }
+  }
+}
+
+template <bool On>
+__global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(DockParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = p.k_slots;
+  const long long item = static_cast<long long>(blockIdx.x) * kWarps + warp;
+  if (item >= static_cast<long long>(p.n_lig) * K) return;
+  const int l = p.order[item / K];
+  const int r = static_cast<int>(item % K);
+  const LigMeta m = p.meta[l];
+  if (m.status != 0) return;
+  const int n = m.n, W = m.words;
+  const WarpMem s =
+      carve(smem + warp * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W, p.max_pairs);
+  const size_t e = static_cast<size_t>(l) * p.top_k + r;
+  Work<On> wk;
+
+  for (int i = lane; i < n; i += 32) s.radius[i] = __ldg(p.radii + m.atom_off + i);
+  for (int i = lane; i < n * W; i += 32) s.far[i] = __ldg(p.far_mask + m.far_off + i);
+  // Chain start: the rigid seed pose (E3) or the given pose.
+  double R[9];
+  if (p.rigid) {
+    const int o = p.seed_slot[e];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(p.orient_R + 9 * o + k);
+  }
+  for (int i = lane; i < n; i += 32) {
+    const double* q = p.xyz + 3 * (m.atom_off + i);
+    double x = q[0], y = q[1], z = q[2];
+    if (p.rigid) {
+      rigid_apply(R, p.cx, p.cy, p.cz, dsub(x, p.cx), dsub(y, p.cy), dsub(z, p.cz), x, y, z);
+      wk.add(kXform, 1);
+    }
+    s.px[i] = x;
+    s.py[i] = y;
+    s.pz[i] = z;
+    s.term[i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+  }
+  __syncwarp();
+  // match_probes_shape prologue (kernel.hpp:215-218).
+  double cur = 0.0;
+  if (lane == 0) {
+    double sum = 0.0;
+    for (int i = 0; i < n; ++i) sum = dadd(sum, s.term[i]);
+    cur = __ddiv_rn(static_cast<double>(n), sum);
+  }
+  cur = __shfl_sync(kFull, cur, 0);
+  if (!p.rigid && lane == 0) p.seed_score[e] = cur;
+  long long evals = 1, checks = 1;
+
+  for (int rep = 0; rep < p.reps; ++rep) {
+    for (int f = 0; f < m.nfrag; ++f) {
+      const int fo = m.frag_off + f;
+      const int axis = __ldg(p.frag_axis + fo), anchor = __ldg(p.frag_anchor + fo);
+      // Dispatch (kernel.hpp:229-239).
+      const bool low = __ldg(p.frag_rel + fo) <= p.threshold;
+      const bool refined = !low && p.refine;
+      const int step = low ? p.lp : p.hp;
+      const int A = 360 / step;
+      if (!refined && A == 1) {  // step 360: only the committed pose
+        checks += 1;
+        evals += 1;
+        continue;
+      }
+      if (lane < W) s.fm[lane] = __ldg(p.frag_mask + m.fmask_off + f * W + lane);
+      // rotate_fragment_into axis (geometry.hpp:165-169), identical in every lane.
+      const double ox = s.px[axis], oy = s.py[axis], oz = s.pz[axis];
+      const double ax = dsub(s.px[anchor], ox), ay = dsub(s.py[anchor], oy),
+                   az = dsub(s.pz[anchor], oz);
+      const double len = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
+      if (len < kMinAxisLength) {  // "rotate_fragment: degenerate rotation axis"
+        if (lane == 0) p.status[l] = 3;
+        return;
+      }
+      const Axis X{ox, oy, oz, __ddiv_rn(ax, len), __ddiv_rn(ay, len), __ddiv_rn(az, len)};
+      __syncwarp();
+      // Fragment atoms, ascending.
+      int nf = 0;
+      for (int b = 0; b < n; b += 32) {
+        const int i = b + lane;
+        const bool in = i < n && in_frag(s.fm, i);
+        const unsigned mask = __ballot_sync(kFull, in);
+        if (in) s.fidx[nf + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint8_t>(i);
+        nf += __popc(mask);
+      }
+      __syncwarp();
+      const int first = s.fidx[0];
+      double pre = 0.0;
+      if (lane == 0)
+        for (int i = 0; i < first; ++i) pre = dadd(pre, s.term[i]);
+      pre = __shfl_sync(kFull, pre, 0);
+      // Surviving bump pairs: drop (i, j) when the circle atom i sweeps never
+      // comes within the cutoff of j: dmin^2 = h^2 + (sigma - rho)^2 > cut^2,
+      // tested without square roots as L = s2 + r2 + h2 - C > 0 && L^2 > 4 s2 r2.
+      // Per-atom axial coordinate a = k.(p - o) and squared axis distance
+      // r2 = |p - o|^2 - a^2 first, lane-parallel, in the (free) v scratch.
+      double* axc = s.v;
+      double* rad2 = s.v + n;
+      for (int i = lane; i < n; i += 32) {
+        const double vx = s.px[i] - ox, vy = s.py[i] - oy, vz = s.pz[i] - oz;
+        const double a = X.kx * vx + X.ky * vy + X.kz * vz;
+        axc[i] = a;
+        rad2[i] = fmax(0.0, vx * vx + vy * vy + vz * vz - a * a);
+      }
+      __syncwarp();
+      int np = 0;
+      for (int sl = 0; sl < nf; ++sl) {
+        const int i = s.fidx[sl];
+        const double ai = axc[i], r2 = rad2[i], ri = s.radius[i];
+        for (int b = 0; b < n; b += 32) {
+          const int j = b + lane;
+          bool keep = false;
+          if (j < n && (((s.far[i * W + (j >> 6)] & ~s.fm[j >> 6]) >> (j & 63)) & 1ull)) {
+            const double h = axc[j] - ai;
+            const double s2 = rad2[j];
+            const double cut = kBumpScale * (ri + s.radius[j]);
+            const double C = cut * cut * (1.0 + 1e-6) + 1e-9;
+            const double Lq = s2 + r2 + h * h - C;
+            keep = !(Lq > 0.0 && Lq * Lq > 4.0 * s2 * r2);
+          }
+          const unsigned mask = __ballot_sync(kFull, keep);
+          if (keep) s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(sl | (j << 8));
+          np += __popc(mask);
+        }
+      }
+      __syncwarp();
+      // Non-fragment terms are the same for every candidate of this step:
+      // pre-fill them into each candidate slot so the fold is a plain sum.
+      for (int t = lane; t < kBatch * n; t += 32) {
+        const int i = t % n;
+        if (!in_frag(s.fm, i)) s.v[t] = s.term[i];
+      }
+      __syncwarp();
+
+      int best_a = 0;
+      double best = cur;
+      if (!refined) {
+        // optimize_fragment_flat (kernel.hpp:125-143).
+        long long nfeas = 0;
+        for (int kb = 0; kb < A - 1; kb += kBatch) {
+          const int nb = min(kBatch, A - 1 - kb);
+          const int a0 = (kb + 1) * step;
+          double sc;
+          unsigned bumped;
+          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, step, nb, lane, sc, bumped, wk);
+          for (int c = 0; c < nb; ++c) {
+            const double v = __shfl_sync(kFull, sc, c);
+            if ((bumped >> c) & 1u) continue;
+            ++nfeas;
+            if (v > best) {
+              best = v;
+              best_a = a0 + c * step;
+            }
+          }
+        }
+        checks += A;
+        evals += 1 + nfeas;
+      } else {
+        // optimize_fragment_refined (kernel.hpp:150-198).
+        const int T = p.tile, tc = 360 / T;
+        bool have = false;
+        int wt = -1;
+        double ws = 0.0;
+        long long nfeas = 0;
+        best = 0.0;
+        for (int kb = 0; kb < tc; kb += kBatch) {
+          const int nb = min(kBatch, tc - kb);
+          const int a0 = kb * T + T / 2;
+          double sc;
+          unsigned bumped;
+          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, T, nb, lane, sc, bumped, wk);
+          for (int c = 0; c < nb; ++c) {
+            const double v = __shfl_sync(kFull, sc, c);
+            if ((bumped >> c) & 1u) continue;
+            ++nfeas;
+            if (!have || v > best) {
+              best = v;
+              best_a = a0 + c * T;
+              have = true;
+            }
+            if (wt < 0 || v > ws) {
+              wt = kb + c;
+              ws = v;
+            }
+          }
+        }
+        checks += tc;
+        if (wt >= 0) {
+          int cnt2 = 0;
+          while ((cnt2 + 1) * p.hp <= T) ++cnt2;
+          for (int kb = 0; kb < cnt2; kb += kBatch) {
+            const int nb = min(kBatch, cnt2 - kb);
+            const int a0 = wt * T + kb * p.hp;
+            double sc;
+            unsigned bumped;
+            eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, p.hp, nb, lane, sc, bumped, wk);
+            for (int c = 0; c < nb; ++c) {
+              const double v = __shfl_sync(kFull, sc, c);
+              if ((bumped >> c) & 1u) continue;
+              ++nfeas;
+              if (!have || v > best) {
+                best = v;
+                best_a = a0 + c * p.hp;
+                have = true;
+              }
+            }
+          }
+          checks += cnt2;
+        }
+        checks += 1;  // entry-pose comparison (kernel.hpp:192-194)
+        if (!have || cur > best) {
+          best = cur;
+          best_a = 0;
+        }
+        evals += nfeas;
+      }
+      // commit_angle (kernel.hpp:115-117): a fresh rotation of the entry pose,
+      // bit-identical to the scored candidate; refresh the fragment's terms.
+      if (best_a != 0) {
+        const double cs = __ldg(p.cos_deg + best_a), sn = __ldg(p.sin_deg + best_a);
+        const double omc = dsub(1.0, cs);
+        for (int sl = lane; sl < nf; sl += 32) {
+          const int i = s.fidx[sl];
+          double qx, qy, qz;
+          rodrigues(X, cs, sn, omc, s.px[i], s.py[i], s.pz[i], qx, qy, qz);
+          wk.add(kRot, 1);
+          s.px[i] = qx;
+          s.py[i] = qy;
+          s.pz[i] = qz;
+          s.term[i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx, qy, qz, wk));
+        }
+      }
+      __syncwarp();
+      cur = best;
+    }
+  }
+  if (lane == 0) {
+    p.st_final[e] = cur;
+    p.st_evals[e] = evals;
+    p.st_checks[e] = checks;
+  }
+  if (p.stage_pose != nullptr) {
+    double* dst = p.stage_pose + 3 * (static_cast<size_t>(p.top_k) * m.atom_off + static_cast<size_t>(r) * n);
+    for (int i = lane; i < n; i += 32) {
+      dst[3 * i] = s.px[i];
+      dst[3 * i + 1] = s.py[i];
+      dst[3 * i + 2] = s.pz[i];
+    }
+  }
+  publish_warp(wk, p.counters, 8, lane);
+}
+
+// (E7) final order: (final score desc, seed rank asc), one rank per thread;
+// each rank's destination is the number of ranks that precede it.
+__global__ void __launch_bounds__(256) finalize_kernel(DockParams p) {
+  const int l = blockIdx.x;
+  const LigMeta m = p.meta[l];
+  if (m.status != 0 || p.status[l] != 0) return;
+  const int K = p.k_slots, slots = p.top_k;
+  __shared__ double fin[256];
+  __shared__ unsigned long long total;
+  const int e = threadIdx.x;
+  if (e < K) fin[e] = p.st_final[static_cast<size_t>(l) * slots + e];
+  if (e == 0) total = 0;
+  __syncthreads();
+  if (e < K) {
+    const double fe = fin[e];
+    int pos = 0;
+    for (int e2 = 0; e2 < K; ++e2) pos += precede(fin[e2], e2, fe, e) ? 1 : 0;
+    const size_t src = static_cast<size_t>(l) * slots + e;
+    const size_t d = static_cast<size_t>(l) * slots + pos;
+    const long long ev = p.st_evals[src];
+    p.out_final[d] = fe;
+    p.out_evals[d] = ev;
+    p.out_checks[d] = p.st_checks[src];
+    p.out_rank[d] = e;
+    p.out_orient[d] = p.rigid ? p.orient_idx[p.seed_slot[src]] : -1;
+    p.out_rigid[d] = p.seed_score[src];
+    if (p.out_pose != nullptr) {
+      const int n = m.n;
+      const double* from = p.stage_pose + 3 * (static_cast<size_t>(slots) * m.atom_off + static_cast<size_t>(e) * n);
+      double* to = p.out_pose + 3 * (static_cast<size_t>(slots) * m.atom_off + static_cast<size_t>(pos) * n);
+      for (int i = 0; i < 3 * n; ++i) to[i] = from[i];
+    }
+    atomicAdd(&total, static_cast<unsigned long long>(ev));
+  }
+  __syncthreads();
+  if (e == 0) {
+    p.poses_scored[l] = static_cast<long long>(total) + (p.rigid ? p.n_orient : 0);
+    p.k_eff[l] = K;
+  }
+}
+
+}  // namespace
+
+size_t flex_smem_bytes(const DockParams& p) {
+  return kWarps * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs);
+}
+
+int launch_flex(const DockParams& p, void* stream) {
+  const long long chains = static_cast<long long>(p.n_lig) * p.k_slots;
+  if (chains == 0) return cudaSuccess;
+  const size_t smem = flex_smem_bytes(p);
+  auto kernel = p.counters ? flex_chain_kernel<true> : flex_chain_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const long long blocks = (chains + kWarps - 1) / kWarps;
+  kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError();
+}
+
+int launch_finalize(const DockParams& p, void* stream) {
+  if (p.n_lig == 0) return cudaSuccess;
+  finalize_kernel<<<p.n_lig, 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace gdb200

@@ -65,14 +65,19 @@ struct DockParams {
   double threshold;
   int32_t top_k;           // slots per ligand in the outputs
   int32_t rigid;           // 1 = rigid sweep + top-K seeds, 0 = dock given pose
-  int32_t chains_per_cta;  // G: chains resident in shared memory at once
+  int32_t k_slots;         // chains per ligand: min(top_k, n_orient) (1 if no sweep)
   int32_t max_n;           // largest ligand in the batch (smem sizing)
-  int32_t amax;            // largest candidate count of one sub-step
+  int32_t max_pairs;       // bump-pair list capacity per warp (floor(max_n^2/4))
 
   // Rigid -> flex hand-off (rank order).
   int32_t* seed_slot;      // [L*K] position in the orientation list
   double* seed_score;      // [L*K]
   int32_t* k_eff;          // [L]
+
+  // Chain results in rank order (flex -> finalize).
+  double* st_final;
+  int64_t* st_evals;
+  int64_t* st_checks;
 
   // Outputs, final order (E7).
   int32_t* out_orient;
@@ -100,7 +105,10 @@ size_t flex_smem_bytes(const DockParams& p);
 
 // Launchers; return cudaError_t as int.  `stream` is a cudaStream_t.
 int launch_rigid_topk(const DockParams& p, int sort_slots, void* stream);
+// One warp per (ligand, seed-rank) chain: n_lig * k_slots chains.
 int launch_flex(const DockParams& p, void* stream);
+// E7 final ordering + poses scored, one CTA per ligand.
+int launch_finalize(const DockParams& p, void* stream);
 int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int n_poses,
                        double* out, void* stream);
 

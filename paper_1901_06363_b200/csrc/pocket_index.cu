@@ -1,0 +1,178 @@
+// Pocket-side kernels: exact voxel candidate-list build, overlap_score of
+// arbitrary poses (drop-in API), and the fp64 pipe probe used as the
+// roofline denominator.
+#include "device_common.cuh"
+
+namespace gdb200 {
+namespace {
+
+// --------------------------------------------------------------------------
+// overlap_score for arbitrary poses: one thread per pose.
+// --------------------------------------------------------------------------
+__global__ void score_poses_kernel(PocketView pk, const double* xyz, int n_atoms, int n_poses,
+                                   double* out) {
+  const int pose = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pose >= n_poses) return;
+  const double* q = xyz + static_cast<size_t>(3) * n_atoms * pose;
+  Work<false> wk;
+  double sum = 0.0;
+  for (int i = 0; i < n_atoms; ++i)
+    sum = dadd(sum, fmax(kMinDistanceSq, min_dist_sq(pk, q[3 * i], q[3 * i + 1], q[3 * i + 2], wk)));
+  out[pose] = __ddiv_rn(static_cast<double>(n_atoms), sum);
+}
+
+// --------------------------------------------------------------------------
+// Voxel candidate lists.  For voxel box B (expanded by kVoxEps):
+//   U    = min_j maxdist^2(B, P_j)          (an upper bound on the NN d^2)
+//   C    = { j : mindist^2(B, P_j) <= U + margin }
+//   keep = { a in C : no b in C with d^2(q,b) < d^2(q,a) - margin at all 8
+//            corners q of B }  (d^2(q,b) - d^2(q,a) is affine in q, so the
+//            corners bound it over B)
+// margin (1e-9 A^2) is orders above fp64 rounding of d^2 (~1e-13), so no
+// dropped point can attain the fp64 minimum anywhere in B.
+// --------------------------------------------------------------------------
+constexpr double kVoxEps = 1e-6;
+constexpr double kVoxMargin = 1e-9;
+constexpr int kVoxMaxCand = 1024;
+
+// Does point b beat point a by more than the margin everywhere in box
+// [bl, bh]?  d^2(q,b) - d^2(q,a) is affine in q, so the 8 corners decide.
+__device__ bool dominates(const P3& b, const P3& a, const double* bl, const double* bh) {
+  for (int corner = 0; corner < 8; ++corner) {
+    const double qx = (corner & 1) ? bh[0] : bl[0];
+    const double qy = (corner & 2) ? bh[1] : bl[1];
+    const double qz = (corner & 4) ? bh[2] : bl[2];
+    const double da = (qx - a.x) * (qx - a.x) + (qy - a.y) * (qy - a.y) + (qz - a.z) * (qz - a.z);
+    const double db = (qx - b.x) * (qx - b.x) + (qy - b.y) * (qy - b.y) + (qz - b.z) * (qz - b.z);
+    if (!(db < da - kVoxMargin)) return false;
+  }
+  return true;
+}
+
+__device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, int* cand) {
+  const int iz = v % g.dim_z;
+  const int iy = (v / g.dim_z) % g.dim_y;
+  const int ix = v / (g.dim_z * g.dim_y);
+  const double bl[3] = {g.lo_x + ix * g.h - kVoxEps, g.lo_y + iy * g.h - kVoxEps,
+                        g.lo_z + iz * g.h - kVoxEps};
+  const double bh[3] = {bl[0] + g.h + 2 * kVoxEps, bl[1] + g.h + 2 * kVoxEps,
+                        bl[2] + g.h + 2 * kVoxEps};
+  const double cx = 0.5 * (bl[0] + bh[0]), cy = 0.5 * (bl[1] + bh[1]), cz = 0.5 * (bl[2] + bh[2]);
+  // Pass 1: U (upper bound on the NN distance^2 anywhere in B) and the point
+  // nearest the box centre, a strong dominator for pass 2's pre-filter.
+  double U = 1e300, dc = 1e300;
+  int jc = 0;
+  for (int j = 0; j < P; ++j) {
+    const P3 q = ldp(pts, j);
+    const double fx = fmax(fabs(q.x - bl[0]), fabs(q.x - bh[0]));
+    const double fy = fmax(fabs(q.y - bl[1]), fabs(q.y - bh[1]));
+    const double fz = fmax(fabs(q.z - bl[2]), fabs(q.z - bh[2]));
+    U = fmin(U, fx * fx + fy * fy + fz * fz);
+    const double d = (q.x - cx) * (q.x - cx) + (q.y - cy) * (q.y - cy) + (q.z - cz) * (q.z - cz);
+    if (d < dc) {
+      dc = d;
+      jc = j;
+    }
+  }
+  const double lim = U * (1.0 + 1e-12) + kVoxMargin;
+  const P3 C = ldp(pts, jc);
+  // Pass 2: points that can be nearest somewhere in B and that jc does not
+  // dominate (a point dominated by anything is dominated by a kept point,
+  // by transitivity, so the final set does not depend on this filter).
+  int k = 0;
+  for (int j = 0; j < P; ++j) {
+    const P3 q = ldp(pts, j);
+    const double nx = fmax(0.0, fmax(bl[0] - q.x, q.x - bh[0]));
+    const double ny = fmax(0.0, fmax(bl[1] - q.y, q.y - bh[1]));
+    const double nz = fmax(0.0, fmax(bl[2] - q.z, q.z - bh[2]));
+    if (nx * nx + ny * ny + nz * nz <= lim && !dominates(C, q, bl, bh)) {
+      if (k >= kVoxMaxCand) return -1;
+      cand[k++] = j;
+    }
+  }
+  // Pass 3: full dominance pruning among the survivors.
+  int kept = 0;
+  for (int a = 0; a < k; ++a) {
+    const P3 A = ldp(pts, cand[a]);
+    bool dominated = false;
+    for (int b = 0; b < k && !dominated; ++b)
+      if (b != a) dominated = dominates(ldp(pts, cand[b]), A, bl, bh);
+    if (!dominated) cand[kept++] = cand[a];
+  }
+  return kept;
+}
+
+__global__ void voxel_count_kernel(const double* pts, int P, VoxelGrid g, int32_t* counts) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nv = g.dim_x * g.dim_y * g.dim_z;
+  if (v >= nv) return;
+  int cand[kVoxMaxCand];
+  const int k = voxel_list(pts, P, g, v, cand);
+  counts[v] = k < 0 ? P : k;  // overflow: keep every point (exact, rare)
+}
+
+__global__ void voxel_fill_kernel(const double* pts, int P, VoxelGrid g, const int32_t* offsets,
+                                  double* vox_pts) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  const int nv = g.dim_x * g.dim_y * g.dim_z;
+  if (v >= nv) return;
+  int cand[kVoxMaxCand];
+  const int k = voxel_list(pts, P, g, v, cand);
+  double* out = vox_pts + 4 * static_cast<size_t>(offsets[v]);
+  for (int a = 0; a < (k < 0 ? P : k); ++a) {
+    const int j = k < 0 ? a : cand[a];
+    for (int c = 0; c < 4; ++c) out[4 * a + c] = pts[4 * j + c];
+  }
+}
+
+// FP64 peak probe: 8 independent chains per thread of a DMUL and a DADD
+// (no FMA: the hot path's recipe forbids it), 2 ops per step per chain.
+__global__ void fp64_probe_kernel(double* sink, int iters) {
+  double a[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) a[c] = 1.0 + 1e-9 * (threadIdx.x + c);
+  const double m = 0.9999999, d = 1e-7;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) a[c] = dadd(dmul(a[c], m), d);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += a[c];
+  if (s == 12345.0) sink[0] = s;  // keeps the chains live
+}
+
+}  // namespace
+
+int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* stream) {
+  fp64_probe_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(sink, iters);
+  return cudaGetLastError();
+}
+
+int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int n_poses,
+                       double* out, void* stream) {
+  if (n_poses <= 0) return cudaSuccess;
+  const int bt = 128;
+  score_poses_kernel<<<(n_poses + bt - 1) / bt, bt, 0, static_cast<cudaStream_t>(stream)>>>(
+      pk, xyz, n_atoms, n_poses, out);
+  return cudaGetLastError();
+}
+
+int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, void* stream) {
+  const int nv = g.dim_x * g.dim_y * g.dim_z;
+  const int bt = 128;
+  voxel_count_kernel<<<(nv + bt - 1) / bt, bt, 0, static_cast<cudaStream_t>(stream)>>>(pts, P, g,
+                                                                                      counts);
+  return cudaGetLastError();
+}
+
+int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets,
+                      double* vox_pts, void* stream) {
+  const int nv = g.dim_x * g.dim_y * g.dim_z;
+  const int bt = 128;
+  voxel_fill_kernel<<<(nv + bt - 1) / bt, bt, 0, static_cast<cudaStream_t>(stream)>>>(
+      pts, P, g, offsets, vox_pts);
+  return cudaGetLastError();
+}
+
+}  // namespace gdb200

@@ -1,0 +1,185 @@
+// Drop-in API test: the reference's own test cases (test_geometry.cpp,
+// test_kernel.cpp, test_screening.cpp), restated against
+// <geodock_b200/geodock.hpp>, which runs them on the GPU through the C-ABI.
+// A plain runner (no Catch2 in this image): prints one line per case and
+// exits non-zero on any failure.  Built and run by tests/test_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "geodock_b200/geodock.hpp"
+
+using namespace geodock;
+
+static int g_failed = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    if (!(cond)) {                                                           \
+      std::printf("  CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #cond);  \
+      ++g_failed;                                                            \
+    }                                                                        \
+  } while (0)
+
+static void run(const char* name, const std::function<void()>& fn) {
+  const int before = g_failed;
+  try {
+    fn();
+  } catch (const std::exception& e) {
+    std::printf("  exception: %s\n", e.what());
+    ++g_failed;
+  }
+  std::printf("%s %s\n", g_failed == before ? "PASS" : "FAIL", name);
+}
+
+static Pose pose_of(std::vector<Vec3> p) { return Pose{std::move(p)}; }
+
+// PeakRig (test_kernel.cpp:19-31).
+static Ligand rig_ligand() {
+  return Ligand("rig", {{0, {0, 0, 0}, 1.0}, {1, {0, 0, 1}, 1.0}, {2, {1, 0, 1}, 1.0}},
+                {{0, 1, true}, {1, 2, false}});
+}
+static Pocket rig_pocket() { return Pocket("p", {{0, 0, 0}, {0, 0, 1.2}, {0, -1, 1}}); }
+
+int main() {
+  run("overlap_score matches hand-computed values", [] {
+    CHECK(overlap_score(pose_of({{0, 0, 0}}), Pocket("p", {{0, 0, 1}})) == 1.0);
+    CHECK(overlap_score(pose_of({{0, 0, 0}, {0, 0, 3}}), Pocket("p", {{0, 0, 0}})) == 2.0 / (1e-12 + 9.0));
+    CHECK(overlap_score(pose_of({{0, 0, 2}}), Pocket("p", {{0, 0, 1}, {0, 0, 4}})) == 1.0);
+  });
+  run("overlap_score decreases as a single atom moves away", [] {
+    const Pocket pocket("p", {{0, 0, 0}});
+    double prev = overlap_score(pose_of({{0, 0, 1}}), pocket);
+    for (double r = 1.5; r < 10.0; r += 0.5) {
+      const double cur = overlap_score(pose_of({{0, 0, r}}), pocket);
+      CHECK(cur < prev);
+      prev = cur;
+    }
+  });
+  run("overlap_score: empty pose is an error", [] {
+    bool threw = false;
+    try {
+      overlap_score(Pose{}, Pocket("p", {{0, 0, 0}}));
+    } catch (const Error&) {
+      threw = true;
+    }
+    CHECK(threw);
+  });
+  run("optimal_tile_size matches the divisor argmin", [] {
+    CHECK(optimal_tile_size(1) == 18);
+    CHECK(optimal_tile_size(4) == 36);
+    CHECK(optimal_tile_size(360) == 360);
+  });
+  run("KnobConfig validation", [] {
+    auto bad = [](KnobConfig k) {
+      try {
+        k.validate();
+      } catch (const Error&) {
+        return true;
+      }
+      return false;
+    };
+    CHECK(!bad(KnobConfig{1, 45, 0.0, 3, false}));
+    CHECK(bad(KnobConfig{7, 45, 0.0, 3, false}));
+    CHECK(bad(KnobConfig{10, 5, 0.0, 3, false}));
+    CHECK(bad(KnobConfig{1, 45, 1.5, 3, false}));
+    CHECK(bad(KnobConfig{1, 45, 0.0, 0, false}));
+    CHECK(bad(KnobConfig{0, 45, 0.0, 3, false}));
+  });
+  run("Ligand validation messages", [] {
+    try {
+      Ligand("x", {{0, {0, 0, 0}, 1.0}}, {});
+      CHECK(false);
+    } catch (const Error& e) {
+      CHECK(std::string(e.what()).find("needs at least 2 atoms") != std::string::npos);
+    }
+    try {
+      Ligand("x", {{0, {0, 0, 0}, 1.0}, {1, {1, 0, 0}, 1.0}, {2, {2, 0, 0}, 1.0}}, {{0, 1, false}});
+      CHECK(false);
+    } catch (const Error& e) {
+      CHECK(std::string(e.what()).find("disconnected") != std::string::npos);
+    }
+  });
+  run("match_probes_shape: baseline checks 360 candidates per fragment pass", [] {
+    const auto r = match_probes_shape(rig_ligand(), rig_pocket(), make_initial_pose(rig_ligand()),
+                                      KnobConfig{1, 45, 0.0, 3, false});
+    CHECK(r.feasibility_checks == 1 + 3 * 2 * 360);
+    CHECK(r.evaluations <= r.feasibility_checks);
+  });
+  run("match_probes_shape: refinement respects the per-fragment budget", [] {
+    const auto r = match_probes_shape(rig_ligand(), rig_pocket(), make_initial_pose(rig_ligand()),
+                                      KnobConfig{1, 45, 0.0, 1, true});
+    CHECK(r.evaluations <= 1 + 1 * 2 * 38);
+  });
+  run("match_probes_shape: threshold 1 sends every fragment to the low step", [] {
+    const auto r = match_probes_shape(rig_ligand(), rig_pocket(), make_initial_pose(rig_ligand()),
+                                      KnobConfig{1, 90, 1.0, 1, false});
+    CHECK(r.feasibility_checks == 1 + 1 * 2 * 4);
+  });
+  run("match_probes_shape: a rigid ligand scores the input pose once", [] {
+    const Ligand rigid("rigid", {{0, {0, 0, 0}, 1.0}, {1, {0, 0, 1.5}, 1.0}}, {{0, 1, false}});
+    const Pocket pocket("p", {{0, 0, 1}});
+    const Pose initial = make_initial_pose(rigid);
+    const auto r = match_probes_shape(rigid, pocket, initial, KnobConfig{});
+    CHECK(r.evaluations == 1);
+    CHECK(r.score == overlap_score(initial, pocket));
+    CHECK(r.final_pose.positions == initial.positions);
+  });
+  run("match_probes_shape: committed, deterministic, never regressing", [] {
+    const Ligand lig = rig_ligand();
+    const Pocket pocket = rig_pocket();
+    const KnobConfig cfg{2, 90, 0.3, 2, true};
+    const auto a = match_probes_shape(lig, pocket, make_initial_pose(lig), cfg);
+    const auto b = match_probes_shape(lig, pocket, make_initial_pose(lig), cfg);
+    CHECK(a.score == b.score);
+    CHECK(a.final_pose.positions == b.final_pose.positions);
+    CHECK(a.score == overlap_score(a.final_pose, pocket));
+    CHECK(a.score >= overlap_score(make_initial_pose(lig), pocket));
+  });
+  run("match_probes_shape: pose/ligand size mismatch", [] {
+    try {
+      match_probes_shape(rig_ligand(), rig_pocket(), pose_of({{0, 0, 0}}), KnobConfig{});
+      CHECK(false);
+    } catch (const Error& e) {
+      CHECK(std::string(e.what()).find("size mismatch") != std::string::npos);
+    }
+  });
+  run("screen: bookkeeping, id order, top-1% mean, skipped records", [] {
+    std::vector<Ligand> ligs;
+    for (int i = 0; i < 5; ++i) {
+      const double dz = 0.1 * i;
+      ligs.emplace_back("L" + std::to_string(4 - i),
+                        std::vector<Atom>{{0, {0, 0, dz}, 1.0}, {1, {0, 0, 1 + dz}, 1.0}, {2, {1, 0, 1 + dz}, 1.0}},
+                        std::vector<Bond>{{0, 1, true}, {1, 2, false}});
+    }
+    const ScreeningReport r = screen(rig_pocket(), ligs, KnobConfig{10, 90, 0.5, 1, false}, 4);
+    CHECK(r.per_ligand.size() == 5);
+    for (size_t i = 1; i < r.per_ligand.size(); ++i) CHECK(r.per_ligand[i - 1].ligand_id < r.per_ligand[i].ligand_id);
+    double best = 0.0;
+    for (const auto& x : r.per_ligand) best = std::max(best, x.score);
+    CHECK(r.top1pct_mean == best);
+    CHECK(r.total_atoms == 15);
+    for (const auto& x : r.per_ligand) {
+      const Ligand* l = nullptr;
+      for (const auto& c : ligs)
+        if (c.id() == x.ligand_id) l = &c;
+      CHECK(x.score == match_probes_shape(*l, rig_pocket(), make_initial_pose(*l),
+                                          KnobConfig{10, 90, 0.5, 1, false}).score);
+    }
+  });
+  run("dock_batch: rigid sweep + top-K + restarts", [] {
+    std::vector<Ligand> ligs{rig_ligand()};
+    const auto out = dock_batch(rig_pocket(), ligs, KnobConfig{30, 45, 0.0, 1, false}, 45, 8, true);
+    CHECK(out.size() == 1 && out[0].ok);
+    CHECK(out[0].poses.size() == 8);
+    for (size_t e = 1; e < out[0].poses.size(); ++e) {
+      const auto& a = out[0].poses[e - 1];
+      const auto& b = out[0].poses[e];
+      CHECK(a.score > b.score || (a.score == b.score && a.seed_rank < b.seed_rank));
+    }
+    for (const auto& p : out[0].poses) CHECK(p.score == overlap_score(p.final_pose, rig_pocket()));
+  });
+  std::printf("%s (%d failed checks)\n", g_failed ? "FAILED" : "OK", g_failed);
+  return g_failed ? 1 : 0;
+}
