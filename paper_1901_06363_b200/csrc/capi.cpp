@@ -7,11 +7,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "geodock_b200.h"
@@ -393,12 +395,31 @@ extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
   int32_t max_n = 1;
   int max_nfrag = 0;
   size_t far_words = 0, fmask_words = 0, nfrag_total = 0;
+  for (int l = 0; l < L; ++l)
+    if (b->atom_offsets[l + 1] < b->atom_offsets[l] || b->bond_offsets[l + 1] < b->bond_offsets[l])
+      return ctx->fail(GD_ERR_INVALID, "gd_upload: offsets not ascending");
+  // Ligand preprocessing is independent per ligand: spread it over the host
+  // cores (the reference's screen parallelises the same work per ligand).
+  {
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int nth = std::min(hw, std::max(1, L / 64));
+    std::atomic<int> next{0};
+    auto work = [&] {
+      for (int l; (l = next.fetch_add(16)) < L;)
+        for (int e = l; e < std::min(L, l + 16); ++e) {
+          const int a0 = b->atom_offsets[e], n = b->atom_offsets[e + 1] - a0;
+          const int b0 = b->bond_offsets[e], nb = b->bond_offsets[e + 1] - b0;
+          prep[e] = prepare_ligand(std::to_string(e), n, b->xyz + 3 * a0, b->radii + a0, nb,
+                                   b->bonds + 2 * b0, b->bond_rotatable + b0);
+        }
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nth; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+  }
   for (int l = 0; l < L; ++l) {
-    const int a0 = b->atom_offsets[l], n = b->atom_offsets[l + 1] - a0;
-    const int b0 = b->bond_offsets[l], nb = b->bond_offsets[l + 1] - b0;
-    if (n < 0 || nb < 0) return ctx->fail(GD_ERR_INVALID, "gd_upload: offsets not ascending");
-    prep[l] = prepare_ligand(std::to_string(l), n, b->xyz + 3 * a0, b->radii + a0, nb,
-                             b->bonds + 2 * b0, b->bond_rotatable + b0);
+    const int n = b->atom_offsets[l + 1] - b->atom_offsets[l];
     ctx->status_host[l] = prep[l].status;
     ctx->errors[l] = prep[l].error;
     if (prep[l].status != 0) continue;

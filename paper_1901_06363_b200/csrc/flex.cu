@@ -43,7 +43,7 @@ __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~si
 
 __host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pairs) {
   return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * kBatch * n) +
-         a16(2ull * max_pairs) + a16(n) + a16(32);
+         a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16);
 }
 
 struct WarpMem {
@@ -55,6 +55,7 @@ struct WarpMem {
   uint16_t* pairs;       // [max_pairs] surviving bump pairs: F-slot | j << 8
   uint8_t* fidx;         // [n] fragment atoms, ascending
   uint64_t* fm;          // [4] fragment membership bits
+  int* count;            // [1] surviving-pair counter
 };
 
 __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
@@ -75,6 +76,7 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   s.pairs = reinterpret_cast<uint16_t*>(take(2ull * max_pairs));
   s.fidx = reinterpret_cast<uint8_t*>(take(n));
   s.fm = reinterpret_cast<uint64_t*>(take(32));
+  s.count = reinterpret_cast<int*>(take(16));
   return s;
 }
 
@@ -265,27 +267,30 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         rad2[i] = fmax(0.0, vx * vx + vy * vy + vz * vz - a * a);
       }
       __syncwarp();
-      int np = 0;
-      for (int sl = 0; sl < nf; ++sl) {
+      // One lane per fragment atom walks its partner bits (far & ~F);
+      // survivors are appended in any order (the bump test is an OR).
+      if (lane == 0) *s.count = 0;
+      __syncwarp();
+      for (int sl = lane; sl < nf; sl += 32) {
         const int i = s.fidx[sl];
         const double ai = axc[i], r2 = rad2[i], ri = s.radius[i];
-        for (int b = 0; b < n; b += 32) {
-          const int j = b + lane;
-          bool keep = false;
-          if (j < n && (((s.far[i * W + (j >> 6)] & ~s.fm[j >> 6]) >> (j & 63)) & 1ull)) {
+        for (int w = 0; w < W; ++w) {
+          uint64_t bits = s.far[i * W + w] & ~s.fm[w];
+          while (bits) {
+            const int j = w * 64 + __ffsll(static_cast<long long>(bits)) - 1;
+            bits &= bits - 1;
             const double h = axc[j] - ai;
             const double s2 = rad2[j];
             const double cut = kBumpScale * (ri + s.radius[j]);
             const double C = cut * cut * (1.0 + 1e-6) + 1e-9;
             const double Lq = s2 + r2 + h * h - C;
-            keep = !(Lq > 0.0 && Lq * Lq > 4.0 * s2 * r2);
+            if (!(Lq > 0.0 && Lq * Lq > 4.0 * s2 * r2))
+              s.pairs[atomicAdd(s.count, 1)] = static_cast<uint16_t>(sl | (j << 8));
           }
-          const unsigned mask = __ballot_sync(kFull, keep);
-          if (keep) s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(sl | (j << 8));
-          np += __popc(mask);
         }
       }
       __syncwarp();
+      const int np = *s.count;
       // Non-fragment terms are the same for every candidate of this step:
       // pre-fill them into each candidate slot so the fold is a plain sum.
       for (int t = lane; t < kBatch * n; t += 32) {
