@@ -72,11 +72,13 @@ __device__ void publish(const Work<On>& w, unsigned long long* out, int base) {
 }
 
 // min_j distance_sq(q, P_j) over every pocket point (geometry.hpp:149-150).
-__device__ __noinline__ double min_dist_sq_brute(const PocketView& pk, double x, double y,
+// Out of line with plain arguments, so the rare call does not force the
+// kernel parameters into local memory.
+__device__ __noinline__ double min_dist_sq_brute(const double* pts, int P, double x, double y,
                                                  double z) {
   double m = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-  for (int j = 0; j < pk.P; ++j) {
-    const P3 p = ldp(pk.pts, j);
+  for (int j = 0; j < P; ++j) {
+    const P3 p = ldp(pts, j);
     m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
   }
   return m;
@@ -114,7 +116,7 @@ __device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, do
     }
   }
   w.add(kPairs, pk.P);
-  return min_dist_sq_brute(pk, x, y, z);
+  return min_dist_sq_brute(pk.pts, pk.P, x, y, z);
 }
 
 // Voxel lookup half of a query: the candidate list of the first grid level
@@ -168,11 +170,11 @@ __device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, do
   }
   if (a.pts == nullptr) {
     w.add(kPairs, pk.P);
-    m0 = min_dist_sq_brute(pk, x0, y0, z0);
+    m0 = min_dist_sq_brute(pk.pts, pk.P, x0, y0, z0);
   }
   if (b.pts == nullptr) {
     w.add(kPairs, pk.P);
-    m1 = min_dist_sq_brute(pk, x1, y1, z1);
+    m1 = min_dist_sq_brute(pk.pts, pk.P, x1, y1, z1);
   }
 }
 

@@ -35,8 +35,11 @@ namespace {
 #ifndef GD_FLEX_MINB
 #define GD_FLEX_MINB 6       // resident CTAs per SM the register budget targets
 #endif
+#ifndef GD_FLEX_BATCH
+#define GD_FLEX_BATCH 4      // candidates evaluated together by one warp
+#endif
 constexpr int kWarps = 4;    // chains per CTA
-constexpr int kBatch = 4;    // candidates evaluated together by one warp
+constexpr int kBatch = GD_FLEX_BATCH;
 constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -84,6 +87,13 @@ __device__ __forceinline__ bool in_frag(const uint64_t* fm, int i) {
   return (fm[i >> 6] >> (i & 63)) & 1ull;
 }
 
+// floor(t / d) for 0 <= t < 2^16, 1 <= d <= 256 via an fp32 reciprocal:
+// (2t+1)/(2d) is never within 1/(2d) >= 2e-3 of an integer, far beyond the
+// ~1e-4 fp32 error at these magnitudes, so truncation is exact.
+__device__ __forceinline__ int qdiv(int t, float rcp) {
+  return static_cast<int>((static_cast<float>(t) + 0.5f) * rcp);
+}
+
 // Evaluates candidates angle(c) = a0 + c*da, c < nb, of the current fragment
 // (CandidateEvaluator::evaluate, kernel.hpp:100-112).  Returns, in lane c,
 // candidate c's overlap score (cur for angle 0), and warp-uniformly the
@@ -96,8 +106,9 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
   // Bump phase.
   unsigned bl = 0;
   const int total = nb * np;
+  const float rnp = 1.0f / static_cast<float>(max(np, 1));
   for (int t = lane; t < total; t += 32) {
-    const int c = t / np;
+    const int c = qdiv(t, rnp);
     if (((bl | zero) >> c) & 1u) continue;
     const int pr = s.pairs[t - c * np];
     const int i = s.fidx[pr & 0xff], j = pr >> 8;
@@ -115,10 +126,11 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
   // Query phase.
   // Two items per lane per iteration (t, t+32): both lookups in flight.
   const int tq = nb * nf;
+  const float rnf = 1.0f / static_cast<float>(nf);
   for (int t = lane; t < tq; t += 64) {
-    const int c0 = t / nf;
+    const int c0 = qdiv(t, rnf);
     const int t1 = t + 32 < tq ? t + 32 : t;
-    const int c1 = t1 / nf;
+    const int c1 = qdiv(t1, rnf);
     const bool l0 = (live >> c0) & 1u, l1 = t1 != t && ((live >> c1) & 1u);
     if (!l0 && !l1) continue;
     const int i0 = s.fidx[t - c0 * nf], i1 = s.fidx[t1 - c1 * nf];
@@ -267,36 +279,39 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         rad2[i] = fmax(0.0, vx * vx + vy * vy + vz * vz - a * a);
       }
       __syncwarp();
-      // One lane per fragment atom walks its partner bits (far & ~F);
-      // survivors are appended in any order (the bump test is an OR).
-      if (lane == 0) *s.count = 0;
-      __syncwarp();
-      for (int sl = lane; sl < nf; sl += 32) {
+      int np = 0;
+      for (int sl = 0; sl < nf; ++sl) {
         const int i = s.fidx[sl];
         const double ai = axc[i], r2 = rad2[i], ri = s.radius[i];
-        for (int w = 0; w < W; ++w) {
-          uint64_t bits = s.far[i * W + w] & ~s.fm[w];
-          while (bits) {
-            const int j = w * 64 + __ffsll(static_cast<long long>(bits)) - 1;
-            bits &= bits - 1;
+        for (int b = 0; b < n; b += 32) {
+          // Partner bits of this 32-atom chunk; uniform skip when empty.
+          const unsigned chunk = static_cast<unsigned>(
+              (s.far[i * W + (b >> 6)] & ~s.fm[b >> 6]) >> (b & 63));
+          if (chunk == 0u) continue;
+          const int j = b + lane;
+          bool keep = false;
+          if (j < n && ((chunk >> lane) & 1u)) {
             const double h = axc[j] - ai;
             const double s2 = rad2[j];
             const double cut = kBumpScale * (ri + s.radius[j]);
             const double C = cut * cut * (1.0 + 1e-6) + 1e-9;
             const double Lq = s2 + r2 + h * h - C;
-            if (!(Lq > 0.0 && Lq * Lq > 4.0 * s2 * r2))
-              s.pairs[atomicAdd(s.count, 1)] = static_cast<uint16_t>(sl | (j << 8));
+            keep = !(Lq > 0.0 && Lq * Lq > 4.0 * s2 * r2);
           }
+          const unsigned mask = __ballot_sync(kFull, keep);
+          if (keep) s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(sl | (j << 8));
+          np += __popc(mask);
         }
       }
       __syncwarp();
-      const int np = *s.count;
       // Non-fragment terms are the same for every candidate of this step:
       // pre-fill them into each candidate slot so the fold is a plain sum.
-      for (int t = lane; t < kBatch * n; t += 32) {
-        const int i = t % n;
-        if (!in_frag(s.fm, i)) s.v[t] = s.term[i];
-      }
+      for (int i = lane; i < n; i += 32)
+        if (!in_frag(s.fm, i)) {
+          const double t = s.term[i];
+#pragma unroll
+          for (int c = 0; c < kBatch; ++c) s.v[c * n + i] = t;
+        }
       __syncwarp();
 
       int best_a = 0;
