@@ -326,30 +326,35 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     GD_CUDA(ctx, cudaMemcpyAsync(cnt.data(), counts.ptr, sizeof(int32_t) * nv,
                                  cudaMemcpyDeviceToHost, ctx->stream));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    std::vector<int32_t> off(nv + 1, 0);
-    int64_t total = 0;
+    // Each voxel's first candidate lives in its 32-byte record; the list
+    // holds candidates 2..count, offsets = exclusive scan of (count - 1).
+    std::vector<int32_t> off(nv, 0);
+    int64_t total = 0, listed = 0;
     int32_t mx = 0;
     for (int c = 0; c < nv; ++c) {
-      off[c] = static_cast<int32_t>(total);
+      off[c] = static_cast<int32_t>(listed);
+      listed += cnt[c] - 1;
       total += cnt[c];
       mx = std::max(mx, cnt[c]);
-      if (total > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
+      if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
     }
-    off[nv] = static_cast<int32_t>(total);
-    GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(int32_t) * (nv + 1)));
-    GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(total, 1)));
-    GD_CUDA(ctx, cudaMemcpyAsync(ctx->vox_off[L].ptr, off.data(), sizeof(int32_t) * (nv + 1),
-                                 cudaMemcpyHostToDevice, ctx->stream));
+    DevBuf doff;
+    GD_CUDA(ctx, doff.ensure(sizeof(int32_t) * nv));
+    GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(double) * 4 * static_cast<size_t>(nv)));
+    GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
+    GD_CUDA(ctx, cudaMemcpyAsync(doff.ptr, off.data(), sizeof(int32_t) * nv, cudaMemcpyHostToDevice,
+                                 ctx->stream));
     GD_CUDA(ctx, static_cast<cudaError_t>(
-                     launch_voxel_fill(ctx->pts.as<double>(), n, g, ctx->vox_off[L].as<int32_t>(),
-                                       ctx->vox_pts[L].as<double>(), ctx->stream)));
+                     launch_voxel_fill(ctx->pts.as<double>(), n, g, doff.as<int32_t>(),
+                                       ctx->vox_off[L].as<double>(), ctx->vox_pts[L].as<double>(),
+                                       ctx->stream)));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->grid[L] = g;
     ctx->n_cand += total;
     ctx->max_cand = std::max(ctx->max_cand, mx);
     GridLevel& gl = v.lv[L];
-    gl.off = ctx->vox_off[L].as<int32_t>();
-    gl.pts = ctx->vox_pts[L].as<double>();
+    gl.rec = ctx->vox_off[L].as<double>();
+    gl.lst = ctx->vox_pts[L].as<double>();
     gl.lo_x = g.lo_x;
     gl.lo_y = g.lo_y;
     gl.lo_z = g.lo_z;

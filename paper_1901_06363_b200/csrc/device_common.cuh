@@ -35,14 +35,21 @@ __device__ __forceinline__ double dist_sq(double ax, double ay, double az, doubl
   return dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
 }
 
-// 32-byte point record (x, y, z, pad) through the read-only path.
+// One 256-bit read-only load (LDG.256 on sm_100a) of a 32-byte record.
+__device__ __forceinline__ void ld256(const double* p, double& a, double& b, double& c, double& d) {
+  asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+      : "l"(p));
+}
+
+// 32-byte point record (x, y, z, pad).
 struct P3 {
   double x, y, z;
 };
 __device__ __forceinline__ P3 ldp(const double* base, int j) {
-  const double2 a = __ldg(reinterpret_cast<const double2*>(base) + 2 * j);
-  const double b = __ldg(base + 4 * j + 2);
-  return P3{a.x, a.y, b};
+  double x, y, z, w;
+  ld256(base + 4 * static_cast<size_t>(j), x, y, z, w);
+  return P3{x, y, z};
 }
 
 // Executed-work counters (exact; DESIGN.md §4 turns them into fp64 FLOPs).
@@ -90,40 +97,12 @@ __device__ __noinline__ double min_dist_sq_brute(const double* pts, int P, doubl
 // reference's PocketIndex makes the same exactness argument,
 // geometry.hpp:45-46).  Fine level first, then the coarse far-field level;
 // queries beyond both fall back to the full scan.
-template <bool On>
-__device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, double y, double z,
-                                              Work<On>& w) {
-  w.add(kQuery, 1);
-  if (pk.use_index) {
-#pragma unroll
-    for (int L = 0; L < kGridLevels; ++L) {
-      const GridLevel& g = pk.lv[L];
-      const double fx = (x - g.lo_x) * g.inv_h;
-      const double fy = (y - g.lo_y) * g.inv_h;
-      const double fz = (z - g.lo_z) * g.inv_h;
-      if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
-        const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
-                      static_cast<int>(fz);
-        const int s = __ldg(g.off + v), e = __ldg(g.off + v + 1);
-        w.add(kPairs, e - s);
-        double m = __longlong_as_double(0x7ff0000000000000ll);
-        for (int k = s; k < e; ++k) {
-          const P3 p = ldp(g.pts, k);
-          m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
-        }
-        return m;
-      }
-    }
-  }
-  w.add(kPairs, pk.P);
-  return min_dist_sq_brute(pk.pts, pk.P, x, y, z);
-}
-
-// Voxel lookup half of a query: the candidate list of the first grid level
-// containing q, or (nullptr, 0, 0) for the full-scan fallback.
+// Voxel lookup: one 256-bit load of the record of the first grid level
+// containing q; lst == nullptr means the full-scan fallback.
 struct Loc {
-  const double* pts;
-  int s, e;
+  const double* lst;  // further candidates (start already applied)
+  int count;          // candidates in the voxel (>= 1)
+  double x0, y0, z0;  // the inline first candidate
 };
 __device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, double z) {
   if (pk.use_index) {
@@ -136,15 +115,39 @@ __device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, 
       if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
         const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
                       static_cast<int>(fz);
-        return Loc{g.pts, __ldg(g.off + v), __ldg(g.off + v + 1)};
+        double hdr;
+        Loc l;
+        ld256(g.rec + 4 * static_cast<size_t>(v), hdr, l.x0, l.y0, l.z0);
+        const long long h = __double_as_longlong(hdr);
+        l.count = static_cast<int>(h >> 32);
+        l.lst = g.lst + 4 * static_cast<size_t>(static_cast<unsigned>(h & 0xffffffffll));
+        return l;
       }
     }
   }
-  return Loc{nullptr, 0, 0};
+  return Loc{nullptr, 0, 0.0, 0.0, 0.0};
 }
 
-// Two independent queries with both lookups issued before either scan and
-// the two candidate scans interleaved (memory-level parallelism 2).
+template <bool On>
+__device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, double y, double z,
+                                              Work<On>& w) {
+  w.add(kQuery, 1);
+  const Loc a = locate(pk, x, y, z);
+  if (a.lst == nullptr) {
+    w.add(kPairs, pk.P);
+    return min_dist_sq_brute(pk.pts, pk.P, x, y, z);
+  }
+  w.add(kPairs, a.count);
+  double m = dist_sq(x, y, z, a.x0, a.y0, a.z0);
+  for (int k = 0; k < a.count - 1; ++k) {
+    const P3 p = ldp(a.lst, k);
+    m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+  }
+  return m;
+}
+
+// Two independent queries with both record loads issued before either scan
+// and the two candidate scans interleaved (memory-level parallelism 2).
 template <bool On>
 __device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, double y0, double z0,
                                              double x1, double y1, double z1, double& m0,
@@ -152,27 +155,26 @@ __device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, do
   w.add(kQuery, 2);
   const Loc a = locate(pk, x0, y0, z0);
   const Loc b = locate(pk, x1, y1, z1);
-  const double inf = __longlong_as_double(0x7ff0000000000000ll);
-  m0 = inf;
-  m1 = inf;
-  const int na = a.pts ? a.e - a.s : 0, nb = b.pts ? b.e - b.s : 0;
-  w.add(kPairs, na + nb);
+  const int na = a.lst ? a.count - 1 : 0, nb = b.lst ? b.count - 1 : 0;
+  w.add(kPairs, (a.lst ? a.count : 0) + (b.lst ? b.count : 0));
+  m0 = dist_sq(x0, y0, z0, a.x0, a.y0, a.z0);
+  m1 = dist_sq(x1, y1, z1, b.x0, b.y0, b.z0);
   const int nmax = max(na, nb);
   for (int k = 0; k < nmax; ++k) {
     if (k < na) {
-      const P3 p = ldp(a.pts, a.s + k);
+      const P3 p = ldp(a.lst, k);
       m0 = fmin(m0, dist_sq(x0, y0, z0, p.x, p.y, p.z));
     }
     if (k < nb) {
-      const P3 p = ldp(b.pts, b.s + k);
+      const P3 p = ldp(b.lst, k);
       m1 = fmin(m1, dist_sq(x1, y1, z1, p.x, p.y, p.z));
     }
   }
-  if (a.pts == nullptr) {
+  if (a.lst == nullptr) {
     w.add(kPairs, pk.P);
     m0 = min_dist_sq_brute(pk.pts, pk.P, x0, y0, z0);
   }
-  if (b.pts == nullptr) {
+  if (b.lst == nullptr) {
     w.add(kPairs, pk.P);
     m1 = min_dist_sq_brute(pk.pts, pk.P, x1, y1, z1);
   }

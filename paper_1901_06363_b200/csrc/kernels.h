@@ -18,10 +18,13 @@ struct LigMeta {
   int32_t status;     // GD_LIG_*
 };
 
-// One level of the exact voxel candidate-list index.
+// One level of the exact voxel candidate-list index.  Voxel v's 32-byte
+// record (one 256-bit load) is {int32 start, int32 count, x0, y0, z0}: the
+// first candidate inline, candidates 2..count at lst[start..start+count-1)
+// as 32-byte (x, y, z, pad) records.
 struct GridLevel {
-  const int32_t* off;      // [nvox+1] candidate-list offsets
-  const double* pts;       // [ncand*4] candidate coordinates, voxel-major
+  const double* rec;       // [nvox*4] voxel records
+  const double* lst;       // [(ncand-nvox)*4] further candidates, voxel-major
   double lo_x, lo_y, lo_z; // grid origin
   double inv_h;            // 1 / voxel edge
   int32_t dim_x, dim_y, dim_z;
@@ -117,8 +120,11 @@ struct VoxelGrid {
   double lo_x, lo_y, lo_z, h;
   int32_t dim_x, dim_y, dim_z;
 };
+// counts[v] = candidates of voxel v (>= 1); the fill pass writes each
+// voxel's record and its candidates 2..count at the host-scanned list
+// offsets (sum over earlier voxels of count - 1).
 int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, void* stream);
-int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets,
-                      double* vox_pts, void* stream);
+int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
+                      double* lst, void* stream);
 
 }  // namespace gdb200

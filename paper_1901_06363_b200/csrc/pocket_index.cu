@@ -112,16 +112,22 @@ __global__ void voxel_count_kernel(const double* pts, int P, VoxelGrid g, int32_
 }
 
 __global__ void voxel_fill_kernel(const double* pts, int P, VoxelGrid g, const int32_t* offsets,
-                                  double* vox_pts) {
+                                  double* rec, double* lst) {
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   const int nv = g.dim_x * g.dim_y * g.dim_z;
   if (v >= nv) return;
   int cand[kVoxMaxCand];
   const int k = voxel_list(pts, P, g, v, cand);
-  double* out = vox_pts + 4 * static_cast<size_t>(offsets[v]);
-  for (int a = 0; a < (k < 0 ? P : k); ++a) {
+  const int len = k < 0 ? P : k;  // >= 1: the nearest point always survives
+  const int start = offsets[v];
+  double* r = rec + 4 * static_cast<size_t>(v);
+  reinterpret_cast<int2*>(r)[0] = make_int2(start, len);
+  const int j0 = k < 0 ? 0 : cand[0];
+  for (int c = 0; c < 3; ++c) r[1 + c] = pts[4 * j0 + c];
+  double* out = lst + 4 * static_cast<size_t>(start);
+  for (int a = 1; a < len; ++a) {
     const int j = k < 0 ? a : cand[a];
-    for (int c = 0; c < 4; ++c) out[4 * a + c] = pts[4 * j + c];
+    for (int c = 0; c < 4; ++c) out[4 * (a - 1) + c] = pts[4 * j + c];
   }
 }
 
@@ -166,12 +172,12 @@ int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, v
   return cudaGetLastError();
 }
 
-int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets,
-                      double* vox_pts, void* stream) {
+int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
+                      double* lst, void* stream) {
   const int nv = g.dim_x * g.dim_y * g.dim_z;
   const int bt = 128;
   voxel_fill_kernel<<<(nv + bt - 1) / bt, bt, 0, static_cast<cudaStream_t>(stream)>>>(
-      pts, P, g, offsets, vox_pts);
+      pts, P, g, offsets, rec, lst);
   return cudaGetLastError();
 }
 
