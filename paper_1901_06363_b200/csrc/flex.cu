@@ -111,7 +111,7 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
     const int c = qdiv(t, rnp);
     if (((bl | zero) >> c) & 1u) continue;
     const int pr = s.pairs[t - c * np];
-    const int i = s.fidx[pr & 0xff], j = pr >> 8;
+    const int i = pr & 0xff, j = pr >> 8;
     const int a = a0 + c * da;
     const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
     double qx, qy, qz;
@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
   cur = __shfl_sync(kFull, cur, 0);
   if (!p.rigid && lane == 0) p.seed_score[e] = cur;
   long long evals = 1, checks = 1;
+  int left_np = -1;  // bump-pair count of the preceding left step, -1 if none
 
   for (int rep = 0; rep < p.reps; ++rep) {
     for (int f = 0; f < m.nfrag; ++f) {
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       if (!refined && A == 1) {  // step 360: only the committed pose
         checks += 1;
         evals += 1;
+        left_np = -1;
         continue;
       }
       if (lane < W) s.fm[lane] = __ldg(p.frag_mask + m.fmask_off + f * W + lane);
@@ -270,40 +272,59 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       // tested without square roots as L = s2 + r2 + h2 - C > 0 && L^2 > 4 s2 r2.
       // Per-atom axial coordinate a = k.(p - o) and squared axis distance
       // r2 = |p - o|^2 - a^2 first, lane-parallel, in the (free) v scratch.
-      double* axc = s.v;
-      double* rad2 = s.v + n;
-      for (int i = lane; i < n; i += 32) {
-        const double vx = s.px[i] - ox, vy = s.py[i] - oy, vz = s.pz[i] - oz;
-        const double a = X.kx * vx + X.ky * vy + X.kz * vz;
-        axc[i] = a;
-        rad2[i] = fmax(0.0, vx * vx + vy * vy + vz * vz - a * a);
-      }
-      __syncwarp();
+      // The pair list holds (moving atom | fixed atom << 8).  A rotamer's
+      // right step reuses its left step's list with the roles swapped: both
+      // rotate about the same bond line, the left commit rotated the left
+      // atoms about that very line, and the circle test depends only on the
+      // atoms' axial and radial coordinates relative to it (rotation
+      // invariants).  The test itself is a conservative filter, so it runs
+      // in fp32 with a wide margin; the kept pairs are decided exactly.
       int np = 0;
-      for (int sl = 0; sl < nf; ++sl) {
-        const int i = s.fidx[sl];
-        const double ai = axc[i], r2 = rad2[i], ri = s.radius[i];
-        for (int b = 0; b < n; b += 32) {
-          // Partner bits of this 32-atom chunk; uniform skip when empty.
-          const unsigned chunk = static_cast<unsigned>(
-              (s.far[i * W + (b >> 6)] & ~s.fm[b >> 6]) >> (b & 63));
-          if (chunk == 0u) continue;
-          const int j = b + lane;
-          bool keep = false;
-          if (j < n && ((chunk >> lane) & 1u)) {
-            const double h = axc[j] - ai;
-            const double s2 = rad2[j];
-            const double cut = kBumpScale * (ri + s.radius[j]);
-            const double C = cut * cut * (1.0 + 1e-6) + 1e-9;
-            const double Lq = s2 + r2 + h * h - C;
-            keep = !(Lq > 0.0 && Lq * Lq > 4.0 * s2 * r2);
+      if ((f & 1) && left_np >= 0) {
+        np = left_np;
+        for (int t = lane; t < np; t += 32) {
+          const unsigned pr = s.pairs[t];
+          s.pairs[t] = static_cast<uint16_t>((pr >> 8) | ((pr & 0xffu) << 8));
+        }
+      } else {
+        float* axc = reinterpret_cast<float*>(s.v);
+        float* rad2 = axc + n;
+        float* rf = rad2 + n;
+        for (int i = lane; i < n; i += 32) {
+          const double vx = s.px[i] - ox, vy = s.py[i] - oy, vz = s.pz[i] - oz;
+          const double a = X.kx * vx + X.ky * vy + X.kz * vz;
+          axc[i] = static_cast<float>(a);
+          rad2[i] = static_cast<float>(fmax(0.0, vx * vx + vy * vy + vz * vz - a * a));
+          rf[i] = static_cast<float>(s.radius[i]);
+        }
+        __syncwarp();
+        for (int sl = 0; sl < nf; ++sl) {
+          const int i = s.fidx[sl];
+          const float ai = axc[i], r2 = rad2[i], ri = rf[i];
+          for (int b = 0; b < n; b += 32) {
+            // Partner bits of this 32-atom chunk; uniform skip when empty.
+            const unsigned chunk = static_cast<unsigned>(
+                (s.far[i * W + (b >> 6)] & ~s.fm[b >> 6]) >> (b & 63));
+            if (chunk == 0u) continue;
+            const int j = b + lane;
+            bool keep = false;
+            if (j < n && ((chunk >> lane) & 1u)) {
+              const float h = axc[j] - ai;
+              const float s2 = rad2[j];
+              const float cut = 0.8f * (ri + rf[j]);
+              const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
+              const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
+              keep = !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
+            }
+            const unsigned mask = __ballot_sync(kFull, keep);
+            if (keep)
+              s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
+            np += __popc(mask);
           }
-          const unsigned mask = __ballot_sync(kFull, keep);
-          if (keep) s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(sl | (j << 8));
-          np += __popc(mask);
         }
       }
       __syncwarp();
+      left_np = (f & 1) ? -1 : np;  // a left step's list serves its right step
       // Non-fragment terms are the same for every candidate of this step:
       // pre-fill them into each candidate slot so the fold is a plain sum.
       for (int i = lane; i < n; i += 32)
