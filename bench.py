@@ -6,7 +6,8 @@ rank's shard goes through the rigid sweep, top-K selection, K restart
 chains of fragment optimisation, and the final ordering (E1-E8).
 
 * ``value``: device-resident throughput -- descriptors already in HBM, CUDA
-  events around the two kernels of each step, L2 flushed between steps.
+  events around each step's kernels (and, for N > 1, the NCCL top-K gather),
+  L2 flushed between steps.
 * ``e2e``: the same metric through the public C-ABI call (gd_dock_batch)
   with host buffers: host preprocessing, pinned H2D, kernels, D2H.
 * ``--impl reference``: the reference's own CPU path (oracle/_ref: the
@@ -14,7 +15,8 @@ chains of fragment optimisation, and the final ordering (E1-E8).
   threads) on a bounded sample of the same workload.
 
 Multi-GPU (torchrun): ligands are sharded by id (weak scaling: every rank
-docks its own 10,000); per-ligand top-K results are all-gathered over NCCL.
+docks its own seeded 10,000); each step all-gathers every rank's per-ligand
+top-K table over NCCL from device memory.
 """
 from __future__ import annotations
 
@@ -107,7 +109,7 @@ def flops_of(work: dict) -> float:
 
 
 def cpu_reference(batch, pocket, knobs, n: int):
-    """The reference CPU path on the first n ligands: (ligands/s, dict)."""
+    """The reference CPU path on the first n ligands: (ligands/s, info)."""
     from oracle import oracle_py as O
     sub = batch.subset(range(min(n, batch.n_ligands)))
     threads = O.threads()
@@ -137,11 +139,10 @@ def run_reference(a):
     batch = w.ligands(range(n), pocket.mean(axis=0))
     for _ in range(a.warmup):
         cpu_reference(batch, pocket, w.knobs, n)
-    rates, info = [], None
+    info = None
     t0 = time.perf_counter()
     for _ in range(a.steps):
-        r, info = cpu_reference(batch, pocket, w.knobs, n)
-        rates.append(r)
+        _, info = cpu_reference(batch, pocket, w.knobs, n)
     wall = time.perf_counter() - t0
     value = n * a.steps / wall
     line = {
@@ -162,17 +163,18 @@ def run_ours(a):
     import torch
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
+    dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1901_06363_b200 import Docker, Knobs, workloads as W
     from paper_1901_06363_b200.native import DockResult, GD_FLAG_COUNT_WORK
+    from paper_1901_06363_b200.sharding import DeviceGather, shard_ids
 
     w = W.config(a.config)
     pocket = w.pocket()
     n_per = a.ligands or w.n_ligands
-    ids = range(rank * n_per, (rank + 1) * n_per)
-    batch = w.ligands(ids, pocket.mean(axis=0))
+    batch = w.ligands(shard_ids(rank, world, n_per, "weak"), pocket.mean(axis=0))
     knobs = w.knobs
     K = knobs.slots
 
@@ -188,27 +190,19 @@ def run_ours(a):
     work = d.work_counters()
     fp64_peak = d.fp64_peak_tflops()
 
+    d.dock_resident(knobs)
+    gather = DeviceGather(d.device_results(), world) if world > 1 else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    res = DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False)
-    gather_bufs = None
 
-    def gather_results():
-        # Top-K gather: every rank's (final score, orientation) to every rank.
-        nonlocal gather_bufs
-        if world == 1:
-            return
-        import torch.distributed as dist
-        d.download(res)
-        fs = torch.from_numpy(res.final_score.reshape(-1)).cuda()
-        if gather_bufs is None:
-            gather_bufs = torch.empty(world * fs.numel(), dtype=fs.dtype, device="cuda")
-        dist.all_gather_into_tensor(gather_bufs, fs)
+    def step():
+        d.dock_resident(knobs)
+        if gather is not None:
+            gather()  # NCCL all-gather of every rank's top-K table
 
     for _ in range(a.warmup):
-        d.dock_resident(knobs)
+        step()
     rigid_ms, flex_ms, step_ms = [], [], []
-    if world > 1:
-        import torch.distributed as dist
+    if dist:
         dist.barrier()
     torch.cuda.synchronize()
     clocks = Clocks(local)
@@ -217,7 +211,7 @@ def run_ours(a):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        d.dock_resident(knobs)
+        step()
         e1.record(stream)
         e1.synchronize()
         t = d.timing()
@@ -225,22 +219,23 @@ def run_ours(a):
         flex_ms.append(t["flex_ms"])
         step_ms.append(e0.elapsed_time(e1))
     torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
     clk = clocks.stop()
     total_ms = float(sum(step_ms))
-    if world > 1:
-        import torch.distributed as dist
+    if dist:
         tt = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
-        gather_results()
-        dist.barrier()
     ms_per_step = total_ms / a.steps
     value = world * batch.n_ligands / (ms_per_step / 1e3)
 
-    d.download(DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False))
-    res_scored = DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False)
-    d.download(res_scored)
-    poses_per_step = float(res_scored.poses_scored.sum()) * world
+    res = d.download(DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False))
+    poses_per_step = float(res.poses_scored.sum())
+    if dist:
+        ps = torch.tensor([poses_per_step], device="cuda", dtype=torch.float64)
+        dist.all_reduce(ps)
+        poses_per_step = float(ps.item())
     poses_per_s = poses_per_step / (ms_per_step / 1e3)
 
     # e2e: host buffers through gd_dock_batch (prep + pinned H2D + kernels + D2H).
@@ -252,12 +247,13 @@ def run_ours(a):
         for _ in range(e2e_steps):
             flush.zero_()
             torch.cuda.synchronize()
+            if dist:
+                dist.barrier()
             t0 = time.perf_counter()
             d.dock(batch, knobs)
             tms.append(time.perf_counter() - t0)
         tt = float(np.mean(tms))
-        if world > 1:
-            import torch.distributed as dist
+        if dist:
             x = torch.tensor([tt], device="cuda", dtype=torch.float64)
             dist.all_reduce(x, op=dist.ReduceOp.MAX)
             tt = float(x.item())
@@ -267,42 +263,46 @@ def run_ours(a):
                "d2h_bytes_per_step": int(tim["d2h_bytes"]), "ms_per_step": 1e3 * tt,
                "steps": e2e_steps, "timer": "host wall clock around gd_dock_batch"}
 
-    if rank != 0:
-        return
-    # Roofline of the dominant kernel: fp64 FLOPs it executed / its time.
-    r_ms, f_ms = float(np.mean(rigid_ms)), float(np.mean(flex_ms))
-    dom = "flex_kernel" if f_ms >= r_ms else "rigid_topk_kernel"
-    dom_work = work["flex" if dom == "flex_kernel" else "rigid"]
-    dom_ms = max(r_ms, f_ms)
-    achieved = flops_of(dom_work) / (dom_ms / 1e3) / 1e12
-    line = {
-        "metric": METRIC, "value": value, "unit": "ligands/s", "n_gpus": world,
-        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded BASELINE generators, DESIGN.md §5)",
-        "config": {"workload": w.name, "ligands_per_gpu": batch.n_ligands,
-                   "pocket_points": len(pocket), "rigid_step": knobs.rigid_step,
-                   "fragment_step": knobs.high_precision_step, "restarts": knobs.repetitions,
-                   "top_k": knobs.top_k, "parallelism": f"ligand-sharded x{world}",
-                   "l2": "flushed between steps (256 MiB write, untimed)",
-                   "voxel_index": {k: (v.tolist() if hasattr(v, "tolist") else v)
-                                   for k, v in info.items()}},
-        "poses_scored_per_s": poses_per_s,
-        "kernel_ms": {"rigid_topk_kernel": r_ms, "flex_kernel": f_ms},
-        "gpu_launches": 2 * a.steps,
-        "roofline": {"kernel": dom, "bound": "fp64", "achieved": achieved, "peak": fp64_peak,
-                     "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": None,
-                     "peak_source": "measured fp64 DADD/DMUL probe (gd_fp64_peak) on this GPU",
-                     "work_per_launch": dom_work},
-        "clocks": clk,
-    }
-    if e2e:
-        line["e2e"] = e2e
-    if world == 1 and not a.no_cpu_baseline:
-        v, inf = cpu_reference(batch, pocket, knobs, CPU_SAMPLE)
-        line["cpu_baseline"] = {"value": v, "unit": "ligands/s", "cores": inf["cores"],
-                                "kind": inf["kind"], "sample": inf["sample"]}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        r_ms, f_ms = float(np.mean(rigid_ms)), float(np.mean(flex_ms))
+        dom = "flex_chain_kernel" if f_ms >= r_ms else "rigid_topk_kernel"
+        dom_work = work["flex" if dom == "flex_chain_kernel" else "rigid"]
+        dom_ms = max(r_ms, f_ms)
+        achieved = flops_of(dom_work) / (dom_ms / 1e3) / 1e12
+        line = {
+            "metric": METRIC, "value": value, "unit": "ligands/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE generators, DESIGN.md §5)",
+            "config": {"workload": w.name, "ligands_per_gpu": batch.n_ligands,
+                       "pocket_points": len(pocket), "rigid_step": knobs.rigid_step,
+                       "fragment_step": knobs.high_precision_step,
+                       "restarts": knobs.repetitions, "top_k": knobs.top_k,
+                       "parallelism": f"ligand-sharded x{world}" + (", NCCL top-K all-gather per step"
+                                                                    if world > 1 else ""),
+                       "l2": "flushed between steps (256 MiB write, untimed)",
+                       "voxel_index": {k: (v.tolist() if hasattr(v, "tolist") else v)
+                                       for k, v in info.items()}},
+            "poses_scored_per_s": poses_per_s,
+            "kernel_ms": {"rigid_topk_kernel": r_ms, "flex_chain_kernel+finalize": f_ms},
+            "gpu_launches": 3 * a.steps,
+            "roofline": {"kernel": dom, "bound": "fp64", "achieved": achieved,
+                         "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                         "traffic": None,
+                         "peak_source": "measured fp64 DADD/DMUL probe (gd_fp64_peak) on this GPU",
+                         "work_per_launch": dom_work},
+            "clocks": clk,
+        }
+        if e2e:
+            line["e2e"] = e2e
+        if world == 1 and not a.no_cpu_baseline:
+            v, inf = cpu_reference(batch, pocket, knobs, CPU_SAMPLE)
+            line["cpu_baseline"] = {"value": v, "unit": "ligands/s", "cores": inf["cores"],
+                                    "kind": inf["kind"], "sample": inf["sample"]}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -141,6 +141,19 @@ int gd_upload(gd_ctx* ctx, const gd_ligand_batch* batch);
 int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs);
 int gd_download(gd_ctx* ctx, gd_result* result);
 int gd_last_timing(const gd_ctx* ctx, gd_timing* out);
+
+/* Device-resident results of the last gd_dock_resident (valid until the
+ * next dock call): [n_ligands*top_k] in final order.  Lets a multi-GPU host
+ * gather per-ligand top-K tables over NCCL without a host round trip. */
+typedef struct {
+  const int32_t* orientation;
+  const int32_t* seed_rank;
+  const double* final_score;
+  const int64_t* evaluations;
+  int32_t n_ligands;
+  int32_t top_k;
+} gd_device_result;
+int gd_device_results(const gd_ctx* ctx, gd_device_result* out);
 /* Exact work executed by the last call made with GD_FLAG_COUNT_WORK:
  * out[0..6] rigid kernel, out[8..14] flex kernel, each {point pairs, rotated
  * atoms, bump pairs, nearest-point queries, score-sum terms, candidate

@@ -741,6 +741,17 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   return GD_OK;
 }
 
+extern "C" int gd_device_results(const gd_ctx* ctx, gd_device_result* out) {
+  if (ctx == nullptr || out == nullptr || !ctx->have_result) return GD_ERR_INVALID;
+  out->orientation = ctx->o_orient.as<int32_t>();
+  out->seed_rank = ctx->o_rank.as<int32_t>();
+  out->final_score = ctx->o_final.as<double>();
+  out->evaluations = ctx->o_evals.as<int64_t>();
+  out->n_ligands = ctx->n_lig;
+  out->top_k = ctx->last_topk;
+  return GD_OK;
+}
+
 extern "C" int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]) {
   if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
   if (!ctx->counted) return GD_ERR_INVALID;

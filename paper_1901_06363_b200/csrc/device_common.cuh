@@ -180,6 +180,42 @@ __device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, do
   }
 }
 
+// M independent queries: all M record loads in flight before any scan, the
+// M candidate scans interleaved (memory-level parallelism M).
+template <int M, bool On>
+__device__ __forceinline__ void min_dist_sqM(const PocketView& pk, const double* x, const double* y,
+                                             const double* z, double* m, Work<On>& w) {
+  w.add(kQuery, M);
+  Loc a[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) a[r] = locate(pk, x[r], y[r], z[r]);
+  int nmax = 0;
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    m[r] = dist_sq(x[r], y[r], z[r], a[r].x0, a[r].y0, a[r].z0);
+    if (a[r].lst) {
+      nmax = max(nmax, a[r].count - 1);
+      w.add(kPairs, a[r].count);
+    }
+  }
+  for (int k = 0; k < nmax; ++k) {
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      if (a[r].lst && k < a[r].count - 1) {
+        const P3 p = ldp(a[r].lst, k);
+        m[r] = fmin(m[r], dist_sq(x[r], y[r], z[r], p.x, p.y, p.z));
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    if (a[r].lst == nullptr) {
+      w.add(kPairs, pk.P);
+      m[r] = min_dist_sq_brute(pk.pts, pk.P, x[r], y[r], z[r]);
+    }
+  }
+}
+
 // Rodrigues rotation of one atom (geometry.hpp:182-184):
 // ((o + v*c) + cross(k,v)*s) + k*(dot(k,v)*(1-c)), v = p - o.
 struct Axis {

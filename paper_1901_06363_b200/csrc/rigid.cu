@@ -14,6 +14,9 @@ namespace {
 #ifndef GD_RIGID_MINB
 #define GD_RIGID_MINB 4  // resident CTAs per SM the register budget targets
 #endif
+#ifndef GD_RIGID_MLP
+#define GD_RIGID_MLP 2   // atoms whose nearest-point lookups are in flight together
+#endif
 constexpr int kRigidThreads = 256;
 
 template <int BT, bool On>
@@ -60,14 +63,21 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_topk_kernel(DockParam
         // fold still strictly in atom order.
         double sum = 0.0;
         int i = 0;
-        for (; i + 1 < n; i += 2) {
-          double x0, y0, z0, x1, y1, z1, m0, m1;
-          rigid_apply(R, p.cx, p.cy, p.cz, vx[i], vy[i], vz[i], x0, y0, z0);
-          rigid_apply(R, p.cx, p.cy, p.cz, vx[i + 1], vy[i + 1], vz[i + 1], x1, y1, z1);
-          wk.add(kXform, 2);
-          min_dist_sq2(p.pocket, x0, y0, z0, x1, y1, z1, m0, m1, wk);
-          sum = dadd(sum, fmax(kMinDistanceSq, m0));
-          sum = dadd(sum, fmax(kMinDistanceSq, m1));
+        for (; i + GD_RIGID_MLP - 1 < n; i += GD_RIGID_MLP) {
+          double x[GD_RIGID_MLP], y[GD_RIGID_MLP], z[GD_RIGID_MLP], mm[GD_RIGID_MLP];
+#pragma unroll
+          for (int r = 0; r < GD_RIGID_MLP; ++r)
+            rigid_apply(R, p.cx, p.cy, p.cz, vx[i + r], vy[i + r], vz[i + r], x[r], y[r], z[r]);
+          wk.add(kXform, GD_RIGID_MLP);
+          min_dist_sqM<GD_RIGID_MLP>(p.pocket, x, y, z, mm, wk);
+#pragma unroll
+          for (int r = 0; r < GD_RIGID_MLP; ++r) sum = dadd(sum, fmax(kMinDistanceSq, mm[r]));
+        }
+        for (; i < n; ++i) {
+          double x, y, z;
+          rigid_apply(R, p.cx, p.cy, p.cz, vx[i], vy[i], vz[i], x, y, z);
+          wk.add(kXform, 1);
+          sum = dadd(sum, fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk)));
         }
         if (i < n) {
           double x, y, z;

@@ -53,6 +53,21 @@ class gd_result(C.Structure):
                 ("poses_scored", _i64p), ("status", _i32p)]
 
 
+class gd_device_result(C.Structure):
+    _fields_ = [("orientation", C.c_void_p), ("seed_rank", C.c_void_p),
+                ("final_score", C.c_void_p), ("evaluations", C.c_void_p),
+                ("n_ligands", C.c_int32), ("top_k", C.c_int32)]
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device buffer owned by the library
+    (lets torch wrap it without a copy, e.g. for an NCCL all-gather)."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, True), "version": 3, "strides": None}
+
+
 class gd_timing(C.Structure):
     _fields_ = [("upload_ms", C.c_float), ("rigid_ms", C.c_float), ("flex_ms", C.c_float),
                 ("download_ms", C.c_float), ("total_ms", C.c_float),
@@ -76,6 +91,7 @@ SIGNATURES = {
     "gd_download": (C.c_int, [C.c_void_p, C.POINTER(gd_result)]),
     "gd_last_timing": (C.c_int, [C.c_void_p, C.POINTER(gd_timing)]),
     "gd_work_counters": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "gd_device_results": (C.c_int, [C.c_void_p, C.POINTER(gd_device_result)]),
     "gd_fp64_peak": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "gd_overlap_score_batch": (C.c_int, [C.c_void_p, _f64p, C.c_int32, C.c_int32, C.c_uint32,
                                          _f64p]),
@@ -317,6 +333,17 @@ class Docker:
         r = result.c_struct()
         self._check(self._lib.gd_download(self._h, C.byref(r)))
         return result
+
+    def device_results(self) -> dict:
+        """Device views (torch tensors, no copy) of the last resident dock's
+        final-order table: final_score/orientation/seed_rank/evaluations [L, K]."""
+        import torch
+        d = gd_device_result()
+        self._check(self._lib.gd_device_results(self._h, C.byref(d)))
+        shape = (d.n_ligands, d.top_k)
+        view = lambda ptr, ts: torch.as_tensor(_CudaArray(ptr, shape, ts), device="cuda")
+        return {"final_score": view(d.final_score, "<f8"), "orientation": view(d.orientation, "<i4"),
+                "seed_rank": view(d.seed_rank, "<i4"), "evaluations": view(d.evaluations, "<i8")}
 
     def work_counters(self) -> dict:
         """Executed work of the last call made with GD_FLAG_COUNT_WORK."""

@@ -20,6 +20,26 @@ def shard_ids(rank: int, world: int, n: int, scaling: str = "weak") -> range:
     return range(start, start + base + (1 if rank < extra else 0))
 
 
+class DeviceGather:
+    """Per-step top-K gather straight from each rank's device-resident result
+    table (Docker.device_results()): one NCCL all-gather per field over
+    NVLink/NVSwitch, no host round trip.  Weak scaling: equal shard shapes."""
+
+    FIELDS = ("final_score", "orientation", "seed_rank", "evaluations")
+
+    def __init__(self, tables: dict, world: int):
+        import torch
+        self.world = world
+        self.tables = tables
+        self.out = {f: [torch.empty_like(tables[f]) for _ in range(world)] for f in self.FIELDS}
+
+    def __call__(self):
+        import torch.distributed as dist
+        for f in self.FIELDS:
+            dist.all_gather(self.out[f], self.tables[f])
+        return self.out
+
+
 def gather_topk(result, world: int, device=None):
     """All-gather every rank's [L, K] top-K table (final score, orientation,
     seed rank, evaluations) and return them concatenated in rank order, i.e.

@@ -67,6 +67,40 @@ def test_sharded_gather_equals_single_process(tmp_path, scaling):
     assert np.array_equal(merged["evaluations"], want.evaluations)
 
 
+def _gather_worker(rank, world, port, out_dir):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+    from paper_1901_06363_b200.sharding import DeviceGather
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    L, K = 3, 4
+    tables = {"final_score": torch.full((L, K), float(rank) + 0.5, dtype=torch.float64),
+              "orientation": torch.full((L, K), rank, dtype=torch.int32),
+              "seed_rank": torch.arange(L * K, dtype=torch.int32).reshape(L, K),
+              "evaluations": torch.full((L, K), 10 * rank, dtype=torch.int64)}
+    out = DeviceGather(tables, world)()
+    if rank == 0:
+        np.savez(Path(out_dir) / "gather.npz",
+                 **{f: torch.stack(out[f]).numpy() for f in DeviceGather.FIELDS})
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_device_gather_all_gathers_every_field(tmp_path):
+    """The per-step top-K gather bench.py runs over NCCL, here over gloo."""
+    import torch.multiprocessing as mp
+    world = 2
+    mp.spawn(_gather_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    z = np.load(tmp_path / "gather.npz")
+    for r in range(world):
+        assert (z["final_score"][r] == r + 0.5).all()
+        assert (z["orientation"][r] == r).all()
+        assert (z["evaluations"][r] == 10 * r).all()
+        assert np.array_equal(z["seed_rank"][r], np.arange(12).reshape(3, 4))
+
+
 def test_shard_ids_cover_exactly():
     from paper_1901_06363_b200.sharding import shard_ids
     for world in (1, 2, 3, 8):
