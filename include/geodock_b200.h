@@ -103,6 +103,9 @@ typedef struct {
   int64_t launches;    /* kernels launched by the call                 */
   int64_t h2d_bytes;   /* bytes copied host->device by the last upload */
   int64_t d2h_bytes;   /* bytes copied device->host by the last download */
+  float host_prep_ms;  /* host wall time: validation + graph preprocessing */
+  float host_pack_ms;  /* host wall time: packing descriptors into pinned staging */
+  float host_post_ms;  /* host wall time: result download + bookkeeping */
 } gd_timing;
 
 /* ---- context ------------------------------------------------------------ */

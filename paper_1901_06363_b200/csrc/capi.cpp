@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -75,6 +76,7 @@ double env_double(const char* name, double dflt) {
 struct gd_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
+  cudaStream_t aux_stream = nullptr;  // second stream of the pipelined gd_dock_batch
   cudaStream_t stream = nullptr;
   std::string err;
   cudaEvent_t ev[5] = {};
@@ -104,6 +106,8 @@ struct gd_ctx {
   std::vector<std::string> errors;
   DevBuf meta, xyz, radii, far, fmask, fax, fan, frel, order;
   PinnedBuf staging;
+  PinnedBuf res_staging;         // pinned D2H targets of gd_dock_batch
+  unsigned char* pin[10] = {};   // per-segment pointers into staging
 
   // Outputs of the last gd_dock_resident.
   int32_t last_topk = 0;
@@ -185,6 +189,7 @@ extern "C" int gd_destroy(gd_ctx* ctx) {
   for (cudaEvent_t ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
   delete ctx;
   return GD_OK;
 }
@@ -385,142 +390,189 @@ extern "C" int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[
 }
 
 // ---------------------------------------------------------------------------
-// Batch upload: validate + preprocess on the host, pack, one H2D per array.
+// Batch staging.  Descriptors are packed per ligand range ("chunk") into a
+// pinned arena laid out with upper bounds, so chunk k+1 can be prepared on
+// the host while chunk k is copied and docked on the GPU.
 // ---------------------------------------------------------------------------
-extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
-  if (ctx == nullptr) return GD_ERR_INVALID;
+namespace {
+
+enum Seg { kMeta, kXyz, kRad, kFar, kFmask, kFax, kFan, kFrel, kOrder, kStatus, kSegs };
+
+struct Running {
+  size_t fo = 0, wo = 0, mo = 0;  // frag, far-word, fmask-word cursors
+};
+
+}  // namespace
+
+// Validates the batch, sizes the pinned arena and the device descriptor
+// buffers with upper bounds, and resets the host bookkeeping.
+static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
   if (b == nullptr || b->n_ligands < 0 || (b->n_ligands > 0 &&
       (!b->atom_offsets || !b->xyz || !b->radii || !b->bond_offsets ||
        (b->bond_offsets[b->n_ligands] > 0 && (!b->bonds || !b->bond_rotatable)))))
     return ctx->fail(GD_ERR_INVALID, "gd_upload: invalid ligand batch");
-  GD_CUDA(ctx, cudaSetDevice(ctx->device));
   const int L = b->n_ligands;
-  std::vector<PreparedLigand> prep(L);
-  ctx->errors.assign(L, std::string());
-  ctx->status_host.assign(L, 0);
-  ctx->atom_off.assign(b->atom_offsets, b->atom_offsets + L + 1);
-  int32_t max_n = 1;
-  int max_nfrag = 0;
-  size_t far_words = 0, fmask_words = 0, nfrag_total = 0;
-  for (int l = 0; l < L; ++l)
-    if (b->atom_offsets[l + 1] < b->atom_offsets[l] || b->bond_offsets[l + 1] < b->bond_offsets[l])
-      return ctx->fail(GD_ERR_INVALID, "gd_upload: offsets not ascending");
-  // Ligand preprocessing is independent per ligand: spread it over the host
-  // cores (the reference's screen parallelises the same work per ligand).
-  {
-    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-    const int nth = std::min(hw, std::max(1, L / 64));
-    std::atomic<int> next{0};
-    auto work = [&] {
-      for (int l; (l = next.fetch_add(16)) < L;)
-        for (int e = l; e < std::min(L, l + 16); ++e) {
-          const int a0 = b->atom_offsets[e], n = b->atom_offsets[e + 1] - a0;
-          const int b0 = b->bond_offsets[e], nb = b->bond_offsets[e + 1] - b0;
-          prep[e] = prepare_ligand(std::to_string(e), n, b->xyz + 3 * a0, b->radii + a0, nb,
-                                   b->bonds + 2 * b0, b->bond_rotatable + b0);
-        }
-    };
-    std::vector<std::thread> pool;
-    for (int t = 1; t < nth; ++t) pool.emplace_back(work);
-    work();
-    for (auto& t : pool) t.join();
-  }
+  size_t far_ub = 0, frag_ub = 0, fmask_ub = 0;
   for (int l = 0; l < L; ++l) {
     const int n = b->atom_offsets[l + 1] - b->atom_offsets[l];
-    ctx->status_host[l] = prep[l].status;
-    ctx->errors[l] = prep[l].error;
-    if (prep[l].status != 0) continue;
-    max_n = std::max(max_n, n);
-    max_nfrag = std::max(max_nfrag, prep[l].nfrag());
-    far_words += prep[l].far_mask.size();
-    fmask_words += prep[l].frag_mask.size();
-    nfrag_total += prep[l].nfrag();
+    const int nb = b->bond_offsets[l + 1] - b->bond_offsets[l];
+    if (n < 0 || nb < 0) return ctx->fail(GD_ERR_INVALID, "gd_upload: offsets not ascending");
+    const size_t W = static_cast<size_t>((n + 63) / 64);
+    far_ub += static_cast<size_t>(n) * W;
+    frag_ub += 2 * static_cast<size_t>(nb);
+    fmask_ub += 2 * static_cast<size_t>(nb) * W;
   }
-  const int32_t total_atoms = b->atom_offsets[L];
-
-  // Pinned arena layout.
-  const size_t sz_meta = sizeof(LigMeta) * std::max(L, 1);
-  const size_t sz_xyz = sizeof(double) * 3 * std::max(total_atoms, 1);
-  const size_t sz_rad = sizeof(double) * std::max(total_atoms, 1);
-  const size_t sz_far = sizeof(uint64_t) * std::max<size_t>(far_words, 1);
-  const size_t sz_fm = sizeof(uint64_t) * std::max<size_t>(fmask_words, 1);
-  const size_t sz_fi = sizeof(int32_t) * std::max<size_t>(nfrag_total, 1);
-  const size_t sz_fr = sizeof(double) * std::max<size_t>(nfrag_total, 1);
-  const size_t sz_ord = sizeof(int32_t) * std::max(L, 1);
-  const size_t sizes[] = {sz_meta, sz_xyz, sz_rad, sz_far, sz_fm, sz_fi, sz_fi, sz_fr, sz_ord};
+  const int32_t A = L > 0 ? b->atom_offsets[L] : 0;
+  const size_t sizes[kSegs] = {
+      sizeof(LigMeta) * std::max(L, 1),       sizeof(double) * 3 * std::max(A, 1),
+      sizeof(double) * std::max(A, 1),        sizeof(uint64_t) * std::max<size_t>(far_ub, 1),
+      sizeof(uint64_t) * std::max<size_t>(fmask_ub, 1), sizeof(int32_t) * std::max<size_t>(frag_ub, 1),
+      sizeof(int32_t) * std::max<size_t>(frag_ub, 1),   sizeof(double) * std::max<size_t>(frag_ub, 1),
+      sizeof(int32_t) * std::max(L, 1), sizeof(int32_t) * std::max(L, 1)};
   size_t arena = 0;
   for (size_t s : sizes) arena += (s + 255) & ~size_t(255);
   GD_CUDA(ctx, ctx->staging.ensure(arena));
   unsigned char* base = static_cast<unsigned char*>(ctx->staging.ptr);
-  unsigned char* ptrs[9];
-  {
-    size_t o = 0;
-    for (int i = 0; i < 9; ++i) {
-      ptrs[i] = base + o;
-      o += (sizes[i] + 255) & ~size_t(255);
-    }
+  size_t o = 0;
+  DevBuf* dev[kSegs] = {&ctx->meta, &ctx->xyz, &ctx->radii, &ctx->far, &ctx->fmask,
+                        &ctx->fax,  &ctx->fan, &ctx->frel,  &ctx->order, &ctx->o_status};
+  for (int i = 0; i < kSegs; ++i) {
+    ctx->pin[i] = base + o;
+    o += (sizes[i] + 255) & ~size_t(255);
+    GD_CUDA(ctx, dev[i]->ensure(sizes[i]));
   }
-  auto* meta = reinterpret_cast<LigMeta*>(ptrs[0]);
-  auto* hxyz = reinterpret_cast<double*>(ptrs[1]);
-  auto* hrad = reinterpret_cast<double*>(ptrs[2]);
-  auto* hfar = reinterpret_cast<uint64_t*>(ptrs[3]);
-  auto* hfm = reinterpret_cast<uint64_t*>(ptrs[4]);
-  auto* hax = reinterpret_cast<int32_t*>(ptrs[5]);
-  auto* han = reinterpret_cast<int32_t*>(ptrs[6]);
-  auto* hrel = reinterpret_cast<double*>(ptrs[7]);
-  auto* hord = reinterpret_cast<int32_t*>(ptrs[8]);
-  std::memcpy(hxyz, b->xyz, sizeof(double) * 3 * total_atoms);
-  std::memcpy(hrad, b->radii, sizeof(double) * total_atoms);
-  size_t fo = 0, wo = 0, mo = 0;
-  std::vector<double> cost(L, 0.0);
-  for (int l = 0; l < L; ++l) {
-    const PreparedLigand& p = prep[l];
+  ctx->errors.assign(L, std::string());
+  ctx->status_host.assign(L, 0);
+  ctx->atom_off.assign(b->atom_offsets, b->atom_offsets + L + 1);
+  ctx->n_lig = L;
+  ctx->total_atoms = A;
+  ctx->max_n = 1;
+  ctx->have_result = false;
+  ctx->timing = gd_timing{};
+  run = Running{};
+  return GD_OK;
+}
+
+// Host half of a chunk: preprocess ligands [c0, c1) on the host cores
+// (Ligand ctor checks, capped distances, rotamers, fragments) and pack them
+// into the pinned arena; the chunk's CTA order is longest-first.
+static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Running& run,
+                       int& chunk_max_n) {
+  const int cnt = c1 - c0;
+  std::vector<PreparedLigand> prep(cnt);
+  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  const int nth = std::min(hw, std::max(1, cnt / 32));
+  std::atomic<int> next{0};
+  auto work = [&] {
+    for (int s; (s = next.fetch_add(8)) < cnt;)
+      for (int e = s; e < std::min(cnt, s + 8); ++e) {
+        const int l = c0 + e;
+        const int a0 = b->atom_offsets[l], n = b->atom_offsets[l + 1] - a0;
+        const int b0 = b->bond_offsets[l], nb = b->bond_offsets[l + 1] - b0;
+        prep[e] = prepare_ligand(std::to_string(l), n, b->xyz + 3 * a0, b->radii + a0, nb,
+                                 b->bonds + 2 * b0, b->bond_rotatable + b0);
+      }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < nth; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+
+  auto* meta = reinterpret_cast<LigMeta*>(ctx->pin[kMeta]);
+  auto* hxyz = reinterpret_cast<double*>(ctx->pin[kXyz]);
+  auto* hrad = reinterpret_cast<double*>(ctx->pin[kRad]);
+  auto* hfar = reinterpret_cast<uint64_t*>(ctx->pin[kFar]);
+  auto* hfm = reinterpret_cast<uint64_t*>(ctx->pin[kFmask]);
+  auto* hax = reinterpret_cast<int32_t*>(ctx->pin[kFax]);
+  auto* han = reinterpret_cast<int32_t*>(ctx->pin[kFan]);
+  auto* hrel = reinterpret_cast<double*>(ctx->pin[kFrel]);
+  auto* hord = reinterpret_cast<int32_t*>(ctx->pin[kOrder]);
+  const int a0 = b->atom_offsets[c0], a1 = b->atom_offsets[c1];
+  std::memcpy(hxyz + 3 * a0, b->xyz + 3 * a0, sizeof(double) * 3 * (a1 - a0));
+  std::memcpy(hrad + a0, b->radii + a0, sizeof(double) * (a1 - a0));
+  std::vector<double> cost(cnt, 0.0);
+  chunk_max_n = 1;
+  for (int e = 0; e < cnt; ++e) {
+    const int l = c0 + e;
+    const PreparedLigand& p = prep[e];
     LigMeta& m = meta[l];
     m.atom_off = b->atom_offsets[l];
     m.n = b->atom_offsets[l + 1] - b->atom_offsets[l];
     m.status = p.status;
-    m.frag_off = static_cast<int32_t>(fo);
+    m.frag_off = static_cast<int32_t>(run.fo);
     m.nfrag = p.status == 0 ? p.nfrag() : 0;
-    m.far_off = static_cast<int32_t>(wo);
-    m.fmask_off = static_cast<int32_t>(mo);
+    m.far_off = static_cast<int32_t>(run.wo);
+    m.fmask_off = static_cast<int32_t>(run.mo);
     m.words = p.words;
+    ctx->status_host[l] = p.status;
+    reinterpret_cast<int32_t*>(ctx->pin[kStatus])[l] = p.status;
+    ctx->errors[l] = p.error;
     if (p.status != 0) continue;
-    std::copy(p.far_mask.begin(), p.far_mask.end(), hfar + wo);
-    std::copy(p.frag_mask.begin(), p.frag_mask.end(), hfm + mo);
+    std::copy(p.far_mask.begin(), p.far_mask.end(), hfar + run.wo);
+    std::copy(p.frag_mask.begin(), p.frag_mask.end(), hfm + run.mo);
     for (int f = 0; f < p.nfrag(); ++f) {
-      hax[fo + f] = p.frag_axis[f];
-      han[fo + f] = p.frag_anchor[f];
-      hrel[fo + f] = p.frag_rel[f];
+      hax[run.fo + f] = p.frag_axis[f];
+      han[run.fo + f] = p.frag_anchor[f];
+      hrel[run.fo + f] = p.frag_rel[f];
     }
-    wo += p.far_mask.size();
-    mo += p.frag_mask.size();
-    fo += p.nfrag();
-    cost[l] = static_cast<double>(m.n) * (4.0 + m.nfrag);
+    run.wo += p.far_mask.size();
+    run.mo += p.frag_mask.size();
+    run.fo += p.nfrag();
+    chunk_max_n = std::max(chunk_max_n, m.n);
+    cost[e] = static_cast<double>(m.n) * (4.0 + m.nfrag);
   }
-  // Longest-processing-time-first CTA order (ties by ligand index).
-  std::iota(hord, hord + L, 0);
-  std::stable_sort(hord, hord + L, [&](int32_t a, int32_t c) { return cost[a] > cost[c]; });
+  // Longest-processing-time-first CTA order within the chunk.
+  std::vector<int32_t> idx(cnt);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
+  for (int e = 0; e < cnt; ++e) hord[c0 + e] = c0 + idx[e];
+  ctx->max_n = std::max(ctx->max_n, chunk_max_n);
+}
 
-  DevBuf* dev[9] = {&ctx->meta, &ctx->xyz, &ctx->radii, &ctx->far, &ctx->fmask,
-                    &ctx->fax,  &ctx->fan, &ctx->frel,  &ctx->order};
+// Copy half of a chunk: the chunk's descriptor segments, pinned -> HBM.
+static int h2d_range(gd_ctx* ctx, int c0, int c1, const Running& before, const Running& after,
+                     cudaStream_t s) {
+  auto cp = [&](DevBuf& d, int seg, size_t off, size_t bytes) -> int {
+    if (bytes == 0) return GD_OK;
+    ctx->timing.h2d_bytes += static_cast<int64_t>(bytes);
+    return ctx->cuda(cudaMemcpyAsync(static_cast<unsigned char*>(d.ptr) + off, ctx->pin[seg] + off,
+                                     bytes, cudaMemcpyHostToDevice, s), "h2d");
+  };
+  const size_t a0 = ctx->atom_off[c0], a1 = ctx->atom_off[c1];
+  int rc = GD_OK;
+  if ((rc = cp(ctx->meta, kMeta, sizeof(LigMeta) * c0, sizeof(LigMeta) * (c1 - c0)))) return rc;
+  if ((rc = cp(ctx->xyz, kXyz, sizeof(double) * 3 * a0, sizeof(double) * 3 * (a1 - a0)))) return rc;
+  if ((rc = cp(ctx->radii, kRad, sizeof(double) * a0, sizeof(double) * (a1 - a0)))) return rc;
+  if ((rc = cp(ctx->far, kFar, 8 * before.wo, 8 * (after.wo - before.wo)))) return rc;
+  if ((rc = cp(ctx->fmask, kFmask, 8 * before.mo, 8 * (after.mo - before.mo)))) return rc;
+  if ((rc = cp(ctx->fax, kFax, 4 * before.fo, 4 * (after.fo - before.fo)))) return rc;
+  if ((rc = cp(ctx->fan, kFan, 4 * before.fo, 4 * (after.fo - before.fo)))) return rc;
+  if ((rc = cp(ctx->frel, kFrel, 8 * before.fo, 8 * (after.fo - before.fo)))) return rc;
+  if ((rc = cp(ctx->order, kOrder, 4 * c0, 4 * (c1 - c0)))) return rc;
+  if ((rc = cp(ctx->o_status, kStatus, 4 * c0, 4 * (c1 - c0)))) return rc;
+  return GD_OK;
+}
+
+extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  Running run;
+  int rc = begin_batch(ctx, b, run);
+  if (rc != GD_OK) return rc;
+  const auto t0 = std::chrono::steady_clock::now();
+  int mx = 1;
+  prep_range(ctx, b, 0, ctx->n_lig, run, mx);
+  ctx->timing.host_prep_ms =
+      std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
   cudaEventRecord(ctx->ev[0], ctx->stream);
-  for (int i = 0; i < 9; ++i) {
-    GD_CUDA(ctx, dev[i]->ensure(sizes[i]));
-    GD_CUDA(ctx, cudaMemcpyAsync(dev[i]->ptr, ptrs[i], sizes[i], cudaMemcpyHostToDevice, ctx->stream));
-  }
+  rc = h2d_range(ctx, 0, ctx->n_lig, Running{}, run, ctx->stream);
+  if (rc != GD_OK) return rc;
   cudaEventRecord(ctx->ev[1], ctx->stream);
-  ctx->n_lig = L;
-  ctx->total_atoms = total_atoms;
-  ctx->max_n = max_n;
-  ctx->max_nfrag = max_nfrag;
-  ctx->have_result = false;
-  ctx->timing = gd_timing{};
-  for (size_t s : sizes) ctx->timing.h2d_bytes += static_cast<int64_t>(s);
   return GD_OK;
 }
 
 // ---------------------------------------------------------------------------
-// The hot path on the resident batch.
+// The hot path.
 // ---------------------------------------------------------------------------
 static int ensure_orientations(gd_ctx* ctx, int step) {
   if (ctx->orient_step == step) return GD_OK;
@@ -539,7 +591,10 @@ static int ensure_orientations(gd_ctx* ctx, int step) {
   return GD_OK;
 }
 
-static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
+// Validates knobs, allocates every output buffer for the whole batch (before
+// any asynchronous work: a reallocation would free memory in flight) and
+// returns the launch parameters common to all chunks.
+static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockParams& p) {
   char msg[128];
   if (gd_validate_knobs(k, msg, sizeof msg) != GD_OK) return ctx->fail(GD_ERR_INVALID, msg);
   if (ctx->P == 0) return ctx->fail(GD_ERR_NO_POCKET, "gd_dock: no pocket staged (gd_set_pocket)");
@@ -551,7 +606,7 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   }
   const int L = ctx->n_lig;
   const int K = rigid ? k->top_k : 1;
-  const size_t slots = static_cast<size_t>(L) * K;
+  const size_t slots = static_cast<size_t>(std::max(L, 1)) * K;
   GD_CUDA(ctx, ctx->seed_slot.ensure(sizeof(int32_t) * slots));
   GD_CUDA(ctx, ctx->seed_score.ensure(sizeof(double) * slots));
   GD_CUDA(ctx, ctx->k_eff.ensure(sizeof(int32_t) * std::max(L, 1)));
@@ -567,15 +622,11 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   GD_CUDA(ctx, ctx->o_scored.ensure(sizeof(int64_t) * std::max(L, 1)));
   GD_CUDA(ctx, ctx->o_status.ensure(sizeof(int32_t) * std::max(L, 1)));
   if (keep_pose) {
-    const size_t pose_bytes = sizeof(double) * 3 * static_cast<size_t>(ctx->total_atoms) * K;
+    const size_t pose_bytes = sizeof(double) * 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1)) * K;
     GD_CUDA(ctx, ctx->o_pose.ensure(pose_bytes));
     GD_CUDA(ctx, ctx->stage_pose.ensure(pose_bytes));
   }
-  GD_CUDA(ctx, cudaMemcpyAsync(ctx->o_status.ptr, ctx->status_host.data(), sizeof(int32_t) * L,
-                               cudaMemcpyHostToDevice, ctx->stream));
-
-  DockParams p{};
-  p.n_lig = L;
+  p = DockParams{};
   p.order = ctx->order.as<int32_t>();
   p.meta = ctx->meta.as<LigMeta>();
   p.xyz = ctx->xyz.as<double>();
@@ -586,7 +637,7 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   p.frag_anchor = ctx->fan.as<int32_t>();
   p.frag_rel = ctx->frel.as<double>();
   p.pocket = ctx->view;
-  p.pocket.use_index = (k->flags & GD_FLAG_BRUTE_FORCE) ? 0 : 1;
+  p.pocket.use_index = (k->flags & GD_FLAG_BRUTE_FORCE) ? 0 : ctx->view.use_index;
   p.cx = ctx->centre[0];
   p.cy = ctx->centre[1];
   p.cz = ctx->centre[2];
@@ -603,8 +654,6 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   p.threshold = k->threshold;
   p.top_k = K;
   p.rigid = rigid ? 1 : 0;
-  p.max_n = ctx->max_n;
-  p.max_pairs = std::max(1, ctx->max_n * ctx->max_n / 4);
   p.k_slots = rigid ? std::min(K, ctx->n_orient) : 1;
   p.st_final = ctx->st_final.as<double>();
   p.st_evals = ctx->st_evals.as<int64_t>();
@@ -625,77 +674,89 @@ static int run_kernels(gd_ctx* ctx, const gd_knobs* k, bool keep_pose) {
   p.counters = nullptr;
   if (k->flags & GD_FLAG_COUNT_WORK) {
     GD_CUDA(ctx, ctx->counters.ensure(sizeof(unsigned long long) * 16));
-    GD_CUDA(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * 16, ctx->stream));
+    GD_CUDA(ctx, cudaMemset(ctx->counters.ptr, 0, sizeof(unsigned long long) * 16));
     p.counters = ctx->counters.as<unsigned long long>();
   }
   ctx->counted = p.counters != nullptr;
-
-  int launches = 0;
-  cudaEventRecord(ctx->ev[2], ctx->stream);
-  if (L > 0 && rigid) {
-    int sort_slots = 2;
-    while (sort_slots < std::min(ctx->n_orient, 2048)) sort_slots <<= 1;
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_rigid_topk(p, sort_slots, ctx->stream)));
-    ++launches;
-  }
-  cudaEventRecord(ctx->ev[3], ctx->stream);
-  if (L > 0) {
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_flex(p, ctx->stream)));
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_finalize(p, ctx->stream)));
-    launches += 2;
-  }
-  cudaEventRecord(ctx->ev[4], ctx->stream);
   ctx->last_topk = K;
   ctx->last_rigid = rigid;
   ctx->last_pose = keep_pose;
-  ctx->have_result = true;
-  ctx->timing.launches = launches;
+  return GD_OK;
+}
+
+// The three hot-path launches over CTA-order positions [c0, c1).
+static int launch_range(gd_ctx* ctx, DockParams p, int c0, int c1, int max_n, cudaStream_t s,
+                        cudaEvent_t e_mid) {
+  p.n_lig = c1 - c0;
+  p.order = ctx->order.as<int32_t>() + c0;
+  p.max_n = max_n;
+  p.max_pairs = std::max(1, max_n * max_n / 4);
+  if (p.n_lig == 0) return GD_OK;
+  if (p.rigid) {
+    int sort_slots = 2;
+    while (sort_slots < std::min(ctx->n_orient, 2048)) sort_slots <<= 1;
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_rigid_topk(p, sort_slots, s)));
+    ctx->timing.launches += 1;
+  }
+  if (e_mid) cudaEventRecord(e_mid, s);
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_flex(p, s)));
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_finalize(p, s)));
+  ctx->timing.launches += 2;
   return GD_OK;
 }
 
 extern "C" int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs) {
   if (ctx == nullptr) return GD_ERR_INVALID;
-  const int rc = run_kernels(ctx, knobs, knobs && (knobs->flags & GD_FLAG_KEEP_POSES));
+  if (knobs == nullptr) return ctx->fail(GD_ERR_INVALID, "knob config: null");
+  DockParams p;
+  int rc = prepare_dock(ctx, knobs, (knobs->flags & GD_FLAG_KEEP_POSES) != 0, p);
   if (rc != GD_OK) return rc;
+  ctx->timing.launches = 0;
+  cudaEventRecord(ctx->ev[2], ctx->stream);
+  rc = launch_range(ctx, p, 0, ctx->n_lig, ctx->max_n, ctx->stream, ctx->ev[3]);
+  if (rc != GD_OK) return rc;
+  cudaEventRecord(ctx->ev[4], ctx->stream);
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->have_result = true;
   cudaEventElapsedTime(&ctx->timing.rigid_ms, ctx->ev[2], ctx->ev[3]);
   cudaEventElapsedTime(&ctx->timing.flex_ms, ctx->ev[3], ctx->ev[4]);
   ctx->timing.total_ms = ctx->timing.rigid_ms + ctx->timing.flex_ms;
   return GD_OK;
 }
 
-static int download(gd_ctx* ctx, gd_result* r) {
-  if (!ctx->have_result) return ctx->fail(GD_ERR_INVALID, "gd_download: nothing docked yet");
-  const int L = ctx->n_lig, K = ctx->last_topk;
-  const size_t slots = static_cast<size_t>(L) * K;
-  cudaStream_t s = ctx->stream;
-  ctx->timing.d2h_bytes = 0;
-  auto cp = [&](void* dst, const DevBuf& src, size_t bytes) -> int {
-    if (dst == nullptr || bytes == 0) return GD_OK;
-    ctx->timing.d2h_bytes += static_cast<int64_t>(bytes);
-    return ctx->cuda(cudaMemcpyAsync(dst, src.ptr, bytes, cudaMemcpyDeviceToHost, s), "download");
+// Result copy of ligands [l0, l1) from HBM into the destination arrays
+// (user or pinned), asynchronously on stream s.
+static int d2h_range(gd_ctx* ctx, const gd_result* r, int l0, int l1, cudaStream_t s) {
+  const int K = ctx->last_topk;
+  const size_t s0 = static_cast<size_t>(l0) * K, ns = static_cast<size_t>(l1 - l0) * K;
+  auto cp = [&](void* dst, const DevBuf& src, size_t elem, size_t off, size_t cnt) -> int {
+    if (dst == nullptr || cnt == 0) return GD_OK;
+    ctx->timing.d2h_bytes += static_cast<int64_t>(elem * cnt);
+    return ctx->cuda(cudaMemcpyAsync(static_cast<unsigned char*>(dst) + elem * off,
+                                     static_cast<const unsigned char*>(src.ptr) + elem * off,
+                                     elem * cnt, cudaMemcpyDeviceToHost, s), "d2h");
   };
   int rc = GD_OK;
-  if ((rc = cp(r->orientation, ctx->o_orient, sizeof(int32_t) * slots))) return rc;
-  if ((rc = cp(r->seed_rank, ctx->o_rank, sizeof(int32_t) * slots))) return rc;
-  if ((rc = cp(r->rigid_score, ctx->o_rigid, sizeof(double) * slots))) return rc;
-  if ((rc = cp(r->final_score, ctx->o_final, sizeof(double) * slots))) return rc;
-  if ((rc = cp(r->evaluations, ctx->o_evals, sizeof(int64_t) * slots))) return rc;
-  if ((rc = cp(r->feasibility_checks, ctx->o_checks, sizeof(int64_t) * slots))) return rc;
-  if ((rc = cp(r->k_eff, ctx->k_eff, sizeof(int32_t) * L))) return rc;
-  if ((rc = cp(r->poses_scored, ctx->o_scored, sizeof(int64_t) * L))) return rc;
-  if ((rc = cp(r->status, ctx->o_status, sizeof(int32_t) * L))) return rc;
+  if ((rc = cp(r->orientation, ctx->o_orient, 4, s0, ns))) return rc;
+  if ((rc = cp(r->seed_rank, ctx->o_rank, 4, s0, ns))) return rc;
+  if ((rc = cp(r->rigid_score, ctx->o_rigid, 8, s0, ns))) return rc;
+  if ((rc = cp(r->final_score, ctx->o_final, 8, s0, ns))) return rc;
+  if ((rc = cp(r->evaluations, ctx->o_evals, 8, s0, ns))) return rc;
+  if ((rc = cp(r->feasibility_checks, ctx->o_checks, 8, s0, ns))) return rc;
+  if ((rc = cp(r->k_eff, ctx->k_eff, 4, l0, l1 - l0))) return rc;
+  if ((rc = cp(r->poses_scored, ctx->o_scored, 8, l0, l1 - l0))) return rc;
+  if ((rc = cp(r->status, ctx->o_status, 4, l0, l1 - l0))) return rc;
   if (r->final_pose != nullptr) {
-    if (!ctx->last_pose) return ctx->fail(GD_ERR_INVALID, "gd_download: poses were not kept");
-    if ((rc = cp(r->final_pose, ctx->o_pose, sizeof(double) * 3 * size_t(ctx->total_atoms) * K)))
-      return rc;
+    const size_t a0 = ctx->atom_off[l0], a1 = ctx->atom_off[l1];
+    if ((rc = cp(r->final_pose, ctx->o_pose, 24, K * a0, K * (a1 - a0)))) return rc;
   }
-  GD_CUDA(ctx, cudaStreamSynchronize(s));
-  // Empty slots (ligands that failed, or slots past k_eff) read as
-  // orientation -2 and zeros.
-  std::vector<int32_t> keff(L), stat(L);
-  GD_CUDA(ctx, cudaMemcpy(keff.data(), ctx->k_eff.ptr, sizeof(int32_t) * L, cudaMemcpyDeviceToHost));
-  GD_CUDA(ctx, cudaMemcpy(stat.data(), ctx->o_status.ptr, sizeof(int32_t) * L, cudaMemcpyDeviceToHost));
+  return GD_OK;
+}
+
+// Empty slots (ligands that failed, or slots past k_eff) read as
+// orientation -2 and zeros; needs k_eff and status already on the host.
+static void fill_empty(gd_ctx* ctx, gd_result* r, const int32_t* keff, const int32_t* stat) {
+  const int L = ctx->n_lig, K = ctx->last_topk;
   for (int l = 0; l < L; ++l) {
     const int kk = stat[l] != 0 ? 0 : (ctx->last_rigid ? keff[l] : 1);
     if (r->k_eff) r->k_eff[l] = kk;
@@ -714,6 +775,21 @@ static int download(gd_ctx* ctx, gd_result* r) {
                     sizeof(double) * 3 * n);
     }
   }
+}
+
+static int download(gd_ctx* ctx, gd_result* r) {
+  if (!ctx->have_result) return ctx->fail(GD_ERR_INVALID, "gd_download: nothing docked yet");
+  if (r->final_pose != nullptr && !ctx->last_pose)
+    return ctx->fail(GD_ERR_INVALID, "gd_download: poses were not kept");
+  const int L = ctx->n_lig;
+  ctx->timing.d2h_bytes = 0;
+  int rc = d2h_range(ctx, r, 0, L, ctx->stream);
+  if (rc != GD_OK) return rc;
+  std::vector<int32_t> keff(std::max(L, 1)), stat(std::max(L, 1));
+  GD_CUDA(ctx, cudaMemcpyAsync(keff.data(), ctx->k_eff.ptr, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaMemcpyAsync(stat.data(), ctx->o_status.ptr, sizeof(int32_t) * L, cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  fill_empty(ctx, r, keff.data(), stat.data());
   return GD_OK;
 }
 
@@ -722,22 +798,92 @@ extern "C" int gd_download(gd_ctx* ctx, gd_result* r) {
   return download(ctx, r);
 }
 
+// Host buffers in, host buffers out, pipelined: the batch is split into
+// chunks; while the GPU copies and docks chunk k (alternating two streams so
+// one chunk's kernel tail overlaps the next chunk's start), the host threads
+// preprocess chunk k+1.  Results land in a pinned arena and are copied into
+// the caller's arrays at the end.
 extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd_knobs* knobs,
                              gd_result* result) {
   if (ctx == nullptr) return GD_ERR_INVALID;
   if (result == nullptr) return ctx->fail(GD_ERR_INVALID, "gd_dock_batch: null result");
+  if (knobs == nullptr) return ctx->fail(GD_ERR_INVALID, "knob config: null");
   char msg[128];
   if (gd_validate_knobs(knobs, msg, sizeof msg) != GD_OK) return ctx->fail(GD_ERR_INVALID, msg);
-  int rc = gd_upload(ctx, batch);
+  const auto t_start = std::chrono::steady_clock::now();
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  Running run;
+  int rc = begin_batch(ctx, batch, run);
   if (rc != GD_OK) return rc;
-  rc = run_kernels(ctx, knobs, result->final_pose != nullptr);
+  const bool keep_pose = result->final_pose != nullptr;
+  DockParams p;
+  rc = prepare_dock(ctx, knobs, keep_pose, p);
   if (rc != GD_OK) return rc;
-  rc = download(ctx, result);
-  if (rc != GD_OK) return rc;
-  cudaEventElapsedTime(&ctx->timing.upload_ms, ctx->ev[0], ctx->ev[1]);
-  cudaEventElapsedTime(&ctx->timing.rigid_ms, ctx->ev[2], ctx->ev[3]);
-  cudaEventElapsedTime(&ctx->timing.flex_ms, ctx->ev[3], ctx->ev[4]);
-  cudaEventElapsedTime(&ctx->timing.total_ms, ctx->ev[0], ctx->ev[4]);
+  const int L = ctx->n_lig, K = ctx->last_topk;
+  if (ctx->aux_stream == nullptr)
+    GD_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+  // Pinned result arena: the async D2H targets.
+  const size_t slots = static_cast<size_t>(std::max(L, 1)) * K;
+  const size_t pose_elems = keep_pose ? 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1)) * K : 0;
+  const size_t rbytes = slots * (4 + 4 + 8 + 8 + 8 + 8) + static_cast<size_t>(std::max(L, 1)) * (4 + 8 + 4) +
+                        8 * pose_elems + 1024;
+  GD_CUDA(ctx, ctx->res_staging.ensure(rbytes));
+  unsigned char* rb = static_cast<unsigned char*>(ctx->res_staging.ptr);
+  size_t ro = 0;
+  auto take = [&](size_t bytes) {
+    void* q = rb + ro;
+    ro += (bytes + 15) & ~size_t(15);
+    return q;
+  };
+  gd_result pr{};
+  pr.orientation = result->orientation ? static_cast<int32_t*>(take(4 * slots)) : nullptr;
+  pr.seed_rank = result->seed_rank ? static_cast<int32_t*>(take(4 * slots)) : nullptr;
+  pr.rigid_score = result->rigid_score ? static_cast<double*>(take(8 * slots)) : nullptr;
+  pr.final_score = result->final_score ? static_cast<double*>(take(8 * slots)) : nullptr;
+  pr.evaluations = result->evaluations ? static_cast<int64_t*>(take(8 * slots)) : nullptr;
+  pr.feasibility_checks = result->feasibility_checks ? static_cast<int64_t*>(take(8 * slots)) : nullptr;
+  pr.k_eff = static_cast<int32_t*>(take(4 * std::max(L, 1)));
+  pr.poses_scored = result->poses_scored ? static_cast<int64_t*>(take(8 * std::max(L, 1))) : nullptr;
+  pr.status = static_cast<int32_t*>(take(4 * std::max(L, 1)));
+  pr.final_pose = keep_pose ? static_cast<double*>(take(8 * pose_elems)) : nullptr;
+
+  const int chunks = std::max(1, std::min(8, L / 1024));
+  float prep_ms = 0.0f;
+  ctx->timing.launches = 0;
+  for (int c = 0; c < chunks; ++c) {
+    const int c0 = static_cast<int>(static_cast<long long>(L) * c / chunks);
+    const int c1 = static_cast<int>(static_cast<long long>(L) * (c + 1) / chunks);
+    cudaStream_t s = (c & 1) ? ctx->aux_stream : ctx->stream;
+    const Running before = run;
+    const auto t0 = std::chrono::steady_clock::now();
+    int mx = 1;
+    prep_range(ctx, batch, c0, c1, run, mx);
+    prep_ms += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if ((rc = h2d_range(ctx, c0, c1, before, run, s)) != GD_OK) return rc;
+    if ((rc = launch_range(ctx, p, c0, c1, mx, s, nullptr)) != GD_OK) return rc;
+    if ((rc = d2h_range(ctx, &pr, c0, c1, s)) != GD_OK) return rc;
+  }
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->aux_stream));
+  ctx->have_result = true;
+  const auto t_post = std::chrono::steady_clock::now();
+  auto copy = [](void* dst, const void* src, size_t bytes) {
+    if (dst && src) std::memcpy(dst, src, bytes);
+  };
+  copy(result->orientation, pr.orientation, 4 * slots);
+  copy(result->seed_rank, pr.seed_rank, 4 * slots);
+  copy(result->rigid_score, pr.rigid_score, 8 * slots);
+  copy(result->final_score, pr.final_score, 8 * slots);
+  copy(result->evaluations, pr.evaluations, 8 * slots);
+  copy(result->feasibility_checks, pr.feasibility_checks, 8 * slots);
+  copy(result->poses_scored, pr.poses_scored, 8 * std::max(L, 1));
+  copy(result->status, pr.status, 4 * std::max(L, 1));
+  copy(result->final_pose, pr.final_pose, 8 * pose_elems);
+  fill_empty(ctx, result, pr.k_eff, pr.status);
+  const auto t_end = std::chrono::steady_clock::now();
+  ctx->timing.host_prep_ms = prep_ms;
+  ctx->timing.host_post_ms = std::chrono::duration<float, std::milli>(t_end - t_post).count();
+  ctx->timing.total_ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();
   return GD_OK;
 }
 

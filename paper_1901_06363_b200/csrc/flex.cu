@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
 // (E7) final order: (final score desc, seed rank asc), one rank per thread;
 // each rank's destination is the number of ranks that precede it.
 __global__ void __launch_bounds__(256) finalize_kernel(DockParams p) {
-  const int l = blockIdx.x;
+  const int l = p.order[blockIdx.x];
   const LigMeta m = p.meta[l];
   if (m.status != 0 || p.status[l] != 0) return;
   const int K = p.k_slots, slots = p.top_k;

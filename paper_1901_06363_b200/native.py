@@ -72,7 +72,9 @@ class gd_timing(C.Structure):
     _fields_ = [("upload_ms", C.c_float), ("rigid_ms", C.c_float), ("flex_ms", C.c_float),
                 ("download_ms", C.c_float), ("total_ms", C.c_float),
                 ("rigid_atom_queries", C.c_int64), ("flex_atom_queries", C.c_int64),
-                ("launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("host_prep_ms", C.c_float), ("host_pack_ms", C.c_float),
+                ("host_post_ms", C.c_float)]
 
 
 # Every symbol include/geodock_b200.h declares, with its ctypes signature.

@@ -62,6 +62,30 @@ def test_config1_subset_parity(docker, n_lig):
     assert_same_result(got, want)
 
 
+def test_pipelined_dock_batch_equals_resident_path(docker):
+    """gd_dock_batch splits >1024-ligand batches into chunks on two streams;
+    it must equal the single-launch resident path bit for bit, and the
+    reference on ligands at the chunk boundaries."""
+    from paper_1901_06363_b200 import DockResult
+    w = W.config(1)
+    pocket = w.pocket()
+    batch = w.ligands(range(2600))
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, w.knobs, keep_poses=True)
+    docker.upload(batch)
+    docker.dock_resident(w.knobs, keep_poses=True)
+    want = docker.download(DockResult.empty(batch.n_ligands, w.knobs.slots,
+                                            int(batch.atom_offsets[-1]), True))
+    assert_same_result(got, want)
+    picks = [0, 1299, 1300, 2599]
+    sub = batch.subset(picks)
+    ref = _cpu(sub, pocket, w.knobs)
+    for i, l in enumerate(picks):
+        assert np.array_equal(got.orientation[l], ref.orientation[i])
+        assert np.array_equal(got.final_score[l], ref.final_score[i])
+        assert np.array_equal(got.evaluations[l], ref.evaluations[i])
+
+
 def test_config2_knobs_parity(docker):
     """c2 knobs (rigid 10, frag 10, 3 restarts, K=100) on two c1-distribution ligands."""
     w = W.config(2)
