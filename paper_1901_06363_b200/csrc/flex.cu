@@ -27,6 +27,8 @@
 // All decisions reproduce the reference: strict '>' with first-encountered
 // ties (kernel.hpp:136, :169, :173, :185, :194), angle 0 = committed pose,
 // feasibility_checks / evaluations counted as CandidateEvaluator does.
+#include <cstdlib>
+
 #include "device_common.cuh"
 
 namespace gdb200 {
@@ -508,6 +510,12 @@ int launch_flex(const DockParams& p, void* stream) {
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
+  // Shared memory and L1 share the SM's 256 KB; the voxel-record gathers
+  // live in L1, so the carveout is an explicit tuning knob.
+  if (const char* cv = std::getenv("GD_FLEX_CARVEOUT")) {
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv));
+    if (e != cudaSuccess) return e;
+  }
   const long long blocks = (chains + kWarps - 1) / kWarps;
   kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError();

@@ -123,6 +123,55 @@ def test_given_pose_match_probes_shape(docker, knobs):
     assert_same_result(got, want)
 
 
+def test_large_ligands_multiword_masks(docker):
+    """Ligands of 65..153 atoms (2-3 mask words) with many rotamers, from the
+    reference's own generator envelope (synthetic.hpp DatasetSpec defaults)."""
+    O = _oracle()
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    pocket, batch = O.ref_generate_synthetic(6, 2718, 65, 153, 8, 30, 400, 10.0)
+    assert batch.sizes.max() > 128
+    docker.set_pocket(pocket)
+    for knobs in (Knobs(30, 45, 0.0, 1, False), Knobs.baseline(45, 30, 1, 8),
+                  Knobs(20, 45, 0.25, 2, True, 45, 4)):
+        got = docker.dock(batch, knobs, keep_poses=True)
+        want = O.dock_batch(batch, pocket, knobs, nthreads=O.threads(), impl="ref")
+        assert_same_result(got, want)
+
+
+def test_config3_rough_pocket(docker):
+    """A config-3 pocket (random semi-axes, 1 A lattice, roughness mask)."""
+    w = W.config(3)
+    pocket = W.pocket_of(w, 5)
+    batch = w.ligands(range(12), pocket.mean(axis=0))
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, w.knobs, keep_poses=True)
+    want = _cpu(batch, pocket, w.knobs)
+    assert_same_result(got, want)
+
+
+def test_edge_ligands(docker):
+    """Two-atom rigid ligand, a ligand with no rotamers, an invalid ligand
+    (disconnected) that must be skipped, and a single-point pocket."""
+    from paper_1901_06363_b200 import LigandBatch
+    from gd_test_helpers import Lig
+    parts = [
+        Lig([[0, 0, 0], [0, 0, 1.5]], [(0, 1, False)]),
+        Lig([[0, 0, 0], [1.5, 0, 0], [3, 0.5, 0], [4.5, 0, 0]], [(0, 1, False), (1, 2, False), (2, 3, False)]),
+        Lig([[0, 0, 0], [1.5, 0, 0], [9, 9, 9]], [(0, 1, True)]),  # disconnected
+        Lig([[0, 0, 0], [0, 0, 1], [1, 0, 1], [1, 1, 1]], [(0, 1, True), (1, 2, True), (2, 3, True)]),
+    ]
+    batch = LigandBatch.from_parts([p.args for p in parts])
+    O = _oracle()
+    for pocket in (np.array([[0.5, 0.2, 0.1]]), W.config(0).pocket()):
+        docker.set_pocket(pocket)
+        for knobs in (Knobs.baseline(90, 30, 2, 5), Knobs(10, 45, 0.0, 1, True)):
+            got = docker.dock(batch, knobs, keep_poses=True)
+            want = O.dock_batch(batch, pocket, knobs, nthreads=1)
+            assert got.status[2] == 1 and got.k_eff[2] == 0
+            assert_same_result(got, want)
+
+
 def test_overlap_score_kats(docker):
     """test_geometry.cpp:45-56 hand values through the GPU scoring kernel."""
     docker.set_pocket(np.array([[0.0, 0.0, 1.0]]))
