@@ -269,6 +269,15 @@ def run_ours(a):
         dom_work = work["flex" if dom == "flex_chain_kernel" else "rigid"]
         dom_ms = max(r_ms, f_ms)
         achieved = flops_of(dom_work) / (dom_ms / 1e3) / 1e12
+        # DRAM traffic per launch from the committed ncu --set full capture of
+        # this exact workload (ncu cannot run inside the bench itself).
+        traffic, traffic_src = None, None
+        tj = ROOT / "profiles" / "ncu_traffic.json"
+        if tj.exists():
+            tr = json.loads(tj.read_text())
+            if tr.get("config") == a.config and tr.get("ligands_per_gpu") == batch.n_ligands:
+                traffic = tr["dram_bytes_per_launch"].get(dom)
+                traffic_src = tr["source"]
         line = {
             "metric": METRIC, "value": value, "unit": "ligands/s", "n_gpus": world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
@@ -288,7 +297,8 @@ def run_ours(a):
             "gpu_launches": 3 * a.steps,
             "roofline": {"kernel": dom, "bound": "fp64", "achieved": achieved,
                          "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-                         "traffic": None,
+                         "traffic": traffic, "traffic_unit": "bytes per launch (DRAM read+write)",
+                         "traffic_source": traffic_src,
                          "peak_source": "measured fp64 DADD/DMUL probe (gd_fp64_peak) on this GPU",
                          "work_per_launch": dom_work},
             "clocks": clk,
