@@ -300,6 +300,59 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
           rf[i] = static_cast<float>(s.radius[i]);
         }
         __syncwarp();
+        auto test = [&](int i, int j) {
+          const float h = axc[j] - axc[i];
+          const float s2 = rad2[j], r2 = rad2[i];
+          const float cut = 0.8f * (rf[i] + rf[j]);
+          const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
+          const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
+          return !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
+        };
+        if (W == 1) {
+          // Flattened over the actual partner pairs: per-slot partner counts,
+          // a warp prefix sum, then lane t finds its slot by binary search and
+          // its partner as the n-th set bit of the slot's partner mask.
+          int* pref = reinterpret_cast<int*>(rf + n);
+          const uint64_t nf0 = ~s.fm[0];
+          int total = 0;
+          for (int b = 0; b < nf; b += 32) {
+            const int sl = b + lane;
+            const int cnt = sl < nf ? __popcll(s.far[s.fidx[sl]] & nf0) : 0;
+            int inc = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const int y = __shfl_up_sync(kFull, inc, o);
+              if (lane >= o) inc += y;
+            }
+            if (sl < nf) pref[sl] = total + inc - cnt;
+            total += __shfl_sync(kFull, inc, 31);
+          }
+          __syncwarp();
+          for (int t0 = 0; t0 < total; t0 += 32) {
+            const int t = t0 + lane;
+            bool keep = false;
+            int i = 0, j = 0;
+            if (t < total) {
+              int lo = 0, hi = nf - 1;  // last slot with pref <= t
+              while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (pref[mid] <= t) lo = mid; else hi = mid - 1;
+              }
+              i = s.fidx[lo];
+              const uint64_t m = s.far[i] & nf0;
+              const int r = t - pref[lo];
+              const unsigned mlo = static_cast<unsigned>(m), mhi = static_cast<unsigned>(m >> 32);
+              const int plo = __popc(mlo);
+              j = r < plo ? static_cast<int>(__fns(mlo, 0, r + 1))
+                          : 32 + static_cast<int>(__fns(mhi, 0, r - plo + 1));
+              keep = test(i, j);
+            }
+            const unsigned mask = __ballot_sync(kFull, keep);
+            if (keep)
+              s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
+            np += __popc(mask);
+          }
+        } else
         for (int sl = 0; sl < nf; ++sl) {
           const int i = s.fidx[sl];
           const float ai = axc[i], r2 = rad2[i], ri = rf[i];
