@@ -847,12 +847,22 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   pr.status = static_cast<int32_t*>(take(4 * std::max(L, 1)));
   pr.final_pose = keep_pose ? static_cast<double*>(take(8 * pose_elems)) : nullptr;
 
-  const int chunks = std::max(1, std::min(8, L / 1024));
+  // Chunk plan: a small head chunk (its host prep is the only part nothing
+  // overlaps), then up to 7 equal chunks.
+  std::vector<int> bounds{0};
+  if (L > 2048) {
+    const int head = 512, rest = L - head, parts = std::min(7, std::max(1, rest / 1024));
+    bounds.push_back(head);
+    for (int c = 1; c <= parts; ++c)
+      bounds.push_back(head + static_cast<int>(static_cast<long long>(rest) * c / parts));
+  } else {
+    bounds.push_back(L);
+  }
+  const int chunks = static_cast<int>(bounds.size()) - 1;
   float prep_ms = 0.0f;
   ctx->timing.launches = 0;
   for (int c = 0; c < chunks; ++c) {
-    const int c0 = static_cast<int>(static_cast<long long>(L) * c / chunks);
-    const int c1 = static_cast<int>(static_cast<long long>(L) * (c + 1) / chunks);
+    const int c0 = bounds[c], c1 = bounds[c + 1];
     cudaStream_t s = (c & 1) ? ctx->aux_stream : ctx->stream;
     const Running before = run;
     const auto t0 = std::chrono::steady_clock::now();
