@@ -89,6 +89,24 @@ __device__ __forceinline__ bool in_frag(const uint64_t* fm, int i) {
   return (fm[i >> 6] >> (i & 63)) & 1ull;
 }
 
+// Position of the r-th (0-based) set bit of a 64-bit mask by a popcount
+// descent (cheaper than __fns on sm_100a).
+__device__ __forceinline__ int nth_bit(uint64_t m, int r) {
+  int pos = 0;
+  int c = __popc(static_cast<unsigned>(m));
+  if (r >= c) { r -= c; m >>= 32; pos = 32; }
+  unsigned w = static_cast<unsigned>(m);
+  c = __popc(w & 0xFFFFu);
+  if (r >= c) { r -= c; w >>= 16; pos += 16; }
+  c = __popc(w & 0xFFu);
+  if (r >= c) { r -= c; w >>= 8; pos += 8; }
+  c = __popc(w & 0xFu);
+  if (r >= c) { r -= c; w >>= 4; pos += 4; }
+  c = __popc(w & 0x3u);
+  if (r >= c) { r -= c; w >>= 2; pos += 2; }
+  return pos + ((r >= static_cast<int>(w & 1u)) ? 1 : 0);
+}
+
 // floor(t / d) for 0 <= t < 2^16, 1 <= d <= 256 via an fp32 reciprocal:
 // (2t+1)/(2d) is never within 1/(2d) >= 2e-3 of an integer, far beyond the
 // ~1e-4 fp32 error at these magnitudes, so truncation is exact.
@@ -340,11 +358,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
               }
               i = s.fidx[lo];
               const uint64_t m = s.far[i] & nf0;
-              const int r = t - pref[lo];
-              const unsigned mlo = static_cast<unsigned>(m), mhi = static_cast<unsigned>(m >> 32);
-              const int plo = __popc(mlo);
-              j = r < plo ? static_cast<int>(__fns(mlo, 0, r + 1))
-                          : 32 + static_cast<int>(__fns(mhi, 0, r - plo + 1));
+              j = nth_bit(m, t - pref[lo]);
               keep = test(i, j);
             }
             const unsigned mask = __ballot_sync(kFull, keep);
