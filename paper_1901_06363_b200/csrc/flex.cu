@@ -51,11 +51,16 @@ __host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pair
          a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16);
 }
 
+// One atom of a chain's committed pose and its overlap term max(1e-12,
+// min_j d^2): 32 bytes, two 128-bit shared loads from one address.
+struct __align__(16) PT {
+  double x, y, z, t;
+};
+
 struct WarpMem {
   double* radius;        // [n]
   uint64_t* far;         // [n*W]  bit j of row i: capped graph distance >= 4
-  double *px, *py, *pz;  // [n]    committed pose of the chain
-  double* term;          // [n]    max(1e-12, min_j d^2) of the committed pose
+  PT* pt;                // [n]    committed pose + terms of the chain
   double* v;             // [kBatch*n] candidate terms of fragment atoms
   uint16_t* pairs;       // [max_pairs] surviving bump pairs: F-slot | j << 8
   uint8_t* fidx;         // [n] fragment atoms, ascending
@@ -73,10 +78,7 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   };
   s.radius = reinterpret_cast<double*>(take(8ull * n));
   s.far = reinterpret_cast<uint64_t*>(take(8ull * n * W));
-  s.px = reinterpret_cast<double*>(take(8ull * n));
-  s.py = reinterpret_cast<double*>(take(8ull * n));
-  s.pz = reinterpret_cast<double*>(take(8ull * n));
-  s.term = reinterpret_cast<double*>(take(8ull * n));
+  s.pt = reinterpret_cast<PT*>(take(32ull * n));
   s.v = reinterpret_cast<double*>(take(8ull * kBatch * n));
   s.pairs = reinterpret_cast<uint16_t*>(take(2ull * max_pairs));
   s.fidx = reinterpret_cast<uint8_t*>(take(n));
@@ -135,11 +137,12 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
     const int a = a0 + c * da;
     const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
     double qx, qy, qz;
-    rodrigues(X, cs, sn, dsub(1.0, cs), s.px[i], s.py[i], s.pz[i], qx, qy, qz);
+    const PT ai = s.pt[i], aj = s.pt[j];
+    rodrigues(X, cs, sn, dsub(1.0, cs), ai.x, ai.y, ai.z, qx, qy, qz);
     wk.add(kRot, 1);
     wk.add(kBump, 1);
     const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
-    if (dist_sq(qx, qy, qz, s.px[j], s.py[j], s.pz[j]) < dmul(cut, cut)) bl |= 1u << c;
+    if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < dmul(cut, cut)) bl |= 1u << c;
   }
   const unsigned bumped = __reduce_or_sync(kFull, bl);
   const unsigned live = ((1u << nb) - 1u) & ~bumped & ~zero;
@@ -158,8 +161,9 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
     const double cs0 = __ldg(p.cos_deg + a0c), sn0 = __ldg(p.sin_deg + a0c);
     const double cs1 = __ldg(p.cos_deg + a1c), sn1 = __ldg(p.sin_deg + a1c);
     double x0, y0, z0, x1, y1, z1, m0, m1;
-    rodrigues(X, cs0, sn0, dsub(1.0, cs0), s.px[i0], s.py[i0], s.pz[i0], x0, y0, z0);
-    rodrigues(X, cs1, sn1, dsub(1.0, cs1), s.px[i1], s.py[i1], s.pz[i1], x1, y1, z1);
+    const PT q0 = s.pt[i0], q1 = s.pt[i1];
+    rodrigues(X, cs0, sn0, dsub(1.0, cs0), q0.x, q0.y, q0.z, x0, y0, z0);
+    rodrigues(X, cs1, sn1, dsub(1.0, cs1), q1.x, q1.y, q1.z, x1, y1, z1);
     wk.add(kRot, 2);
     min_dist_sq2(p.pocket, x0, y0, z0, x1, y1, z1, m0, m1, wk);
     if (l0) s.v[c0 * n + i0] = fmax(kMinDistanceSq, m0);
@@ -227,17 +231,14 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       rigid_apply(R, p.cx, p.cy, p.cz, dsub(x, p.cx), dsub(y, p.cy), dsub(z, p.cz), x, y, z);
       wk.add(kXform, 1);
     }
-    s.px[i] = x;
-    s.py[i] = y;
-    s.pz[i] = z;
-    s.term[i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+    s.pt[i] = PT{x, y, z, fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk))};
   }
   __syncwarp();
   // match_probes_shape prologue (kernel.hpp:215-218).
   double cur = 0.0;
   if (lane == 0) {
     double sum = 0.0;
-    for (int i = 0; i < n; ++i) sum = dadd(sum, s.term[i]);
+    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt[i].t);
     cur = __ddiv_rn(static_cast<double>(n), sum);
   }
   cur = __shfl_sync(kFull, cur, 0);
@@ -262,9 +263,9 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       }
       if (lane < W) s.fm[lane] = __ldg(p.frag_mask + m.fmask_off + f * W + lane);
       // rotate_fragment_into axis (geometry.hpp:165-169), identical in every lane.
-      const double ox = s.px[axis], oy = s.py[axis], oz = s.pz[axis];
-      const double ax = dsub(s.px[anchor], ox), ay = dsub(s.py[anchor], oy),
-                   az = dsub(s.pz[anchor], oz);
+      const PT pa = s.pt[axis], pb = s.pt[anchor];
+      const double ox = pa.x, oy = pa.y, oz = pa.z;
+      const double ax = dsub(pb.x, ox), ay = dsub(pb.y, oy), az = dsub(pb.z, oz);
       const double len = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
       if (len < kMinAxisLength) {  // "rotate_fragment: degenerate rotation axis"
         if (lane == 0) p.status[l] = 3;
@@ -285,7 +286,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       const int first = s.fidx[0];
       double pre = 0.0;
       if (lane == 0)
-        for (int i = 0; i < first; ++i) pre = dadd(pre, s.term[i]);
+        for (int i = 0; i < first; ++i) pre = dadd(pre, s.pt[i].t);
       pre = __shfl_sync(kFull, pre, 0);
       // Surviving bump pairs: drop (i, j) when the circle atom i sweeps never
       // comes within the cutoff of j: dmin^2 = h^2 + (sigma - rho)^2 > cut^2,
@@ -311,7 +312,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         float* rad2 = axc + n;
         float* rf = rad2 + n;
         for (int i = lane; i < n; i += 32) {
-          const double vx = s.px[i] - ox, vy = s.py[i] - oy, vz = s.pz[i] - oz;
+          const PT q = s.pt[i];
+          const double vx = q.x - ox, vy = q.y - oy, vz = q.z - oz;
           const double a = X.kx * vx + X.ky * vy + X.kz * vz;
           axc[i] = static_cast<float>(a);
           rad2[i] = static_cast<float>(fmax(0.0, vx * vx + vy * vy + vz * vz - a * a));
@@ -398,7 +400,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       // pre-fill them into each candidate slot so the fold is a plain sum.
       for (int i = lane; i < n; i += 32)
         if (!in_frag(s.fm, i)) {
-          const double t = s.term[i];
+          const double t = s.pt[i].t;
 #pragma unroll
           for (int c = 0; c < kBatch; ++c) s.v[c * n + i] = t;
         }
@@ -494,12 +496,10 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         for (int sl = lane; sl < nf; sl += 32) {
           const int i = s.fidx[sl];
           double qx, qy, qz;
-          rodrigues(X, cs, sn, omc, s.px[i], s.py[i], s.pz[i], qx, qy, qz);
+          const PT q = s.pt[i];
+          rodrigues(X, cs, sn, omc, q.x, q.y, q.z, qx, qy, qz);
           wk.add(kRot, 1);
-          s.px[i] = qx;
-          s.py[i] = qy;
-          s.pz[i] = qz;
-          s.term[i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx, qy, qz, wk));
+          s.pt[i] = PT{qx, qy, qz, fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx, qy, qz, wk))};
         }
       }
       __syncwarp();
@@ -514,9 +514,10 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
   if (p.stage_pose != nullptr) {
     double* dst = p.stage_pose + 3 * (static_cast<size_t>(p.top_k) * m.atom_off + static_cast<size_t>(r) * n);
     for (int i = lane; i < n; i += 32) {
-      dst[3 * i] = s.px[i];
-      dst[3 * i + 1] = s.py[i];
-      dst[3 * i + 2] = s.pz[i];
+      const PT q = s.pt[i];
+      dst[3 * i] = q.x;
+      dst[3 * i + 1] = q.y;
+      dst[3 * i + 2] = q.z;
     }
   }
   publish_warp(wk, p.counters, 8, lane);
