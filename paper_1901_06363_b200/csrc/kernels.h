@@ -103,7 +103,6 @@ struct DockParams {
 int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* stream);
 
 // Bytes of dynamic shared memory the kernels need for these params.
-size_t rigid_smem_bytes(const DockParams& p, int sort_slots);
 size_t flex_smem_bytes(const DockParams& p);
 
 // Launchers; return cudaError_t as int.  `stream` is a cudaStream_t.
