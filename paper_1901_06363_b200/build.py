@@ -39,6 +39,11 @@ def _stale(target: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+# -D flags shared by device and host objects (layout knobs such as
+# GD_VOX_INLINE must agree on both sides); GD_NVCC_EXTRA is device-only.
+DEFS = os.environ.get("GD_DEFS", "").split()
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
     inc = ["-I", str(ROOT / "include"), "-I", str(CSRC)]
@@ -48,14 +53,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         obj = BUILD / (src + ".o")
         if force or _stale(obj, [CSRC / src] + hdrs):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-                  *os.environ.get("GD_NVCC_EXTRA", "").split(),
+                  *os.environ.get("GD_NVCC_EXTRA", "").split(), *DEFS,
                   "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *inc,
                   "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
     for src in HOST_SRCS:
         obj = BUILD / (src + ".o")
         if force or _stale(obj, [CSRC / src] + hdrs):
-            _run(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall",
+            _run(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", *DEFS,
                   "-I/usr/local/cuda/include", *inc, "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
     if force or _stale(LIB, objs):

@@ -333,21 +333,21 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     GD_CUDA(ctx, cudaMemcpyAsync(cnt.data(), counts.ptr, sizeof(int32_t) * nv,
                                  cudaMemcpyDeviceToHost, ctx->stream));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    // Each voxel's first candidate lives in its 32-byte record; the list
-    // holds candidates 2..count, offsets = exclusive scan of (count - 1).
+    // Each voxel's first kVoxInline candidates live in its record; the list
+    // holds the rest, offsets = exclusive scan of max(count - kVoxInline, 0).
     std::vector<int32_t> off(nv, 0);
     int64_t total = 0, listed = 0;
     int32_t mx = 0;
     for (int c = 0; c < nv; ++c) {
       off[c] = static_cast<int32_t>(listed);
-      listed += cnt[c] - 1;
+      listed += std::max(cnt[c] - kVoxInline, 0);
       total += cnt[c];
       mx = std::max(mx, cnt[c]);
       if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
     }
     DevBuf doff;
     GD_CUDA(ctx, doff.ensure(sizeof(int32_t) * nv));
-    GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(double) * 4 * static_cast<size_t>(nv)));
+    GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
     GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
     GD_CUDA(ctx, cudaMemcpyAsync(doff.ptr, off.data(), sizeof(int32_t) * nv, cudaMemcpyHostToDevice,
                                  ctx->stream));

@@ -22,6 +22,7 @@ namespace {
 constexpr double kMinDistanceSq = 1e-12;  // geometry.hpp:33
 constexpr double kBumpScale = 0.8;        // geometry.hpp:37
 constexpr double kMinAxisLength = 1e-9;   // geometry.hpp:43
+constexpr double kInfinity = __builtin_huge_val();
 constexpr double kInfeasible = -1.0;      // scores are > 0
 
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
@@ -97,12 +98,14 @@ __device__ __noinline__ double min_dist_sq_brute(const double* pts, int P, doubl
 // reference's PocketIndex makes the same exactness argument,
 // geometry.hpp:45-46).  Fine level first, then the coarse far-field level;
 // queries beyond both fall back to the full scan.
-// Voxel lookup: one 256-bit load of the record of the first grid level
-// containing q; lst == nullptr means the full-scan fallback.
+// Voxel lookup: the record of the first grid level containing q (one or
+// two independent 256-bit loads); lst == nullptr means the full-scan
+// fallback.
 struct Loc {
   const double* lst;  // further candidates (start already applied)
   int count;          // candidates in the voxel (>= 1)
-  double x0, y0, z0;  // the inline first candidate
+  double x0, y0, z0;  // the inline candidates (the second repeats the first
+  double x1, y1, z1;  // when count == 1; unused when kVoxInline == 1)
 };
 __device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, double z) {
   if (pk.use_index) {
@@ -115,9 +118,11 @@ __device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, 
       if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
         const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
                       static_cast<int>(fz);
-        double hdr;
+        const double* r = g.rec + kRecDoubles * static_cast<size_t>(v);
+        double hdr, pad;
         Loc l;
-        ld256(g.rec + 4 * static_cast<size_t>(v), hdr, l.x0, l.y0, l.z0);
+        ld256(r, hdr, l.x0, l.y0, l.z0);
+        if constexpr (kVoxInline == 2) ld256(r + 4, l.x1, l.y1, l.z1, pad);
         const long long h = __double_as_longlong(hdr);
         l.count = static_cast<int>(h >> 32);
         l.lst = g.lst + 4 * static_cast<size_t>(static_cast<unsigned>(h & 0xffffffffll));
@@ -125,8 +130,16 @@ __device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, 
       }
     }
   }
-  return Loc{nullptr, 0, 0.0, 0.0, 0.0};
+  return Loc{nullptr, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 }
+
+// min over the inline candidates; the list scan covers count - kVoxInline.
+__device__ __forceinline__ double inline_min(const Loc& a, double x, double y, double z) {
+  double m = dist_sq(x, y, z, a.x0, a.y0, a.z0);
+  if constexpr (kVoxInline == 2) m = fmin(m, dist_sq(x, y, z, a.x1, a.y1, a.z1));
+  return m;
+}
+__device__ __forceinline__ int listed(const Loc& a) { return a.lst ? a.count - kVoxInline : 0; }
 
 template <bool On>
 __device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, double y, double z,
@@ -138,8 +151,8 @@ __device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, do
     return min_dist_sq_brute(pk.pts, pk.P, x, y, z);
   }
   w.add(kPairs, a.count);
-  double m = dist_sq(x, y, z, a.x0, a.y0, a.z0);
-  for (int k = 0; k < a.count - 1; ++k) {
+  double m = inline_min(a, x, y, z);
+  for (int k = 0; k < a.count - kVoxInline; ++k) {
     const P3 p = ldp(a.lst, k);
     m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
   }
@@ -155,10 +168,10 @@ __device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, do
   w.add(kQuery, 2);
   const Loc a = locate(pk, x0, y0, z0);
   const Loc b = locate(pk, x1, y1, z1);
-  const int na = a.lst ? a.count - 1 : 0, nb = b.lst ? b.count - 1 : 0;
+  const int na = listed(a), nb = listed(b);
   w.add(kPairs, (a.lst ? a.count : 0) + (b.lst ? b.count : 0));
-  m0 = dist_sq(x0, y0, z0, a.x0, a.y0, a.z0);
-  m1 = dist_sq(x1, y1, z1, b.x0, b.y0, b.z0);
+  m0 = inline_min(a, x0, y0, z0);
+  m1 = inline_min(b, x1, y1, z1);
   const int nmax = max(na, nb);
   for (int k = 0; k < nmax; ++k) {
     if (k < na) {
@@ -192,16 +205,14 @@ __device__ __forceinline__ void min_dist_sqM(const PocketView& pk, const double*
   int nmax = 0;
 #pragma unroll
   for (int r = 0; r < M; ++r) {
-    m[r] = dist_sq(x[r], y[r], z[r], a[r].x0, a[r].y0, a[r].z0);
-    if (a[r].lst) {
-      nmax = max(nmax, a[r].count - 1);
-      w.add(kPairs, a[r].count);
-    }
+    m[r] = inline_min(a[r], x[r], y[r], z[r]);
+    nmax = max(nmax, listed(a[r]));
+    if (a[r].lst) w.add(kPairs, a[r].count);
   }
   for (int k = 0; k < nmax; ++k) {
 #pragma unroll
     for (int r = 0; r < M; ++r) {
-      if (a[r].lst && k < a[r].count - 1) {
+      if (k < listed(a[r])) {
         const P3 p = ldp(a[r].lst, k);
         m[r] = fmin(m[r], dist_sq(x[r], y[r], z[r], p.x, p.y, p.z));
       }

@@ -18,13 +18,22 @@ struct LigMeta {
   int32_t status;     // GD_LIG_*
 };
 
-// One level of the exact voxel candidate-list index.  Voxel v's 32-byte
-// record (one 256-bit load) is {int32 start, int32 count, x0, y0, z0}: the
-// first candidate inline, candidates 2..count at lst[start..start+count-1)
-// as 32-byte (x, y, z, pad) records.
+// One level of the exact voxel candidate-list index.  Voxel v's record is
+// {int32 start, int32 count, x0, y0, z0[, x1, y1, z1, pad]}: the first
+// kVoxInline candidates inline (a voxel with one candidate repeats it), the
+// rest at lst[start..) as 32-byte (x, y, z, pad) records.  Two inline
+// candidates (a 64-byte record, two independent 256-bit loads) spare most
+// queries their dependent list load but double the record traffic; on
+// config 1 that is 7% slower, so one is the default.
+#ifndef GD_VOX_INLINE
+#define GD_VOX_INLINE 1
+#endif
+constexpr int kVoxInline = GD_VOX_INLINE;
+static_assert(kVoxInline == 1 || kVoxInline == 2, "1 or 2 inline candidates");
+constexpr int kRecDoubles = kVoxInline == 1 ? 4 : 8;
 struct GridLevel {
-  const double* rec;       // [nvox*4] voxel records
-  const double* lst;       // [(ncand-nvox)*4] further candidates, voxel-major
+  const double* rec;       // [nvox*kRecDoubles] voxel records
+  const double* lst;       // [sum max(count-kVoxInline,0) * 4] further candidates, voxel-major
   double lo_x, lo_y, lo_z; // grid origin
   double inv_h;            // 1 / voxel edge
   int32_t dim_x, dim_y, dim_z;
@@ -120,8 +129,9 @@ struct VoxelGrid {
   int32_t dim_x, dim_y, dim_z;
 };
 // counts[v] = candidates of voxel v (>= 1); the fill pass writes each
-// voxel's record and its candidates 2..count at the host-scanned list
-// offsets (sum over earlier voxels of count - 1).
+// voxel's record and its candidates past the inline ones at the
+// host-scanned list offsets (sum over earlier voxels of
+// max(count - kVoxInline, 0)).
 int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, void* stream);
 int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
                       double* lst, void* stream);

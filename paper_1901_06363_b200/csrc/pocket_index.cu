@@ -120,14 +120,18 @@ __global__ void voxel_fill_kernel(const double* pts, int P, VoxelGrid g, const i
   const int k = voxel_list(pts, P, g, v, cand);
   const int len = k < 0 ? P : k;  // >= 1: the nearest point always survives
   const int start = offsets[v];
-  double* r = rec + 4 * static_cast<size_t>(v);
+  double* r = rec + kRecDoubles * static_cast<size_t>(v);
   reinterpret_cast<int2*>(r)[0] = make_int2(start, len);
-  const int j0 = k < 0 ? 0 : cand[0];
-  for (int c = 0; c < 3; ++c) r[1 + c] = pts[4 * j0 + c];
-  double* out = lst + 4 * static_cast<size_t>(start);
-  for (int a = 1; a < len; ++a) {
+  for (int q = 0; q < kVoxInline; ++q) {
+    const int a = min(q, len - 1);  // one candidate: repeat it
     const int j = k < 0 ? a : cand[a];
-    for (int c = 0; c < 4; ++c) out[4 * (a - 1) + c] = pts[4 * j + c];
+    for (int c = 0; c < 3; ++c) r[1 + 3 * q + c] = pts[4 * j + c];
+  }
+  if (kRecDoubles == 8) r[7] = 0.0;
+  double* out = lst + 4 * static_cast<size_t>(start);
+  for (int a = kVoxInline; a < len; ++a) {
+    const int j = k < 0 ? a : cand[a];
+    for (int c = 0; c < 4; ++c) out[4 * (a - kVoxInline) + c] = pts[4 * j + c];
   }
 }
 
