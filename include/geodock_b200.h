@@ -145,6 +145,42 @@ int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs);
 int gd_download(gd_ctx* ctx, gd_result* result);
 int gd_last_timing(const gd_ctx* ctx, gd_timing* out);
 
+/* ---- rotation profiles (analysis) --------------------------------------- */
+/* rotation_profile (analysis.hpp:37-56) of every fragment of the batch staged
+ * by the last gd_upload (or gd_dock_batch), from each ligand's pose in that
+ * batch's xyz.
+ * Fragments are numbered ligand by ligand in the reference order (rotamer r
+ * -> left 2r, right 2r+1; kernel.hpp:221-227).  For fragment f and integer
+ * angle a: valid[360 f + a] = check_bumps of the pose with the fragment
+ * rotated by a degrees (angle 0 = the pose itself), scores[360 f + a] its
+ * overlap_score where valid and 0 elsewhere.  frag_offsets[L+1] receives
+ * the per-ligand fragment prefix (skipped ligands have none);
+ * relative_size[f] (nullable) Fragment::relative_size; status[L] (nullable)
+ * GD_LIG_* per ligand (GD_LIG_DEGENERATE: a fragment's axis is degenerate,
+ * its profile is all-invalid).  `capacity` is in fragments; twice the
+ * number of rotatable bonds always suffices. */
+int gd_rotation_profiles(gd_ctx* ctx, double* scores, uint8_t* valid, double* relative_size,
+                         int32_t* frag_offsets, int32_t* status, int64_t capacity);
+
+/* One peak of a rotation profile (analysis.hpp:25-29). */
+typedef struct {
+  int32_t start_angle;  /* first angle of the run (circular) */
+  int32_t width;        /* degrees */
+  double height_ratio;  /* (peak max - min) / delta, in [0, 1] */
+} gd_peak;
+/* detect_peaks (analysis.hpp:61-126) on one 360-angle profile: a peak is a
+ * maximal circularly-contiguous run of valid angles scoring strictly above
+ * min + delta/2; runs through 359 -> 0 merge.  peaks needs room for 180.
+ * Returns GD_ERR_INVALID when no angle is valid (the reference throws
+ * "detect_peaks: no feasible rotation"). */
+int gd_detect_peaks(const double* scores, const uint8_t* valid, double* delta_overlap,
+                    int32_t* best_peak_width, gd_peak* peaks, int32_t* n_peaks);
+/* tile_hit_probability (analysis.hpp:133-147): per tile size, the fraction
+ * of profiles whose best peak is wider than the tile and the two-phase
+ * evaluation count 360/tile + tile.  GD_ERR_INVALID on an empty dataset. */
+int gd_tile_hit_probability(const int32_t* best_peak_widths, int64_t n, const int32_t* tiles,
+                            int32_t n_tiles, double* probability, double* eval_count);
+
 /* Device-resident results of the last gd_dock_resident (valid until the
  * next dock call): [n_ligands*top_k] in final order.  Lets a multi-GPU host
  * gather per-ligand top-K tables over NCCL without a host round trip. */
@@ -162,6 +198,14 @@ int gd_device_results(const gd_ctx* ctx, gd_device_result* out);
  * atoms, bump pairs, nearest-point queries, score-sum terms, candidate
  * evaluations, rigid-transformed atoms}.  DESIGN.md §4 turns them into FLOPs. */
 int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]);
+/* Diagnostic: SM clock cycles the flex kernel's warps spent per phase in
+ * the last GD_FLAG_COUNT_WORK call, summed over warps: out[0] chain start,
+ * [1] step setup (axis, fragment list, prefix), [2] bump-pair prefilter,
+ * [3] term pre-fill, [4] bump checks, [5] nearest-point queries, [6] score
+ * folds, [7] search decisions, [8] commit.  All zero unless the library was
+ * built with -DGD_PHASE_CLOCKS=1 (GD_DEFS); the clocks cost registers, so
+ * such builds are for attribution, not timing. */
+int gd_phase_clocks(const gd_ctx* ctx, uint64_t out[16]);
 /* Measures this device's fp64 DADD/DMUL issue rate (TFLOP/s, no FMA) with
  * a probe kernel; the denominator of the fp64 roofline. */
 int gd_fp64_peak(gd_ctx* ctx, double* tflops);

@@ -680,3 +680,43 @@ int gdo_rotate_fragment(int n, const double* xyz, const double* radii, int nb, c
   free(rad);
   return rc;
 }
+
+/* rotation_profile (analysis.hpp:37-56) of every fragment of one ligand,
+ * from the pose `xyz` (reference fragment order): for angle a, valid =
+ * check_bumps of the pose with the fragment rotated by a degrees (angle 0 =
+ * the pose itself) and score = overlap_score where valid, 0 elsewhere.
+ * Writes *nfrag; returns 0, GD_LIG_INVALID, GD_LIG_DEGENERATE (that
+ * fragment's profile left all-invalid), or -1 when cap < *nfrag. */
+int gdo_rotation_profiles(int n, const double* xyz, const double* radii, int nb,
+                          const int32_t* bonds, const uint8_t* rot, const double* pocket, int P,
+                          double* scores, uint8_t* valid, double* rel, int cap, int* nfrag) {
+  olig L;
+  double* rad = (double*)malloc(sizeof(double) * (n > 0 ? n : 1));
+  if (n > 0) memcpy(rad, radii, sizeof(double) * n);
+  int rc = olig_build(&L, n, xyz, rad, nb, bonds, rot);
+  *nfrag = rc == 0 ? L.nfrag : 0;
+  if (rc == 0 && L.nfrag > cap) rc = -1;
+  double* cand = (double*)malloc(sizeof(double) * 3 * (n > 0 ? n : 1));
+  for (int f = 0; rc >= 0 && f < *nfrag; ++f) {
+    rel[f] = L.frel[f];
+    for (int a = 0; a < 360; ++a) {
+      double* sc = scores + 360 * f + a;
+      uint8_t* ok = valid + 360 * f + a;
+      *sc = 0.0;
+      *ok = 0;
+      if (rotate_into(&L, xyz, f, (double)a, cand)) {
+        rc = GD_LIG_DEGENERATE;
+        memset(valid + 360 * f, 0, 360);
+        for (int b = 0; b < 360; ++b) scores[360 * f + b] = 0.0;
+        break;
+      }
+      if (!bumps_ok(&L, cand, f)) continue;
+      *ok = 1;
+      *sc = gdo_overlap_score(cand, n, pocket, P);
+    }
+  }
+  free(cand);
+  olig_free(&L);
+  free(rad);
+  return rc;
+}

@@ -63,6 +63,9 @@ def oracle() -> C.CDLL:
         h.gdo_orientations.argtypes = [C.c_int, C.POINTER(_i32p), C.POINTER(_f64p)]
         h.gdo_pocket_centre.argtypes = [_f64p, C.c_int, _f64p]
         h.gdo_free.argtypes = [C.c_void_p]
+        h.gdo_rotation_profiles.argtypes = [C.c_int, _f64p, _f64p, C.c_int, _i32p, _u8p, _f64p,
+                                            C.c_int, _f64p, _u8p, _f64p, C.c_int,
+                                            C.POINTER(C.c_int)]
         _oracle = h
     return _oracle
 
@@ -95,6 +98,13 @@ def ref() -> C.CDLL:
         h.gdref_dock_batch.argtypes = [C.POINTER(gd_ligand_batch), _f64p, C.c_int,
                                        C.POINTER(gd_knobs), C.c_int, C.c_int,
                                        C.POINTER(gd_result)]
+        h.gdref_rotation_profiles.restype = C.c_longlong
+        h.gdref_rotation_profiles.argtypes = [C.POINTER(gd_ligand_batch), _f64p, C.c_int, C.c_int,
+                                              C.c_int, _f64p, _u8p, _f64p, _i32p, _i32p,
+                                              C.c_longlong]
+        h.gdref_detect_peaks.argtypes = [_f64p, _u8p, _f64p, C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int), _i32p, _i32p, _f64p]
+        h.gdref_tile_hits.argtypes = [_i32p, C.c_int, _i32p, C.c_int, _f64p, _f64p]
         _ref = h
     return _ref
 
@@ -198,6 +208,73 @@ def rotate_fragment(xyz, radii, bonds, rot, pose, f: int, angle: float, impl: st
         msg = ref().gdref_last_error().decode() if impl != "oracle" else f"oracle error {rc}"
         raise RuntimeError(msg)
     return out, bool(feas.value)
+
+
+def rotation_profiles(batch: LigandBatch, pocket: np.ndarray, impl: str = "oracle",
+                      nthreads: int = 1):
+    """rotation_profile (analysis.hpp:37-56) of every fragment of every ligand
+    from its batch pose, laid out like gd_rotation_profiles: returns
+    (scores [F,360], valid [F,360] bool, relative_size [F], frag_offsets
+    [L+1], status [L]).  impl 'oracle' = C restatement (brute force), 'ref'
+    = the reference's own rotation_profile with its PocketIndex."""
+    pk = np.ascontiguousarray(pocket, dtype=np.float64)
+    L = batch.n_ligands
+    cap = max(1, 2 * int(batch.rotatable.sum()))
+    scores = np.zeros((cap, 360), np.float64)
+    valid = np.zeros((cap, 360), np.uint8)
+    rel = np.zeros(cap, np.float64)
+    offs = np.zeros(L + 1, np.int32)
+    status = np.zeros(max(L, 1), np.int32)
+    if impl == "oracle":
+        nfrag = C.c_int()
+        for l in range(L):
+            xyz, radii, bonds, rot = batch.ligand(l)
+            o = int(offs[l])
+            rc = oracle().gdo_rotation_profiles(
+                len(xyz), _p(xyz, _f64p), _p(radii, _f64p), len(bonds), _p(bonds, _i32p),
+                _p(rot, _u8p), _p(pk, _f64p), len(pk), _p(scores[o:], _f64p), _p(valid[o:], _u8p),
+                _p(rel[o:], _f64p), cap - o, C.byref(nfrag))
+            if rc < 0:
+                raise RuntimeError("rotation_profiles: capacity")
+            status[l] = rc
+            offs[l + 1] = o + nfrag.value
+    else:
+        b = batch.c_struct()
+        n = ref().gdref_rotation_profiles(C.byref(b), _p(pk, _f64p), len(pk), 1, nthreads,
+                                          _p(scores, _f64p), _p(valid, _u8p), _p(rel, _f64p),
+                                          _p(offs, _i32p), _p(status, _i32p), cap)
+        if n < 0:
+            raise RuntimeError("rotation_profiles: capacity")
+    F = int(offs[-1])
+    return scores[:F], valid[:F].astype(bool), rel[:F], offs, status[:L]
+
+
+def ref_detect_peaks(scores, valid):
+    """The reference detect_peaks (analysis.hpp:61-126): (delta, best_peak_width,
+    [(start, width, height_ratio), ...]) or None when it throws."""
+    s = np.ascontiguousarray(scores, dtype=np.float64)
+    v = np.ascontiguousarray(valid, dtype=np.uint8)
+    d, bw, npk = C.c_double(), C.c_int(), C.c_int()
+    st = np.zeros(360, np.int32)
+    wd = np.zeros(360, np.int32)
+    ht = np.zeros(360, np.float64)
+    if ref().gdref_detect_peaks(_p(s, _f64p), _p(v, _u8p), C.byref(d), C.byref(bw), C.byref(npk),
+                                _p(st, _i32p), _p(wd, _i32p), _p(ht, _f64p)):
+        return None
+    k = npk.value
+    return d.value, bw.value, [(int(st[i]), int(wd[i]), float(ht[i])) for i in range(k)]
+
+
+def ref_tile_hits(best_widths, tiles):
+    """The reference tile_hit_probability (analysis.hpp:133-147)."""
+    bw = np.ascontiguousarray(best_widths, dtype=np.int32)
+    t = np.ascontiguousarray(tiles, dtype=np.int32)
+    prob = np.zeros(len(t))
+    ev = np.zeros(len(t))
+    if ref().gdref_tile_hits(_p(bw, _i32p), len(bw), _p(t, _i32p), len(t), _p(prob, _f64p),
+                             _p(ev, _f64p)):
+        raise RuntimeError(ref().gdref_last_error().decode())
+    return prob, ev
 
 
 def orientations(step: int):

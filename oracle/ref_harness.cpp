@@ -10,16 +10,22 @@
 //     optional geodock::PocketIndex and a std::thread pool like
 //     geodock::screen (screening.hpp:96-178).  This is bench.py's reference
 //     arm and the generator of tests/golden fixtures.
+//   * gdref_rotation_profiles / gdref_detect_peaks / gdref_tile_hits: the
+//     reference analysis (analysis.hpp:37-147) over a batch, in the layout
+//     of gd_rotation_profiles -- the parity anchor of that C-ABI entry.
 //   * fine-grained wrappers for known-answer tests.
 // Only the Eigen-free headers are included.
 #include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <cstring>
+#include <memory>
+#include <optional>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "geodock/analysis.hpp"
 #include "geodock/geometry.hpp"
 #include "geodock/kernel.hpp"
 #include "geodock/molecule.hpp"
@@ -305,4 +311,119 @@ extern "C" int gdref_dock_batch(const gd_ligand_batch* b, const double* pocket, 
   gdo_free(oidx);
   gdo_free(oR);
   return 0;
+}
+
+// geodock::rotation_profile of every fragment of every ligand, from each
+// ligand's batch pose, numbered like gd_rotation_profiles (ligand order,
+// rotamer r -> left 2r, right 2r+1).  A ligand that fails the Ligand ctor
+// gets status 1 and no fragments; a fragment whose rotation throws
+// (degenerate axis) sets status 3 and is reported all-invalid.  Returns the
+// number of fragments, or -1 when `capacity` is too small.
+extern "C" long long gdref_rotation_profiles(const gd_ligand_batch* b, const double* pocket, int P,
+                                             int use_index, int threads, double* scores,
+                                             uint8_t* valid, double* rel, int32_t* frag_offsets,
+                                             int32_t* status, long long capacity) {
+  const geodock::Pocket pk = make_pocket(pocket, P);
+  std::unique_ptr<geodock::PocketIndex> index;
+  if (use_index) index = std::make_unique<geodock::PocketIndex>(pk);
+  const int L = b->n_ligands;
+  std::vector<std::optional<geodock::Ligand>> ligs(L);
+  std::vector<std::vector<geodock::Rotamer>> rots(L);
+  frag_offsets[0] = 0;
+  for (int l = 0; l < L; ++l) {
+    const int a0 = b->atom_offsets[l], n = b->atom_offsets[l + 1] - a0;
+    const int b0 = b->bond_offsets[l], nb = b->bond_offsets[l + 1] - b0;
+    status[l] = GD_LIG_OK;
+    try {
+      ligs[l].emplace(make_ligand("L" + std::to_string(l), n, b->xyz + 3 * a0, b->radii + a0, nb,
+                                  b->bonds + 2 * b0, b->bond_rotatable + b0));
+      rots[l] = geodock::find_rotamers(*ligs[l]);
+    } catch (const std::exception&) {
+      ligs[l].reset();
+      status[l] = GD_LIG_INVALID;
+    }
+    frag_offsets[l + 1] = frag_offsets[l] + (ligs[l] ? 2 * static_cast<int>(rots[l].size()) : 0);
+  }
+  if (frag_offsets[L] > capacity) return -1;
+  std::atomic<int> next{0};
+  auto work = [&] {
+    for (int l; (l = next.fetch_add(1)) < L;) {
+      if (!ligs[l]) continue;
+      const geodock::Ligand& lig = *ligs[l];
+      const geodock::Pose pose = geodock::make_initial_pose(lig);
+      for (size_t ri = 0; ri < rots[l].size(); ++ri) {
+        const auto frags = geodock::grow_fragments(lig, rots[l][ri]);
+        const geodock::Fragment* fs[2] = {&frags.first, &frags.second};
+        for (int side = 0; side < 2; ++side) {
+          const long long f = frag_offsets[l] + 2 * static_cast<long long>(ri) + side;
+          rel[f] = fs[side]->relative_size;
+          try {
+            const geodock::RotationProfile pr =
+                geodock::rotation_profile(pose, lig, *fs[side], pk, index.get());
+            for (int a = 0; a < 360; ++a) {
+              scores[360 * f + a] = pr.scores[a];
+              valid[360 * f + a] = pr.valid[a] ? 1 : 0;
+            }
+          } catch (const std::exception&) {
+            status[l] = GD_LIG_DEGENERATE;
+            for (int a = 0; a < 360; ++a) {
+              scores[360 * f + a] = 0.0;
+              valid[360 * f + a] = 0;
+            }
+          }
+        }
+      }
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < std::max(1, threads); ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+  return frag_offsets[L];
+}
+
+// geodock::detect_peaks on one profile.  Returns 0, or 1 when it throws (no
+// feasible rotation; message in gdref_last_error()).  Peaks go to
+// starts/widths/heights (capacity 360, ordered as the reference orders them).
+extern "C" int gdref_detect_peaks(const double* scores, const uint8_t* valid, double* delta,
+                                  int* best_width, int* n_peaks, int32_t* starts, int32_t* widths,
+                                  double* heights) {
+  geodock::RotationProfile pr;
+  for (int a = 0; a < 360; ++a) {
+    pr.scores[a] = scores[a];
+    pr.valid[a] = valid[a] != 0;
+  }
+  try {
+    const geodock::PeakStats st = geodock::detect_peaks(pr);
+    *delta = st.delta_overlap;
+    *best_width = st.best_peak_width;
+    *n_peaks = static_cast<int>(st.peaks.size());
+    for (size_t k = 0; k < st.peaks.size(); ++k) {
+      starts[k] = st.peaks[k].start_angle;
+      widths[k] = st.peaks[k].width;
+      heights[k] = st.peaks[k].height_ratio;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// geodock::tile_hit_probability over datasets given by their best peak widths.
+extern "C" int gdref_tile_hits(const int32_t* best_widths, int n, const int32_t* tiles, int nt,
+                               double* probability, double* eval_count) {
+  std::vector<geodock::PeakStats> ds(n);
+  for (int i = 0; i < n; ++i) ds[i].best_peak_width = best_widths[i];
+  try {
+    const auto hits = geodock::tile_hit_probability(ds, std::vector<int>(tiles, tiles + nt));
+    for (int k = 0; k < nt; ++k) {
+      probability[k] = hits[k].probability;
+      eval_count[k] = hits[k].eval_count;
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
 }

@@ -10,6 +10,7 @@ BASELINE workload definitions (``workloads.py``).
 from .native import (  # noqa: F401
     Docker,
     DockResult,
+    Profiles,
     GeoDockError,
     Knobs,
     LigandBatch,

@@ -116,6 +116,8 @@ struct gd_ctx {
   bool have_result = false;
   DevBuf counters;
   bool counted = false;
+  DevBuf prof_items, prof_scores, prof_valid;
+  bool staged = false;  // a batch is staged (gd_upload / gd_dock_batch)
   DevBuf st_final, st_evals, st_checks;
   DevBuf seed_slot, seed_score, k_eff, o_orient, o_rank, o_rigid, o_final, o_evals, o_checks,
       o_pose, stage_pose, o_scored, o_status;
@@ -448,6 +450,7 @@ static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
   ctx->total_atoms = A;
   ctx->max_n = 1;
   ctx->have_result = false;
+  ctx->staged = false;
   ctx->timing = gd_timing{};
   run = Running{};
   return GD_OK;
@@ -568,6 +571,7 @@ extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
   rc = h2d_range(ctx, 0, ctx->n_lig, Running{}, run, ctx->stream);
   if (rc != GD_OK) return rc;
   cudaEventRecord(ctx->ev[1], ctx->stream);
+  ctx->staged = true;
   return GD_OK;
 }
 
@@ -673,8 +677,8 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockPara
   p.status = ctx->o_status.as<int32_t>();
   p.counters = nullptr;
   if (k->flags & GD_FLAG_COUNT_WORK) {
-    GD_CUDA(ctx, ctx->counters.ensure(sizeof(unsigned long long) * 16));
-    GD_CUDA(ctx, cudaMemset(ctx->counters.ptr, 0, sizeof(unsigned long long) * 16));
+    GD_CUDA(ctx, ctx->counters.ensure(sizeof(unsigned long long) * kCounterSlots));
+    GD_CUDA(ctx, cudaMemset(ctx->counters.ptr, 0, sizeof(unsigned long long) * kCounterSlots));
     p.counters = ctx->counters.as<unsigned long long>();
   }
   ctx->counted = p.counters != nullptr;
@@ -876,6 +880,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->aux_stream));
   ctx->have_result = true;
+  ctx->staged = true;
   const auto t_post = std::chrono::steady_clock::now();
   auto copy = [](void* dst, const void* src, size_t bytes) {
     if (dst && src) std::memcpy(dst, src, bytes);
@@ -897,6 +902,73 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   return GD_OK;
 }
 
+extern "C" int gd_rotation_profiles(gd_ctx* ctx, double* scores, uint8_t* valid,
+                                    double* relative_size, int32_t* frag_offsets, int32_t* status,
+                                    int64_t capacity) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  if (!ctx->staged) return ctx->fail(GD_ERR_INVALID, "gd_rotation_profiles: no batch staged (gd_upload)");
+  if (ctx->P == 0)
+    return ctx->fail(GD_ERR_NO_POCKET, "gd_rotation_profiles: no pocket staged (gd_set_pocket)");
+  if (frag_offsets == nullptr || (capacity > 0 && (scores == nullptr || valid == nullptr)))
+    return ctx->fail(GD_ERR_INVALID, "gd_rotation_profiles: null output");
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int L = ctx->n_lig;
+  const auto* meta = reinterpret_cast<const LigMeta*>(ctx->pin[kMeta]);
+  const auto* hrel = reinterpret_cast<const double*>(ctx->pin[kFrel]);
+  std::vector<int32_t> items;
+  frag_offsets[0] = 0;
+  for (int l = 0; l < L; ++l) {
+    const int nf = ctx->status_host[l] == 0 ? meta[l].nfrag : 0;
+    for (int f = 0; f < nf; ++f) {
+      items.push_back(l);
+      items.push_back(f);
+    }
+    frag_offsets[l + 1] = frag_offsets[l] + nf;
+  }
+  const int64_t n_items = static_cast<int64_t>(items.size() / 2);
+  if (n_items > capacity) {
+    return ctx->fail(GD_ERR_INVALID, "gd_rotation_profiles: capacity " + std::to_string(capacity) +
+                                         " < " + std::to_string(n_items) + " fragments");
+  }
+  if (relative_size)
+    for (int64_t it = 0; it < n_items; ++it)
+      relative_size[it] = hrel[meta[items[2 * it]].frag_off + items[2 * it + 1]];
+  if (n_items > 0) {
+    GD_CUDA(ctx, ctx->prof_items.ensure(sizeof(int32_t) * items.size()));
+    GD_CUDA(ctx, ctx->prof_scores.ensure(sizeof(double) * 360 * n_items));
+    GD_CUDA(ctx, ctx->prof_valid.ensure(360 * n_items));
+    GD_CUDA(ctx, cudaMemcpyAsync(ctx->prof_items.ptr, items.data(), sizeof(int32_t) * items.size(),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+    DockParams p{};
+    p.meta = ctx->meta.as<LigMeta>();
+    p.xyz = ctx->xyz.as<double>();
+    p.radii = ctx->radii.as<double>();
+    p.far_mask = ctx->far.as<uint64_t>();
+    p.frag_mask = ctx->fmask.as<uint64_t>();
+    p.frag_axis = ctx->fax.as<int32_t>();
+    p.frag_anchor = ctx->fan.as<int32_t>();
+    p.frag_rel = ctx->frel.as<double>();
+    p.pocket = ctx->view;
+    p.cos_deg = ctx->cos_t.as<double>();
+    p.sin_deg = ctx->sin_t.as<double>();
+    p.max_n = ctx->max_n;
+    p.max_pairs = std::max(1, ctx->max_n * ctx->max_n / 4);
+    p.status = ctx->o_status.as<int32_t>();
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_profiles(
+                     p, ctx->prof_items.as<int32_t>(), static_cast<int>(n_items),
+                     ctx->prof_scores.as<double>(), ctx->prof_valid.as<uint8_t>(), ctx->stream)));
+    GD_CUDA(ctx, cudaMemcpyAsync(scores, ctx->prof_scores.ptr, sizeof(double) * 360 * n_items,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    GD_CUDA(ctx, cudaMemcpyAsync(valid, ctx->prof_valid.ptr, 360 * n_items, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+  }
+  if (status && L > 0)
+    GD_CUDA(ctx, cudaMemcpyAsync(status, ctx->o_status.ptr, sizeof(int32_t) * L,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}
+
 extern "C" int gd_device_results(const gd_ctx* ctx, gd_device_result* out) {
   if (ctx == nullptr || out == nullptr || !ctx->have_result) return GD_ERR_INVALID;
   out->orientation = ctx->o_orient.as<int32_t>();
@@ -912,6 +984,15 @@ extern "C" int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]) {
   if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
   if (!ctx->counted) return GD_ERR_INVALID;
   if (cudaMemcpy(out, ctx->counters.ptr, sizeof(uint64_t) * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+    return GD_ERR_CUDA;
+  return GD_OK;
+}
+
+extern "C" int gd_phase_clocks(const gd_ctx* ctx, uint64_t out[16]) {
+  if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
+  if (!ctx->counted) return GD_ERR_INVALID;
+  if (cudaMemcpy(out, ctx->counters.as<unsigned long long>() + kPhaseBase, sizeof(uint64_t) * 16,
+                 cudaMemcpyDeviceToHost) != cudaSuccess)
     return GD_ERR_CUDA;
   return GD_OK;
 }

@@ -40,6 +40,15 @@ namespace {
 #ifndef GD_FLEX_BATCH
 #define GD_FLEX_BATCH 4      // candidates evaluated together by one warp
 #endif
+#ifndef GD_BUMP_ILP2
+#define GD_BUMP_ILP2 0       // bump phase: two pairs per lane per iteration (A/B: no gain)
+#endif
+#ifndef GD_QUERY_MLP
+#define GD_QUERY_MLP 2       // lookups in flight per lane (3, 4 spill: measured slower)
+#endif
+#ifndef GD_PHASE_CLOCKS
+#define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
+#endif
 constexpr int kWarps = 4;    // chains per CTA
 constexpr int kBatch = GD_FLEX_BATCH;
 constexpr unsigned kFull = 0xffffffffu;
@@ -116,19 +125,79 @@ __device__ __forceinline__ int qdiv(int t, float rcp) {
   return static_cast<int>((static_cast<float>(t) + 0.5f) * rcp);
 }
 
+// Per-phase SM-clock attribution of a chain (diagnostic builds only; the
+// disabled form compiles to nothing).
+enum Phase { kPhInit, kPhSetup, kPhPrefilter, kPhPrefill, kPhBump, kPhQuery, kPhFold, kPhDecide,
+             kPhCommit, kPhases };
+template <bool On>
+struct Clocks {
+  long long last;
+  unsigned long long acc[kPhases];
+  __device__ Clocks() {
+    if constexpr (On) {
+      last = clock64();
+      for (int k = 0; k < kPhases; ++k) acc[k] = 0;
+    }
+  }
+  __device__ __forceinline__ void mark(int k) {
+    if constexpr (On) {
+      const long long t = clock64();
+      acc[k] += static_cast<unsigned long long>(t - last);
+      last = t;
+    }
+  }
+  __device__ void publish(unsigned long long* c, int lane) const {
+    if constexpr (On) {
+      if (c != nullptr && lane == 0)
+        for (int k = 0; k < kPhases; ++k) atomicAdd(c + kPhaseBase + k, acc[k]);
+    }
+  }
+};
+
 // Evaluates candidates angle(c) = a0 + c*da, c < nb, of the current fragment
 // (CandidateEvaluator::evaluate, kernel.hpp:100-112).  Returns, in lane c,
 // candidate c's overlap score (cur for angle 0), and warp-uniformly the
 // mask of candidates that bumped.
-template <bool On>
+template <bool On, class CK>
 __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X, int n, int nf,
                            int np, int first, double pre, double cur, int a0, int da, int nb,
-                           int lane, double& score_out, unsigned& bumped_out, Work<On>& wk) {
+                           int lane, double& score_out, unsigned& bumped_out, Work<On>& wk,
+                           CK& ck) {
+  ck.mark(kPhDecide);
   const unsigned zero = (a0 == 0) ? 1u : 0u;  // only c = 0 can be angle 0
   // Bump phase.
   unsigned bl = 0;
   const int total = nb * np;
   const float rnp = 1.0f / static_cast<float>(max(np, 1));
+#if GD_BUMP_ILP2
+  // Two pairs per lane per iteration (t, t + 32): independent dependency
+  // chains for the fp64 pipe.
+  for (int t = lane; t < total; t += 64) {
+    const int t1 = t + 32;
+    const int c0 = qdiv(t, rnp);
+    const int c1 = t1 < total ? qdiv(t1, rnp) : c0;
+    const bool d0 = !(((bl | zero) >> c0) & 1u);
+    const bool d1 = t1 < total && !(((bl | zero) >> c1) & 1u);
+    if (!d0 && !d1) continue;
+    const int ta = d0 ? t : t1, ca = d0 ? c0 : c1;
+    const int tb = d1 ? t1 : ta, cb = d1 ? c1 : ca;
+    const int pa = s.pairs[ta - ca * np], pb = s.pairs[tb - cb * np];
+    const int ia = pa & 0xff, ja = pa >> 8, ib = pb & 0xff, jb = pb >> 8;
+    const int aa = a0 + ca * da, ab = a0 + cb * da;
+    const double csa = __ldg(p.cos_deg + aa), sna = __ldg(p.sin_deg + aa);
+    const double csb = __ldg(p.cos_deg + ab), snb = __ldg(p.sin_deg + ab);
+    const PT ai = s.pt[ia], aj = s.pt[ja], bi = s.pt[ib], bj = s.pt[jb];
+    double xa, ya, za, xb, yb, zb;
+    rodrigues(X, csa, sna, dsub(1.0, csa), ai.x, ai.y, ai.z, xa, ya, za);
+    rodrigues(X, csb, snb, dsub(1.0, csb), bi.x, bi.y, bi.z, xb, yb, zb);
+    wk.add(kRot, (d0 ? 1 : 0) + (d1 ? 1 : 0));
+    wk.add(kBump, (d0 ? 1 : 0) + (d1 ? 1 : 0));
+    const double cuta = dmul(kBumpScale, dadd(s.radius[ia], s.radius[ja]));
+    const double cutb = dmul(kBumpScale, dadd(s.radius[ib], s.radius[jb]));
+    if (dist_sq(xa, ya, za, aj.x, aj.y, aj.z) < dmul(cuta, cuta)) bl |= 1u << ca;
+    if (dist_sq(xb, yb, zb, bj.x, bj.y, bj.z) < dmul(cutb, cutb)) bl |= 1u << cb;
+  }
+#else
   for (int t = lane; t < total; t += 32) {
     const int c = qdiv(t, rnp);
     if (((bl | zero) >> c) & 1u) continue;
@@ -144,9 +213,12 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
     const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
     if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < dmul(cut, cut)) bl |= 1u << c;
   }
+#endif
   const unsigned bumped = __reduce_or_sync(kFull, bl);
   const unsigned live = ((1u << nb) - 1u) & ~bumped & ~zero;
+  ck.mark(kPhBump);
   // Query phase.
+#if GD_QUERY_MLP == 2
   // Two items per lane per iteration (t, t+32): both lookups in flight.
   const int tq = nb * nf;
   const float rnf = 1.0f / static_cast<float>(nf);
@@ -169,7 +241,41 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
     if (l0) s.v[c0 * n + i0] = fmax(kMinDistanceSq, m0);
     if (l1) s.v[c1 * n + i1] = fmax(kMinDistanceSq, m1);
   }
+#else
+  // M items per lane per iteration (t + 32 r): all M lookups in flight.
+  constexpr int M = GD_QUERY_MLP;
+  const int tq = nb * nf;
+  const float rnf = 1.0f / static_cast<float>(nf);
+  for (int t = lane; t < tq; t += 32 * M) {
+    int cc[M], ii[M];
+    bool ll[M];
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      const int tr = t + 32 * r < tq ? t + 32 * r : t;
+      cc[r] = qdiv(tr, rnf);
+      ll[r] = (r == 0 || tr != t) && ((live >> cc[r]) & 1u);
+      ii[r] = s.fidx[tr - cc[r] * nf];
+      any |= ll[r];
+    }
+    if (!any) continue;
+    double x[M], y[M], z[M], m[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      const int a = a0 + cc[r] * da;
+      const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
+      const PT q = s.pt[ii[r]];
+      rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x[r], y[r], z[r]);
+    }
+    wk.add(kRot, M);
+    min_dist_sqM<M>(p.pocket, x, y, z, m, wk);
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+      if (ll[r]) s.v[cc[r] * n + ii[r]] = fmax(kMinDistanceSq, m[r]);
+  }
+#endif
   __syncwarp();
+  ck.mark(kPhQuery);
   // Fold phase: lane c, atom order.
   double score = cur;
   if (lane < nb && ((live >> lane) & 1u)) {
@@ -182,6 +288,7 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
     wk.add(kEvals, 1);
   }
   __syncwarp();
+  ck.mark(kPhFold);
   score_out = score;
   bumped_out = bumped;
 }
@@ -196,6 +303,176 @@ __device__ void publish_warp(const Work<On>& w, unsigned long long* c, int base,
       if (lane == 0) atomicAdd(c + base + k, static_cast<unsigned long long>(s));
     }
   }
+}
+
+// Fragment step setup, shared by the search and the profile kernels: the
+// fragment mask, the rotation axis (rotate_fragment_into, geometry.hpp:
+// 165-169, identical in every lane), the ascending fragment atoms, the fold
+// prefix of the atoms before the first fragment atom, the surviving bump
+// pairs and the per-candidate pre-fill of the non-fragment terms.  `left_np`
+// carries a left step's pair count to its right step (-1: rebuild).
+// Returns false on a degenerate axis.
+struct StepInfo {
+  Axis X;
+  int nf, first, np;
+  double pre;
+};
+
+template <class CK>
+__device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p, const LigMeta& m,
+                                           int f, int axis, int anchor, int lane, int& left_np,
+                                           StepInfo& st, CK& ck) {
+  const int n = m.n, W = m.words;
+  if (lane < W) s.fm[lane] = __ldg(p.frag_mask + m.fmask_off + f * W + lane);
+  // rotate_fragment_into axis (geometry.hpp:165-169), identical in every lane.
+  const PT pa = s.pt[axis], pb = s.pt[anchor];
+  const double ox = pa.x, oy = pa.y, oz = pa.z;
+  const double ax = dsub(pb.x, ox), ay = dsub(pb.y, oy), az = dsub(pb.z, oz);
+  const double len = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
+  if (len < kMinAxisLength) return false;  // "rotate_fragment: degenerate rotation axis"
+  st.X = Axis{ox, oy, oz, __ddiv_rn(ax, len), __ddiv_rn(ay, len), __ddiv_rn(az, len)};
+  const Axis& X = st.X;
+  __syncwarp();
+  // Fragment atoms, ascending.
+  int nf = 0;
+  for (int b = 0; b < n; b += 32) {
+    const int i = b + lane;
+    const bool in = i < n && in_frag(s.fm, i);
+    const unsigned mask = __ballot_sync(kFull, in);
+    if (in) s.fidx[nf + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint8_t>(i);
+    nf += __popc(mask);
+  }
+  __syncwarp();
+  const int first = s.fidx[0];
+  double pre = 0.0;
+  if (lane == 0)
+    for (int i = 0; i < first; ++i) pre = dadd(pre, s.pt[i].t);
+  pre = __shfl_sync(kFull, pre, 0);
+  ck.mark(kPhSetup);
+  // Surviving bump pairs: drop (i, j) when the circle atom i sweeps never
+  // comes within the cutoff of j: dmin^2 = h^2 + (sigma - rho)^2 > cut^2,
+  // tested without square roots as L = s2 + r2 + h2 - C > 0 && L^2 > 4 s2 r2.
+  // Per-atom axial coordinate a = k.(p - o) and squared axis distance
+  // r2 = |p - o|^2 - a^2 first, lane-parallel, in the (free) v scratch.
+  // The pair list holds (moving atom | fixed atom << 8).  A rotamer's
+  // right step reuses its left step's list with the roles swapped: both
+  // rotate about the same bond line, the left commit rotated the left
+  // atoms about that very line, and the circle test depends only on the
+  // atoms' axial and radial coordinates relative to it (rotation
+  // invariants).  The test itself is a conservative filter, so it runs
+  // in fp32 with a wide margin; the kept pairs are decided exactly.
+  int np = 0;
+  if ((f & 1) && left_np >= 0) {
+    np = left_np;
+    for (int t = lane; t < np; t += 32) {
+      const unsigned pr = s.pairs[t];
+      s.pairs[t] = static_cast<uint16_t>((pr >> 8) | ((pr & 0xffu) << 8));
+    }
+  } else {
+    float* axc = reinterpret_cast<float*>(s.v);
+    float* rad2 = axc + n;
+    float* rf = rad2 + n;
+    for (int i = lane; i < n; i += 32) {
+      const PT q = s.pt[i];
+      const double vx = q.x - ox, vy = q.y - oy, vz = q.z - oz;
+      const double a = X.kx * vx + X.ky * vy + X.kz * vz;
+      axc[i] = static_cast<float>(a);
+      rad2[i] = static_cast<float>(fmax(0.0, vx * vx + vy * vy + vz * vz - a * a));
+      rf[i] = static_cast<float>(s.radius[i]);
+    }
+    __syncwarp();
+    auto test = [&](int i, int j) {
+      const float h = axc[j] - axc[i];
+      const float s2 = rad2[j], r2 = rad2[i];
+      const float cut = 0.8f * (rf[i] + rf[j]);
+      const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
+      const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
+      return !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
+    };
+    if (W == 1) {
+      // Flattened over the actual partner pairs: per-slot partner counts,
+      // a warp prefix sum, then lane t finds its slot by binary search and
+      // its partner as the n-th set bit of the slot's partner mask.
+      int* pref = reinterpret_cast<int*>(rf + n);
+      const uint64_t nf0 = ~s.fm[0];
+      int total = 0;
+      for (int b = 0; b < nf; b += 32) {
+        const int sl = b + lane;
+        const int cnt = sl < nf ? __popcll(s.far[s.fidx[sl]] & nf0) : 0;
+        int inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(kFull, inc, o);
+          if (lane >= o) inc += y;
+        }
+        if (sl < nf) pref[sl] = total + inc - cnt;
+        total += __shfl_sync(kFull, inc, 31);
+      }
+      __syncwarp();
+      for (int t0 = 0; t0 < total; t0 += 32) {
+        const int t = t0 + lane;
+        bool keep = false;
+        int i = 0, j = 0;
+        if (t < total) {
+          int lo = 0, hi = nf - 1;  // last slot with pref <= t
+          while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (pref[mid] <= t) lo = mid; else hi = mid - 1;
+          }
+          i = s.fidx[lo];
+          const uint64_t m = s.far[i] & nf0;
+          j = nth_bit(m, t - pref[lo]);
+          keep = test(i, j);
+        }
+        const unsigned mask = __ballot_sync(kFull, keep);
+        if (keep)
+          s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
+        np += __popc(mask);
+      }
+    } else
+    for (int sl = 0; sl < nf; ++sl) {
+      const int i = s.fidx[sl];
+      const float ai = axc[i], r2 = rad2[i], ri = rf[i];
+      for (int b = 0; b < n; b += 32) {
+        // Partner bits of this 32-atom chunk; uniform skip when empty.
+        const unsigned chunk = static_cast<unsigned>(
+            (s.far[i * W + (b >> 6)] & ~s.fm[b >> 6]) >> (b & 63));
+        if (chunk == 0u) continue;
+        const int j = b + lane;
+        bool keep = false;
+        if (j < n && ((chunk >> lane) & 1u)) {
+          const float h = axc[j] - ai;
+          const float s2 = rad2[j];
+          const float cut = 0.8f * (ri + rf[j]);
+          const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
+          const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
+          keep = !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
+        }
+        const unsigned mask = __ballot_sync(kFull, keep);
+        if (keep)
+          s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
+        np += __popc(mask);
+      }
+    }
+  }
+  __syncwarp();
+  left_np = (f & 1) ? -1 : np;  // a left step's list serves its right step
+  ck.mark(kPhPrefilter);
+  // Non-fragment terms are the same for every candidate of this step:
+  // pre-fill them into each candidate slot so the fold is a plain sum.
+  for (int i = lane; i < n; i += 32)
+    if (!in_frag(s.fm, i)) {
+      const double t = s.pt[i].t;
+#pragma unroll
+      for (int c = 0; c < kBatch; ++c) s.v[c * n + i] = t;
+    }
+  __syncwarp();
+  ck.mark(kPhPrefill);
+  st.nf = nf;
+  st.first = first;
+  st.pre = pre;
+  st.np = np;
+  return true;
 }
 
 template <bool On>
@@ -214,6 +491,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       carve(smem + warp * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W, p.max_pairs);
   const size_t e = static_cast<size_t>(l) * p.top_k + r;
   Work<On> wk;
+  Clocks<On && GD_PHASE_CLOCKS> ck;
 
   for (int i = lane; i < n; i += 32) s.radius[i] = __ldg(p.radii + m.atom_off + i);
   for (int i = lane; i < n * W; i += 32) s.far[i] = __ldg(p.far_mask + m.far_off + i);
@@ -245,6 +523,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
   if (!p.rigid && lane == 0) p.seed_score[e] = cur;
   long long evals = 1, checks = 1;
   int left_np = -1;  // bump-pair count of the preceding left step, -1 if none
+  ck.mark(kPhInit);
 
   for (int rep = 0; rep < p.reps; ++rep) {
     for (int f = 0; f < m.nfrag; ++f) {
@@ -261,150 +540,14 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         left_np = -1;
         continue;
       }
-      if (lane < W) s.fm[lane] = __ldg(p.frag_mask + m.fmask_off + f * W + lane);
-      // rotate_fragment_into axis (geometry.hpp:165-169), identical in every lane.
-      const PT pa = s.pt[axis], pb = s.pt[anchor];
-      const double ox = pa.x, oy = pa.y, oz = pa.z;
-      const double ax = dsub(pb.x, ox), ay = dsub(pb.y, oy), az = dsub(pb.z, oz);
-      const double len = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
-      if (len < kMinAxisLength) {  // "rotate_fragment: degenerate rotation axis"
-        if (lane == 0) p.status[l] = 3;
+      StepInfo st;
+      if (!setup_step(s, p, m, f, axis, anchor, lane, left_np, st, ck)) {
+        if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
         return;
       }
-      const Axis X{ox, oy, oz, __ddiv_rn(ax, len), __ddiv_rn(ay, len), __ddiv_rn(az, len)};
-      __syncwarp();
-      // Fragment atoms, ascending.
-      int nf = 0;
-      for (int b = 0; b < n; b += 32) {
-        const int i = b + lane;
-        const bool in = i < n && in_frag(s.fm, i);
-        const unsigned mask = __ballot_sync(kFull, in);
-        if (in) s.fidx[nf + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint8_t>(i);
-        nf += __popc(mask);
-      }
-      __syncwarp();
-      const int first = s.fidx[0];
-      double pre = 0.0;
-      if (lane == 0)
-        for (int i = 0; i < first; ++i) pre = dadd(pre, s.pt[i].t);
-      pre = __shfl_sync(kFull, pre, 0);
-      // Surviving bump pairs: drop (i, j) when the circle atom i sweeps never
-      // comes within the cutoff of j: dmin^2 = h^2 + (sigma - rho)^2 > cut^2,
-      // tested without square roots as L = s2 + r2 + h2 - C > 0 && L^2 > 4 s2 r2.
-      // Per-atom axial coordinate a = k.(p - o) and squared axis distance
-      // r2 = |p - o|^2 - a^2 first, lane-parallel, in the (free) v scratch.
-      // The pair list holds (moving atom | fixed atom << 8).  A rotamer's
-      // right step reuses its left step's list with the roles swapped: both
-      // rotate about the same bond line, the left commit rotated the left
-      // atoms about that very line, and the circle test depends only on the
-      // atoms' axial and radial coordinates relative to it (rotation
-      // invariants).  The test itself is a conservative filter, so it runs
-      // in fp32 with a wide margin; the kept pairs are decided exactly.
-      int np = 0;
-      if ((f & 1) && left_np >= 0) {
-        np = left_np;
-        for (int t = lane; t < np; t += 32) {
-          const unsigned pr = s.pairs[t];
-          s.pairs[t] = static_cast<uint16_t>((pr >> 8) | ((pr & 0xffu) << 8));
-        }
-      } else {
-        float* axc = reinterpret_cast<float*>(s.v);
-        float* rad2 = axc + n;
-        float* rf = rad2 + n;
-        for (int i = lane; i < n; i += 32) {
-          const PT q = s.pt[i];
-          const double vx = q.x - ox, vy = q.y - oy, vz = q.z - oz;
-          const double a = X.kx * vx + X.ky * vy + X.kz * vz;
-          axc[i] = static_cast<float>(a);
-          rad2[i] = static_cast<float>(fmax(0.0, vx * vx + vy * vy + vz * vz - a * a));
-          rf[i] = static_cast<float>(s.radius[i]);
-        }
-        __syncwarp();
-        auto test = [&](int i, int j) {
-          const float h = axc[j] - axc[i];
-          const float s2 = rad2[j], r2 = rad2[i];
-          const float cut = 0.8f * (rf[i] + rf[j]);
-          const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
-          const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
-          return !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
-        };
-        if (W == 1) {
-          // Flattened over the actual partner pairs: per-slot partner counts,
-          // a warp prefix sum, then lane t finds its slot by binary search and
-          // its partner as the n-th set bit of the slot's partner mask.
-          int* pref = reinterpret_cast<int*>(rf + n);
-          const uint64_t nf0 = ~s.fm[0];
-          int total = 0;
-          for (int b = 0; b < nf; b += 32) {
-            const int sl = b + lane;
-            const int cnt = sl < nf ? __popcll(s.far[s.fidx[sl]] & nf0) : 0;
-            int inc = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-              const int y = __shfl_up_sync(kFull, inc, o);
-              if (lane >= o) inc += y;
-            }
-            if (sl < nf) pref[sl] = total + inc - cnt;
-            total += __shfl_sync(kFull, inc, 31);
-          }
-          __syncwarp();
-          for (int t0 = 0; t0 < total; t0 += 32) {
-            const int t = t0 + lane;
-            bool keep = false;
-            int i = 0, j = 0;
-            if (t < total) {
-              int lo = 0, hi = nf - 1;  // last slot with pref <= t
-              while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (pref[mid] <= t) lo = mid; else hi = mid - 1;
-              }
-              i = s.fidx[lo];
-              const uint64_t m = s.far[i] & nf0;
-              j = nth_bit(m, t - pref[lo]);
-              keep = test(i, j);
-            }
-            const unsigned mask = __ballot_sync(kFull, keep);
-            if (keep)
-              s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
-            np += __popc(mask);
-          }
-        } else
-        for (int sl = 0; sl < nf; ++sl) {
-          const int i = s.fidx[sl];
-          const float ai = axc[i], r2 = rad2[i], ri = rf[i];
-          for (int b = 0; b < n; b += 32) {
-            // Partner bits of this 32-atom chunk; uniform skip when empty.
-            const unsigned chunk = static_cast<unsigned>(
-                (s.far[i * W + (b >> 6)] & ~s.fm[b >> 6]) >> (b & 63));
-            if (chunk == 0u) continue;
-            const int j = b + lane;
-            bool keep = false;
-            if (j < n && ((chunk >> lane) & 1u)) {
-              const float h = axc[j] - ai;
-              const float s2 = rad2[j];
-              const float cut = 0.8f * (ri + rf[j]);
-              const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
-              const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
-              keep = !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
-            }
-            const unsigned mask = __ballot_sync(kFull, keep);
-            if (keep)
-              s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
-            np += __popc(mask);
-          }
-        }
-      }
-      __syncwarp();
-      left_np = (f & 1) ? -1 : np;  // a left step's list serves its right step
-      // Non-fragment terms are the same for every candidate of this step:
-      // pre-fill them into each candidate slot so the fold is a plain sum.
-      for (int i = lane; i < n; i += 32)
-        if (!in_frag(s.fm, i)) {
-          const double t = s.pt[i].t;
-#pragma unroll
-          for (int c = 0; c < kBatch; ++c) s.v[c * n + i] = t;
-        }
-      __syncwarp();
+      const Axis& X = st.X;
+      const int nf = st.nf, first = st.first, np = st.np;
+      const double pre = st.pre;
 
       int best_a = 0;
       double best = cur;
@@ -416,7 +559,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
           const int a0 = (kb + 1) * step;
           double sc;
           unsigned bumped;
-          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, step, nb, lane, sc, bumped, wk);
+          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, step, nb, lane, sc, bumped, wk, ck);
           for (int c = 0; c < nb; ++c) {
             const double v = __shfl_sync(kFull, sc, c);
             if ((bumped >> c) & 1u) continue;
@@ -442,7 +585,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
           const int a0 = kb * T + T / 2;
           double sc;
           unsigned bumped;
-          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, T, nb, lane, sc, bumped, wk);
+          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, T, nb, lane, sc, bumped, wk, ck);
           for (int c = 0; c < nb; ++c) {
             const double v = __shfl_sync(kFull, sc, c);
             if ((bumped >> c) & 1u) continue;
@@ -467,7 +610,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
             const int a0 = wt * T + kb * p.hp;
             double sc;
             unsigned bumped;
-            eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, p.hp, nb, lane, sc, bumped, wk);
+            eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, p.hp, nb, lane, sc, bumped, wk, ck);
             for (int c = 0; c < nb; ++c) {
               const double v = __shfl_sync(kFull, sc, c);
               if ((bumped >> c) & 1u) continue;
@@ -488,6 +631,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         }
         evals += nfeas;
       }
+      ck.mark(kPhDecide);
       // commit_angle (kernel.hpp:115-117): a fresh rotation of the entry pose,
       // bit-identical to the scored candidate; refresh the fragment's terms.
       if (best_a != 0) {
@@ -503,6 +647,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         }
       }
       __syncwarp();
+      ck.mark(kPhCommit);
       cur = best;
     }
   }
@@ -521,6 +666,85 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
     }
   }
   publish_warp(wk, p.counters, 8, lane);
+  ck.publish(p.counters, lane);
+}
+
+// Rotation profiles (reference rotation_profile, analysis.hpp:37-56): one
+// warp per (ligand, fragment) item scores the fragment at every integer
+// angle about its bond, from the ligand's staged pose.  Angle 0 is the pose
+// itself with its own bump check (check_bumps over the surviving pairs:
+// a dropped pair cannot bump at any angle); angles 1..359 go through
+// eval_batch exactly like search candidates.  Invalid angles report score 0,
+// the reference's value-initialised array entry.
+__global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
+    profile_kernel(DockParams p, const int32_t* items, int n_items, double* scores, uint8_t* valid) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = blockIdx.x * kWarps + warp;
+  if (item >= n_items) return;
+  const int l = items[2 * item], f = items[2 * item + 1];
+  const LigMeta m = p.meta[l];
+  const int n = m.n, W = m.words;
+  const WarpMem s =
+      carve(smem + warp * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W, p.max_pairs);
+  Work<false> wk;
+  Clocks<false> ck;
+  double* out = scores + 360ll * item;
+  uint8_t* vout = valid + 360ll * item;
+
+  for (int i = lane; i < n; i += 32) s.radius[i] = __ldg(p.radii + m.atom_off + i);
+  for (int i = lane; i < n * W; i += 32) s.far[i] = __ldg(p.far_mask + m.far_off + i);
+  for (int i = lane; i < n; i += 32) {
+    const double* q = p.xyz + 3 * (m.atom_off + i);
+    s.pt[i] = PT{q[0], q[1], q[2], fmax(kMinDistanceSq, min_dist_sq(p.pocket, q[0], q[1], q[2], wk))};
+  }
+  __syncwarp();
+  double cur = 0.0;
+  if (lane == 0) {
+    double sum = 0.0;
+    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt[i].t);
+    cur = __ddiv_rn(static_cast<double>(n), sum);
+  }
+  cur = __shfl_sync(kFull, cur, 0);
+
+  const int fo = m.frag_off + f;
+  int left_np = -1;
+  StepInfo st;
+  if (!setup_step(s, p, m, f, __ldg(p.frag_axis + fo), __ldg(p.frag_anchor + fo), lane, left_np, st,
+                  ck)) {
+    if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
+    for (int a = lane; a < 360; a += 32) {
+      out[a] = 0.0;
+      vout[a] = 0;
+    }
+    return;
+  }
+  bool b0 = false;
+  for (int t = lane; t < st.np; t += 32) {
+    const int pr = s.pairs[t];
+    const int i = pr & 0xff, j = pr >> 8;
+    const PT ai = s.pt[i], aj = s.pt[j];
+    const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
+    if (dist_sq(ai.x, ai.y, ai.z, aj.x, aj.y, aj.z) < dmul(cut, cut)) b0 = true;
+  }
+  b0 = __any_sync(kFull, b0);
+  if (lane == 0) {
+    vout[0] = b0 ? 0 : 1;
+    out[0] = b0 ? 0.0 : cur;
+  }
+  for (int kb = 0; kb < 359; kb += kBatch) {
+    const int nb = min(kBatch, 359 - kb);
+    const int a0 = 1 + kb;
+    double sc;
+    unsigned bumped;
+    eval_batch(s, p, st.X, n, st.nf, st.np, st.first, st.pre, cur, a0, 1, nb, lane, sc, bumped, wk,
+               ck);
+    if (lane < nb) {
+      const bool ok = !((bumped >> lane) & 1u);
+      vout[a0 + lane] = ok ? 1 : 0;
+      out[a0 + lane] = ok ? sc : 0.0;
+    }
+  }
 }
 
 // (E7) final order: (final score desc, seed rank asc), one rank per thread;
@@ -586,6 +810,19 @@ int launch_flex(const DockParams& p, void* stream) {
   }
   const long long blocks = (chains + kWarps - 1) / kWarps;
   kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError();
+}
+
+int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
+                    uint8_t* valid, void* stream) {
+  if (n_items == 0) return cudaSuccess;
+  const size_t smem = flex_smem_bytes(p);
+  cudaError_t e = cudaFuncSetAttribute(profile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int blocks = (n_items + kWarps - 1) / kWarps;
+  profile_kernel<<<blocks, kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p, items, n_items,
+                                                                                  scores, valid);
   return cudaGetLastError();
 }
 

@@ -41,6 +41,8 @@ struct GridLevel {
 };
 
 constexpr int kGridLevels = 2;  // fine (near field) + coarse (far field)
+constexpr int kPhaseBase = 16;     // counters[16..32): flex phase clocks
+constexpr int kCounterSlots = 32;
 
 // Exact nearest-pocket-point structure staged in HBM.
 struct PocketView {
@@ -104,7 +106,8 @@ struct DockParams {
   int32_t* status;         // [L]
   // Optional exact work counters: [0..6] rigid kernel, [8..14] flex kernel,
   // each {pairs, rotated atoms, bump pairs, queries, sum terms, candidate
-  // evaluations, rigid-transformed atoms}.
+  // evaluations, rigid-transformed atoms}; [kPhaseBase..+16) flex phase
+  // clocks (GD_PHASE_CLOCKS builds).
   unsigned long long* counters;
 };
 
@@ -118,6 +121,10 @@ size_t flex_smem_bytes(const DockParams& p);
 int launch_rigid_topk(const DockParams& p, int sort_slots, void* stream);
 // One warp per (ligand, seed-rank) chain: n_lig * k_slots chains.
 int launch_flex(const DockParams& p, void* stream);
+// Rotation profiles: one warp per (ligand, fragment) item of `items`
+// ([2*n_items] ligand, fragment), 360 scores + validity flags per item.
+int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
+                    uint8_t* valid, void* stream);
 // E7 final ordering + poses scored, one CTA per ligand.
 int launch_finalize(const DockParams& p, void* stream);
 int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int n_poses,

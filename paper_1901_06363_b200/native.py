@@ -93,6 +93,16 @@ SIGNATURES = {
     "gd_download": (C.c_int, [C.c_void_p, C.POINTER(gd_result)]),
     "gd_last_timing": (C.c_int, [C.c_void_p, C.POINTER(gd_timing)]),
     "gd_work_counters": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "gd_phase_clocks": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "gd_detect_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_void_p,
+                                  C.POINTER(C.c_int32)]),
+    "gd_tile_hit_probability": (C.c_int, [C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_int32),
+                                          C.c_int32, C.POINTER(C.c_double),
+                                          C.POINTER(C.c_double)]),
+    "gd_rotation_profiles": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_int32),
+                                       C.POINTER(C.c_int32), C.c_int64]),
     "gd_device_results": (C.c_int, [C.c_void_p, C.POINTER(gd_device_result)]),
     "gd_fp64_peak": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "gd_overlap_score_batch": (C.c_int, [C.c_void_p, _f64p, C.c_int32, C.c_int32, C.c_uint32,
@@ -230,6 +240,17 @@ class Knobs:
 
 
 @dataclass
+class Profiles:
+    """Rotation profiles of a batch: fragment f of ligand l is row
+    frag_offsets[l] + f (rotamer f // 2, left if f is even)."""
+    scores: np.ndarray         # [F, 360] overlap score where valid, else 0
+    valid: np.ndarray          # [F, 360] bool, check_bumps
+    relative_size: np.ndarray  # [F]
+    frag_offsets: np.ndarray   # [L+1]
+    status: np.ndarray         # [L] GD_LIG_*
+
+
+@dataclass
 class DockResult:
     """gd_result as [L, K] numpy arrays (final order: score desc, seed rank asc)."""
     orientation: np.ndarray
@@ -317,6 +338,7 @@ class Docker:
         res = DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), keep_poses)
         b, k, r = batch.c_struct(), knobs.c_struct(), res.c_struct()
         self._check(self._lib.gd_dock_batch(self._h, C.byref(b), C.byref(k), C.byref(r)))
+        self._batch = batch
         return res
 
     def upload(self, batch: LigandBatch):
@@ -352,6 +374,34 @@ class Docker:
         out = (C.c_uint64 * 16)()
         self._check(self._lib.gd_work_counters(self._h, out))
         return {"rigid": dict(zip(WORK_FIELDS, out[0:7])), "flex": dict(zip(WORK_FIELDS, out[8:15]))}
+
+    def phase_clocks(self) -> list:
+        """Flex-kernel SM cycles per phase (GD_PHASE_CLOCKS builds; zeros otherwise)."""
+        out = (C.c_uint64 * 16)()
+        self._check(self._lib.gd_phase_clocks(self._h, out))
+        return list(out)
+
+    def rotation_profiles(self, batch: "LigandBatch | None" = None) -> "Profiles":
+        """rotation_profile (analysis.hpp:37-56) of every fragment of `batch`
+        (uploaded first) or of the batch staged last, from its poses."""
+        if batch is not None:
+            self.upload(batch)
+        staged = self._batch
+        if staged is None:
+            raise GeoDockError(GD_ERR_INVALID, "rotation_profiles: no batch staged")
+        L = staged.n_ligands
+        cap = max(1, 2 * int(staged.rotatable.sum()))
+        scores = np.zeros((cap, 360), np.float64)
+        valid = np.zeros((cap, 360), np.uint8)
+        rel = np.zeros(cap, np.float64)
+        offs = np.zeros(L + 1, np.int32)
+        status = np.zeros(max(L, 1), np.int32)
+        self._check(self._lib.gd_rotation_profiles(
+            self._h, _p(scores, C.POINTER(C.c_double)), _p(valid, C.POINTER(C.c_uint8)),
+            _p(rel, C.POINTER(C.c_double)), _p(offs, C.POINTER(C.c_int32)),
+            _p(status, C.POINTER(C.c_int32)), cap))
+        F = int(offs[-1])
+        return Profiles(scores[:F], valid[:F].astype(bool), rel[:F], offs, status[:L])
 
     def fp64_peak_tflops(self) -> float:
         t = C.c_double()
