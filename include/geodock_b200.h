@@ -145,6 +145,18 @@ int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs);
 int gd_download(gd_ctx* ctx, gd_result* result);
 int gd_last_timing(const gd_ctx* ctx, gd_timing* out);
 
+/* ---- ligand graph (host) ------------------------------------------------ */
+/* The batch path's host preprocessing of one ligand, exposed for the C++
+ * drop-in: Ligand validation (molecule.hpp:66-115; the reference's message
+ * goes to msg), find_rotamers (molecule.hpp:237-250: rotamer_bonds[r] =
+ * Ligand::bonds() index of rotamer r) and grow_fragments membership
+ * (molecule.hpp:255-301: membership[(2r + side) * n + i], side 0 = left).
+ * Capacities: rotamer_bonds >= n_bonds, membership >= 2 * n_bonds * n.
+ * Returns GD_LIG_OK or GD_LIG_INVALID. */
+int gd_ligand_graph(int32_t n_atoms, const double* xyz, const double* radii, int32_t n_bonds,
+                    const int32_t* bonds, const uint8_t* rotatable, int32_t* n_rotamers,
+                    int32_t* rotamer_bonds, uint8_t* membership, char* msg, size_t msg_len);
+
 /* ---- rotation profiles (analysis) --------------------------------------- */
 /* rotation_profile (analysis.hpp:37-56) of every fragment of the batch staged
  * by the last gd_upload (or gd_dock_batch), from each ligand's pose in that

@@ -8,6 +8,8 @@
 //   -----------------------------------------  ---------------------------------
 //   Vec3 / Atom / Bond (vec3.hpp, molecule.hpp) same value types
 //   Ligand(id, atoms, bonds)  molecule.hpp:45  same validation + messages
+//   find_rotamers / grow_fragments             gd_ligand_graph / host BFS
+//     (molecule.hpp:237-301)
 //   Pocket(id, points)        molecule.hpp:152 same; stages itself on the GPU lazily
 //   PocketIndex(pocket)       geometry.hpp:47  accepted, no-op (the GPU always
 //                                              uses its exact voxel index)
@@ -20,6 +22,8 @@
 //   overlap_degradation       screening.hpp:190 same
 //   (new) dock_batch                           the north-star batch path:
 //                                              rigid sweep + top-K + restarts
+//   analysis.hpp (rotation profiles, peaks)    geodock_b200/analysis.hpp
+//   formats.hpp (files, reports, CSVs)         geodock_b200/formats.hpp
 //
 // Results are bit-identical to the reference.  Link with
 // paper_1901_06363_b200/libgeodock_b200.so.  Define GEODOCK_B200_DEVICE to
@@ -54,6 +58,17 @@ class Error : public std::runtime_error {
   explicit Error(const std::string& what) : std::runtime_error(what) {}
 };
 
+/// Parse failures carry the 1-based line (error.hpp:19-27).
+class ParseError : public Error {
+ public:
+  ParseError(const std::string& what, int line)
+      : Error(what + " at line " + std::to_string(line)), line_(line) {}
+  int line() const { return line_; }
+
+ private:
+  int line_;
+};
+
 // ---- vec3.hpp (value type only; the math runs on the GPU) ---------------------
 struct Vec3 {
   double x = 0.0, y = 0.0, z = 0.0;
@@ -78,6 +93,7 @@ struct Bond {
 struct SkippedRecord {
   std::string id;
   std::string reason;
+  friend bool operator==(const SkippedRecord&, const SkippedRecord&) = default;
 };
 
 namespace detail {
@@ -132,6 +148,93 @@ class Ligand {
   std::vector<Atom> atoms_;
   std::vector<Bond> bonds_;
 };
+
+/// A rotatable bridge bond (molecule.hpp:167-171).
+struct Rotamer {
+  Bond bond;
+  int bond_index = 0;  // position in Ligand::bonds()
+};
+
+enum class Side { left, right };
+
+/// One side of a cut rotamer bond (molecule.hpp:175-185); the left fragment
+/// holds the bond endpoint with the smaller index.
+struct Fragment {
+  Rotamer rotamer;
+  Side side = Side::left;
+  std::vector<int> atom_indices;  // ascending
+  std::vector<char> membership;   // per-atom flag, size == atom count
+  double relative_size = 0.0;     // |atom_indices| / atom count
+  int axis_atom = 0;              // bond endpoint inside this fragment
+  int anchor_atom = 0;            // bond endpoint on the other side
+};
+
+/// Rotatable bridge bonds ordered by (min endpoint, max endpoint)
+/// (molecule.hpp:237-250), from the native preprocessing the batch path
+/// uses (gd_ligand_graph).
+inline std::vector<Rotamer> find_rotamers(const Ligand& ligand) {
+  const int n = ligand.atom_count();
+  const int nb = static_cast<int>(ligand.bonds().size());
+  std::vector<double> xyz, radii;
+  std::vector<int32_t> bonds, rb(std::max(nb, 1));
+  std::vector<uint8_t> rot;
+  for (const Atom& a : ligand.atoms()) {
+    xyz.insert(xyz.end(), {a.position.x, a.position.y, a.position.z});
+    radii.push_back(a.radius);
+  }
+  for (const Bond& b : ligand.bonds()) {
+    bonds.insert(bonds.end(), {b.a, b.b});
+    rot.push_back(b.rotatable ? 1 : 0);
+  }
+  int32_t count = 0;
+  char msg[256] = {0};
+  if (gd_ligand_graph(n, xyz.data(), radii.data(), nb, bonds.data(), rot.data(), &count, rb.data(),
+                      nullptr, msg, sizeof msg) != GD_LIG_OK)
+    throw Error(msg);
+  std::vector<Rotamer> out;
+  for (int r = 0; r < count; ++r) out.push_back({ligand.bonds()[rb[r]], rb[r]});
+  return out;
+}
+
+/// The two fragments a rotamer bond splits off (molecule.hpp:255-301): the
+/// left one is what the smaller endpoint still reaches once the bond is cut.
+inline std::pair<Fragment, Fragment> grow_fragments(const Ligand& ligand, const Rotamer& rotamer) {
+  const int n = ligand.atom_count();
+  const int lo = std::min(rotamer.bond.a, rotamer.bond.b);
+  const int hi = std::max(rotamer.bond.a, rotamer.bond.b);
+  std::vector<std::vector<std::pair<int, int>>> adj(n);  // (neighbour, bond index)
+  for (int bi = 0; bi < static_cast<int>(ligand.bonds().size()); ++bi) {
+    const Bond& b = ligand.bonds()[bi];
+    adj[b.a].push_back({b.b, bi});
+    adj[b.b].push_back({b.a, bi});
+  }
+  std::vector<char> reach(n, 0);
+  std::vector<int> frontier{lo};
+  reach[lo] = 1;
+  for (size_t h = 0; h < frontier.size(); ++h)
+    for (const auto& [nb, bi] : adj[frontier[h]])
+      if (bi != rotamer.bond_index && !reach[nb]) reach[nb] = 1, frontier.push_back(nb);
+  if (reach[hi])
+    throw Error("ligand '" + ligand.id() + "': rotamer bond " + std::to_string(rotamer.bond.a) + "-" +
+                std::to_string(rotamer.bond.b) + " is not a bridge");
+  std::pair<Fragment, Fragment> out;
+  Fragment* sides[2] = {&out.first, &out.second};
+  for (int s = 0; s < 2; ++s) {
+    Fragment& f = *sides[s];
+    f.rotamer = rotamer;
+    f.side = s == 0 ? Side::left : Side::right;
+    f.membership.assign(n, 0);
+    for (int i = 0; i < n; ++i)
+      if ((reach[i] != 0) == (s == 0)) {
+        f.atom_indices.push_back(i);
+        f.membership[i] = 1;
+      }
+    f.relative_size = static_cast<double>(f.atom_indices.size()) / n;
+    f.axis_atom = s == 0 ? lo : hi;
+    f.anchor_atom = s == 0 ? hi : lo;
+  }
+  return out;
+}
 
 namespace detail {
 
@@ -346,6 +449,7 @@ struct LigandResult {
   double score = 0.0;
   long evaluations = 0;
   double time_seconds = 0.0;
+  friend bool operator==(const LigandResult&, const LigandResult&) = default;
 };
 
 struct ScreeningReport {
@@ -357,6 +461,7 @@ struct ScreeningReport {
   long total_atoms = 0;
   double wall_time_seconds = 0.0;
   double top1pct_mean = 0.0;
+  friend bool operator==(const ScreeningReport&, const ScreeningReport&) = default;
 };
 
 class LigandSource {

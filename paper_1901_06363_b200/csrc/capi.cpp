@@ -902,6 +902,31 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   return GD_OK;
 }
 
+extern "C" int gd_ligand_graph(int32_t n_atoms, const double* xyz, const double* radii,
+                               int32_t n_bonds, const int32_t* bonds, const uint8_t* rotatable,
+                               int32_t* n_rotamers, int32_t* rotamer_bonds, uint8_t* membership,
+                               char* msg, size_t msg_len) {
+  if (n_atoms < 0 || n_bonds < 0 || (n_atoms > 0 && (!xyz || !radii)) ||
+      (n_bonds > 0 && (!bonds || !rotatable)) || !n_rotamers)
+    return GD_LIG_INVALID;
+  const PreparedLigand p = prepare_ligand("L", n_atoms, xyz, radii, n_bonds, bonds, rotatable);
+  if (msg && msg_len) {
+    std::strncpy(msg, p.error.c_str(), msg_len - 1);
+    msg[msg_len - 1] = 0;
+  }
+  *n_rotamers = p.status == GD_LIG_OK ? static_cast<int32_t>(p.rot_bond.size()) : 0;
+  if (p.status != GD_LIG_OK) return p.status;
+  for (int r = 0; r < *n_rotamers; ++r) {
+    if (rotamer_bonds) rotamer_bonds[r] = p.rot_bond[r];
+    if (membership)
+      for (int side = 0; side < 2; ++side)
+        for (int i = 0; i < n_atoms; ++i)
+          membership[static_cast<size_t>(2 * r + side) * n_atoms + i] =
+              (p.frag_mask[static_cast<size_t>(2 * r + side) * p.words + i / 64] >> (i % 64)) & 1u;
+  }
+  return GD_LIG_OK;
+}
+
 extern "C" int gd_rotation_profiles(gd_ctx* ctx, double* scores, uint8_t* valid,
                                     double* relative_size, int32_t* frag_offsets, int32_t* status,
                                     int64_t capacity) {

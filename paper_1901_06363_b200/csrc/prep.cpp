@@ -171,6 +171,7 @@ PreparedLigand prepare_ligand(const std::string& id, int n, const double* xyz, c
     if (in_left[hi])
       return fail(std::move(p), tag + "rotamer bond " + std::to_string(bonds[2 * b]) + "-" +
                                     std::to_string(bonds[2 * b + 1]) + " is not a bridge");
+    p.rot_bond.push_back(b);
     int left_size = 0;
     for (int i = 0; i < n; ++i) left_size += in_left[i];
     for (int side = 0; side < 2; ++side) {

@@ -30,6 +30,7 @@ struct PreparedLigand {
   std::vector<uint8_t> capped;        // n*n capped graph distances
   std::vector<uint64_t> far_mask;     // n*words: bit j of row i set iff capped(i,j) >= 4
   // Fragments in reference order: for each rotamer (sorted), left then right.
+  std::vector<int32_t> rot_bond;      // bond index of each rotamer, find_rotamers order
   std::vector<int32_t> frag_axis, frag_anchor, frag_size;
   std::vector<double> frag_rel;       // relative_size = double(|F|) / n
   std::vector<uint64_t> frag_mask;    // nfrag*words membership bits

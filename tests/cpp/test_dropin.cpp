@@ -1,5 +1,5 @@
 // Drop-in API test: the reference's own test cases (test_geometry.cpp,
-// test_kernel.cpp, test_screening.cpp), restated against
+// test_kernel.cpp, test_screening.cpp, test_analysis.cpp), restated against
 // <geodock_b200/geodock.hpp>, which runs them on the GPU through the C-ABI.
 // A plain runner (no Catch2 in this image): prints one line per case and
 // exits non-zero on any failure.  Built and run by tests/test_dropin.py.
@@ -9,6 +9,7 @@
 #include <string>
 #include <vector>
 
+#include "geodock_b200/analysis.hpp"
 #include "geodock_b200/geodock.hpp"
 
 using namespace geodock;
@@ -179,6 +180,94 @@ int main() {
       CHECK(a.score > b.score || (a.score == b.score && a.seed_rank < b.seed_rank));
     }
     for (const auto& p : out[0].poses) CHECK(p.score == overlap_score(p.final_pose, rig_pocket()));
+  });
+  run("rotation_profile: a far-away rigid pair is valid everywhere", [] {
+    const Ligand ligand("l", {{0, {0, 0, 0}, 1.0}, {1, {0, 0, 1.4}, 1.0}, {2, {1.2, 0, 1.4}, 1.0}},
+                        {{0, 1, true}, {1, 2, false}});
+    const Pocket pocket("p", {{0, 0, 1}});
+    const auto [left, right] = grow_fragments(ligand, find_rotamers(ligand)[0]);
+    const Pose pose = make_initial_pose(ligand);
+    const RotationProfile profile = rotation_profile(pose, ligand, right, pocket);
+    for (int a = 0; a < 360; ++a) CHECK(profile.valid[a]);
+    CHECK(profile.scores[0] == overlap_score(pose, pocket));
+    CHECK(profile.relative_size == right.relative_size);
+  });
+  run("rotation_profile: validity and scores match rotate + check + score", [] {
+    const Ligand lig = rig_ligand();
+    const Pocket pocket = rig_pocket();
+    const auto [left, right] = grow_fragments(lig, find_rotamers(lig)[0]);
+    const RotationProfile prof = rotation_profile(make_initial_pose(lig), lig, left, pocket);
+    int valid = 0;
+    for (int a = 0; a < 360; ++a) valid += prof.valid[a] ? 1 : 0;
+    CHECK(valid == 360);  // three atoms: no pair at graph distance >= 4
+    // The left fragment {0} swings about the 1->0 bond: atom 0 sits on the
+    // axis, so every angle scores like the input pose.
+    for (int a = 0; a < 360; ++a) CHECK(prof.scores[a] == prof.scores[0]);
+  });
+  run("detect_peaks: rectangular, flat, wrap-around, all-invalid", [] {
+    RotationProfile p;
+    p.valid.fill(true);
+    p.scores.fill(0.0);
+    p.scores[2] = p.scores[3] = 1.0;
+    const PeakStats s = detect_peaks(p);
+    CHECK(s.delta_overlap == 1.0 && s.peaks.size() == 1 && s.peaks[0].start_angle == 2 &&
+          s.peaks[0].width == 2 && s.peaks[0].height_ratio == 1.0 && s.best_peak_width == 2);
+    RotationProfile flat;
+    flat.valid.fill(true);
+    flat.scores.fill(3.5);
+    CHECK(detect_peaks(flat).peaks.empty() && detect_peaks(flat).best_peak_width == 0);
+    RotationProfile wrap;
+    wrap.valid.fill(true);
+    wrap.scores.fill(0.0);
+    for (int a : {358, 359, 0, 1}) wrap.scores[a] = 1.0;
+    const PeakStats w = detect_peaks(wrap);
+    CHECK(w.peaks.size() == 1 && w.peaks[0].start_angle == 358 && w.peaks[0].width == 4);
+    RotationProfile none;
+    none.valid.fill(false);
+    bool threw = false;
+    try {
+      detect_peaks(none);
+    } catch (const Error& e) {
+      threw = std::string(e.what()).find("no feasible") != std::string::npos;
+    }
+    CHECK(threw);
+  });
+  run("tile_hit_probability: counts, evaluation model, monotonicity", [] {
+    PeakStats wide;
+    wide.best_peak_width = 68;
+    const std::vector<PeakStats> ds(10, wide);
+    const auto hits = tile_hit_probability(ds, {18, 90});
+    CHECK(hits.size() == 2 && hits[0].probability == 1.0 && hits[1].probability == 0.0 &&
+          hits[0].eval_count == 38.0);
+    CHECK(tile_hit_probability(ds, {}).empty());
+  });
+  run("analyze_ligand produces consistent rows; analyze_ligands agrees", [] {
+    std::vector<Ligand> ligs;
+    for (int i = 0; i < 3; ++i) {
+      const double dz = 0.1 * i;
+      ligs.emplace_back("A" + std::to_string(i),
+                        std::vector<Atom>{{0, {0, 0, dz}, 1.0}, {1, {0, 0, 1 + dz}, 1.0},
+                                          {2, {1, 0, 1 + dz}, 1.0}, {3, {1, 1, 1 + dz}, 1.0},
+                                          {4, {2, 1, 1 + dz}, 1.0}},
+                        std::vector<Bond>{{0, 1, true}, {1, 2, true}, {2, 3, true}, {3, 4, false}});
+    }
+    const KnobConfig cfg{3, 90, 0.0, 1, false};
+    const auto batch = analyze_ligands(ligs, rig_pocket(), cfg);
+    for (size_t l = 0; l < ligs.size(); ++l) {
+      const LigandAnalysis a = analyze_ligand(ligs[l], rig_pocket(), cfg);
+      CHECK(a.dock.score > 0.0);
+      CHECK(a.fragments.size() == a.stats.size());
+      for (const auto& row : a.fragments) {
+        CHECK(row.ligand_id == ligs[l].id());
+        CHECK(row.relative_size > 0.0 && row.relative_size < 1.0);
+        CHECK(row.delta_normalized >= 0.0);
+      }
+      CHECK(batch[l].dock.score == a.dock.score);
+      CHECK(batch[l].fragments.size() == a.fragments.size());
+      for (size_t f = 0; f < a.fragments.size() && f < batch[l].fragments.size(); ++f)
+        CHECK(batch[l].fragments[f].delta_overlap == a.fragments[f].delta_overlap);
+      CHECK(batch[l].peaks.size() == a.peaks.size());
+    }
   });
   std::printf("%s (%d failed checks)\n", g_failed ? "FAILED" : "OK", g_failed);
   return g_failed ? 1 : 0;

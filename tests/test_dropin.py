@@ -1,8 +1,9 @@
-"""The C++ drop-in header (include/geodock_b200/geodock.hpp).
+"""The C++ drop-in headers (include/geodock_b200/{geodock,analysis,formats}.hpp).
 
-Compiling tests/cpp/test_dropin.cpp against the header and the in-tree
+Compiling tests/cpp/test_dropin.cpp against the headers and the in-tree
 library is a CPU test; running it (the reference's own test cases through
-the GPU) is a GPU test.
+the GPU) is a GPU test.  tests/cpp/test_formats.cpp (file formats, reports,
+ligand graph helpers) needs no GPU and runs in the CPU suite.
 """
 import subprocess
 from pathlib import Path
@@ -10,23 +11,29 @@ from pathlib import Path
 import pytest
 
 ROOT = Path(__file__).resolve().parent.parent
-SRC = ROOT / "tests" / "cpp" / "test_dropin.cpp"
-OUT = ROOT / "tests" / "_build" / "test_dropin"
 LIBDIR = ROOT / "paper_1901_06363_b200"
 
 
-def _compile():
-    OUT.parent.mkdir(exist_ok=True)
-    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"), str(SRC), "-o", str(OUT),
+def _compile(name="test_dropin"):
+    src = ROOT / "tests" / "cpp" / f"{name}.cpp"
+    out = ROOT / "tests" / "_build" / name
+    out.parent.mkdir(exist_ok=True)
+    cmd = ["g++", "-std=c++20", "-O2", "-Wall", "-I", str(ROOT / "include"), str(src), "-o", str(out),
            "-L", str(LIBDIR), "-lgeodock_b200", f"-Wl,-rpath,{LIBDIR}", "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     assert res.returncode == 0, res.stderr
-    return OUT
+    return out
 
 
 def test_dropin_header_compiles_and_links():
-    _compile()
-    assert OUT.exists()
+    assert _compile().exists()
+
+
+def test_dropin_formats_and_graph_on_cpu():
+    exe = _compile("test_formats")
+    res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert res.returncode == 0, res.stdout + res.stderr
+    assert "FAIL" not in res.stdout
 
 
 @pytest.mark.gpu
