@@ -13,6 +13,12 @@ chains of fragment optimisation, and the final ordering (E1-E8).
 * ``--impl reference``: the reference's own CPU path (oracle/_ref: the
   reference headers compiled from /root/reference, PocketIndex, all host
   threads) on a bounded sample of the same workload.
+* ``--workload profiles``: the analysis row -- rotation
+  profiles (analysis.hpp:37-56, 360 integer angles per fragment) of every
+  fragment of the config's ligands from their given poses; metric
+  fragments/s, same keys (roofline of the profile kernel, e2e through
+  gd_upload + gd_rotation_profiles, the reference's rotation_profile on the
+  host cores as cpu_baseline / --impl reference).
 
 Multi-GPU (torchrun): ligands are sharded by id (weak scaling: every rank
 docks its own seeded 10,000); each step all-gathers every rank's per-ligand
@@ -52,6 +58,7 @@ def args_():
     ap.add_argument("--ligands", type=int, default=0, help="override ligands per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--workload", default="dock", choices=["dock", "profiles"])
     return ap.parse_args()
 
 
@@ -315,9 +322,144 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+PROFILE_METRIC = "fragment rotation profiles/s (360 integer angles each, analysis.hpp rotation_profile)"
+PROFILE_LIGANDS = 2000  # ligands per step (about 9,000 fragments on config 1)
+PROFILE_CPU_SAMPLE = 256
+
+
+def cpu_profiles(batch, pocket, n: int):
+    """The reference's rotation_profile on the first n ligands: (fragments/s, info)."""
+    from oracle import oracle_py as O
+    sub = batch.subset(range(min(n, batch.n_ligands)))
+    threads = O.threads()
+    kind = "reference" if O.have_ref() else "port"
+    t0 = time.perf_counter()
+    out = O.rotation_profiles(sub, pocket, "ref" if kind == "reference" else "oracle",
+                              nthreads=threads)
+    dt = time.perf_counter() - t0
+    return len(out[0]) / dt, {
+        "kind": kind, "cores": threads if kind == "reference" else 1,
+        "sample": (f"first {sub.n_ligands} ligands ({len(out[0])} fragments) of the workload, "
+                   + ("reference rotation_profile (oracle/_ref) with PocketIndex"
+                      if kind == "reference" else "C oracle, brute force")),
+        "seconds": dt}
+
+
+def profile_batch_of(a):
+    from paper_1901_06363_b200 import workloads as W
+    w = W.config(a.config)
+    pocket = w.pocket()
+    n = a.ligands or PROFILE_LIGANDS
+    return w, pocket, w.ligands(range(n), pocket.mean(axis=0))
+
+
+def run_profiles_reference(a):
+    rank, _, _ = dist_env()
+    if rank != 0:
+        return
+    w, pocket, batch = profile_batch_of(a)
+    for _ in range(a.warmup):
+        cpu_profiles(batch, pocket, PROFILE_CPU_SAMPLE)
+    t0 = time.perf_counter()
+    frags = 0
+    info = None
+    for _ in range(a.steps):
+        v, info = cpu_profiles(batch, pocket, PROFILE_CPU_SAMPLE)
+        frags += v * info["seconds"]
+    wall = time.perf_counter() - t0
+    value = frags / wall
+    print(json.dumps({
+        "impl": "reference", "metric": PROFILE_METRIC, "value": value, "unit": "fragments/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * wall / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"profiles of {w.name}", "ligands_per_step": PROFILE_CPU_SAMPLE},
+        "cpu_baseline": {"value": value, "unit": "fragments/s", "cores": info["cores"],
+                         "kind": info["kind"], "sample": info["sample"]},
+        "e2e": {"value": value, "unit": "fragments/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0}}), flush=True)
+
+
+def run_profiles(a):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    from paper_1901_06363_b200 import Docker
+    from paper_1901_06363_b200.native import GD_FLAG_COUNT_WORK
+    w, pocket, batch = profile_batch_of(a)
+    stream = torch.cuda.current_stream()
+    d = Docker(local)
+    d.set_stream(stream.cuda_stream)
+    d.set_pocket(pocket)
+    d.upload(batch)
+    prof = d.rotation_profiles(flags=GD_FLAG_COUNT_WORK)  # counted, untimed
+    work = d.work_counters()["flex"]
+    F = len(prof.scores)
+    fp64_peak = d.fp64_peak_tflops()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    for _ in range(a.warmup):
+        d.rotation_profiles()
+    kern_ms, call_ms = [], []
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    for _ in range(a.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        d.rotation_profiles()
+        t = d.timing()
+        kern_ms.append(t["flex_ms"])
+        call_ms.append(t["total_ms"])
+    clk = clocks.stop()
+    ms = float(np.mean(kern_ms))
+    value = F / (ms / 1e3)
+    e2e = None
+    if not a.no_e2e:
+        tms = []
+        for _ in range(max(1, min(a.steps, 5))):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            d.rotation_profiles(batch)  # host prep + H2D + kernel + D2H of 360 x 9 B per fragment
+            tms.append(time.perf_counter() - t0)
+        tt = float(np.mean(tms))
+        t = d.timing()
+        e2e = {"value": F / tt, "unit": "fragments/s",
+               "h2d_bytes_per_step": int(batch.xyz.nbytes + batch.radii.nbytes + t["h2d_bytes"]),
+               "d2h_bytes_per_step": int(t["d2h_bytes"]), "ms_per_step": 1e3 * tt,
+               "timer": "host wall clock around gd_upload + gd_rotation_profiles"}
+    achieved = flops_of(work) / (ms / 1e3) / 1e12
+    line = {
+        "metric": PROFILE_METRIC, "value": value, "unit": "fragments/s", "n_gpus": 1,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE generators, DESIGN.md §5)",
+        "config": {"workload": f"profiles of {w.name} (given poses)",
+                   "ligands": batch.n_ligands, "fragments": F, "angles_per_fragment": 360,
+                   "pocket_points": len(pocket),
+                   "l2": "flushed between steps (256 MiB write, untimed)"},
+        "kernel_ms": {"profile_kernel": ms}, "call_ms": float(np.mean(call_ms)),
+        "gpu_launches": a.steps,
+        "roofline": {"kernel": "profile_kernel", "bound": "fp64", "achieved": achieved,
+                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+                     "traffic": None, "peak_source": "measured fp64 DADD/DMUL probe (gd_fp64_peak)",
+                     "work_per_launch": work},
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not a.no_cpu_baseline:
+        v, inf = cpu_profiles(batch, pocket, PROFILE_CPU_SAMPLE)
+        line["cpu_baseline"] = {"value": v, "unit": "fragments/s", "cores": inf["cores"],
+                                "kind": inf["kind"], "sample": inf["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 if __name__ == "__main__":
     a = args_()
-    if a.impl == "reference":
+    if a.workload == "profiles":
+        run_profiles_reference(a) if a.impl == "reference" else run_profiles(a)
+    elif a.impl == "reference":
         run_reference(a)
     else:
         run_ours(a)

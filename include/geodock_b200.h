@@ -170,9 +170,12 @@ int gd_ligand_graph(int32_t n_atoms, const double* xyz, const double* radii, int
  * relative_size[f] (nullable) Fragment::relative_size; status[L] (nullable)
  * GD_LIG_* per ligand (GD_LIG_DEGENERATE: a fragment's axis is degenerate,
  * its profile is all-invalid).  `capacity` is in fragments; twice the
- * number of rotatable bonds always suffices. */
-int gd_rotation_profiles(gd_ctx* ctx, double* scores, uint8_t* valid, double* relative_size,
-                         int32_t* frag_offsets, int32_t* status, int64_t capacity);
+ * number of rotatable bonds always suffices.  flags: GD_FLAG_BRUTE_FORCE,
+ * GD_FLAG_COUNT_WORK (work lands in gd_work_counters' flex slots); the
+ * kernel time goes to gd_last_timing's flex_ms. */
+int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores, uint8_t* valid,
+                         double* relative_size, int32_t* frag_offsets, int32_t* status,
+                         int64_t capacity);
 
 /* One peak of a rotation profile (analysis.hpp:25-29). */
 typedef struct {

@@ -101,7 +101,7 @@ inline std::vector<RotationProfile> profile_batch(const std::vector<const Ligand
     std::lock_guard<std::mutex> lock(d.mu());
     pocket.stage(d);
     check(gd_upload(d.ctx(), &b));
-    check(gd_rotation_profiles(d.ctx(), scores.data(), valid.data(), rel.data(), offsets.data(),
+    check(gd_rotation_profiles(d.ctx(), 0u, scores.data(), valid.data(), rel.data(), offsets.data(),
                                status.data(), static_cast<int64_t>(cap)));
   }
   std::vector<RotationProfile> out(offsets.back());

@@ -927,7 +927,7 @@ extern "C" int gd_ligand_graph(int32_t n_atoms, const double* xyz, const double*
   return GD_LIG_OK;
 }
 
-extern "C" int gd_rotation_profiles(gd_ctx* ctx, double* scores, uint8_t* valid,
+extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores, uint8_t* valid,
                                     double* relative_size, int32_t* frag_offsets, int32_t* status,
                                     int64_t capacity) {
   if (ctx == nullptr) return GD_ERR_INVALID;
@@ -974,23 +974,42 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, double* scores, uint8_t* valid,
     p.frag_anchor = ctx->fan.as<int32_t>();
     p.frag_rel = ctx->frel.as<double>();
     p.pocket = ctx->view;
+    p.pocket.use_index = (flags & GD_FLAG_BRUTE_FORCE) ? 0 : ctx->view.use_index;
     p.cos_deg = ctx->cos_t.as<double>();
     p.sin_deg = ctx->sin_t.as<double>();
     p.max_n = ctx->max_n;
     p.max_pairs = std::max(1, ctx->max_n * ctx->max_n / 4);
     p.status = ctx->o_status.as<int32_t>();
+    if (flags & GD_FLAG_COUNT_WORK) {
+      GD_CUDA(ctx, ctx->counters.ensure(sizeof(unsigned long long) * kCounterSlots));
+      GD_CUDA(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * kCounterSlots,
+                                   ctx->stream));
+      p.counters = ctx->counters.as<unsigned long long>();
+    }
+    ctx->counted = p.counters != nullptr;
+    ctx->timing = gd_timing{};
+    cudaEventRecord(ctx->ev[2], ctx->stream);
     GD_CUDA(ctx, static_cast<cudaError_t>(launch_profiles(
                      p, ctx->prof_items.as<int32_t>(), static_cast<int>(n_items),
                      ctx->prof_scores.as<double>(), ctx->prof_valid.as<uint8_t>(), ctx->stream)));
+    cudaEventRecord(ctx->ev[3], ctx->stream);
     GD_CUDA(ctx, cudaMemcpyAsync(scores, ctx->prof_scores.ptr, sizeof(double) * 360 * n_items,
                                  cudaMemcpyDeviceToHost, ctx->stream));
     GD_CUDA(ctx, cudaMemcpyAsync(valid, ctx->prof_valid.ptr, 360 * n_items, cudaMemcpyDeviceToHost,
                                  ctx->stream));
+    cudaEventRecord(ctx->ev[4], ctx->stream);
+    ctx->timing.launches = 1;
+    ctx->timing.h2d_bytes = static_cast<int64_t>(sizeof(int32_t) * items.size());
+    ctx->timing.d2h_bytes = static_cast<int64_t>(9 * 360 * n_items);
   }
   if (status && L > 0)
     GD_CUDA(ctx, cudaMemcpyAsync(status, ctx->o_status.ptr, sizeof(int32_t) * L,
                                  cudaMemcpyDeviceToHost, ctx->stream));
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (n_items > 0) {
+    cudaEventElapsedTime(&ctx->timing.flex_ms, ctx->ev[2], ctx->ev[3]);
+    cudaEventElapsedTime(&ctx->timing.total_ms, ctx->ev[2], ctx->ev[4]);
+  }
   return GD_OK;
 }
 

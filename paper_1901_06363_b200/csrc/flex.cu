@@ -676,6 +676,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
 // a dropped pair cannot bump at any angle); angles 1..359 go through
 // eval_batch exactly like search candidates.  Invalid angles report score 0,
 // the reference's value-initialised array entry.
+template <bool On>
 __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
     profile_kernel(DockParams p, const int32_t* items, int n_items, double* scores, uint8_t* valid) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -687,7 +688,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
   const int n = m.n, W = m.words;
   const WarpMem s =
       carve(smem + warp * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W, p.max_pairs);
-  Work<false> wk;
+  Work<On> wk;
   Clocks<false> ck;
   double* out = scores + 360ll * item;
   uint8_t* vout = valid + 360ll * item;
@@ -717,6 +718,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
       out[a] = 0.0;
       vout[a] = 0;
     }
+    publish_warp(wk, p.counters, 8, lane);
     return;
   }
   bool b0 = false;
@@ -725,6 +727,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
     const int i = pr & 0xff, j = pr >> 8;
     const PT ai = s.pt[i], aj = s.pt[j];
     const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
+    wk.add(kBump, 1);
     if (dist_sq(ai.x, ai.y, ai.z, aj.x, aj.y, aj.z) < dmul(cut, cut)) b0 = true;
   }
   b0 = __any_sync(kFull, b0);
@@ -745,6 +748,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
       out[a0 + lane] = ok ? sc : 0.0;
     }
   }
+  publish_warp(wk, p.counters, 8, lane);
 }
 
 // (E7) final order: (final score desc, seed rank asc), one rank per thread;
@@ -817,12 +821,13 @@ int launch_profiles(const DockParams& p, const int32_t* items, int n_items, doub
                     uint8_t* valid, void* stream) {
   if (n_items == 0) return cudaSuccess;
   const size_t smem = flex_smem_bytes(p);
-  cudaError_t e = cudaFuncSetAttribute(profile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kernel = p.counters ? profile_kernel<true> : profile_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
   const int blocks = (n_items + kWarps - 1) / kWarps;
-  profile_kernel<<<blocks, kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p, items, n_items,
-                                                                                  scores, valid);
+  kernel<<<blocks, kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p, items, n_items, scores,
+                                                                          valid);
   return cudaGetLastError();
 }
 

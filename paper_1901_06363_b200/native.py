@@ -100,7 +100,8 @@ SIGNATURES = {
     "gd_tile_hit_probability": (C.c_int, [C.POINTER(C.c_int32), C.c_int64, C.POINTER(C.c_int32),
                                           C.c_int32, C.POINTER(C.c_double),
                                           C.POINTER(C.c_double)]),
-    "gd_rotation_profiles": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+    "gd_rotation_profiles": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_uint8),
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.c_int64]),
     "gd_device_results": (C.c_int, [C.c_void_p, C.POINTER(gd_device_result)]),
@@ -381,7 +382,7 @@ class Docker:
         self._check(self._lib.gd_phase_clocks(self._h, out))
         return list(out)
 
-    def rotation_profiles(self, batch: "LigandBatch | None" = None) -> "Profiles":
+    def rotation_profiles(self, batch: "LigandBatch | None" = None, flags: int = 0) -> "Profiles":
         """rotation_profile (analysis.hpp:37-56) of every fragment of `batch`
         (uploaded first) or of the batch staged last, from its poses."""
         if batch is not None:
@@ -397,7 +398,7 @@ class Docker:
         offs = np.zeros(L + 1, np.int32)
         status = np.zeros(max(L, 1), np.int32)
         self._check(self._lib.gd_rotation_profiles(
-            self._h, _p(scores, C.POINTER(C.c_double)), _p(valid, C.POINTER(C.c_uint8)),
+            self._h, flags, _p(scores, C.POINTER(C.c_double)), _p(valid, C.POINTER(C.c_uint8)),
             _p(rel, C.POINTER(C.c_double)), _p(offs, C.POINTER(C.c_int32)),
             _p(status, C.POINTER(C.c_int32)), cap))
         F = int(offs[-1])
