@@ -239,6 +239,9 @@ def run_ours(a):
 
     res = d.download(DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), False))
     poses_per_step = float(res.poses_scored.sum())
+    # executed point pairs vs the brute-force scan's n*P per scored pose.
+    brute_pairs = float((res.poses_scored * batch.sizes).sum()) * len(pocket)
+    exec_pairs = float(work["rigid"]["pairs"] + work["flex"]["pairs"])
     if dist:
         ps = torch.tensor([poses_per_step], device="cuda", dtype=torch.float64)
         dist.all_reduce(ps)
@@ -300,6 +303,11 @@ def run_ours(a):
                        "voxel_index": {k: (v.tolist() if hasattr(v, "tolist") else v)
                                        for k, v in info.items()}},
             "poses_scored_per_s": poses_per_s,
+            "pairs": {"executed_per_s": world * exec_pairs / (ms_per_step / 1e3),
+                      "brute_equivalent_per_s": world * brute_pairs / (ms_per_step / 1e3),
+                      "brute_equivalent_fp32_tflops": 8 * world * brute_pairs / (ms_per_step / 1e3) / 1e12,
+                      "note": "brute-force equivalent = n_atoms x pocket points per scored pose "
+                              "(reference distance_sq calls in brute mode, 8 FLOPs each)"},
             "kernel_ms": {"rigid_topk_kernel": r_ms, "flex_chain_kernel+finalize": f_ms},
             "gpu_launches": 3 * a.steps,
             "roofline": {"kernel": dom, "bound": "fp64", "achieved": achieved,
