@@ -697,9 +697,7 @@ static int launch_range(gd_ctx* ctx, DockParams p, int c0, int c1, int max_n, cu
   p.max_pairs = std::max(1, max_n * max_n / 4);
   if (p.n_lig == 0) return GD_OK;
   if (p.rigid) {
-    int sort_slots = 2;
-    while (sort_slots < std::min(ctx->n_orient, 2048)) sort_slots <<= 1;
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_rigid_topk(p, sort_slots, s)));
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_rigid_topk(p, s)));
     ctx->timing.launches += 1;
   }
   if (e_mid) cudaEventRecord(e_mid, s);

@@ -260,29 +260,5 @@ __device__ __forceinline__ bool precede(double ka, int ia, double kb, int ib) {
   return ka > kb || (ka == kb && ia < ib);
 }
 
-template <int BT>
-__device__ void bitonic_sort(double* key, int* idx, int n) {
-  for (int k = 2; k <= n; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n; i += BT) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const double ki = key[i], kj = key[ixj];
-          const int ii = idx[i], ij = idx[ixj];
-          const bool sw = up ? precede(kj, ij, ki, ii) : precede(ki, ii, kj, ij);
-          if (sw) {
-            key[i] = kj;
-            key[ixj] = ki;
-            idx[i] = ij;
-            idx[ixj] = ii;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-}
-
 }  // namespace
 }  // namespace gdb200

@@ -118,7 +118,7 @@ int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* st
 size_t flex_smem_bytes(const DockParams& p);
 
 // Launchers; return cudaError_t as int.  `stream` is a cudaStream_t.
-int launch_rigid_topk(const DockParams& p, int sort_slots, void* stream);
+int launch_rigid_topk(const DockParams& p, void* stream);
 // One warp per (ligand, seed-rank) chain: n_lig * k_slots chains.
 int launch_flex(const DockParams& p, void* stream);
 // Rotation profiles: one warp per (ligand, fragment) item of `items`

@@ -7,6 +7,8 @@
 // orientation index asc) (E5): for K <= 32 each warp keeps a sorted top-32
 // in registers (shuffle networks) and a 3-level tree merges the 8 warp
 // lists; larger K goes through a shared-memory bitonic sort chunk by chunk.
+#include <algorithm>
+
 #include "device_common.cuh"
 
 namespace gdb200 {
@@ -156,24 +158,38 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_top32_kernel(DockPara
   publish(wk, p.counters, 0);
 }
 
-// --- general K: shared-memory bitonic sort over chunks -----------------------
+// --- general K: threshold + compaction + rank merge --------------------------
+// Orientations are scored in rounds of BT (one per thread).  Only scores
+// that precede the current K-th entry are compacted into a pending buffer;
+// the pending entries are ranked among themselves (O(pending) each) and
+// merged into the sorted list by rank: an entry's new position is its rank
+// in its own list plus the number of entries of the other list preceding it
+// (a binary search).  A round whose scores all lose costs one ballot.
 template <int BT, bool On>
-__global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_topk_kernel(DockParams p, int sort_slots) {
+__global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_topk_kernel(DockParams p) {
   const int l = p.order[blockIdx.x];
   const LigMeta m = p.meta[l];
   if (m.status != 0) {
     if (threadIdx.x == 0) p.k_eff[l] = 0;
     return;
   }
-  extern __shared__ __align__(16) unsigned char smem[];
   const int n = m.n;
+  const int No = p.n_orient;
+  const int K = min(p.top_k, No);
+  extern __shared__ __align__(16) unsigned char smem[];
   double* vx = reinterpret_cast<double*>(smem);
   double* vy = vx + n;
   double* vz = vy + n;
-  double* key = vz + n;
-  int* slot = reinterpret_cast<int*>(key + sort_slots);
+  double* lk = vz + n;   // [K] sorted list (keys) ...
+  double* nk = lk + K;   // [K] ... and its merge target
+  double* pk = nk + K;   // [BT] pending, arrival order
+  double* qk = pk + BT;  // [BT] pending, sorted
+  int* ls = reinterpret_cast<int*>(qk + BT);
+  int* ns = ls + K;
+  int* ps = ns + K;
+  int* qs = ps + BT;
+  __shared__ int wcnt[BT / 32];
 
-  // v = p - c once per atom (the first operation of E3).
   for (int i = threadIdx.x; i < n; i += BT) {
     const double* q = p.xyz + 3 * (m.atom_off + i);
     vx[i] = dsub(q[0], p.cx);
@@ -182,37 +198,81 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_topk_kernel(DockParam
   }
   __syncthreads();
 
-  const int No = p.n_orient;
-  const int K = min(p.top_k, No);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   Work<On> wk;
-  int carry = 0;
-  for (int base = 0; base < No;) {
-    const int take = min(sort_slots - carry, No - base);
-    for (int t = threadIdx.x; t < sort_slots - carry; t += BT) {
-      double score = kInfeasible;
-      int s = INT_MAX;
-      if (t < take) {
-        s = base + t;
-        score = score_orientation(p, s, n, vx, vy, vz, wk);
-      }
-      key[carry + t] = score;
-      slot[carry + t] = s;
+  int kept = 0;
+  for (int base = 0; base < No; base += BT) {
+    const int s = base + threadIdx.x;
+    double score = kInfeasible;
+    bool q = false;
+    if (s < No) {
+      score = score_orientation(p, s, n, vx, vy, vz, wk);
+      q = kept < K || precede(score, s, lk[K - 1], ls[K - 1]);
     }
-    base += take;
+    const unsigned bal = __ballot_sync(0xffffffffu, q);
+    if (lane == 0) wcnt[warp] = __popc(bal);
     __syncthreads();
-    bitonic_sort<BT>(key, slot, sort_slots);
-    carry = min(K, carry + take);
+    int off = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < BT / 32; ++w) {
+      const int c = wcnt[w];
+      off += w < warp ? c : 0;
+      total += c;
+    }
+    if (q) {
+      const int at = off + __popc(bal & ((1u << lane) - 1u));
+      pk[at] = score;
+      ps[at] = s;
+    }
+    __syncthreads();
+    if (total == 0) continue;
+    if (threadIdx.x < total) {
+      const double k0 = pk[threadIdx.x];
+      const int s0 = ps[threadIdx.x];
+      int r = 0;
+      for (int j = 0; j < total; ++j) r += precede(pk[j], ps[j], k0, s0) ? 1 : 0;
+      qk[r] = k0;
+      qs[r] = s0;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < kept + total; j += BT) {
+      const bool old = j < kept;
+      const int t = old ? j : j - kept;
+      const double k0 = old ? lk[t] : qk[t];
+      const int s0 = old ? ls[t] : qs[t];
+      const double* ok = old ? qk : lk;
+      const int* os = old ? qs : ls;
+      int lo = 0, hi = old ? total : kept;  // entries of the other list preceding (k0, s0)
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (precede(ok[mid], os[mid], k0, s0)) lo = mid + 1;
+        else hi = mid;
+      }
+      const int pos = t + lo;
+      if (pos < K) {
+        nk[pos] = k0;
+        ns[pos] = s0;
+      }
+    }
+    __syncthreads();
+    kept = min(K, kept + total);
+    double* tk = lk;
+    lk = nk;
+    nk = tk;
+    int* ts = ls;
+    ls = ns;
+    ns = ts;
   }
   for (int r = threadIdx.x; r < K; r += BT) {
-    p.seed_slot[l * p.top_k + r] = slot[r];
-    p.seed_score[l * p.top_k + r] = key[r];
+    p.seed_slot[l * p.top_k + r] = ls[r];
+    p.seed_score[l * p.top_k + r] = lk[r];
   }
   if (threadIdx.x == 0) p.k_eff[l] = K;
   publish(wk, p.counters, 0);
 }
 
 template <bool On>
-int launch(const DockParams& p, int sort_slots, cudaStream_t stream) {
+int launch(const DockParams& p, cudaStream_t stream) {
   if (p.top_k <= 32) {
     const size_t smem = sizeof(double) * 3 * p.max_n;
     cudaError_t e = cudaFuncSetAttribute(rigid_top32_kernel<kRigidThreads, On>,
@@ -222,20 +282,22 @@ int launch(const DockParams& p, int sort_slots, cudaStream_t stream) {
     rigid_top32_kernel<kRigidThreads, On><<<p.n_lig, kRigidThreads, smem, stream>>>(p);
     return cudaGetLastError();
   }
-  const size_t smem = sizeof(double) * 3 * p.max_n + (sizeof(double) + sizeof(int)) * sort_slots;
+  const int K = std::min(p.top_k, p.n_orient);
+  const size_t smem = sizeof(double) * 3 * p.max_n +
+                      (sizeof(double) + sizeof(int)) * (2 * static_cast<size_t>(K) + 2 * kRigidThreads);
   cudaError_t e = cudaFuncSetAttribute(rigid_topk_kernel<kRigidThreads, On>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
-  rigid_topk_kernel<kRigidThreads, On><<<p.n_lig, kRigidThreads, smem, stream>>>(p, sort_slots);
+  rigid_topk_kernel<kRigidThreads, On><<<p.n_lig, kRigidThreads, smem, stream>>>(p);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-int launch_rigid_topk(const DockParams& p, int sort_slots, void* stream) {
+int launch_rigid_topk(const DockParams& p, void* stream) {
   const auto s = static_cast<cudaStream_t>(stream);
-  return p.counters ? launch<true>(p, sort_slots, s) : launch<false>(p, sort_slots, s);
+  return p.counters ? launch<true>(p, s) : launch<false>(p, s);
 }
 
 }  // namespace gdb200

@@ -98,6 +98,21 @@ def test_config2_knobs_parity(docker):
     assert_same_result(got, want)
 
 
+@pytest.mark.parametrize("top_k", [1, 32, 33, 64, 207, 208, 250])
+def test_topk_sizes(docker, top_k):
+    """Both top-K kernels (warp registers for K <= 32, rank merge above),
+    including K >= #orientations (208 at 45 degrees: K = all of them)."""
+    w = W.config(1)
+    pocket = w.pocket()
+    batch = w.ligands(range(4))
+    knobs = Knobs.baseline(45, 90, 1, top_k)
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, knobs, keep_poses=False)
+    want = _cpu(batch, pocket, knobs)
+    assert (got.k_eff == min(top_k, 208)).all()
+    assert_same_result(got, want, poses=False)
+
+
 @pytest.mark.parametrize("knobs", [
     Knobs(1, 45, 0.0, 1, False),    # Algorithm-1 baseline (test_kernel.cpp:241-250)
     Knobs(2, 90, 0.3, 2, True),     # determinism test config (test_kernel.cpp:205-220)
