@@ -7,7 +7,7 @@
 // chains (usually of the same ligand, in longest-ligand-first order) with
 // private shared-memory state.  Within a chain the greedy dependency
 // (rep -> rotamer -> left/right fragment, kernel.hpp:225-242) is sequential;
-// each fragment search evaluates its candidate angles in batches of kBatch:
+// each fragment search evaluates its candidate angles in batches of B:
 //
 //   * bump phase  -- lanes over (candidate, surviving bump pair): Rodrigues
 //                    rotation (geometry.hpp:182-184) + the clash rule
@@ -37,8 +37,10 @@ namespace {
 #ifndef GD_FLEX_MINB
 #define GD_FLEX_MINB 6       // resident CTAs per SM the register budget targets
 #endif
+// Candidates evaluated together by one warp: a template parameter (4 or 8,
+// chosen per launch from the knobs, launch_flex); GD_FLEX_BATCH forces one.
 #ifndef GD_FLEX_BATCH
-#define GD_FLEX_BATCH 4      // candidates evaluated together by one warp
+#define GD_FLEX_BATCH 0
 #endif
 #ifndef GD_BUMP_ILP2
 #define GD_BUMP_ILP2 0       // bump phase: two pairs per lane per iteration (A/B: no gain)
@@ -50,13 +52,13 @@ namespace {
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
 constexpr int kWarps = 4;    // chains per CTA
-constexpr int kBatch = GD_FLEX_BATCH;
 constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
+template <int B>
 __host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pairs) {
-  return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * kBatch * n) +
+  return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * B * n) +
          a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16);
 }
 
@@ -70,13 +72,14 @@ struct WarpMem {
   double* radius;        // [n]
   uint64_t* far;         // [n*W]  bit j of row i: capped graph distance >= 4
   PT* pt;                // [n]    committed pose + terms of the chain
-  double* v;             // [kBatch*n] candidate terms of fragment atoms
+  double* v;             // [B*n] candidate terms of fragment atoms
   uint16_t* pairs;       // [max_pairs] surviving bump pairs: F-slot | j << 8
   uint8_t* fidx;         // [n] fragment atoms, ascending
   uint64_t* fm;          // [4] fragment membership bits
   int* count;            // [1] surviving-pair counter
 };
 
+template <int B>
 __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   WarpMem s;
   size_t o = 0;
@@ -88,7 +91,7 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   s.radius = reinterpret_cast<double*>(take(8ull * n));
   s.far = reinterpret_cast<uint64_t*>(take(8ull * n * W));
   s.pt = reinterpret_cast<PT*>(take(32ull * n));
-  s.v = reinterpret_cast<double*>(take(8ull * kBatch * n));
+  s.v = reinterpret_cast<double*>(take(8ull * B * n));
   s.pairs = reinterpret_cast<uint16_t*>(take(2ull * max_pairs));
   s.fidx = reinterpret_cast<uint8_t*>(take(n));
   s.fm = reinterpret_cast<uint64_t*>(take(32));
@@ -318,7 +321,7 @@ struct StepInfo {
   double pre;
 };
 
-template <class CK>
+template <int B, class CK>
 __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p, const LigMeta& m,
                                            int f, int axis, int anchor, int lane, int& left_np,
                                            StepInfo& st, CK& ck) {
@@ -464,7 +467,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
     if (!in_frag(s.fm, i)) {
       const double t = s.pt[i].t;
 #pragma unroll
-      for (int c = 0; c < kBatch; ++c) s.v[c * n + i] = t;
+      for (int c = 0; c < B; ++c) s.v[c * n + i] = t;
     }
   __syncwarp();
   ck.mark(kPhPrefill);
@@ -475,7 +478,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   return true;
 }
 
-template <bool On>
+template <bool On, int B>
 __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(DockParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -488,7 +491,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
   if (m.status != 0) return;
   const int n = m.n, W = m.words;
   const WarpMem s =
-      carve(smem + warp * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W, p.max_pairs);
+      carve<B>(smem + warp * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W,
+               p.max_pairs);
   const size_t e = static_cast<size_t>(l) * p.top_k + r;
   Work<On> wk;
   Clocks<On && GD_PHASE_CLOCKS> ck;
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         continue;
       }
       StepInfo st;
-      if (!setup_step(s, p, m, f, axis, anchor, lane, left_np, st, ck)) {
+      if (!setup_step<B>(s, p, m, f, axis, anchor, lane, left_np, st, ck)) {
         if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
         return;
       }
@@ -554,8 +558,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
       if (!refined) {
         // optimize_fragment_flat (kernel.hpp:125-143).
         long long nfeas = 0;
-        for (int kb = 0; kb < A - 1; kb += kBatch) {
-          const int nb = min(kBatch, A - 1 - kb);
+        for (int kb = 0; kb < A - 1; kb += B) {
+          const int nb = min(B, A - 1 - kb);
           const int a0 = (kb + 1) * step;
           double sc;
           unsigned bumped;
@@ -580,8 +584,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         double ws = 0.0;
         long long nfeas = 0;
         best = 0.0;
-        for (int kb = 0; kb < tc; kb += kBatch) {
-          const int nb = min(kBatch, tc - kb);
+        for (int kb = 0; kb < tc; kb += B) {
+          const int nb = min(B, tc - kb);
           const int a0 = kb * T + T / 2;
           double sc;
           unsigned bumped;
@@ -605,8 +609,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
         if (wt >= 0) {
           int cnt2 = 0;
           while ((cnt2 + 1) * p.hp <= T) ++cnt2;
-          for (int kb = 0; kb < cnt2; kb += kBatch) {
-            const int nb = min(kBatch, cnt2 - kb);
+          for (int kb = 0; kb < cnt2; kb += B) {
+            const int nb = min(B, cnt2 - kb);
             const int a0 = wt * T + kb * p.hp;
             double sc;
             unsigned bumped;
@@ -676,7 +680,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
 // a dropped pair cannot bump at any angle); angles 1..359 go through
 // eval_batch exactly like search candidates.  Invalid angles report score 0,
 // the reference's value-initialised array entry.
-template <bool On>
+template <bool On, int B>
 __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
     profile_kernel(DockParams p, const int32_t* items, int n_items, double* scores, uint8_t* valid) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -687,7 +691,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
   const LigMeta m = p.meta[l];
   const int n = m.n, W = m.words;
   const WarpMem s =
-      carve(smem + warp * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W, p.max_pairs);
+      carve<B>(smem + warp * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W,
+               p.max_pairs);
   Work<On> wk;
   Clocks<false> ck;
   double* out = scores + 360ll * item;
@@ -711,8 +716,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
   const int fo = m.frag_off + f;
   int left_np = -1;
   StepInfo st;
-  if (!setup_step(s, p, m, f, __ldg(p.frag_axis + fo), __ldg(p.frag_anchor + fo), lane, left_np, st,
-                  ck)) {
+  if (!setup_step<B>(s, p, m, f, __ldg(p.frag_axis + fo), __ldg(p.frag_anchor + fo), lane, left_np,
+                     st, ck)) {
     if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
     for (int a = lane; a < 360; a += 32) {
       out[a] = 0.0;
@@ -735,8 +740,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
     vout[0] = b0 ? 0 : 1;
     out[0] = b0 ? 0.0 : cur;
   }
-  for (int kb = 0; kb < 359; kb += kBatch) {
-    const int nb = min(kBatch, 359 - kb);
+  for (int kb = 0; kb < 359; kb += B) {
+    const int nb = min(B, 359 - kb);
     const int a0 = 1 + kb;
     double sc;
     unsigned bumped;
@@ -792,17 +797,24 @@ __global__ void __launch_bounds__(256) finalize_kernel(DockParams p) {
   }
 }
 
-}  // namespace
-
+template <int B>
 size_t flex_smem_bytes(const DockParams& p) {
-  return kWarps * warp_bytes(p.max_n, (p.max_n + 63) / 64, p.max_pairs);
+  return kWarps * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs);
 }
 
-int launch_flex(const DockParams& p, void* stream) {
-  const long long chains = static_cast<long long>(p.n_lig) * p.k_slots;
-  if (chains == 0) return cudaSuccess;
-  const size_t smem = flex_smem_bytes(p);
-  auto kernel = p.counters ? flex_chain_kernel<true> : flex_chain_kernel<false>;
+// Batch size: 8 candidates when the high-precision step has >= 16 of them
+// (fewer, partly empty batches), else 4 (less shared memory, more L1).
+// Measured: c1 (hp 30, 11 candidates) 18.6 ms at 4 vs 19+ at 6/8; c2 (hp 10,
+// 35 candidates) 81 ms at 8 vs 89 ms at 4.
+int flex_batch(const DockParams& p) {
+  if (GD_FLEX_BATCH) return GD_FLEX_BATCH;
+  return 360 / p.hp - 1 >= 16 ? 8 : 4;
+}
+
+template <int B>
+int launch_flex_b(const DockParams& p, long long chains, cudaStream_t stream) {
+  const size_t smem = flex_smem_bytes<B>(p);
+  auto kernel = p.counters ? flex_chain_kernel<true, B> : flex_chain_kernel<false, B>;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -813,22 +825,37 @@ int launch_flex(const DockParams& p, void* stream) {
     if (e != cudaSuccess) return e;
   }
   const long long blocks = (chains + kWarps - 1) / kWarps;
-  kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(p);
   return cudaGetLastError();
+}
+
+template <int B>
+int launch_profiles_b(const DockParams& p, const int32_t* items, int n_items, double* scores,
+                      uint8_t* valid, cudaStream_t stream) {
+  const size_t smem = flex_smem_bytes<B>(p);
+  auto kernel = p.counters ? profile_kernel<true, B> : profile_kernel<false, B>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int blocks = (n_items + kWarps - 1) / kWarps;
+  kernel<<<blocks, kWarps * 32, smem, stream>>>(p, items, n_items, scores, valid);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_flex(const DockParams& p, void* stream) {
+  const long long chains = static_cast<long long>(p.n_lig) * p.k_slots;
+  if (chains == 0) return cudaSuccess;
+  const auto s = static_cast<cudaStream_t>(stream);
+  return flex_batch(p) == 8 ? launch_flex_b<8>(p, chains, s) : launch_flex_b<4>(p, chains, s);
 }
 
 int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
                     uint8_t* valid, void* stream) {
   if (n_items == 0) return cudaSuccess;
-  const size_t smem = flex_smem_bytes(p);
-  auto kernel = p.counters ? profile_kernel<true> : profile_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  const int blocks = (n_items + kWarps - 1) / kWarps;
-  kernel<<<blocks, kWarps * 32, smem, static_cast<cudaStream_t>(stream)>>>(p, items, n_items, scores,
-                                                                          valid);
-  return cudaGetLastError();
+  // 359 candidates per fragment: the wide batch.
+  return launch_profiles_b<8>(p, items, n_items, scores, valid, static_cast<cudaStream_t>(stream));
 }
 
 int launch_finalize(const DockParams& p, void* stream) {

@@ -114,9 +114,6 @@ struct DockParams {
 // FP64 pipe probe: independent DADD/DMUL chains, returns fp64 ops executed.
 int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* stream);
 
-// Bytes of dynamic shared memory the kernels need for these params.
-size_t flex_smem_bytes(const DockParams& p);
-
 // Launchers; return cudaError_t as int.  `stream` is a cudaStream_t.
 int launch_rigid_topk(const DockParams& p, void* stream);
 // One warp per (ligand, seed-rank) chain: n_lig * k_slots chains.
