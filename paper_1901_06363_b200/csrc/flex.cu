@@ -42,12 +42,6 @@ namespace {
 #ifndef GD_FLEX_BATCH
 #define GD_FLEX_BATCH 0
 #endif
-#ifndef GD_BUMP_ILP2
-#define GD_BUMP_ILP2 0       // bump phase: two pairs per lane per iteration (A/B: no gain)
-#endif
-#ifndef GD_QUERY_MLP
-#define GD_QUERY_MLP 2       // lookups in flight per lane (3, 4 spill: measured slower)
-#endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
@@ -157,72 +151,36 @@ struct Clocks {
   }
 };
 
-// Evaluates candidates angle(c) = a0 + c*da, c < nb, of the current fragment
-// (CandidateEvaluator::evaluate, kernel.hpp:100-112).  Returns, in lane c,
-// candidate c's overlap score (cur for angle 0), and warp-uniformly the
-// mask of candidates that bumped.
-template <bool On, class CK>
-__device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X, int n, int nf,
-                           int np, int first, double pre, double cur, int a0, int da, int nb,
-                           int lane, double& score_out, unsigned& bumped_out, Work<On>& wk,
-                           CK& ck) {
-  ck.mark(kPhDecide);
-  const unsigned zero = (a0 == 0) ? 1u : 0u;  // only c = 0 can be angle 0
-  // Bump phase.
-  unsigned bl = 0;
-  const int total = nb * np;
-  const float rnp = 1.0f / static_cast<float>(max(np, 1));
-#if GD_BUMP_ILP2
-  // Two pairs per lane per iteration (t, t + 32): independent dependency
-  // chains for the fp64 pipe.
-  for (int t = lane; t < total; t += 64) {
-    const int t1 = t + 32;
-    const int c0 = qdiv(t, rnp);
-    const int c1 = t1 < total ? qdiv(t1, rnp) : c0;
-    const bool d0 = !(((bl | zero) >> c0) & 1u);
-    const bool d1 = t1 < total && !(((bl | zero) >> c1) & 1u);
-    if (!d0 && !d1) continue;
-    const int ta = d0 ? t : t1, ca = d0 ? c0 : c1;
-    const int tb = d1 ? t1 : ta, cb = d1 ? c1 : ca;
-    const int pa = s.pairs[ta - ca * np], pb = s.pairs[tb - cb * np];
-    const int ia = pa & 0xff, ja = pa >> 8, ib = pb & 0xff, jb = pb >> 8;
-    const int aa = a0 + ca * da, ab = a0 + cb * da;
-    const double csa = __ldg(p.cos_deg + aa), sna = __ldg(p.sin_deg + aa);
-    const double csb = __ldg(p.cos_deg + ab), snb = __ldg(p.sin_deg + ab);
-    const PT ai = s.pt[ia], aj = s.pt[ja], bi = s.pt[ib], bj = s.pt[jb];
-    double xa, ya, za, xb, yb, zb;
-    rodrigues(X, csa, sna, dsub(1.0, csa), ai.x, ai.y, ai.z, xa, ya, za);
-    rodrigues(X, csb, snb, dsub(1.0, csb), bi.x, bi.y, bi.z, xb, yb, zb);
-    wk.add(kRot, (d0 ? 1 : 0) + (d1 ? 1 : 0));
-    wk.add(kBump, (d0 ? 1 : 0) + (d1 ? 1 : 0));
-    const double cuta = dmul(kBumpScale, dadd(s.radius[ia], s.radius[ja]));
-    const double cutb = dmul(kBumpScale, dadd(s.radius[ib], s.radius[jb]));
-    if (dist_sq(xa, ya, za, aj.x, aj.y, aj.z) < dmul(cuta, cuta)) bl |= 1u << ca;
-    if (dist_sq(xb, yb, zb, bj.x, bj.y, bj.z) < dmul(cutb, cutb)) bl |= 1u << cb;
-  }
-#else
-  for (int t = lane; t < total; t += 32) {
-    const int c = qdiv(t, rnp);
-    if (((bl | zero) >> c) & 1u) continue;
-    const int pr = s.pairs[t - c * np];
-    const int i = pr & 0xff, j = pr >> 8;
-    const int a = a0 + c * da;
-    const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
-    double qx, qy, qz;
-    const PT ai = s.pt[i], aj = s.pt[j];
-    rodrigues(X, cs, sn, dsub(1.0, cs), ai.x, ai.y, ai.z, qx, qy, qz);
-    wk.add(kRot, 1);
-    wk.add(kBump, 1);
-    const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
-    if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < dmul(cut, cut)) bl |= 1u << c;
-  }
-#endif
-  const unsigned bumped = __reduce_or_sync(kFull, bl);
-  const unsigned live = ((1u << nb) - 1u) & ~bumped & ~zero;
-  ck.mark(kPhBump);
-  // Query phase.
-#if GD_QUERY_MLP == 2
-  // Two items per lane per iteration (t, t+32): both lookups in flight.
+// One bump-check item t of a batch: candidate c = t / np against surviving
+// pair t % np (Rodrigues rotation of the moving atom, geometry.hpp:182-184,
+// then the clash rule, geometry.hpp:199-213).  Candidates already known to
+// bump (or the angle-0 candidate, always feasible) are skipped.
+template <bool On>
+__device__ __forceinline__ void bump_item(const WarpMem& s, const DockParams& p, const Axis& X, int t,
+                                          float rnp, int np, int a0, int da, unsigned skip,
+                                          unsigned& bl, Work<On>& wk) {
+  const int c = qdiv(t, rnp);
+  if (((bl | skip) >> c) & 1u) return;
+  const int pr = s.pairs[t - c * np];
+  const int i = pr & 0xff, j = pr >> 8;
+  const int a = a0 + c * da;
+  const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
+  double qx, qy, qz;
+  const PT ai = s.pt[i], aj = s.pt[j];
+  rodrigues(X, cs, sn, dsub(1.0, cs), ai.x, ai.y, ai.z, qx, qy, qz);
+  wk.add(kRot, 1);
+  wk.add(kBump, 1);
+  const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
+  if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < dmul(cut, cut)) bl |= 1u << c;
+}
+
+// Query phase: lanes over (live candidate, fragment atom), two items per
+// lane per iteration (t, t + 32) so both nearest-point lookups are in flight;
+// candidate c's term of atom i lands in v[c * n + i].
+template <bool On>
+__device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& p, const Axis& X,
+                                            int n, int nf, unsigned live, int a0, int da, int nb,
+                                            int lane, Work<On>& wk) {
   const int tq = nb * nf;
   const float rnf = 1.0f / static_cast<float>(nf);
   for (int t = lane; t < tq; t += 64) {
@@ -244,39 +202,27 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
     if (l0) s.v[c0 * n + i0] = fmax(kMinDistanceSq, m0);
     if (l1) s.v[c1 * n + i1] = fmax(kMinDistanceSq, m1);
   }
-#else
-  // M items per lane per iteration (t + 32 r): all M lookups in flight.
-  constexpr int M = GD_QUERY_MLP;
-  const int tq = nb * nf;
-  const float rnf = 1.0f / static_cast<float>(nf);
-  for (int t = lane; t < tq; t += 32 * M) {
-    int cc[M], ii[M];
-    bool ll[M];
-    bool any = false;
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      const int tr = t + 32 * r < tq ? t + 32 * r : t;
-      cc[r] = qdiv(tr, rnf);
-      ll[r] = (r == 0 || tr != t) && ((live >> cc[r]) & 1u);
-      ii[r] = s.fidx[tr - cc[r] * nf];
-      any |= ll[r];
-    }
-    if (!any) continue;
-    double x[M], y[M], z[M], m[M];
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      const int a = a0 + cc[r] * da;
-      const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
-      const PT q = s.pt[ii[r]];
-      rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x[r], y[r], z[r]);
-    }
-    wk.add(kRot, M);
-    min_dist_sqM<M>(p.pocket, x, y, z, m, wk);
-#pragma unroll
-    for (int r = 0; r < M; ++r)
-      if (ll[r]) s.v[cc[r] * n + ii[r]] = fmax(kMinDistanceSq, m[r]);
-  }
-#endif
+}
+
+// Evaluates candidates angle(c) = a0 + c*da, c < nb, of the current fragment
+// (CandidateEvaluator::evaluate, kernel.hpp:100-112).  Returns, in lane c,
+// candidate c's overlap score (cur for angle 0), and warp-uniformly the
+// mask of candidates that bumped.
+template <bool On, class CK>
+__device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X, int n, int nf,
+                           int np, int first, double pre, double cur, int a0, int da, int nb,
+                           int lane, double& score_out, unsigned& bumped_out, Work<On>& wk,
+                           CK& ck) {
+  ck.mark(kPhDecide);
+  const unsigned zero = (a0 == 0) ? 1u : 0u;  // only c = 0 can be angle 0
+  unsigned bl = 0;
+  const int total = nb * np;
+  const float rnp = 1.0f / static_cast<float>(max(np, 1));
+  for (int t = lane; t < total; t += 32) bump_item(s, p, X, t, rnp, np, a0, da, zero, bl, wk);
+  const unsigned bumped = __reduce_or_sync(kFull, bl);
+  const unsigned live = ((1u << nb) - 1u) & ~bumped & ~zero;
+  ck.mark(kPhBump);
+  query_phase(s, p, X, n, nf, live, a0, da, nb, lane, wk);
   __syncwarp();
   ck.mark(kPhQuery);
   // Fold phase: lane c, atom order.
