@@ -304,11 +304,15 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   v.use_index = 1;
   ctx->n_cand = 0;
   ctx->max_cand = 0;
-  // Edges/margins measured on config 1 (profiles/r1_voxel_ab.md): 0.25 A
-  // fine voxels average 2.2 candidates per query.
-  const double hs[kGridLevels] = {env_double("GD_VOXEL_H", 0.25), env_double("GD_VOXEL_H2", 1.0)};
+  // Edges/margins from A/B on config 1 (profiles/r1_voxel_ab.md, DESIGN
+  // §10): 0.2 A fine / 0.75 A far-field voxels.  A level whose grid would
+  // exceed kMaxVoxels grows its edge (x1.25 steps) until it fits, so both
+  // levels' records (32 B each) stay well inside the 126 MB L2 even for the
+  // largest config-3 pockets.
+  const double hs[kGridLevels] = {env_double("GD_VOXEL_H", 0.2), env_double("GD_VOXEL_H2", 0.75)};
   const double ms[kGridLevels] = {env_double("GD_VOXEL_MARGIN", 3.0),
                                   env_double("GD_VOXEL_MARGIN2", 32.0)};
+  const long kMaxVoxels = static_cast<long>(env_double("GD_VOXEL_MAX", 1.5e6));
   for (int L = 0; L < kGridLevels; ++L) {
     double h = hs[L];
     const double margin = ms[L];
@@ -320,7 +324,7 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
         dims[k] = static_cast<int>(std::floor((hi[k] - lo[k] + 2 * margin) / h)) + 1;
         total *= dims[k];
       }
-      if (total <= (1l << 22)) {
+      if (total <= kMaxVoxels) {
         g = VoxelGrid{lo[0] - margin, lo[1] - margin, lo[2] - margin, h, dims[0], dims[1], dims[2]};
         break;
       }

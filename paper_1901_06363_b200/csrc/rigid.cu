@@ -15,7 +15,7 @@ namespace gdb200 {
 namespace {
 
 #ifndef GD_RIGID_MINB
-#define GD_RIGID_MINB 4  // resident CTAs per SM the register budget targets
+#define GD_RIGID_MINB 5  // resident CTAs per SM the register budget targets
 #endif
 #ifndef GD_RIGID_MLP
 #define GD_RIGID_MLP 2   // atoms whose nearest-point lookups are in flight together
