@@ -49,7 +49,25 @@ __device__ bool dominates(const P3& b, const P3& a, const double* bl, const doub
   return true;
 }
 
-__device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, int* cand) {
+// The two coarse passes (the upper bound U and the distance pre-filter)
+// stream every pocket point, so they run over shared-memory tiles of fp32
+// copies with margins far above fp32 rounding (coordinates < ~1e2 A, so
+// |error of a d^2| < ~1e-2 A^2): the pre-filter can only admit more points,
+// never drop one the exact rule keeps.  Every decision that shapes the list
+// -- dominance by the centre-nearest point and the pairwise dominance pass
+// -- stays exact fp64 on the exact coordinates.  (Any superset of the
+// candidates that can attain the minimum gives the same, exact, query
+// result; the margins only cost list length.)
+constexpr int kBuildThreads = 128;
+constexpr int kTile = 1024;
+constexpr float kPassRel = 1e-4f;   // relative margin on U
+constexpr float kPassAbs = 5e-2f;   // absolute margin, A^2
+
+// Candidate list of voxel v; every thread of the CTA must call it (tiles),
+// `active` false for threads past the grid.  Returns the count, or -1 when
+// more than kVoxMaxCand points survive (the caller then keeps every point).
+__device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, bool active,
+                          int* cand, float4* tile) {
   const int iz = v % g.dim_z;
   const int iy = (v / g.dim_z) % g.dim_y;
   const int ix = v / (g.dim_z * g.dim_y);
@@ -57,40 +75,69 @@ __device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, i
                         g.lo_z + iz * g.h - kVoxEps};
   const double bh[3] = {bl[0] + g.h + 2 * kVoxEps, bl[1] + g.h + 2 * kVoxEps,
                         bl[2] + g.h + 2 * kVoxEps};
-  const double cx = 0.5 * (bl[0] + bh[0]), cy = 0.5 * (bl[1] + bh[1]), cz = 0.5 * (bl[2] + bh[2]);
-  // Pass 1: U (upper bound on the NN distance^2 anywhere in B) and the point
-  // nearest the box centre, a strong dominator for pass 2's pre-filter.
-  double U = 1e300, dc = 1e300;
+  const float lx = static_cast<float>(bl[0]), ly = static_cast<float>(bl[1]),
+              lz = static_cast<float>(bl[2]);
+  const float hx = static_cast<float>(bh[0]), hy = static_cast<float>(bh[1]),
+              hz = static_cast<float>(bh[2]);
+  const float cx = 0.5f * (lx + hx), cy = 0.5f * (ly + hy), cz = 0.5f * (lz + hz);
+  auto load_tile = [&](int t0, int cnt) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+      const double* q = pts + 4 * static_cast<size_t>(t0 + i);
+      tile[i] = make_float4(static_cast<float>(q[0]), static_cast<float>(q[1]),
+                            static_cast<float>(q[2]), 0.0f);
+    }
+    __syncthreads();
+  };
+  // Pass 1 (fp32): U = min_j maxdist^2(B, P_j), and the point nearest the
+  // box centre (a strong dominator for pass 2; any choice is correct).
+  float U = 3.0e38f, dc = 3.0e38f;
   int jc = 0;
-  for (int j = 0; j < P; ++j) {
-    const P3 q = ldp(pts, j);
-    const double fx = fmax(fabs(q.x - bl[0]), fabs(q.x - bh[0]));
-    const double fy = fmax(fabs(q.y - bl[1]), fabs(q.y - bh[1]));
-    const double fz = fmax(fabs(q.z - bl[2]), fabs(q.z - bh[2]));
-    U = fmin(U, fx * fx + fy * fy + fz * fz);
-    const double d = (q.x - cx) * (q.x - cx) + (q.y - cy) * (q.y - cy) + (q.z - cz) * (q.z - cz);
-    if (d < dc) {
-      dc = d;
-      jc = j;
+  for (int t0 = 0; t0 < P; t0 += kTile) {
+    const int cnt = min(kTile, P - t0);
+    load_tile(t0, cnt);
+    if (!active) continue;
+    for (int i = 0; i < cnt; ++i) {
+      const float4 q = tile[i];
+      const float fx = fmaxf(fabsf(q.x - lx), fabsf(q.x - hx));
+      const float fy = fmaxf(fabsf(q.y - ly), fabsf(q.y - hy));
+      const float fz = fmaxf(fabsf(q.z - lz), fabsf(q.z - hz));
+      U = fminf(U, fx * fx + fy * fy + fz * fz);
+      const float d = (q.x - cx) * (q.x - cx) + (q.y - cy) * (q.y - cy) + (q.z - cz) * (q.z - cz);
+      if (d < dc) {
+        dc = d;
+        jc = t0 + i;
+      }
     }
   }
-  const double lim = U * (1.0 + 1e-12) + kVoxMargin;
-  const P3 C = ldp(pts, jc);
-  // Pass 2: points that can be nearest somewhere in B and that jc does not
-  // dominate (a point dominated by anything is dominated by a kept point,
-  // by transitivity, so the final set does not depend on this filter).
+  const float lim = U * (1.0f + kPassRel) + kPassAbs;
+  const P3 C = ldp(pts, active ? jc : 0);
+  // Pass 2: points that may be nearest somewhere in B (fp32 with margins)
+  // and that the centre-nearest point does not dominate (exact).
   int k = 0;
-  for (int j = 0; j < P; ++j) {
-    const P3 q = ldp(pts, j);
-    const double nx = fmax(0.0, fmax(bl[0] - q.x, q.x - bh[0]));
-    const double ny = fmax(0.0, fmax(bl[1] - q.y, q.y - bh[1]));
-    const double nz = fmax(0.0, fmax(bl[2] - q.z, q.z - bh[2]));
-    if (nx * nx + ny * ny + nz * nz <= lim && !dominates(C, q, bl, bh)) {
-      if (k >= kVoxMaxCand) return -1;
-      cand[k++] = j;
+  bool over = false;
+  for (int t0 = 0; t0 < P; t0 += kTile) {
+    const int cnt = min(kTile, P - t0);
+    load_tile(t0, cnt);
+    if (!active || over) continue;
+    for (int i = 0; i < cnt; ++i) {
+      const float4 q = tile[i];
+      const float nx = fmaxf(0.0f, fmaxf(lx - q.x, q.x - hx));
+      const float ny = fmaxf(0.0f, fmaxf(ly - q.y, q.y - hy));
+      const float nz = fmaxf(0.0f, fmaxf(lz - q.z, q.z - hz));
+      if (nx * nx + ny * ny + nz * nz > lim) continue;
+      const P3 Q = ldp(pts, t0 + i);
+      if (dominates(C, Q, bl, bh)) continue;
+      if (k >= kVoxMaxCand) {
+        over = true;
+        break;
+      }
+      cand[k++] = t0 + i;
     }
   }
-  // Pass 3: full dominance pruning among the survivors.
+  if (!active) return 0;
+  if (over) return -1;
+  // Pass 3 (exact): full dominance pruning among the survivors.
   int kept = 0;
   for (int a = 0; a < k; ++a) {
     const P3 A = ldp(pts, cand[a]);
@@ -102,22 +149,26 @@ __device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, i
   return kept;
 }
 
-__global__ void voxel_count_kernel(const double* pts, int P, VoxelGrid g, int32_t* counts) {
+__global__ void __launch_bounds__(kBuildThreads) voxel_count_kernel(const double* pts, int P,
+                                                                    VoxelGrid g, int32_t* counts) {
+  __shared__ float4 tile[kTile];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   const int nv = g.dim_x * g.dim_y * g.dim_z;
-  if (v >= nv) return;
   int cand[kVoxMaxCand];
-  const int k = voxel_list(pts, P, g, v, cand);
-  counts[v] = k < 0 ? P : k;  // overflow: keep every point (exact, rare)
+  const int k = voxel_list(pts, P, g, min(v, nv - 1), v < nv, cand, tile);
+  if (v < nv) counts[v] = k < 0 ? P : k;  // overflow: keep every point (exact, rare)
 }
 
-__global__ void voxel_fill_kernel(const double* pts, int P, VoxelGrid g, const int32_t* offsets,
-                                  double* rec, double* lst) {
+__global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double* pts, int P,
+                                                                   VoxelGrid g,
+                                                                   const int32_t* offsets,
+                                                                   double* rec, double* lst) {
+  __shared__ float4 tile[kTile];
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   const int nv = g.dim_x * g.dim_y * g.dim_z;
-  if (v >= nv) return;
   int cand[kVoxMaxCand];
-  const int k = voxel_list(pts, P, g, v, cand);
+  const int k = voxel_list(pts, P, g, min(v, nv - 1), v < nv, cand, tile);
+  if (v >= nv) return;
   const int len = k < 0 ? P : k;  // >= 1: the nearest point always survives
   const int start = offsets[v];
   double* r = rec + kRecDoubles * static_cast<size_t>(v);
