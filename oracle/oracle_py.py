@@ -105,6 +105,7 @@ def ref() -> C.CDLL:
         h.gdref_detect_peaks.argtypes = [_f64p, _u8p, _f64p, C.POINTER(C.c_int),
                                          C.POINTER(C.c_int), _i32p, _i32p, _f64p]
         h.gdref_tile_hits.argtypes = [_i32p, C.c_int, _i32p, C.c_int, _f64p, _f64p]
+        h.gdref_ligand_graph.argtypes = [C.c_int, _f64p, _f64p, C.c_int, _i32p, _u8p, _i32p, _u8p]
         _ref = h
     return _ref
 
@@ -275,6 +276,23 @@ def ref_tile_hits(best_widths, tiles):
                              _p(ev, _f64p)):
         raise RuntimeError(ref().gdref_last_error().decode())
     return prob, ev
+
+
+def ref_ligand_graph(xyz, radii, bonds, rot):
+    """The reference's find_rotamers + grow_fragments: (bond indices, membership)
+    or None when the Ligand ctor throws."""
+    x = np.ascontiguousarray(xyz, dtype=np.float64)
+    r = np.ascontiguousarray(radii, dtype=np.float64)
+    b = np.ascontiguousarray(bonds, dtype=np.int32)
+    ro = np.ascontiguousarray(rot, dtype=np.uint8)
+    n, nb = len(x), len(b)
+    rb = np.zeros(max(nb, 1), np.int32)
+    mem = np.zeros((max(2 * nb, 1), max(n, 1)), np.uint8)
+    k = ref().gdref_ligand_graph(n, _p(x, _f64p), _p(r, _f64p), nb, _p(b, _i32p), _p(ro, _u8p),
+                                 _p(rb, _i32p), _p(mem, _u8p))
+    if k < 0:
+        return None
+    return rb[:k].copy(), mem[:2 * k, :n].astype(bool)
 
 
 def orientations(step: int):

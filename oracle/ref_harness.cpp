@@ -427,3 +427,27 @@ extern "C" int gdref_tile_hits(const int32_t* best_widths, int n, const int32_t*
     return 1;
   }
 }
+
+// geodock::find_rotamers + grow_fragments: rotamer bond indices and the
+// fragments' membership (row 2r = left, 2r+1 = right).  Returns the rotamer
+// count, or -1 when the Ligand ctor throws (message in gdref_last_error()).
+extern "C" int gdref_ligand_graph(int n, const double* xyz, const double* radii, int nb,
+                                  const int32_t* bonds, const uint8_t* rot, int32_t* rot_bonds,
+                                  uint8_t* membership) {
+  try {
+    const geodock::Ligand lig = make_ligand("L", n, xyz, radii, nb, bonds, rot);
+    const auto rots = geodock::find_rotamers(lig);
+    for (size_t r = 0; r < rots.size(); ++r) {
+      rot_bonds[r] = rots[r].bond_index;
+      const auto fr = geodock::grow_fragments(lig, rots[r]);
+      for (int i = 0; i < n; ++i) {
+        membership[(2 * r) * n + i] = fr.first.membership[i] ? 1 : 0;
+        membership[(2 * r + 1) * n + i] = fr.second.membership[i] ? 1 : 0;
+      }
+    }
+    return static_cast<int>(rots.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}

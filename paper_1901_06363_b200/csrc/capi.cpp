@@ -34,13 +34,23 @@ struct DevBuf {
   ~DevBuf() {
     if (ptr) cudaFree(ptr);
   }
+  // Grows geometrically (x1.5): pockets and batches of slowly rising size
+  // must not pay a cudaFree + cudaMalloc each (those stall for hundreds of
+  // ms when large allocations are live).
   cudaError_t ensure(size_t n) {
     if (n <= bytes && ptr) return cudaSuccess;
+    const size_t want = std::max<size_t>({n, 256, bytes + bytes / 2});
     if (ptr) cudaFree(ptr);
     ptr = nullptr;
     bytes = 0;
-    const cudaError_t e = cudaMalloc(&ptr, std::max<size_t>(n, 256));
-    if (e == cudaSuccess) bytes = std::max<size_t>(n, 256);
+    cudaError_t e = cudaMalloc(&ptr, want);
+    if (e != cudaSuccess && want > n) {  // tight on memory: exactly n
+      cudaGetLastError();
+      e = cudaMalloc(&ptr, std::max<size_t>(n, 256));
+      if (e == cudaSuccess) bytes = std::max<size_t>(n, 256);
+      return e;
+    }
+    if (e == cudaSuccess) bytes = want;
     return e;
   }
   template <class T>
@@ -84,7 +94,7 @@ struct gd_ctx {
   // Pocket.
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels];
+  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels], vox_counts, vox_doff;
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
@@ -331,7 +341,7 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
       h *= 1.25;
     }
     const int nv = g.dim_x * g.dim_y * g.dim_z;
-    DevBuf counts;
+    DevBuf& counts = ctx->vox_counts;
     GD_CUDA(ctx, counts.ensure(sizeof(int32_t) * nv));
     GD_CUDA(ctx, static_cast<cudaError_t>(launch_voxel_count(ctx->pts.as<double>(), n, g,
                                                              counts.as<int32_t>(), ctx->stream)));
@@ -351,7 +361,7 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
       mx = std::max(mx, cnt[c]);
       if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
     }
-    DevBuf doff;
+    DevBuf& doff = ctx->vox_doff;
     GD_CUDA(ctx, doff.ensure(sizeof(int32_t) * nv));
     GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
     GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));

@@ -94,6 +94,10 @@ SIGNATURES = {
     "gd_last_timing": (C.c_int, [C.c_void_p, C.POINTER(gd_timing)]),
     "gd_work_counters": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
     "gd_phase_clocks": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "gd_ligand_graph": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                  C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_uint8),
+                                  C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                  C.POINTER(C.c_uint8), C.c_char_p, C.c_size_t]),
     "gd_detect_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_uint8),
                                   C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_void_p,
                                   C.POINTER(C.c_int32)]),
@@ -431,6 +435,27 @@ class Docker:
 # ---------------------------------------------------------------------------
 def optimal_tile_size(step: int) -> int:
     return int(lib().gd_optimal_tile_size(step))
+
+
+def ligand_graph(xyz, radii, bonds, rotatable):
+    """Native find_rotamers + grow_fragments (gd_ligand_graph): returns
+    (rotamer bond indices [R], membership [2R, n] bool: row 2r = left), or
+    raises GeoDockError with the Ligand validation message."""
+    x = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+    r = np.ascontiguousarray(radii, dtype=np.float64)
+    b = np.ascontiguousarray(bonds, dtype=np.int32).reshape(-1, 2)
+    ro = np.ascontiguousarray(rotatable, dtype=np.uint8)
+    n, nb = len(x), len(b)
+    rb = np.zeros(max(nb, 1), np.int32)
+    mem = np.zeros((max(2 * nb, 1), max(n, 1)), np.uint8)
+    cnt = C.c_int32()
+    msg = C.create_string_buffer(256)
+    rc = lib().gd_ligand_graph(n, _p(x, _f64p), _p(r, _f64p), nb, _p(b, _i32p), _p(ro, _u8p),
+                               C.byref(cnt), _p(rb, _i32p), _p(mem, _u8p), msg, 256)
+    if rc != GD_OK:
+        raise GeoDockError(GD_ERR_INVALID, msg.value.decode())
+    k = cnt.value
+    return rb[:k].copy(), mem[:2 * k, :n].astype(bool)
 
 
 def orientations(step: int):

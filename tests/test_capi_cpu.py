@@ -131,3 +131,23 @@ def test_pocket_counts():
     assert len(synth_pocket(10, 8, 6, 1.0)) == 1989
     rough = synth_pocket(10, 8, 6, 1.0, 0.2, 5)
     assert 0.8 * 1989 <= len(rough) <= 1989
+
+
+def test_ligand_graph_matches_reference():
+    """gd_ligand_graph (native find_rotamers + grow_fragments) against the
+    reference's own functions, on the reference generator's ligands (with
+    rings) and on invalid ligands."""
+    from oracle import oracle_py as O
+    from paper_1901_06363_b200.native import GeoDockError, ligand_graph
+    if not O.have_ref():
+        pytest.skip("oracle/_ref not built")
+    pocket, batch = O.ref_generate_synthetic(40, 77, 6, 60, 0, 12)
+    for l in range(batch.n_ligands):
+        args = batch.ligand(l)
+        want = O.ref_ligand_graph(*args)
+        got = ligand_graph(*args)
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    bad = (np.zeros((3, 3)), np.ones(3), np.array([[0, 0]]), np.array([1]))
+    assert O.ref_ligand_graph(*bad) is None
+    with pytest.raises(GeoDockError, match="self-bond"):
+        ligand_graph(*bad)

@@ -48,9 +48,12 @@ def main():
     best = []
     for pk_i in range(a.pockets):
         pocket = W.pocket_of(w, pk_i)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
         d.set_pocket(pocket)
-        build_ms += 1e3 * (time.perf_counter() - t0)
+        dt = 1e3 * (time.perf_counter() - t0)
+        build_ms += dt
+        print(f"pocket {pk_i}: index build {dt:.1f} ms", file=sys.stderr, flush=True)
         batch = base.__class__(base.atom_offsets, base.xyz + pocket.mean(axis=0), base.radii,
                                base.bond_offsets, base.bonds, base.rotatable)
         d.upload(batch)
