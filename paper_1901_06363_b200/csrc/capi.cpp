@@ -14,6 +14,9 @@
 #include <cstring>
 #include <numeric>
 #include <string>
+#include <condition_variable>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -83,6 +86,65 @@ double env_double(const char* name, double dflt) {
 
 }  // namespace
 
+namespace {
+
+// Persistent host workers for ligand preprocessing: run(fn) executes fn on
+// every worker and on the caller and returns when all have finished (fn
+// pulls its items from a shared atomic cursor).  Created once per context,
+// so a pipelined batch does not pay thread creation per chunk.
+class WorkerPool {
+ public:
+  explicit WorkerPool(int workers) {
+    for (int i = 0; i < workers; ++i) th_.emplace_back([this] { loop(); });
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  void run(const std::function<void()>& fn) {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &fn;
+      busy_ = static_cast<int>(th_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    fn();
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return busy_ == 0; });
+  }
+
+ private:
+  void loop() {
+    int seen = 0;
+    for (;;) {
+      const std::function<void()>* job;
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        job = job_;
+      }
+      (*job)();
+      std::lock_guard<std::mutex> g(mu_);
+      if (--busy_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void()>* job_ = nullptr;
+  int gen_ = 0, busy_ = 0;
+  bool stop_ = false;
+};
+
+}  // namespace
+
 struct gd_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
@@ -90,6 +152,8 @@ struct gd_ctx {
   cudaStream_t stream = nullptr;
   std::string err;
   cudaEvent_t ev[5] = {};
+  std::vector<cudaEvent_t> chunk_ev;       // one per pipelined chunk (no timing)
+  std::unique_ptr<WorkerPool> pool;        // host preprocessing workers
 
   // Pocket.
   int32_t P = 0;
@@ -200,6 +264,7 @@ extern "C" int gd_destroy(gd_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   for (cudaEvent_t ev : ctx->ev)
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : ctx->chunk_ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
   if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
   delete ctx;
@@ -477,8 +542,6 @@ static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
                        int& chunk_max_n) {
   const int cnt = c1 - c0;
   std::vector<PreparedLigand> prep(cnt);
-  const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-  const int nth = std::min(hw, std::max(1, cnt / 32));
   std::atomic<int> next{0};
   auto work = [&] {
     for (int s; (s = next.fetch_add(8)) < cnt;)
@@ -490,10 +553,15 @@ static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
                                  b->bonds + 2 * b0, b->bond_rotatable + b0);
       }
   };
-  std::vector<std::thread> pool;
-  for (int t = 1; t < nth; ++t) pool.emplace_back(work);
-  work();
-  for (auto& t : pool) t.join();
+  if (cnt < 64) {
+    work();
+  } else {
+    if (!ctx->pool) {
+      const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+      ctx->pool = std::make_unique<WorkerPool>(hw - 1);
+    }
+    ctx->pool->run(work);
+  }
 
   auto* meta = reinterpret_cast<LigMeta*>(ctx->pin[kMeta]);
   auto* hxyz = reinterpret_cast<double*>(ctx->pin[kXyz]);
@@ -771,9 +839,11 @@ static int d2h_range(gd_ctx* ctx, const gd_result* r, int l0, int l1, cudaStream
 
 // Empty slots (ligands that failed, or slots past k_eff) read as
 // orientation -2 and zeros; needs k_eff and status already on the host.
-static void fill_empty(gd_ctx* ctx, gd_result* r, const int32_t* keff, const int32_t* stat) {
-  const int L = ctx->n_lig, K = ctx->last_topk;
-  for (int l = 0; l < L; ++l) {
+static void fill_empty(gd_ctx* ctx, gd_result* r, const int32_t* keff, const int32_t* stat,
+                       int l0 = 0, int l1 = -1) {
+  const int K = ctx->last_topk;
+  if (l1 < 0) l1 = ctx->n_lig;
+  for (int l = l0; l < l1; ++l) {
     const int kk = stat[l] != 0 ? 0 : (ctx->last_rigid ? keff[l] : 1);
     if (r->k_eff) r->k_eff[l] = kk;
     if (stat[l] != 0 && r->poses_scored) r->poses_scored[l] = 0;
@@ -864,10 +934,10 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   pr.final_pose = keep_pose ? static_cast<double*>(take(8 * pose_elems)) : nullptr;
 
   // Chunk plan: a small head chunk (its host prep is the only part nothing
-  // overlaps), then up to 7 equal chunks.
+  // overlaps), then up to 15 equal chunks (a short tail after the last prep).
   std::vector<int> bounds{0};
   if (L > 2048) {
-    const int head = 512, rest = L - head, parts = std::min(7, std::max(1, rest / 1024));
+    const int head = 256, rest = L - head, parts = std::min(15, std::max(1, rest / 512));
     bounds.push_back(head);
     for (int c = 1; c <= parts; ++c)
       bounds.push_back(head + static_cast<int>(static_cast<long long>(rest) * c / parts));
@@ -875,6 +945,11 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
     bounds.push_back(L);
   }
   const int chunks = static_cast<int>(bounds.size()) - 1;
+  while (static_cast<int>(ctx->chunk_ev.size()) < chunks) {
+    cudaEvent_t e;
+    GD_CUDA(ctx, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->chunk_ev.push_back(e);
+  }
   float prep_ms = 0.0f;
   ctx->timing.launches = 0;
   for (int c = 0; c < chunks; ++c) {
@@ -888,28 +963,45 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
     if ((rc = h2d_range(ctx, c0, c1, before, run, s)) != GD_OK) return rc;
     if ((rc = launch_range(ctx, p, c0, c1, mx, s, nullptr)) != GD_OK) return rc;
     if ((rc = d2h_range(ctx, &pr, c0, c1, s)) != GD_OK) return rc;
+    GD_CUDA(ctx, cudaEventRecord(ctx->chunk_ev[c], s));
   }
+  // Results chunk by chunk, in order: pinned arena -> caller arrays while the
+  // later chunks are still on the GPU.
+  float post_ms = 0.0f;
+  for (int c = 0; c < chunks; ++c) {
+    GD_CUDA(ctx, cudaEventSynchronize(ctx->chunk_ev[c]));
+    const auto t_post = std::chrono::steady_clock::now();
+    const int l0 = bounds[c], l1 = bounds[c + 1];
+    const size_t s0 = static_cast<size_t>(l0) * K, sn = static_cast<size_t>(l1 - l0) * K;
+    auto copy = [](void* dst, const void* src, size_t elem, size_t off, size_t cnt) {
+      if (dst && src && cnt)
+        std::memcpy(static_cast<unsigned char*>(dst) + elem * off,
+                    static_cast<const unsigned char*>(src) + elem * off, elem * cnt);
+    };
+    copy(result->orientation, pr.orientation, 4, s0, sn);
+    copy(result->seed_rank, pr.seed_rank, 4, s0, sn);
+    copy(result->rigid_score, pr.rigid_score, 8, s0, sn);
+    copy(result->final_score, pr.final_score, 8, s0, sn);
+    copy(result->evaluations, pr.evaluations, 8, s0, sn);
+    copy(result->feasibility_checks, pr.feasibility_checks, 8, s0, sn);
+    copy(result->poses_scored, pr.poses_scored, 8, l0, l1 - l0);
+    copy(result->status, pr.status, 4, l0, l1 - l0);
+    if (keep_pose) {
+      const size_t p0 = 3 * static_cast<size_t>(K) * ctx->atom_off[l0];
+      const size_t p1 = 3 * static_cast<size_t>(K) * ctx->atom_off[l1];
+      copy(result->final_pose, pr.final_pose, 8, p0, p1 - p0);
+    }
+    fill_empty(ctx, result, pr.k_eff, pr.status, l0, l1);
+    post_ms += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_post).count();
+  }
+  if (L == 0) fill_empty(ctx, result, pr.k_eff, pr.status);
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->aux_stream));
   ctx->have_result = true;
   ctx->staged = true;
-  const auto t_post = std::chrono::steady_clock::now();
-  auto copy = [](void* dst, const void* src, size_t bytes) {
-    if (dst && src) std::memcpy(dst, src, bytes);
-  };
-  copy(result->orientation, pr.orientation, 4 * slots);
-  copy(result->seed_rank, pr.seed_rank, 4 * slots);
-  copy(result->rigid_score, pr.rigid_score, 8 * slots);
-  copy(result->final_score, pr.final_score, 8 * slots);
-  copy(result->evaluations, pr.evaluations, 8 * slots);
-  copy(result->feasibility_checks, pr.feasibility_checks, 8 * slots);
-  copy(result->poses_scored, pr.poses_scored, 8 * std::max(L, 1));
-  copy(result->status, pr.status, 4 * std::max(L, 1));
-  copy(result->final_pose, pr.final_pose, 8 * pose_elems);
-  fill_empty(ctx, result, pr.k_eff, pr.status);
   const auto t_end = std::chrono::steady_clock::now();
   ctx->timing.host_prep_ms = prep_ms;
-  ctx->timing.host_post_ms = std::chrono::duration<float, std::milli>(t_end - t_post).count();
+  ctx->timing.host_post_ms = post_ms;
   ctx->timing.total_ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();
   return GD_OK;
 }
