@@ -27,6 +27,7 @@
 // All decisions reproduce the reference: strict '>' with first-encountered
 // ties (kernel.hpp:136, :169, :173, :185, :194), angle 0 = committed pose,
 // feasibility_checks / evaluations counted as CandidateEvaluator does.
+#include <algorithm>
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -748,13 +749,17 @@ size_t flex_smem_bytes(const DockParams& p) {
   return kWarps * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs);
 }
 
-// Batch size: 8 candidates when the high-precision step has >= 16 of them
-// (fewer, partly empty batches), else 4 (less shared memory, more L1).
-// Measured: c1 (hp 30, 11 candidates) 18.6 ms at 4 vs 19+ at 6/8; c2 (hp 10,
-// 35 candidates) 81 ms at 8 vs 89 ms at 4.
+// Batch size from the high-precision step's c = 360/hp - 1 candidates: the
+// fewest batches of at most 8, evenly filled, rounded up to an
+// instantiated size (4, 6, 8).  Measured (c1: c = 11 -> 6; c2: c = 35 -> 8):
+// c1 flex 17.29 / 16.84 / 17.07 / 17.78 ms at B = 4 / 6 / 8 / 12; c2 74.1 ms
+// at 8 vs 75.5 at 6 and 78.1 at 12.
 int flex_batch(const DockParams& p) {
   if (GD_FLEX_BATCH) return GD_FLEX_BATCH;
-  return 360 / p.hp - 1 >= 16 ? 8 : 4;
+  const int c = std::max(1, 360 / p.hp - 1);
+  const int batches = (c + 7) / 8;
+  const int b = (c + batches - 1) / batches;
+  return b <= 4 ? 4 : b <= 6 ? 6 : 8;
 }
 
 template <int B>
@@ -794,7 +799,14 @@ int launch_flex(const DockParams& p, void* stream) {
   const long long chains = static_cast<long long>(p.n_lig) * p.k_slots;
   if (chains == 0) return cudaSuccess;
   const auto s = static_cast<cudaStream_t>(stream);
-  return flex_batch(p) == 8 ? launch_flex_b<8>(p, chains, s) : launch_flex_b<4>(p, chains, s);
+  switch (flex_batch(p)) {
+    case 8: return launch_flex_b<8>(p, chains, s);
+    case 6: return launch_flex_b<6>(p, chains, s);
+#if GD_FLEX_BATCH == 12
+    case 12: return launch_flex_b<12>(p, chains, s);  // A/B builds
+#endif
+    default: return launch_flex_b<4>(p, chains, s);
+  }
 }
 
 int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
