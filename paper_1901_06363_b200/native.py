@@ -244,6 +244,26 @@ class Knobs:
         return self.top_k if self.rigid_step > 0 else 1
 
 
+class ProfileBuffers:
+    """Host output buffers of gd_rotation_profiles, sized for a batch (2 x
+    its rotatable bonds fragments) and reusable across calls."""
+
+    def __init__(self, cap: int, n_ligands: int):
+        self.scores = np.empty((cap, 360), np.float64)
+        self.valid = np.empty((cap, 360), np.uint8)
+        self.rel = np.empty(cap, np.float64)
+        self.offs = np.empty(n_ligands + 1, np.int32)
+        self.status = np.empty(max(n_ligands, 1), np.int32)
+
+    @staticmethod
+    def for_batch(batch: "LigandBatch") -> "ProfileBuffers":
+        return ProfileBuffers(max(1, 2 * int(batch.rotatable.sum())), batch.n_ligands)
+
+    def fits(self, batch: "LigandBatch") -> bool:
+        return (len(self.rel) >= 2 * int(batch.rotatable.sum())
+                and len(self.offs) >= batch.n_ligands + 1)
+
+
 @dataclass
 class Profiles:
     """Rotation profiles of a batch: fragment f of ligand l is row
@@ -386,27 +406,26 @@ class Docker:
         self._check(self._lib.gd_phase_clocks(self._h, out))
         return list(out)
 
-    def rotation_profiles(self, batch: "LigandBatch | None" = None, flags: int = 0) -> "Profiles":
+    def rotation_profiles(self, batch: "LigandBatch | None" = None, flags: int = 0,
+                          out: "ProfileBuffers | None" = None) -> "Profiles":
         """rotation_profile (analysis.hpp:37-56) of every fragment of `batch`
-        (uploaded first) or of the batch staged last, from its poses."""
+        (uploaded first) or of the batch staged last, from its poses.  `out`
+        (ProfileBuffers.for_batch) reuses host output buffers across calls."""
         if batch is not None:
             self.upload(batch)
         staged = self._batch
         if staged is None:
             raise GeoDockError(GD_ERR_INVALID, "rotation_profiles: no batch staged")
         L = staged.n_ligands
-        cap = max(1, 2 * int(staged.rotatable.sum()))
-        scores = np.zeros((cap, 360), np.float64)
-        valid = np.zeros((cap, 360), np.uint8)
-        rel = np.zeros(cap, np.float64)
-        offs = np.zeros(L + 1, np.int32)
-        status = np.zeros(max(L, 1), np.int32)
+        buf = out if out is not None and out.fits(staged) else ProfileBuffers.for_batch(staged)
         self._check(self._lib.gd_rotation_profiles(
-            self._h, flags, _p(scores, C.POINTER(C.c_double)), _p(valid, C.POINTER(C.c_uint8)),
-            _p(rel, C.POINTER(C.c_double)), _p(offs, C.POINTER(C.c_int32)),
-            _p(status, C.POINTER(C.c_int32)), cap))
-        F = int(offs[-1])
-        return Profiles(scores[:F], valid[:F].astype(bool), rel[:F], offs, status[:L])
+            self._h, flags, _p(buf.scores, C.POINTER(C.c_double)),
+            _p(buf.valid, C.POINTER(C.c_uint8)), _p(buf.rel, C.POINTER(C.c_double)),
+            _p(buf.offs, C.POINTER(C.c_int32)), _p(buf.status, C.POINTER(C.c_int32)),
+            len(buf.rel)))
+        F = int(buf.offs[L])
+        return Profiles(buf.scores[:F], buf.valid[:F].view(bool), buf.rel[:F], buf.offs[:L + 1],
+                        buf.status[:L])
 
     def fp64_peak_tflops(self) -> float:
         t = C.c_double()
