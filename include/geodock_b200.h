@@ -145,6 +145,19 @@ int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs);
 int gd_download(gd_ctx* ctx, gd_result* result);
 int gd_last_timing(const gd_ctx* ctx, gd_timing* out);
 
+/* ---- planner (host) ------------------------------------------------------ */
+/* The seven interaction features (perf_model.hpp:36-47) of one dataset
+ * summary {pocket points, avg atoms, avg rotamers}: x[7]. */
+void gd_cost_features(const double* features, double* x);
+/* fit (perf_model.hpp:57-105): OLS of seconds per ligand on the seven
+ * features plus an intercept, column-pivoting Householder QR.  features:
+ * n x 3 summaries; times: n seconds per ligand; out: coef[7], intercept,
+ * adjusted R^2.  GD_ERR_INVALID with the reference's message in msg for
+ * n < 9, a non-positive time or a rank-deficient design ("collinear
+ * columns: ..."). */
+int gd_fit_cost_model(const double* features, const double* times, int32_t n, double* coef,
+                      double* intercept, double* adjusted_r2, char* msg, size_t msg_len);
+
 /* ---- ligand graph (host) ------------------------------------------------ */
 /* The batch path's host preprocessing of one ligand, exposed for the C++
  * drop-in: Ligand validation (molecule.hpp:66-115; the reference's message

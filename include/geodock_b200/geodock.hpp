@@ -23,6 +23,7 @@
 //   (new) dock_batch                           the north-star batch path:
 //                                              rigid sweep + top-K + restarts
 //   analysis.hpp (rotation profiles, peaks)    geodock_b200/analysis.hpp
+//   perf_model.hpp + autotuner.hpp (planner)   geodock_b200/planner.hpp
 //   formats.hpp (files, reports, CSVs)         geodock_b200/formats.hpp
 //
 // Results are bit-identical to the reference.  Link with
@@ -40,6 +41,7 @@
 #include <optional>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <variant>
 #include <vector>
@@ -354,6 +356,13 @@ struct KnobConfig {
   }
   friend bool operator==(const KnobConfig&, const KnobConfig&) = default;
 };
+
+/// Canonical knob order (kernel.hpp:44-48): the planner's final tie-break.
+inline bool knob_order_less(const KnobConfig& a, const KnobConfig& b) {
+  return std::tie(a.high_precision_step, a.low_precision_step, a.threshold, a.repetitions,
+                  a.enable_refinement) < std::tie(b.high_precision_step, b.low_precision_step,
+                                                  b.threshold, b.repetitions, b.enable_refinement);
+}
 
 struct PoseResult {
   std::string ligand_id;

@@ -98,6 +98,10 @@ SIGNATURES = {
                                   C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_uint8),
                                   C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                   C.POINTER(C.c_uint8), C.c_char_p, C.c_size_t]),
+    "gd_cost_features": (None, [C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "gd_fit_cost_model": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32,
+                                    C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
     "gd_detect_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_uint8),
                                   C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_void_p,
                                   C.POINTER(C.c_int32)]),
@@ -454,6 +458,22 @@ class Docker:
 # ---------------------------------------------------------------------------
 def optimal_tile_size(step: int) -> int:
     return int(lib().gd_optimal_tile_size(step))
+
+
+def fit_cost_model(features, times):
+    """fit (perf_model.hpp:57-105) via gd_fit_cost_model: features [n, 3]
+    (pocket points, avg atoms, avg rotamers), times [n] s/ligand ->
+    (coefficients [7], intercept, adjusted R^2)."""
+    f = np.ascontiguousarray(features, dtype=np.float64).reshape(-1, 3)
+    t = np.ascontiguousarray(times, dtype=np.float64)
+    coef = np.zeros(7)
+    icpt, r2 = C.c_double(), C.c_double()
+    msg = C.create_string_buffer(512)
+    rc = lib().gd_fit_cost_model(_p(f, _f64p), _p(t, _f64p), len(t), _p(coef, _f64p),
+                                 C.byref(icpt), C.byref(r2), msg, 512)
+    if rc != GD_OK:
+        raise GeoDockError(rc, msg.value.decode())
+    return coef, icpt.value, r2.value
 
 
 def ligand_graph(xyz, radii, bonds, rotatable):

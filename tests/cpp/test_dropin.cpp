@@ -1,5 +1,6 @@
 // Drop-in API test: the reference's own test cases (test_geometry.cpp,
-// test_kernel.cpp, test_screening.cpp, test_analysis.cpp), restated against
+// test_kernel.cpp, test_screening.cpp, test_analysis.cpp, test_autotuner.cpp),
+// restated against
 // <geodock_b200/geodock.hpp>, which runs them on the GPU through the C-ABI.
 // A plain runner (no Catch2 in this image): prints one line per case and
 // exits non-zero on any failure.  Built and run by tests/test_dropin.py.
@@ -11,6 +12,7 @@
 
 #include "geodock_b200/analysis.hpp"
 #include "geodock_b200/geodock.hpp"
+#include "geodock_b200/planner.hpp"
 
 using namespace geodock;
 
@@ -268,6 +270,52 @@ int main() {
         CHECK(batch[l].fragments[f].delta_overlap == a.fragments[f].delta_overlap);
       CHECK(batch[l].peaks.size() == a.peaks.size());
     }
+  });
+  run("build_knowledge_base profiles a small design space end to end", [] {
+    // Nine small training sets from the seeded generator; the three data
+    // features (pocket size, atoms, rotamers) all vary across them.
+    std::vector<TrainingSet> sets;
+    for (int s = 0; s < 9; ++s) {
+      std::vector<double> pts(3 * 4000);
+      const int P = gd_synth_pocket(3.0 + 0.4 * s, 2.5 + 0.3 * (s % 4), 2.0 + 0.25 * (s % 3), 1.0, 0.0,
+                                    100 + s, pts.data(), 4000);
+      std::vector<Vec3> pv;
+      for (int j = 0; j < P; ++j) pv.push_back({pts[3 * j], pts[3 * j + 1], pts[3 * j + 2]});
+      std::vector<Ligand> ligs;
+      for (int l = 0; l < 12; ++l) {
+        const double c[3] = {0, 0, 0};
+        const int lo = 8 + 2 * (s % 3), hi = 16 + 2 * (s % 4);
+        int32_t n = 0;
+        gd_synth_ligand_size(1000 + 17 * s, l, lo, hi, 0, &n);
+        std::vector<double> xyz(3 * n), radii(n);
+        std::vector<int32_t> bonds(2 * (n - 1));
+        std::vector<uint8_t> rot(n - 1);
+        gd_synth_ligand(1000 + 17 * s, l, lo, hi, 0, 1 + s % 3, -1, c, xyz.data(), radii.data(),
+                        bonds.data(), rot.data());
+        std::vector<Atom> atoms;
+        std::vector<Bond> bs;
+        for (int i = 0; i < n; ++i) atoms.push_back({i, {xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2]}, radii[i]});
+        for (int b = 0; b < n - 1; ++b) bs.push_back({bonds[2 * b], bonds[2 * b + 1], rot[b] != 0});
+        ligs.emplace_back("S" + std::to_string(s) + "L" + std::to_string(l), atoms, bs);
+      }
+      sets.push_back({Pocket("P" + std::to_string(s), pv), ligs});
+    }
+    const KnobConfig baseline{1, 45, 0.0, 2, false};
+    const std::vector<KnobConfig> space{baseline, {3, 45, 0.0, 1, false}, {1, 45, 0.0, 1, true}};
+    const KnowledgeBase kb = build_knowledge_base(space, sets, baseline, 2);
+    CHECK(kb.profiles.size() == 3);
+    CHECK(kb.warnings.empty());
+    CHECK(kb.profiles.size() == 3 && kb.profiles[0].config == baseline && kb.profiles[0].mean_degradation == 0.0);
+    for (const ConfigProfile& p : kb.profiles) CHECK(p.perf.n_observations == 9 && p.perf.config == p.config);
+    // Cheaper configurations never score better than the exhaustive baseline on average.
+    for (const ConfigProfile& p : kb.profiles) CHECK(p.mean_degradation >= -1e-9);
+    bool threw = false;
+    try {
+      build_knowledge_base({{3, 45, 0.0, 1, false}}, sets, baseline, 1);
+    } catch (const Error&) {
+      threw = true;
+    }
+    CHECK(threw);
   });
   std::printf("%s (%d failed checks)\n", g_failed ? "FAILED" : "OK", g_failed);
   return g_failed ? 1 : 0;

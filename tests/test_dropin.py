@@ -3,7 +3,8 @@
 Compiling tests/cpp/test_dropin.cpp against the headers and the in-tree
 library is a CPU test; running it (the reference's own test cases through
 the GPU) is a GPU test.  tests/cpp/test_formats.cpp (file formats, reports,
-ligand graph helpers) needs no GPU and runs in the CPU suite.
+ligand graph helpers) and tests/cpp/test_planner.cpp (cost model, config
+selection, planner files) need no GPU and run in the CPU suite.
 """
 import subprocess
 from pathlib import Path
@@ -29,8 +30,10 @@ def test_dropin_header_compiles_and_links():
     assert _compile().exists()
 
 
-def test_dropin_formats_and_graph_on_cpu():
-    exe = _compile("test_formats")
+@pytest.mark.parametrize("name", ["test_formats", "test_planner"])
+def test_dropin_host_parts_on_cpu(name):
+    """File formats, ligand graph helpers and the planner need no GPU."""
+    exe = _compile(name)
     res = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "FAIL" not in res.stdout
