@@ -6,7 +6,8 @@
 // (reference overlap_score, geometry.hpp:143-154).  Top K by (score desc,
 // orientation index asc) (E5): for K <= 32 each warp keeps a sorted top-32
 // in registers (shuffle networks) and a 3-level tree merges the 8 warp
-// lists; larger K goes through a shared-memory bitonic sort chunk by chunk.
+// lists; larger K keeps a sorted shared-memory list into which each round's
+// winners (scores beating the current K-th) are merged by rank.
 #include <algorithm>
 
 #include "device_common.cuh"
