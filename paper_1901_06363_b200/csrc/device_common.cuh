@@ -249,18 +249,34 @@ __device__ __forceinline__ void min_dist_sqM(const PocketView& pk, const double*
 struct Axis {
   double ox, oy, oz, kx, ky, kz;
 };
+// The angle-independent part of a Rodrigues rotation of point p about the
+// axis: v = p - o, k x v and k . v (geometry.hpp:180-184) ...
+struct Arm {
+  double vx, vy, vz, crx, cry, crz, d;
+};
+__device__ __forceinline__ Arm arm_of(const Axis& a, double px, double py, double pz) {
+  Arm r;
+  r.vx = dsub(px, a.ox);
+  r.vy = dsub(py, a.oy);
+  r.vz = dsub(pz, a.oz);
+  r.crx = dsub(dmul(a.ky, r.vz), dmul(a.kz, r.vy));
+  r.cry = dsub(dmul(a.kz, r.vx), dmul(a.kx, r.vz));
+  r.crz = dsub(dmul(a.kx, r.vy), dmul(a.ky, r.vx));
+  r.d = dadd(dadd(dmul(a.kx, r.vx), dmul(a.ky, r.vy)), dmul(a.kz, r.vz));
+  return r;
+}
+// ... and the per-angle part: ((o + v c) + (k x v) s) + k ((k . v)(1 - c)).
+__device__ __forceinline__ void turn(const Axis& a, const Arm& r, double c, double s, double omc,
+                                     double& qx, double& qy, double& qz) {
+  const double w = dmul(r.d, omc);
+  qx = dadd(dadd(dadd(a.ox, dmul(r.vx, c)), dmul(r.crx, s)), dmul(a.kx, w));
+  qy = dadd(dadd(dadd(a.oy, dmul(r.vy, c)), dmul(r.cry, s)), dmul(a.ky, w));
+  qz = dadd(dadd(dadd(a.oz, dmul(r.vz, c)), dmul(r.crz, s)), dmul(a.kz, w));
+}
 __device__ __forceinline__ void rodrigues(const Axis& a, double c, double s, double omc, double px,
                                           double py, double pz, double& qx, double& qy,
                                           double& qz) {
-  const double vx = dsub(px, a.ox), vy = dsub(py, a.oy), vz = dsub(pz, a.oz);
-  const double crx = dsub(dmul(a.ky, vz), dmul(a.kz, vy));
-  const double cry = dsub(dmul(a.kz, vx), dmul(a.kx, vz));
-  const double crz = dsub(dmul(a.kx, vy), dmul(a.ky, vx));
-  const double d = dadd(dadd(dmul(a.kx, vx), dmul(a.ky, vy)), dmul(a.kz, vz));
-  const double w = dmul(d, omc);
-  qx = dadd(dadd(dadd(a.ox, dmul(vx, c)), dmul(crx, s)), dmul(a.kx, w));
-  qy = dadd(dadd(dadd(a.oy, dmul(vy, c)), dmul(cry, s)), dmul(a.ky, w));
-  qz = dadd(dadd(dadd(a.oz, dmul(vz, c)), dmul(crz, s)), dmul(a.kz, w));
+  turn(a, arm_of(a, px, py, pz), c, s, omc, qx, qy, qz);
 }
 
 // Rigid pose (E3): p' = c + R (p - c), rows summed left to right.
