@@ -2,7 +2,9 @@
 # box, from the repo root.  Usage: bash tools/ab_defs.sh "-DA=1 -DB=2" ...
 mkdir -p gpurun_out
 for v in "$@"; do
-  GD_DEFS="$v" python paper_1901_06363_b200/build.py --force > /dev/null 2>&1
+  if ! GD_DEFS="$v" python paper_1901_06363_b200/build.py --force > /dev/null 2>&1; then
+    echo "variant $v BUILD FAILED" >> gpurun_out/ab_defs.log; continue
+  fi
   echo "variant $v" >> gpurun_out/ab_defs.log
   timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/ab_defs.log 2>&1
 done
