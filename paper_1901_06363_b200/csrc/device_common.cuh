@@ -244,6 +244,7 @@ __device__ __forceinline__ void min_dist_sqM(const PocketView& pk, const double*
   }
 }
 
+
 // Rodrigues rotation of one atom (geometry.hpp:182-184):
 // ((o + v*c) + cross(k,v)*s) + k*(dot(k,v)*(1-c)), v = p - o.
 struct Axis {
