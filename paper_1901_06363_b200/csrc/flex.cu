@@ -35,8 +35,12 @@
 namespace gdb200 {
 namespace {
 
-#ifndef GD_FLEX_MINB
-#define GD_FLEX_MINB 6       // resident CTAs per SM the register budget targets
+// CTA shape: W chains (warps) per CTA, 24 / W CTAs per SM (the register
+// budget: 65536 / (24 * 32) = 85 registers).  12-chain CTAs for batches of
+// up to 6 candidates (c1: 16.09 ms vs 16.57 with 4), 4-chain CTAs for 8-
+// candidate batches, whose larger v rows fit better (c2: 74.3 vs 75.0 ms).
+#ifndef GD_FLEX_RESIDENT
+#define GD_FLEX_RESIDENT 24  // warps per SM the register budget targets
 #endif
 // Candidates evaluated together by one warp: a template parameter (4 or 8,
 // chosen per launch from the knobs, launch_flex); GD_FLEX_BATCH forces one.
@@ -49,7 +53,10 @@ namespace {
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
-constexpr int kWarps = 4;    // chains per CTA
+template <int B>
+constexpr int warps_for() {
+  return B == 8 ? 4 : 12;
+}
 constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -465,8 +472,9 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   return true;
 }
 
-template <bool On, int B>
-__global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(DockParams p) {
+template <bool On, int B, int kWarps = warps_for<B>()>
+__global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
+    flex_chain_kernel(DockParams p) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.k_slots;
@@ -667,8 +675,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB) flex_chain_kernel(D
 // a dropped pair cannot bump at any angle); angles 1..359 go through
 // eval_batch exactly like search candidates.  Invalid angles report score 0,
 // the reference's value-initialised array entry.
-template <bool On, int B>
-__global__ void __launch_bounds__(kWarps * 32, GD_FLEX_MINB)
+template <bool On, int B, int kWarps = warps_for<B>()>
+__global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     profile_kernel(DockParams p, const int32_t* items, int n_items, double* scores, uint8_t* valid) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -784,9 +792,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(DockParams p) {
   }
 }
 
-template <int B>
+template <int B, int W>
 size_t flex_smem_bytes(const DockParams& p) {
-  return kWarps * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs);
+  return W * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs);
 }
 
 // Batch size from the high-precision step's c = 360/hp - 1 candidates: the
@@ -802,10 +810,20 @@ int flex_batch(const DockParams& p) {
   return b <= 4 ? 4 : b <= 6 ? 6 : 8;
 }
 
-template <int B>
-int launch_flex_b(const DockParams& p, long long chains, cudaStream_t stream) {
-  const size_t smem = flex_smem_bytes<B>(p);
-  auto kernel = p.counters ? flex_chain_kernel<true, B> : flex_chain_kernel<false, B>;
+int max_smem_optin() {
+  static int v = [] {
+    int dev = 0, bytes = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&bytes, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return bytes;
+  }();
+  return v;
+}
+
+template <int B, int W>
+int launch_flex_bw(const DockParams& p, long long chains, cudaStream_t stream) {
+  const size_t smem = flex_smem_bytes<B, W>(p);
+  auto kernel = p.counters ? flex_chain_kernel<true, B, W> : flex_chain_kernel<false, B, W>;
   cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return e;
@@ -815,22 +833,46 @@ int launch_flex_b(const DockParams& p, long long chains, cudaStream_t stream) {
     e = cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(cv));
     if (e != cudaSuccess) return e;
   }
-  const long long blocks = (chains + kWarps - 1) / kWarps;
-  kernel<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(p);
+  const long long blocks = (chains + W - 1) / W;
+  kernel<<<static_cast<unsigned>(blocks), W * 32, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+// The preferred CTA shape when its shared memory fits the opt-in limit,
+// else narrower CTAs (large ligands: ~30 KB per chain at 150 atoms).
+template <int B>
+int launch_flex_b(const DockParams& p, long long chains, cudaStream_t stream) {
+  const size_t lim = static_cast<size_t>(max_smem_optin());
+  constexpr int W0 = warps_for<B>();
+  if (flex_smem_bytes<B, W0>(p) <= lim) return launch_flex_bw<B, W0>(p, chains, stream);
+  if (flex_smem_bytes<B, 4>(p) <= lim) return launch_flex_bw<B, 4>(p, chains, stream);
+  if (flex_smem_bytes<B, 2>(p) <= lim) return launch_flex_bw<B, 2>(p, chains, stream);
+  return launch_flex_bw<B, 1>(p, chains, stream);
+}
+
+template <int B, int W>
+int launch_profiles_bw(const DockParams& p, const int32_t* items, int n_items, double* scores,
+                       uint8_t* valid, cudaStream_t stream) {
+  const size_t smem = flex_smem_bytes<B, W>(p);
+  auto kernel = p.counters ? profile_kernel<true, B, W> : profile_kernel<false, B, W>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  const int blocks = (n_items + W - 1) / W;
+  kernel<<<blocks, W * 32, smem, stream>>>(p, items, n_items, scores, valid);
   return cudaGetLastError();
 }
 
 template <int B>
 int launch_profiles_b(const DockParams& p, const int32_t* items, int n_items, double* scores,
                       uint8_t* valid, cudaStream_t stream) {
-  const size_t smem = flex_smem_bytes<B>(p);
-  auto kernel = p.counters ? profile_kernel<true, B> : profile_kernel<false, B>;
-  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
-  if (e != cudaSuccess) return e;
-  const int blocks = (n_items + kWarps - 1) / kWarps;
-  kernel<<<blocks, kWarps * 32, smem, stream>>>(p, items, n_items, scores, valid);
-  return cudaGetLastError();
+  const size_t lim = static_cast<size_t>(max_smem_optin());
+  constexpr int W0 = warps_for<B>();
+  if (flex_smem_bytes<B, W0>(p) <= lim)
+    return launch_profiles_bw<B, W0>(p, items, n_items, scores, valid, stream);
+  if (flex_smem_bytes<B, 2>(p) <= lim)
+    return launch_profiles_bw<B, 2>(p, items, n_items, scores, valid, stream);
+  return launch_profiles_bw<B, 1>(p, items, n_items, scores, valid, stream);
 }
 
 }  // namespace
