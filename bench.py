@@ -196,6 +196,7 @@ def run_ours(a):
     d.dock_resident(Knobs(**{**knobs.__dict__, "flags": GD_FLAG_COUNT_WORK}))
     work = d.work_counters()
     fp64_peak = d.fp64_peak_tflops()
+    l2_peak = d.l2_gather_peak_gbs()
 
     d.dock_resident(knobs)
     gather = DeviceGather(d.device_results(), world) if world > 1 else None
@@ -316,6 +317,15 @@ def run_ours(a):
                          "traffic_source": traffic_src,
                          "peak_source": "measured fp64 DADD/DMUL probe (gd_fp64_peak) on this GPU",
                          "work_per_launch": dom_work},
+            # North star: the fraction of the L2-gather roofline.  Every
+            # candidate point costs one 32-byte index gather (its voxel record
+            # or list entry); peak = the same access pattern measured alone.
+            "roofline_l2_gather": {"kernel": dom, "bound": "l2",
+                                   "achieved": 32.0 * dom_work["pairs"] / (dom_ms / 1e3) / 1e9,
+                                   "peak": l2_peak, "unit": "GB/s",
+                                   "frac": 32.0 * dom_work["pairs"] / (dom_ms / 1e3) / 1e9 / l2_peak,
+                                   "peak_source": "measured random 32 B L1-bypassing gathers over "
+                                                  "an L2-resident 48 MB buffer (gd_l2_gather_peak)"},
             "clocks": clk,
         }
         if e2e:

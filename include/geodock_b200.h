@@ -237,6 +237,11 @@ int gd_phase_clocks(const gd_ctx* ctx, uint64_t out[16]);
 /* Measures this device's fp64 DADD/DMUL issue rate (TFLOP/s, no FMA) with
  * a probe kernel; the denominator of the fp64 roofline. */
 int gd_fp64_peak(gd_ctx* ctx, double* tflops);
+/* Measures this device's L2 random-gather rate (GB/s): 32-byte read-only
+ * loads, not allocated in L1, at random over an L2-resident 48 MB buffer --
+ * the access pattern of the voxel-index gathers; the denominator of the
+ * L2-gather roofline. */
+int gd_l2_gather_peak(gd_ctx* ctx, double* gbs);
 
 /* ---- fine-grained kernels ------------------------------------------------ */
 /* overlap_score (geometry.hpp:140-155) of n_poses poses of n_atoms atoms

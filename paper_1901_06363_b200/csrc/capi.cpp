@@ -1169,6 +1169,33 @@ extern "C" int gd_fp64_peak(gd_ctx* ctx, double* tflops) {
   return GD_OK;
 }
 
+extern "C" int gd_l2_gather_peak(gd_ctx* ctx, double* gbs) {
+  if (ctx == nullptr || gbs == nullptr) return GD_ERR_INVALID;
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  int sms = 0;
+  GD_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const unsigned long long n_rec = (48ull << 20) / 32;  // 48 MB of 32-byte records
+  DevBuf buf, sink;
+  GD_CUDA(ctx, buf.ensure(32 * n_rec));
+  GD_CUDA(ctx, sink.ensure(64));
+  GD_CUDA(ctx, cudaMemsetAsync(buf.ptr, 0, 32 * n_rec, ctx->stream));
+  const int blocks = sms * 8, threads = 256, iters = 256;
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {  // the first pass warms L2
+    GD_CUDA(ctx, cudaEventRecord(ctx->ev[0], ctx->stream));
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_l2_gather_probe(
+                     buf.as<double>(), n_rec, blocks, threads, iters, sink.as<double>(), ctx->stream)));
+    GD_CUDA(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
+    GD_CUDA(ctx, cudaEventSynchronize(ctx->ev[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  const double bytes = 32.0 * 4.0 * static_cast<double>(blocks) * threads * iters;
+  *gbs = bytes / (best * 1e-3) / 1e9;
+  return GD_OK;
+}
+
 extern "C" int gd_last_timing(const gd_ctx* ctx, gd_timing* out) {
   if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
   *out = ctx->timing;

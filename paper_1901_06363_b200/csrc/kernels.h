@@ -113,6 +113,10 @@ struct DockParams {
 
 // FP64 pipe probe: independent DADD/DMUL chains, returns fp64 ops executed.
 int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* stream);
+// L2 gather probe: random 32-byte loads over an L2-resident buffer of n_rec
+// records; blocks * threads * iters * 4 loads.
+int launch_l2_gather_probe(const double* buf, unsigned long long n_rec, int blocks, int threads,
+                           int iters, double* sink, void* stream);
 
 // Launchers; return cudaError_t as int.  `stream` is a cudaStream_t.
 int launch_rigid_topk(const DockParams& p, void* stream);

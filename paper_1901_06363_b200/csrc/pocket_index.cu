@@ -203,7 +203,38 @@ __global__ void fp64_probe_kernel(double* sink, int iters) {
   if (s == 12345.0) sink[0] = s;  // keeps the chains live
 }
 
+// L2 gather probe: random 32-byte read-only loads (L1::no_allocate, as the
+// index gathers) over a buffer that stays L2-resident, four independent
+// loads in flight per thread.  The achieved rate is the denominator of the
+// L2-gather roofline.
+__global__ void l2_gather_probe_kernel(const double* buf, unsigned long long n_rec, int iters,
+                                       double* sink) {
+  unsigned long long h = (blockIdx.x * 0x9E3779B97F4A7C15ull) ^ (threadIdx.x * 0xBF58476D1CE4E5B9ull);
+  double acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    double a[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      h ^= h >> 31;
+      h *= 0x94D049BB133111EBull;
+      h ^= h >> 29;
+      double x, y, z, w;
+      ld256<true>(buf + 4 * (h % n_rec), x, y, z, w);
+      a[k] = x + w;
+    }
+    acc += (a[0] + a[1]) + (a[2] + a[3]);
+  }
+  if (acc == 12345.678) sink[0] = acc;  // keeps the loads live
+}
+
 }  // namespace
+
+int launch_l2_gather_probe(const double* buf, unsigned long long n_rec, int blocks, int threads,
+                           int iters, double* sink, void* stream) {
+  l2_gather_probe_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(buf, n_rec,
+                                                                                   iters, sink);
+  return cudaGetLastError();
+}
 
 int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* stream) {
   fp64_probe_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(sink, iters);

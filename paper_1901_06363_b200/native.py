@@ -102,6 +102,7 @@ SIGNATURES = {
     "gd_fit_cost_model": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_int32,
                                     C.POINTER(C.c_double), C.POINTER(C.c_double),
                                     C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
+    "gd_l2_gather_peak": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "gd_detect_peaks": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_uint8),
                                   C.POINTER(C.c_double), C.POINTER(C.c_int32), C.c_void_p,
                                   C.POINTER(C.c_int32)]),
@@ -430,6 +431,11 @@ class Docker:
         F = int(buf.offs[L])
         return Profiles(buf.scores[:F], buf.valid[:F].view(bool), buf.rel[:F], buf.offs[:L + 1],
                         buf.status[:L])
+
+    def l2_gather_peak_gbs(self) -> float:
+        g = C.c_double()
+        self._check(self._lib.gd_l2_gather_peak(self._h, C.byref(g)))
+        return g.value
 
     def fp64_peak_tflops(self) -> float:
         t = C.c_double()
