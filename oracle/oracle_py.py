@@ -319,8 +319,9 @@ def ref_generate_synthetic(count, seed, atom_lo=6, atom_hi=14, rot_lo=2, rot_hi=
     h = ref()
     ta, tb = C.c_int(), C.c_int()
     args = [count, seed, atom_lo, atom_hi, rot_lo, rot_hi, pocket_points, pocket_radius]
-    h.gdref_generate_synthetic(*args, C.byref(ta), C.byref(tb), None, None, None, None, None,
-                               None, None)
+    if h.gdref_generate_synthetic(*args, C.byref(ta), C.byref(tb), None, None, None, None, None,
+                                  None, None):
+        raise RuntimeError(h.gdref_last_error().decode())
     pocket = np.zeros((pocket_points, 3))
     ao = np.zeros(count + 1, np.int32)
     xyz = np.zeros((ta.value, 3))

@@ -160,7 +160,14 @@ extern "C" int gdref_generate_synthetic(int count, uint64_t seed, int atom_lo, i
   spec.pocket_points = pocket_points;
   spec.pocket_radius = pocket_radius;
   spec.seed = seed;
-  const auto ds = geodock::generate_synthetic(spec);
+  std::optional<geodock::SyntheticDataset> maybe;
+  try {
+    maybe.emplace(geodock::generate_synthetic(spec));
+  } catch (const std::exception& e) {  // infeasible spec: report, do not abort
+    g_err = e.what();
+    return -1;
+  }
+  const auto& ds = *maybe;
   int ta = 0, tb = 0;
   for (const auto& l : ds.ligands) {
     ta += l.atom_count();

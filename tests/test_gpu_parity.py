@@ -154,6 +154,26 @@ def test_large_ligands_multiword_masks(docker):
         assert_same_result(got, want)
 
 
+def test_ligands_at_the_atom_limit(docker):
+    """220-256 atoms (four mask words; the flex CTA narrows to fit shared
+    memory) against the reference; 257 atoms is skipped, not docked."""
+    from paper_1901_06363_b200 import LigandBatch, synth_ligands
+    pocket = W.config(1).pocket()
+    batch = synth_ligands(777, [0, 1], n_lo=220, n_hi=256, r_cap=12, centre=pocket.mean(axis=0))
+    assert batch.sizes.min() >= 220 and batch.sizes.max() <= 256
+    docker.set_pocket(pocket)
+    knobs = Knobs(90, 90, 0.0, 1, False, 90, 3)
+    got = docker.dock(batch, knobs, keep_poses=True)
+    want = _cpu(batch, pocket, knobs)
+    assert_same_result(got, want)
+    n = 257
+    xyz = np.stack([np.arange(n) * 1.5, np.zeros(n), np.zeros(n)], axis=1)
+    big = LigandBatch.from_parts([(xyz, np.full(n, 1.2), np.stack([np.arange(n - 1), np.arange(1, n)], 1),
+                                   np.zeros(n - 1, np.uint8))])
+    res = docker.dock(big, knobs)
+    assert res.status[0] == 1 and res.k_eff[0] == 0
+
+
 def test_config3_rough_pocket(docker):
     """A config-3 pocket (random semi-axes, 1 A lattice, roughness mask)."""
     w = W.config(3)
