@@ -936,8 +936,10 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   // Chunk plan: a small head chunk (its host prep is the only part nothing
   // overlaps), then up to 15 equal chunks (a short tail after the last prep).
   std::vector<int> bounds{0};
+  static const int kHead = static_cast<int>(env_double("GD_E2E_HEAD", 256));
+  static const int kParts = static_cast<int>(env_double("GD_E2E_CHUNKS", 15));
   if (L > 2048) {
-    const int head = 256, rest = L - head, parts = std::min(15, std::max(1, rest / 512));
+    const int head = kHead, rest = L - head, parts = std::min(kParts, std::max(1, rest / 512));
     bounds.push_back(head);
     for (int c = 1; c <= parts; ++c)
       bounds.push_back(head + static_cast<int>(static_cast<long long>(rest) * c / parts));

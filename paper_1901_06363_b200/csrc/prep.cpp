@@ -10,55 +10,62 @@
 namespace gdb200 {
 namespace {
 
-struct Edge {
-  int nb;
-  int bond;
-};
-
-// Bridges of an undirected multigraph by iterative DFS lowpoints.  The set
-// of bridges does not depend on visiting order.
-std::vector<char> bridges(int n, const std::vector<std::vector<Edge>>& adj, int n_bonds) {
-  std::vector<char> is_bridge(n_bonds, 0);
-  std::vector<int> disc(n, -1), low(n, 0);
+// Per-thread scratch reused across ligands: the batch path preprocesses
+// every ligand once per call on the host workers, so these hot loops do
+// no heap allocation after warm-up.
+struct Scratch {
+  std::vector<int> off, nb, bond;  // CSR adjacency in bond order (both directions)
+  std::vector<int> queue, dist, disc, low;
+  std::vector<std::pair<int, int>> seen;
   struct Frame {
-    int atom, parent_bond;
-    size_t next;
+    int atom, parent_bond, next;
   };
   std::vector<Frame> stack;
+  std::vector<char> is_bridge;
+  std::vector<int> rot;
+};
+
+Scratch& scratch() {
+  thread_local Scratch s;
+  return s;
+}
+
+// Bridges of an undirected multigraph by iterative DFS lowpoints
+// (molecule.hpp:190-231).  The set of bridges does not depend on visiting
+// order.
+void bridges(int n, int n_bonds, Scratch& s) {
+  s.is_bridge.assign(n_bonds, 0);
+  s.disc.assign(n, -1);
+  s.low.assign(n, 0);
+  s.stack.clear();
   int timer = 0;
   for (int root = 0; root < n; ++root) {
-    if (disc[root] >= 0) continue;
-    disc[root] = low[root] = timer++;
-    stack.push_back({root, -1, 0});
-    while (!stack.empty()) {
-      Frame& f = stack.back();
-      if (f.next < adj[f.atom].size()) {
-        const Edge e = adj[f.atom][f.next++];
-        if (e.bond == f.parent_bond) continue;
-        if (disc[e.nb] >= 0) {
-          low[f.atom] = std::min(low[f.atom], disc[e.nb]);
+    if (s.disc[root] >= 0) continue;
+    s.disc[root] = s.low[root] = timer++;
+    s.stack.push_back({root, -1, s.off[root]});
+    while (!s.stack.empty()) {
+      Scratch::Frame& f = s.stack.back();
+      if (f.next < s.off[f.atom + 1]) {
+        const int e = f.next++;
+        const int nb = s.nb[e], bond = s.bond[e];
+        if (bond == f.parent_bond) continue;
+        if (s.disc[nb] >= 0) {
+          s.low[f.atom] = std::min(s.low[f.atom], s.disc[nb]);
         } else {
-          disc[e.nb] = low[e.nb] = timer++;
-          stack.push_back({e.nb, e.bond, 0});
+          s.disc[nb] = s.low[nb] = timer++;
+          s.stack.push_back({nb, bond, s.off[nb]});
         }
       } else {
         const int atom = f.atom, pb = f.parent_bond;
-        stack.pop_back();
-        if (!stack.empty()) {
-          const int parent = stack.back().atom;
-          low[parent] = std::min(low[parent], low[atom]);
-          if (low[atom] > disc[parent]) is_bridge[pb] = 1;
+        s.stack.pop_back();
+        if (!s.stack.empty()) {
+          const int parent = s.stack.back().atom;
+          s.low[parent] = std::min(s.low[parent], s.low[atom]);
+          if (s.low[atom] > s.disc[parent]) s.is_bridge[pb] = 1;
         }
       }
     }
   }
-  return is_bridge;
-}
-
-PreparedLigand fail(PreparedLigand p, std::string msg) {
-  p.status = GD_LIG_INVALID;
-  p.error = std::move(msg);
-  return p;
 }
 
 }  // namespace
@@ -67,118 +74,142 @@ PreparedLigand prepare_ligand(const std::string& id, int n, const double* xyz, c
                               int n_bonds, const int32_t* bonds, const uint8_t* rotatable) {
   PreparedLigand p;
   p.n = n;
-  const std::string tag = "ligand '" + id + "': ";
+  auto fail = [&](const std::string& what) {
+    p.status = GD_LIG_INVALID;
+    p.error = "ligand '" + id + "': " + what;
+    return std::move(p);
+  };
   // Ligand::validate (molecule.hpp:66-89), same checks in the same order.
-  if (n < 2) return fail(std::move(p), tag + "needs at least 2 atoms");
-  if (n > kMaxAtoms) return fail(std::move(p), tag + "more than 256 atoms is not supported");
+  if (n < 2) return fail("needs at least 2 atoms");
+  if (n > kMaxAtoms) return fail("more than 256 atoms is not supported");
   for (int i = 0; i < n; ++i) {
-    if (!(radii[i] > 0.0)) return fail(std::move(p), tag + "non-positive radius on atom " + std::to_string(i));
+    if (!(radii[i] > 0.0)) return fail("non-positive radius on atom " + std::to_string(i));
     if (!(std::isfinite(xyz[3 * i]) && std::isfinite(xyz[3 * i + 1]) && std::isfinite(xyz[3 * i + 2])))
-      return fail(std::move(p), tag + "non-finite position on atom " + std::to_string(i));
+      return fail("non-finite position on atom " + std::to_string(i));
   }
-  std::vector<std::pair<int, int>> seen;
-  seen.reserve(n_bonds);
+  Scratch& s = scratch();
+  s.seen.clear();
   for (int b = 0; b < n_bonds; ++b) {
     const int a0 = bonds[2 * b], a1 = bonds[2 * b + 1];
-    if (a0 == a1) return fail(std::move(p), tag + "self-bond on atom " + std::to_string(a0));
-    if (a0 < 0 || a0 >= n || a1 < 0 || a1 >= n) return fail(std::move(p), tag + "bond index out of range");
-    seen.emplace_back(std::min(a0, a1), std::max(a0, a1));
+    if (a0 == a1) return fail("self-bond on atom " + std::to_string(a0));
+    if (a0 < 0 || a0 >= n || a1 < 0 || a1 >= n) return fail("bond index out of range");
+    s.seen.emplace_back(std::min(a0, a1), std::max(a0, a1));
   }
-  std::sort(seen.begin(), seen.end());
-  if (std::adjacent_find(seen.begin(), seen.end()) != seen.end())
-    return fail(std::move(p), tag + "duplicate bond");
+  std::sort(s.seen.begin(), s.seen.end());
+  if (std::adjacent_find(s.seen.begin(), s.seen.end()) != s.seen.end()) return fail("duplicate bond");
 
-  // Adjacency in bond order (molecule.hpp:91-96) and BFS connectivity (:97-114).
-  std::vector<std::vector<Edge>> adj(n);
+  // Adjacency in bond order (molecule.hpp:91-96), CSR, and BFS
+  // connectivity (:97-114).
+  s.off.assign(n + 1, 0);
   for (int b = 0; b < n_bonds; ++b) {
-    adj[bonds[2 * b]].push_back({bonds[2 * b + 1], b});
-    adj[bonds[2 * b + 1]].push_back({bonds[2 * b], b});
+    ++s.off[bonds[2 * b] + 1];
+    ++s.off[bonds[2 * b + 1] + 1];
   }
-  std::vector<int> queue(n);
+  for (int i = 0; i < n; ++i) s.off[i + 1] += s.off[i];
+  s.nb.resize(2 * static_cast<size_t>(n_bonds));
+  s.bond.resize(2 * static_cast<size_t>(n_bonds));
+  s.dist.assign(n, 0);  // fill cursor per atom
+  for (int b = 0; b < n_bonds; ++b) {
+    const int u = bonds[2 * b], v = bonds[2 * b + 1];
+    int k = s.off[u] + s.dist[u]++;
+    s.nb[k] = v, s.bond[k] = b;
+    k = s.off[v] + s.dist[v]++;
+    s.nb[k] = u, s.bond[k] = b;
+  }
+  s.queue.resize(n);
   {
-    std::vector<char> seen_atom(n, 0);
+    s.dist.assign(n, -1);
     int head = 0, tail = 0;
-    queue[tail++] = 0;
-    seen_atom[0] = 1;
+    s.queue[tail++] = 0;
+    s.dist[0] = 0;
     while (head < tail) {
-      const int at = queue[head++];
-      for (const Edge& e : adj[at])
-        if (!seen_atom[e.nb]) {
-          seen_atom[e.nb] = 1;
-          queue[tail++] = e.nb;
+      const int at = s.queue[head++];
+      for (int e = s.off[at]; e < s.off[at + 1]; ++e)
+        if (s.dist[s.nb[e]] < 0) {
+          s.dist[s.nb[e]] = 0;
+          s.queue[tail++] = s.nb[e];
         }
     }
-    if (tail != n) return fail(std::move(p), tag + "disconnected ligand");
+    if (tail != n) return fail("disconnected ligand");
   }
 
-  // Capped all-pairs graph distances (molecule.hpp:117-140).
+  // Capped all-pairs graph distances (molecule.hpp:117-140), kept only as
+  // the kernels need them: bit j of row i set iff distance(i, j) >= 4.
   p.words = (n + 63) / 64;
-  p.capped.assign(static_cast<size_t>(n) * n, kGraphDistanceCap);
-  std::vector<int> dist(n);
+  p.far_mask.assign(static_cast<size_t>(n) * p.words, 0);
   for (int src = 0; src < n; ++src) {
-    std::fill(dist.begin(), dist.end(), -1);
+    uint64_t near[kMaxWords] = {0, 0, 0, 0};
+    s.dist.assign(n, -1);
     int head = 0, tail = 0;
-    queue[tail++] = src;
-    dist[src] = 0;
-    p.capped[static_cast<size_t>(src) * n + src] = 0;
+    s.queue[tail++] = src;
+    s.dist[src] = 0;
     while (head < tail) {
-      const int at = queue[head++];
-      if (dist[at] >= kGraphDistanceCap) continue;
-      for (const Edge& e : adj[at])
-        if (dist[e.nb] < 0) {
-          dist[e.nb] = dist[at] + 1;
-          p.capped[static_cast<size_t>(src) * n + e.nb] = static_cast<uint8_t>(dist[e.nb]);
-          queue[tail++] = e.nb;
+      const int at = s.queue[head++];
+      near[at / 64] |= 1ull << (at % 64);
+      if (s.dist[at] + 1 >= kGraphDistanceCap) continue;
+      for (int e = s.off[at]; e < s.off[at + 1]; ++e)
+        if (s.dist[s.nb[e]] < 0) {
+          s.dist[s.nb[e]] = s.dist[at] + 1;
+          s.queue[tail++] = s.nb[e];
         }
     }
+    uint64_t* row = &p.far_mask[static_cast<size_t>(src) * p.words];
+    for (int w = 0; w < p.words; ++w) {
+      const int bits = std::min(64, n - 64 * w);
+      const uint64_t valid = bits == 64 ? ~0ull : ((1ull << bits) - 1);
+      row[w] = ~near[w] & valid;
+    }
   }
-  p.far_mask.assign(static_cast<size_t>(n) * p.words, 0);
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j)
-      if (p.capped[static_cast<size_t>(i) * n + j] >= kGraphDistanceCap)
-        p.far_mask[static_cast<size_t>(i) * p.words + j / 64] |= 1ull << (j % 64);
 
   // Rotamers: rotatable bridges sorted by (min, max) endpoint (molecule.hpp:237-250).
-  const std::vector<char> is_bridge = bridges(n, adj, n_bonds);
-  std::vector<int> rot;
+  bridges(n, n_bonds, s);
+  s.rot.clear();
   for (int b = 0; b < n_bonds; ++b)
-    if (rotatable[b] && is_bridge[b]) rot.push_back(b);
-  std::stable_sort(rot.begin(), rot.end(), [&](int x, int y) {
+    if (rotatable[b] && s.is_bridge[b]) s.rot.push_back(b);
+  std::stable_sort(s.rot.begin(), s.rot.end(), [&](int x, int y) {
     const auto kx = std::minmax(bonds[2 * x], bonds[2 * x + 1]);
     const auto ky = std::minmax(bonds[2 * y], bonds[2 * y + 1]);
     return kx < ky;
   });
 
-  // Fragments (molecule.hpp:255-301).
-  std::vector<char> in_left(n);
-  for (int b : rot) {
+  // Fragments (molecule.hpp:255-301): left = what the smaller endpoint
+  // still reaches with the bond cut.
+  const size_t R = s.rot.size();
+  p.rot_bond.reserve(R);
+  p.frag_mask.reserve(2 * R * p.words);
+  p.frag_axis.reserve(2 * R);
+  p.frag_anchor.reserve(2 * R);
+  p.frag_size.reserve(2 * R);
+  p.frag_rel.reserve(2 * R);
+  for (const int b : s.rot) {
     const int lo = std::min(bonds[2 * b], bonds[2 * b + 1]);
     const int hi = std::max(bonds[2 * b], bonds[2 * b + 1]);
-    std::fill(in_left.begin(), in_left.end(), 0);
+    uint64_t left[kMaxWords] = {0, 0, 0, 0};
     int head = 0, tail = 0;
-    queue[tail++] = lo;
-    in_left[lo] = 1;
+    s.queue[tail++] = lo;
+    left[lo / 64] |= 1ull << (lo % 64);
     while (head < tail) {
-      const int at = queue[head++];
-      for (const Edge& e : adj[at]) {
-        if (e.bond == b) continue;
-        if (!in_left[e.nb]) {
-          in_left[e.nb] = 1;
-          queue[tail++] = e.nb;
+      const int at = s.queue[head++];
+      for (int e = s.off[at]; e < s.off[at + 1]; ++e) {
+        if (s.bond[e] == b) continue;
+        const int v = s.nb[e];
+        if (!((left[v / 64] >> (v % 64)) & 1ull)) {
+          left[v / 64] |= 1ull << (v % 64);
+          s.queue[tail++] = v;
         }
       }
     }
-    if (in_left[hi])
-      return fail(std::move(p), tag + "rotamer bond " + std::to_string(bonds[2 * b]) + "-" +
-                                    std::to_string(bonds[2 * b + 1]) + " is not a bridge");
+    if ((left[hi / 64] >> (hi % 64)) & 1ull)
+      return fail("rotamer bond " + std::to_string(bonds[2 * b]) + "-" +
+                  std::to_string(bonds[2 * b + 1]) + " is not a bridge");
     p.rot_bond.push_back(b);
-    int left_size = 0;
-    for (int i = 0; i < n; ++i) left_size += in_left[i];
+    const int left_size = tail;
     for (int side = 0; side < 2; ++side) {
-      const size_t base = p.frag_mask.size();
-      p.frag_mask.resize(base + p.words, 0);
-      for (int i = 0; i < n; ++i)
-        if ((in_left[i] != 0) == (side == 0)) p.frag_mask[base + i / 64] |= 1ull << (i % 64);
+      for (int w = 0; w < p.words; ++w) {
+        const int bits = std::min(64, n - 64 * w);
+        const uint64_t valid = bits == 64 ? ~0ull : ((1ull << bits) - 1);
+        p.frag_mask.push_back(side == 0 ? left[w] : (~left[w] & valid));
+      }
       const int size = side == 0 ? left_size : n - left_size;
       p.frag_size.push_back(size);
       p.frag_rel.push_back(static_cast<double>(size) / n);

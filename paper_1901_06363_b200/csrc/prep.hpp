@@ -27,7 +27,6 @@ struct PreparedLigand {
   int words = 0;  // ceil(n / 64)
   int status = 0; // GD_LIG_*
   std::string error;
-  std::vector<uint8_t> capped;        // n*n capped graph distances
   std::vector<uint64_t> far_mask;     // n*words: bit j of row i set iff capped(i,j) >= 4
   // Fragments in reference order: for each rotamer (sorted), left then right.
   std::vector<int32_t> rot_bond;      // bond index of each rotamer, find_rotamers order
