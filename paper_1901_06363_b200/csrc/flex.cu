@@ -342,8 +342,10 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   __syncwarp();
   const int first = s.fidx[0];
   double pre = 0.0;
-  if (lane == 0)
+  if (lane == 0) {
+#pragma unroll 4
     for (int i = 0; i < first; ++i) pre = dadd(pre, s.pt[i].t);
+  }
   pre = __shfl_sync(kFull, pre, 0);
   ck.mark(kPhSetup);
   // Surviving bump pairs: drop (i, j) when the circle atom i sweeps never
@@ -528,8 +530,9 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     for (int f = 0; f < m.nfrag; ++f) {
       const int fo = m.frag_off + f;
       const int axis = __ldg(p.frag_axis + fo), anchor = __ldg(p.frag_anchor + fo);
+      const double rel = __ldg(p.frag_rel + fo);
       // Dispatch (kernel.hpp:229-239).
-      const bool low = __ldg(p.frag_rel + fo) <= p.threshold;
+      const bool low = rel <= p.threshold;
       const bool refined = !low && p.refine;
       const int step = low ? p.lp : p.hp;
       const int A = 360 / step;
