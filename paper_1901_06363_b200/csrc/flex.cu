@@ -50,6 +50,9 @@ namespace {
 #ifndef GD_BUMP_PAIRMAJOR
 #define GD_BUMP_PAIRMAJOR 1  // bump checks pair-major (0: (candidate, pair) items)
 #endif
+#ifndef GD_PREFILTER_OWNER
+#define GD_PREFILTER_OWNER 1  // pair -> slot owner table instead of a binary search
+#endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
@@ -408,16 +411,30 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
         total += __shfl_sync(kFull, inc, 31);
       }
       __syncwarp();
+#if GD_PREFILTER_OWNER
+      // Owner table: pair index -> slot (u8; total <= n^2/4 <= 1024 bytes
+      // after the per-atom floats and pref in the v scratch, n <= 64).
+      uint8_t* owner = reinterpret_cast<uint8_t*>(pref + nf);
+      for (int sl = lane; sl < nf; sl += 32) {
+        const int b0 = pref[sl], b1 = sl + 1 < nf ? pref[sl + 1] : total;
+        for (int k = b0; k < b1; ++k) owner[k] = static_cast<uint8_t>(sl);
+      }
+      __syncwarp();
+#endif
       for (int t0 = 0; t0 < total; t0 += 32) {
         const int t = t0 + lane;
         bool keep = false;
         int i = 0, j = 0;
         if (t < total) {
+#if GD_PREFILTER_OWNER
+          const int lo = owner[t];
+#else
           int lo = 0, hi = nf - 1;  // last slot with pref <= t
           while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
             if (pref[mid] <= t) lo = mid; else hi = mid - 1;
           }
+#endif
           i = s.fidx[lo];
           const uint64_t m = s.far[i] & nf0;
           j = nth_bit(m, t - pref[lo]);
