@@ -50,9 +50,6 @@ namespace {
 #ifndef GD_BUMP_PAIRMAJOR
 #define GD_BUMP_PAIRMAJOR 1  // bump checks pair-major (0: (candidate, pair) items)
 #endif
-#ifndef GD_PREFILTER_OWNER
-#define GD_PREFILTER_OWNER 1  // pair -> slot owner table instead of a binary search
-#endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
@@ -109,24 +106,6 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
 
 __device__ __forceinline__ bool in_frag(const uint64_t* fm, int i) {
   return (fm[i >> 6] >> (i & 63)) & 1ull;
-}
-
-// Position of the r-th (0-based) set bit of a 64-bit mask by a popcount
-// descent (cheaper than __fns on sm_100a).
-__device__ __forceinline__ int nth_bit(uint64_t m, int r) {
-  int pos = 0;
-  int c = __popc(static_cast<unsigned>(m));
-  if (r >= c) { r -= c; m >>= 32; pos = 32; }
-  unsigned w = static_cast<unsigned>(m);
-  c = __popc(w & 0xFFFFu);
-  if (r >= c) { r -= c; w >>= 16; pos += 16; }
-  c = __popc(w & 0xFFu);
-  if (r >= c) { r -= c; w >>= 8; pos += 8; }
-  c = __popc(w & 0xFu);
-  if (r >= c) { r -= c; w >>= 4; pos += 4; }
-  c = __popc(w & 0x3u);
-  if (r >= c) { r -= c; w >>= 2; pos += 2; }
-  return pos + ((r >= static_cast<int>(w & 1u)) ? 1 : 0);
 }
 
 // floor(t / d) for 0 <= t < 2^16, 1 <= d <= 256 via an fp32 reciprocal:
@@ -391,16 +370,26 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
       const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
       return !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
     };
-    if (W == 1) {
-      // Flattened over the actual partner pairs: per-slot partner counts,
-      // a warp prefix sum, then lane t finds its slot by binary search and
-      // its partner as the n-th set bit of the slot's partner mask.
+    {
+      // Flattened over the actual partner pairs: per-slot partner counts and
+      // a warp prefix sum give each slot its range of pair indices; slot
+      // lanes then write every candidate pair in place (walking their
+      // partner bits; total <= nf (n - nf) <= the pair buffer's n^2/4), and
+      // the warp tests and compacts them in place (writes never pass the
+      // chunk being read).
       int* pref = reinterpret_cast<int*>(rf + n);
-      const uint64_t nf0 = ~s.fm[0];
       int total = 0;
       for (int b = 0; b < nf; b += 32) {
         const int sl = b + lane;
-        const int cnt = sl < nf ? __popcll(s.far[s.fidx[sl]] & nf0) : 0;
+        int cnt = 0;
+        if (sl < nf) {
+          const int i = s.fidx[sl];
+          if (W == 1) {
+            cnt = __popcll(s.far[i] & ~s.fm[0]);
+          } else {
+            for (int w = 0; w < W; ++w) cnt += __popcll(s.far[i * W + w] & ~s.fm[w]);
+          }
+        }
         int inc = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -411,62 +400,39 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
         total += __shfl_sync(kFull, inc, 31);
       }
       __syncwarp();
-#if GD_PREFILTER_OWNER
-      // Owner table: pair index -> slot (u8; total <= n^2/4 <= 1024 bytes
-      // after the per-atom floats and pref in the v scratch, n <= 64).
-      uint8_t* owner = reinterpret_cast<uint8_t*>(pref + nf);
       for (int sl = lane; sl < nf; sl += 32) {
-        const int b0 = pref[sl], b1 = sl + 1 < nf ? pref[sl + 1] : total;
-        for (int k = b0; k < b1; ++k) owner[k] = static_cast<uint8_t>(sl);
+        const int i = s.fidx[sl];
+        int pos = pref[sl];
+        if (W == 1) {
+          uint64_t m = s.far[i] & ~s.fm[0];
+          while (m) {
+            const int j = __ffsll(static_cast<long long>(m)) - 1;
+            m &= m - 1;
+            s.pairs[pos++] = static_cast<uint16_t>(i | (j << 8));
+          }
+        } else {
+          for (int w = 0; w < W; ++w) {
+            uint64_t m = s.far[i * W + w] & ~s.fm[w];
+            while (m) {
+              const int j = 64 * w + __ffsll(static_cast<long long>(m)) - 1;
+              m &= m - 1;
+              s.pairs[pos++] = static_cast<uint16_t>(i | (j << 8));
+            }
+          }
+        }
       }
       __syncwarp();
-#endif
       for (int t0 = 0; t0 < total; t0 += 32) {
         const int t = t0 + lane;
         bool keep = false;
-        int i = 0, j = 0;
+        unsigned pr = 0;
         if (t < total) {
-#if GD_PREFILTER_OWNER
-          const int lo = owner[t];
-#else
-          int lo = 0, hi = nf - 1;  // last slot with pref <= t
-          while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (pref[mid] <= t) lo = mid; else hi = mid - 1;
-          }
-#endif
-          i = s.fidx[lo];
-          const uint64_t m = s.far[i] & nf0;
-          j = nth_bit(m, t - pref[lo]);
-          keep = test(i, j);
+          pr = s.pairs[t];
+          keep = test(static_cast<int>(pr & 0xffu), static_cast<int>(pr >> 8));
         }
         const unsigned mask = __ballot_sync(kFull, keep);
-        if (keep)
-          s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
-        np += __popc(mask);
-      }
-    } else
-    for (int sl = 0; sl < nf; ++sl) {
-      const int i = s.fidx[sl];
-      const float ai = axc[i], r2 = rad2[i], ri = rf[i];
-      for (int b = 0; b < n; b += 32) {
-        // Partner bits of this 32-atom chunk; uniform skip when empty.
-        const unsigned chunk = static_cast<unsigned>(
-            (s.far[i * W + (b >> 6)] & ~s.fm[b >> 6]) >> (b & 63));
-        if (chunk == 0u) continue;
-        const int j = b + lane;
-        bool keep = false;
-        if (j < n && ((chunk >> lane) & 1u)) {
-          const float h = axc[j] - ai;
-          const float s2 = rad2[j];
-          const float cut = 0.8f * (ri + rf[j]);
-          const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
-          const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
-          keep = !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
-        }
-        const unsigned mask = __ballot_sync(kFull, keep);
-        if (keep)
-          s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(i | (j << 8));
+        __syncwarp();
+        if (keep) s.pairs[np + __popc(mask & ((1u << lane) - 1u))] = static_cast<uint16_t>(pr);
         np += __popc(mask);
       }
     }
