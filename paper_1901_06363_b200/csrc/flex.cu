@@ -299,10 +299,10 @@ struct StepInfo {
 
 template <int B, class CK>
 __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p, const LigMeta& m,
-                                           int f, int axis, int anchor, int lane, int& left_np,
-                                           StepInfo& st, CK& ck) {
+                                           int f, int axis, int anchor, uint64_t fm_word, int lane,
+                                           int& left_np, StepInfo& st, CK& ck) {
   const int n = m.n, W = m.words;
-  if (lane < W) s.fm[lane] = __ldg(p.frag_mask + m.fmask_off + f * W + lane);
+  if (lane < W) s.fm[lane] = fm_word;  // loaded by the caller with the descriptors
   // rotate_fragment_into axis (geometry.hpp:165-169), identical in every lane.
   const PT pa = s.pt[axis], pb = s.pt[anchor];
   const double ox = pa.x, oy = pa.y, oz = pa.z;
@@ -512,8 +512,10 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   for (int rep = 0; rep < p.reps; ++rep) {
     for (int f = 0; f < m.nfrag; ++f) {
       const int fo = m.frag_off + f;
+      // The step's descriptors and fragment-mask words, all in flight at once.
       const int axis = __ldg(p.frag_axis + fo), anchor = __ldg(p.frag_anchor + fo);
       const double rel = __ldg(p.frag_rel + fo);
+      const uint64_t fm_word = lane < W ? __ldg(p.frag_mask + m.fmask_off + f * W + lane) : 0ull;
       // Dispatch (kernel.hpp:229-239).
       const bool low = rel <= p.threshold;
       const bool refined = !low && p.refine;
@@ -526,7 +528,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
         continue;
       }
       StepInfo st;
-      if (!setup_step<B>(s, p, m, f, axis, anchor, lane, left_np, st, ck)) {
+      if (!setup_step<B>(s, p, m, f, axis, anchor, fm_word, lane, left_np, st, ck)) {
         if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
         return;
       }
@@ -697,8 +699,9 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   const int fo = m.frag_off + f;
   int left_np = -1;
   StepInfo st;
-  if (!setup_step<B>(s, p, m, f, __ldg(p.frag_axis + fo), __ldg(p.frag_anchor + fo), lane, left_np,
-                     st, ck)) {
+  const uint64_t fm_word = lane < W ? __ldg(p.frag_mask + m.fmask_off + f * W + lane) : 0ull;
+  if (!setup_step<B>(s, p, m, f, __ldg(p.frag_axis + fo), __ldg(p.frag_anchor + fo), fm_word, lane,
+                     left_np, st, ck)) {
     if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
     for (int a = lane; a < 360; a += 32) {
       out[a] = 0.0;
