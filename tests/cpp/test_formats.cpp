@@ -200,6 +200,51 @@ int main() {
     CHECK(left.relative_size == 2.0 / 6.0 && right.side == Side::right);
     CHECK(contains(error_of([&] { grow_fragments(l, Rotamer{{3, 4, true}, 3}); }), "is not a bridge"));
   });
+  run("parsers survive random corruption (parse or throw geodock::Error, never crash)", [] {
+    const std::string pocket = render_pocket(Pocket("pk", {{0, 0, 0}, {1.5, -2, 3}, {4, 5, 6.25}}));
+    const std::string ligs = render_ligands(random_ligands(3, 11));
+    ScreeningReport rep;
+    rep.pocket_id = "P";
+    rep.per_ligand = {{"A", 1.5, 3, 0.25}};
+    const std::string csv = render_report_csv(rep), summary = render_report_summary(rep);
+    const std::string space = "hp_step = 1, 5\nrepetitions = 1,3\n";
+    std::mt19937_64 rng(2024);
+    const std::string alphabet = "0123456789 .-+eE\n\t#,=:RFABLIGNDPOCKETXYZ";
+    auto mutate = [&](std::string t) {
+      const int edits = 1 + static_cast<int>(rng() % 4);
+      for (int e = 0; e < edits && !t.empty(); ++e) {
+        const size_t at = rng() % t.size();
+        switch (rng() % 3) {
+          case 0: t[at] = alphabet[rng() % alphabet.size()]; break;
+          case 1: t.erase(at, 1 + rng() % 3); break;
+          default: t.insert(at, 1, alphabet[rng() % alphabet.size()]); break;
+        }
+      }
+      return t;
+    };
+    int parsed = 0, rejected = 0;
+    for (int k = 0; k < 3000; ++k) {
+      try {
+        switch (k % 5) {
+          case 0: parse_pocket(mutate(pocket)); break;
+          case 1: parse_ligands(mutate(ligs)); break;
+          case 2: {
+            std::istringstream in(mutate(ligs));
+            LigandParser parser(in);
+            while (parser.next()) {
+            }
+            break;
+          }
+          case 3: parse_report(mutate(csv), mutate(summary)); break;
+          default: parse_design_space(mutate(space)); break;
+        }
+        ++parsed;
+      } catch (const Error&) {
+        ++rejected;
+      }
+    }
+    CHECK(parsed > 0 && rejected > 0 && parsed + rejected == 3000);
+  });
   std::printf("%s (%d failed checks)\n", g_failed ? "FAILED" : "OK", g_failed);
   return g_failed ? 1 : 0;
 }
