@@ -28,6 +28,7 @@
 // ties (kernel.hpp:136, :169, :173, :185, :194), angle 0 = committed pose,
 // feasibility_checks / evaluations counted as CandidateEvaluator does.
 #include <algorithm>
+#include <cassert>
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -49,6 +50,16 @@ namespace {
 #endif
 #ifndef GD_BUMP_PAIRMAJOR
 #define GD_BUMP_PAIRMAJOR 1  // bump checks pair-major (0: (candidate, pair) items)
+#endif
+// Debug builds (-DGD_DEBUG_BOUNDS=1, tools/sanitize_small.py) assert the
+// shared-memory capacity invariants the kernels rely on.
+#ifndef GD_DEBUG_BOUNDS
+#define GD_DEBUG_BOUNDS 0
+#endif
+#if GD_DEBUG_BOUNDS
+#define GD_BOUND(cond) assert(cond)
+#else
+#define GD_BOUND(cond) ((void)0)
 #endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
@@ -101,6 +112,7 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   s.fidx = reinterpret_cast<uint8_t*>(take(n));
   s.fm = reinterpret_cast<uint64_t*>(take(32));
   s.count = reinterpret_cast<int*>(take(16));
+  GD_BOUND(o <= warp_bytes<B>(n, W, max_pairs));
   return s;
 }
 
@@ -322,6 +334,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
     nf += __popc(mask);
   }
   __syncwarp();
+  GD_BOUND(nf >= 1 && nf < n);
   const int first = s.fidx[0];
   double pre = 0.0;
   if (lane == 0) {
@@ -378,6 +391,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
       // the warp tests and compacts them in place (writes never pass the
       // chunk being read).
       int* pref = reinterpret_cast<int*>(rf + n);
+      GD_BOUND(12 * n + 4 * nf <= 8 * B * n);  // per-atom floats + pref fit the v scratch
       int total = 0;
       for (int b = 0; b < nf; b += 32) {
         const int sl = b + lane;
@@ -400,6 +414,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
         total += __shfl_sync(kFull, inc, 31);
       }
       __syncwarp();
+      GD_BOUND(total <= p.max_pairs);  // nf (n - nf) <= n^2 / 4
       for (int sl = lane; sl < nf; sl += 32) {
         const int i = s.fidx[sl];
         int pos = pref[sl];
