@@ -61,6 +61,9 @@ namespace {
 #else
 #define GD_BOUND(cond) ((void)0)
 #endif
+#ifndef GD_BUMP_SHARE
+#define GD_BUMP_SHARE 1      // pair-major: share found bumps across the warp per pair chunk
+#endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
@@ -255,6 +258,7 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
         wk.add(kBump, 1);
         if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < cut2) bl |= 1u << c;
       }
+      if (GD_BUMP_SHARE) bl = __reduce_or_sync(kFull, bl);  // later pairs skip known bumps
     }
   } else {
     const int total = nb * np;
