@@ -258,7 +258,10 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
         wk.add(kBump, 1);
         if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < cut2) bl |= 1u << c;
       }
-      if (GD_BUMP_SHARE) bl = __reduce_or_sync(kFull, bl);  // later pairs skip known bumps
+      if (GD_BUMP_SHARE) {
+        bl = __reduce_or_sync(kFull, bl);  // later pairs skip known bumps
+        if ((bl | zero) == (1u << nb) - 1u) break;  // every candidate has bumped
+      }
     }
   } else {
     const int total = nb * np;
