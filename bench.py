@@ -253,7 +253,7 @@ def run_ours(a):
     e2e = None
     if not a.no_e2e:
         e2e_steps = max(1, min(a.steps, 5))
-        d.dock(batch, knobs)  # warm
+        host_out = d.dock(batch, knobs)  # warm; host result arrays reused, as a caller would
         tms = []
         for _ in range(e2e_steps):
             flush.zero_()
@@ -261,7 +261,7 @@ def run_ours(a):
             if dist:
                 dist.barrier()
             t0 = time.perf_counter()
-            d.dock(batch, knobs)
+            d.dock(batch, knobs, out=host_out)
             tms.append(time.perf_counter() - t0)
         tt = float(np.mean(tms))
         if dist:

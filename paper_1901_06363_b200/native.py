@@ -302,6 +302,11 @@ class DockResult:
                           np.zeros(L, np.int64), np.zeros(L, np.int32),
                           np.zeros(K * total_atoms * 3) if poses else None)
 
+    def fits(self, L: int, K: int, total_atoms: int, poses: bool) -> bool:
+        return (self.orientation.shape == (L, K)
+                and (self.final_pose is not None) == poses
+                and (not poses or len(self.final_pose) == K * total_atoms * 3))
+
     def c_struct(self) -> gd_result:
         return gd_result(_p(self.orientation, _i32p), _p(self.seed_rank, _i32p),
                          _p(self.rigid_score, _f64p), _p(self.final_score, _f64p),
@@ -362,10 +367,14 @@ class Docker:
         return {"centre": c, "dims": d, "voxel": h.value, "n_candidates": n.value,
                 "max_candidates": m.value}
 
-    def dock(self, batch: LigandBatch, knobs: Knobs, keep_poses: bool = False) -> DockResult:
-        """gd_dock_batch: host buffers in, host buffers out."""
+    def dock(self, batch: LigandBatch, knobs: Knobs, keep_poses: bool = False,
+             out: "DockResult | None" = None) -> DockResult:
+        """gd_dock_batch: host buffers in, host buffers out.  `out` (a
+        DockResult of the right shape) is reused instead of allocating."""
         K = knobs.slots
-        res = DockResult.empty(batch.n_ligands, K, int(batch.atom_offsets[-1]), keep_poses)
+        A = int(batch.atom_offsets[-1])
+        res = out if out is not None and out.fits(batch.n_ligands, K, A, keep_poses) \
+            else DockResult.empty(batch.n_ligands, K, A, keep_poses)
         b, k, r = batch.c_struct(), knobs.c_struct(), res.c_struct()
         self._check(self._lib.gd_dock_batch(self._h, C.byref(b), C.byref(k), C.byref(r)))
         self._batch = batch
