@@ -10,6 +10,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -148,7 +149,7 @@ class WorkerPool {
 struct gd_ctx {
   int device = 0;
   cudaStream_t own_stream = nullptr;
-  cudaStream_t aux_stream = nullptr;  // second stream of the pipelined gd_dock_batch
+  std::vector<cudaStream_t> aux_streams;  // further streams of the pipelined gd_dock_batch
   cudaStream_t stream = nullptr;
   std::string err;
   cudaEvent_t ev[5] = {};
@@ -266,7 +267,7 @@ extern "C" int gd_destroy(gd_ctx* ctx) {
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : ctx->chunk_ev) cudaEventDestroy(ev);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
-  if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+  for (cudaStream_t st : ctx->aux_streams) cudaStreamDestroy(st);
   delete ctx;
   return GD_OK;
 }
@@ -906,8 +907,12 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   rc = prepare_dock(ctx, knobs, keep_pose, p);
   if (rc != GD_OK) return rc;
   const int L = ctx->n_lig, K = ctx->last_topk;
-  if (ctx->aux_stream == nullptr)
-    GD_CUDA(ctx, cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking));
+  static const int kStreams = std::max(1, static_cast<int>(env_double("GD_E2E_STREAMS", 2)));
+  while (static_cast<int>(ctx->aux_streams.size()) < kStreams - 1) {
+    cudaStream_t st;
+    GD_CUDA(ctx, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    ctx->aux_streams.push_back(st);
+  }
   // Pinned result arena: the async D2H targets.
   const size_t slots = static_cast<size_t>(std::max(L, 1)) * K;
   const size_t pose_elems = keep_pose ? 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1)) * K : 0;
@@ -934,11 +939,24 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   pr.final_pose = keep_pose ? static_cast<double*>(take(8 * pose_elems)) : nullptr;
 
   // Chunk plan: a small head chunk (its host prep is the only part nothing
-  // overlaps), then up to 15 equal chunks (a short tail after the last prep).
+  // overlaps), then chunks growing geometrically by 1.5x: host prep runs
+  // ~1.7x faster than the GPU docks, so each chunk is prepared before the
+  // GPU drains the previous ones, and few launch tails remain (c1: 19.36 ms
+  // vs 19.85 with 15 equal chunks; tools/e2e_plan_ab.sh).  GD_E2E_GROWTH<=1
+  // selects the equal split into GD_E2E_CHUNKS parts.
   std::vector<int> bounds{0};
   static const int kHead = static_cast<int>(env_double("GD_E2E_HEAD", 256));
   static const int kParts = static_cast<int>(env_double("GD_E2E_CHUNKS", 15));
-  if (L > 2048) {
+  static const double kGrowth = env_double("GD_E2E_GROWTH", 1.5);
+  if (L > 2048 && kGrowth > 1.0) {
+    bounds.push_back(kHead);
+    double sz = kHead;
+    while (bounds.back() < L) {
+      sz *= kGrowth;
+      const int nxt = static_cast<int>(std::min<double>(L, bounds.back() + sz));
+      bounds.push_back(L - nxt < sz / 2 ? L : nxt);
+    }
+  } else if (L > 2048) {
     const int head = kHead, rest = L - head, parts = std::min(kParts, std::max(1, rest / 512));
     bounds.push_back(head);
     for (int c = 1; c <= parts; ++c)
@@ -954,17 +972,36 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   }
   float prep_ms = 0.0f;
   ctx->timing.launches = 0;
+  // Diagnostic timeline (GD_E2E_TRACE=1): per chunk, host prep interval and
+  // GPU start/end relative to the call, printed to stderr at the end.
+  static const bool kTrace = env_double("GD_E2E_TRACE", 0) != 0;
+  std::vector<cudaEvent_t> tev;
+  std::vector<double> tprep;
+  cudaEvent_t tev0 = nullptr;
+  if (kTrace) {
+    tev.resize(2 * chunks);
+    for (auto& e : tev) GD_CUDA(ctx, cudaEventCreate(&e));
+    GD_CUDA(ctx, cudaEventCreate(&tev0));
+    GD_CUDA(ctx, cudaEventRecord(tev0, ctx->stream));
+  }
   for (int c = 0; c < chunks; ++c) {
     const int c0 = bounds[c], c1 = bounds[c + 1];
-    cudaStream_t s = (c & 1) ? ctx->aux_stream : ctx->stream;
+    cudaStream_t s = (c % kStreams) ? ctx->aux_streams[c % kStreams - 1] : ctx->stream;
     const Running before = run;
     const auto t0 = std::chrono::steady_clock::now();
     int mx = 1;
     prep_range(ctx, batch, c0, c1, run, mx);
-    prep_ms += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const auto t1 = std::chrono::steady_clock::now();
+    prep_ms += std::chrono::duration<float, std::milli>(t1 - t0).count();
+    if (kTrace) {
+      tprep.push_back(std::chrono::duration<double, std::milli>(t0 - t_start).count());
+      tprep.push_back(std::chrono::duration<double, std::milli>(t1 - t_start).count());
+      GD_CUDA(ctx, cudaEventRecord(tev[2 * c], s));
+    }
     if ((rc = h2d_range(ctx, c0, c1, before, run, s)) != GD_OK) return rc;
     if ((rc = launch_range(ctx, p, c0, c1, mx, s, nullptr)) != GD_OK) return rc;
     if ((rc = d2h_range(ctx, &pr, c0, c1, s)) != GD_OK) return rc;
+    if (kTrace) GD_CUDA(ctx, cudaEventRecord(tev[2 * c + 1], s));
     GD_CUDA(ctx, cudaEventRecord(ctx->chunk_ev[c], s));
   }
   // Results chunk by chunk, in order: pinned arena -> caller arrays while the
@@ -975,10 +1012,20 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
     const auto t_post = std::chrono::steady_clock::now();
     const int l0 = bounds[c], l1 = bounds[c + 1];
     const size_t s0 = static_cast<size_t>(l0) * K, sn = static_cast<size_t>(l1 - l0) * K;
-    auto copy = [](void* dst, const void* src, size_t elem, size_t off, size_t cnt) {
-      if (dst && src && cnt)
-        std::memcpy(static_cast<unsigned char*>(dst) + elem * off,
-                    static_cast<const unsigned char*>(src) + elem * off, elem * cnt);
+    struct Seg {
+      unsigned char* dst;
+      const unsigned char* src;
+      size_t bytes;
+    };
+    Seg segs[9];
+    int nseg = 0;
+    size_t total = 0;
+    auto copy = [&](void* dst, const void* src, size_t elem, size_t off, size_t cnt) {
+      if (dst && src && cnt) {
+        segs[nseg++] = Seg{static_cast<unsigned char*>(dst) + elem * off,
+                           static_cast<const unsigned char*>(src) + elem * off, elem * cnt};
+        total += elem * cnt;
+      }
     };
     copy(result->orientation, pr.orientation, 4, s0, sn);
     copy(result->seed_rank, pr.seed_rank, 4, s0, sn);
@@ -993,15 +1040,49 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
       const size_t p1 = 3 * static_cast<size_t>(K) * ctx->atom_off[l1];
       copy(result->final_pose, pr.final_pose, 8, p0, p1 - p0);
     }
+    // Pinned arena -> caller arrays: large chunks in 64 KiB blocks over the
+    // worker pool (the last chunk's copy is on the critical path).
+    constexpr size_t kBlock = 64 << 10;
+    if (total >= 4 * kBlock && ctx->pool) {
+      size_t starts[10];
+      starts[0] = 0;
+      for (int k = 0; k < nseg; ++k) starts[k + 1] = starts[k] + (segs[k].bytes + kBlock - 1) / kBlock;
+      std::atomic<size_t> next{0};
+      const size_t blocks = starts[nseg];
+      ctx->pool->run([&] {
+        for (size_t bi; (bi = next.fetch_add(1)) < blocks;) {
+          int k = 0;
+          while (starts[k + 1] <= bi) ++k;
+          const size_t off = (bi - starts[k]) * kBlock;
+          std::memcpy(segs[k].dst + off, segs[k].src + off, std::min(kBlock, segs[k].bytes - off));
+        }
+      });
+    } else {
+      for (int k = 0; k < nseg; ++k) std::memcpy(segs[k].dst, segs[k].src, segs[k].bytes);
+    }
     fill_empty(ctx, result, pr.k_eff, pr.status, l0, l1);
     post_ms += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_post).count();
   }
   if (L == 0) fill_empty(ctx, result, pr.k_eff, pr.status);
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-  GD_CUDA(ctx, cudaStreamSynchronize(ctx->aux_stream));
+  for (cudaStream_t st : ctx->aux_streams) GD_CUDA(ctx, cudaStreamSynchronize(st));
   ctx->have_result = true;
   ctx->staged = true;
   const auto t_end = std::chrono::steady_clock::now();
+  if (kTrace) {
+    // GPU times are relative to tev0, recorded right after the call began.
+    for (int c = 0; c < chunks; ++c) {
+      float g0 = 0.0f, g1 = 0.0f;
+      cudaEventElapsedTime(&g0, tev0, tev[2 * c]);
+      cudaEventElapsedTime(&g1, tev0, tev[2 * c + 1]);
+      std::fprintf(stderr, "chunk %2d ligands %5d-%5d host prep %7.3f-%7.3f ms  gpu %7.3f-%7.3f ms\n", c,
+                   bounds[c], bounds[c + 1], tprep[2 * c], tprep[2 * c + 1], g0, g1);
+    }
+    std::fprintf(stderr, "call total %.3f ms\n",
+                 std::chrono::duration<double, std::milli>(t_end - t_start).count());
+    for (auto e : tev) cudaEventDestroy(e);
+    cudaEventDestroy(tev0);
+  }
   ctx->timing.host_prep_ms = prep_ms;
   ctx->timing.host_post_ms = post_ms;
   ctx->timing.total_ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();
