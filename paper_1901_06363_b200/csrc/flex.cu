@@ -64,12 +64,21 @@ namespace {
 #ifndef GD_BUMP_SHARE
 #define GD_BUMP_SHARE 1      // pair-major: share found bumps across the warp per pair chunk
 #endif
+#ifndef GD_AXIS_SMEM
+#define GD_AXIS_SMEM 1       // the step's rotation axis read from the warp's shared slot
+#endif
+#ifndef GD_META_RELOAD
+#define GD_META_RELOAD 1     // ligand descriptor fields re-read from global when used
+#endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
+#ifndef GD_FLEX_WARPS6
+#define GD_FLEX_WARPS6 12    // chains per CTA for batches of up to 6 candidates
+#endif
 template <int B>
 constexpr int warps_for() {
-  return B == 8 ? 4 : 12;
+  return B == 8 ? 4 : GD_FLEX_WARPS6;
 }
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -78,7 +87,7 @@ __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~si
 template <int B>
 __host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pairs) {
   return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * B * n) +
-         a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16);
+         a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16) + a16(sizeof(Axis));
 }
 
 // One atom of a chain's committed pose and its overlap term max(1e-12,
@@ -95,7 +104,8 @@ struct WarpMem {
   uint16_t* pairs;       // [max_pairs] surviving bump pairs: F-slot | j << 8
   uint8_t* fidx;         // [n] fragment atoms, ascending
   uint64_t* fm;          // [4] fragment membership bits
-  int* count;            // [1] surviving-pair counter
+  long long* tally;      // [2] the chain's evaluations, feasibility checks (lane 0)
+  Axis* ax;              // [1] the step's rotation axis (GD_AXIS_SMEM)
 };
 
 template <int B>
@@ -114,7 +124,8 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   s.pairs = reinterpret_cast<uint16_t*>(take(2ull * max_pairs));
   s.fidx = reinterpret_cast<uint8_t*>(take(n));
   s.fm = reinterpret_cast<uint64_t*>(take(32));
-  s.count = reinterpret_cast<int*>(take(16));
+  s.tally = reinterpret_cast<long long*>(take(16));
+  s.ax = reinterpret_cast<Axis*>(take(sizeof(Axis)));
   GD_BOUND(o <= warp_bytes<B>(n, W, max_pairs));
   return s;
 }
@@ -289,6 +300,25 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
   ck.mark(kPhFold);
   score_out = score;
   bumped_out = bumped;
+}
+
+// A batch's contribution to the running argmax under the reference's
+// sequential rule (strict '>' against the running best, first-encountered
+// ties; kernel.hpp:136, :169, :185): the scan ends on the batch maximum M
+// over the feasible candidates, first reached at the lowest candidate
+// holding M, and it replaces the best iff M > best.  Lane c < nb holds
+// candidate c's score; returns M warp-uniformly and that candidate in
+// `first_c` (-1 when nothing is feasible).  B <= 8: one 8-lane butterfly.
+__device__ __forceinline__ double batch_max(double sc, unsigned bumped, int nb, int lane,
+                                            int& first_c) {
+  const bool feas = lane < nb && !((bumped >> lane) & 1u);
+  const double v = feas ? sc : -kInfinity;
+  double m = v;
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) m = fmax(m, __shfl_xor_sync(kFull, m, o));
+  m = __shfl_sync(kFull, m, 0);
+  first_c = __ffs(__ballot_sync(kFull, feas && v == m)) - 1;
+  return m;
 }
 
 template <bool On>
@@ -489,7 +519,11 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   if (item >= static_cast<long long>(p.n_lig) * K) return;
   const int l = p.order[item / K];
   const int r = static_cast<int>(item % K);
+#if GD_META_RELOAD
+  const LigMeta& m = p.meta[l];
+#else
   const LigMeta m = p.meta[l];
+#endif
   if (m.status != 0) return;
   const int n = m.n, W = m.words;
   const WarpMem s =
@@ -527,7 +561,15 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   }
   cur = __shfl_sync(kFull, cur, 0);
   if (!p.rigid && lane == 0) p.seed_score[e] = cur;
-  long long evals = 1, checks = 1;
+  // The chain's evaluation / feasibility-check counts live in the warp's
+  // shared slot (lane 0), not in registers the batch loop needs.
+  if (lane == 0) s.tally[0] = s.tally[1] = 1;
+  auto tally = [&](int ev, int ck) {
+    if (lane == 0) {
+      s.tally[0] += ev;
+      s.tally[1] += ck;
+    }
+  };
   int left_np = -1;  // bump-pair count of the preceding left step, -1 if none
   ck.mark(kPhInit);
 
@@ -544,8 +586,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       const int step = low ? p.lp : p.hp;
       const int A = 360 / step;
       if (!refined && A == 1) {  // step 360: only the committed pose
-        checks += 1;
-        evals += 1;
+        tally(1, 1);
         left_np = -1;
         continue;
       }
@@ -554,7 +595,13 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
         if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
         return;
       }
+#if GD_AXIS_SMEM
+      if (lane == 0) *s.ax = st.X;
+      __syncwarp();
+      const Axis& X = *s.ax;
+#else
       const Axis& X = st.X;
+#endif
       const int nf = st.nf, first = st.first, np = st.np;
       const double pre = st.pre;
 
@@ -562,32 +609,29 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       double best = cur;
       if (!refined) {
         // optimize_fragment_flat (kernel.hpp:125-143).
-        long long nfeas = 0;
+        int nfeas = 0;
         for (int kb = 0; kb < A - 1; kb += B) {
           const int nb = min(B, A - 1 - kb);
           const int a0 = (kb + 1) * step;
           double sc;
           unsigned bumped;
           eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, step, nb, lane, sc, bumped, wk, ck);
-          for (int c = 0; c < nb; ++c) {
-            const double v = __shfl_sync(kFull, sc, c);
-            if ((bumped >> c) & 1u) continue;
-            ++nfeas;
-            if (v > best) {
-              best = v;
-              best_a = a0 + c * step;
-            }
+          int c;
+          const double v = batch_max(sc, bumped, nb, lane, c);
+          nfeas += __popc(~bumped & ((1u << nb) - 1u));
+          if (c >= 0 && v > best) {
+            best = v;
+            best_a = a0 + c * step;
           }
         }
-        checks += A;
-        evals += 1 + nfeas;
+        tally(1 + nfeas, A);
       } else {
         // optimize_fragment_refined (kernel.hpp:150-198).
         const int T = p.tile, tc = 360 / T;
         bool have = false;
         int wt = -1;
         double ws = 0.0;
-        long long nfeas = 0;
+        int nfeas = 0;
         best = 0.0;
         for (int kb = 0; kb < tc; kb += B) {
           const int nb = min(B, tc - kb);
@@ -595,22 +639,20 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
           double sc;
           unsigned bumped;
           eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, T, nb, lane, sc, bumped, wk, ck);
-          for (int c = 0; c < nb; ++c) {
-            const double v = __shfl_sync(kFull, sc, c);
-            if ((bumped >> c) & 1u) continue;
-            ++nfeas;
-            if (!have || v > best) {
-              best = v;
-              best_a = a0 + c * T;
-              have = true;
-            }
-            if (wt < 0 || v > ws) {
-              wt = kb + c;
-              ws = v;
-            }
+          int c;
+          const double v = batch_max(sc, bumped, nb, lane, c);
+          nfeas += __popc(~bumped & ((1u << nb) - 1u));
+          if (c >= 0 && (!have || v > best)) {
+            best = v;
+            best_a = a0 + c * T;
+            have = true;
+          }
+          if (c >= 0 && (wt < 0 || v > ws)) {
+            wt = kb + c;
+            ws = v;
           }
         }
-        checks += tc;
+        tally(0, tc);
         if (wt >= 0) {
           int cnt2 = 0;
           while ((cnt2 + 1) * p.hp <= T) ++cnt2;
@@ -620,25 +662,23 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
             double sc;
             unsigned bumped;
             eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, p.hp, nb, lane, sc, bumped, wk, ck);
-            for (int c = 0; c < nb; ++c) {
-              const double v = __shfl_sync(kFull, sc, c);
-              if ((bumped >> c) & 1u) continue;
-              ++nfeas;
-              if (!have || v > best) {
-                best = v;
-                best_a = a0 + c * p.hp;
-                have = true;
-              }
+            int c;
+            const double v = batch_max(sc, bumped, nb, lane, c);
+            nfeas += __popc(~bumped & ((1u << nb) - 1u));
+            if (c >= 0 && (!have || v > best)) {
+              best = v;
+              best_a = a0 + c * p.hp;
+              have = true;
             }
           }
-          checks += cnt2;
+          tally(0, cnt2);
         }
-        checks += 1;  // entry-pose comparison (kernel.hpp:192-194)
+        tally(0, 1);  // entry-pose comparison (kernel.hpp:192-194)
         if (!have || cur > best) {
           best = cur;
           best_a = 0;
         }
-        evals += nfeas;
+        tally(nfeas, 0);
       }
       ck.mark(kPhDecide);
       // commit_angle (kernel.hpp:115-117): a fresh rotation of the entry pose,
@@ -662,8 +702,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   }
   if (lane == 0) {
     p.st_final[e] = cur;
-    p.st_evals[e] = evals;
-    p.st_checks[e] = checks;
+    p.st_evals[e] = s.tally[0];
+    p.st_checks[e] = s.tally[1];
   }
   if (p.stage_pose != nullptr) {
     double* dst = p.stage_pose + 3 * (static_cast<size_t>(p.top_k) * m.atom_off + static_cast<size_t>(r) * n);

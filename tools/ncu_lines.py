@@ -7,6 +7,7 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
+by = sys.argv[4] if len(sys.argv) > 4 else "stall"  # or "inst"
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}",
                       "--print-source", "cuda,sass"], capture_output=True, text=True).stdout
 cur, hdr, res = None, None, []
@@ -29,5 +30,5 @@ for r in csv.reader(io.StringIO(out)):
 tot = sum(x[0] for x in res) or 1
 tst = sum(x[1] for x in res) or 1
 print(f"total warp instructions {tot:.3g}; columns: inst% stall%")
-for ex, st, f, ln, src in sorted(res, key=lambda x: -x[1])[:top]:
+for ex, st, f, ln, src in sorted(res, key=lambda x: -(x[0] if by == "inst" else x[1]))[:top]:
     print(f"{ex / tot * 100:5.1f}% {st / tst * 100:5.1f}% {f}:{ln} {src}")
