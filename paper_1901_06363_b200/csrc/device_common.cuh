@@ -47,6 +47,9 @@ __device__ __forceinline__ double dist_sq(double ax, double ay, double az, doubl
 #ifndef GD_LST_NA
 #define GD_LST_NA 1
 #endif
+#ifndef GD_WHATIF_NOLIST
+#define GD_WHATIF_NOLIST 0
+#endif
 template <bool NoAlloc = false>
 __device__ __forceinline__ void ld256(const double* p, double& a, double& b, double& c, double& d) {
   if constexpr (NoAlloc)
@@ -189,7 +192,11 @@ __device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, do
   w.add(kPairs, (a.lst ? a.count : 0) + (b.lst ? b.count : 0));
   m0 = inline_min(a, x0, y0, z0);
   m1 = inline_min(b, x1, y1, z1);
+#if GD_WHATIF_NOLIST
+  const int nmax = 0;  // timing experiment only: wrong minima
+#else
   const int nmax = max(na, nb);
+#endif
   for (int k = 0; k < nmax; ++k) {
     if (k < na) {
       const P3 p = ldp<GD_LST_NA>(a.lst, k);
