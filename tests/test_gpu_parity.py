@@ -86,6 +86,37 @@ def test_pipelined_dock_batch_equals_resident_path(docker):
         assert np.array_equal(got.evaluations[l], ref.evaluations[i])
 
 
+def test_device_results_views_match_download(docker):
+    """gd_device_results: zero-copy torch views of the resident top-K table
+    (what the multi-GPU gather all-gathers) equal gd_download's copy."""
+    from paper_1901_06363_b200 import DockResult
+    w = W.config(1)
+    pocket = w.pocket()
+    batch = w.ligands(range(300))
+    docker.set_pocket(pocket)
+    docker.upload(batch)
+    docker.dock_resident(w.knobs)
+    host = docker.download(DockResult.empty(batch.n_ligands, w.knobs.slots,
+                                            int(batch.atom_offsets[-1]), False))
+    dev = docker.device_results()
+    for f in ("final_score", "orientation", "seed_rank", "evaluations"):
+        assert np.array_equal(dev[f].cpu().numpy(), getattr(host, f)), f
+    # The bench's N>1 gather over those views (a world-1 NCCL group here).
+    import socket
+    import torch.distributed as dist
+    from paper_1901_06363_b200.sharding import DeviceGather
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        out = DeviceGather(dev, 1)()
+        for f in DeviceGather.FIELDS:
+            assert np.array_equal(out[f][0].cpu().numpy(), getattr(host, f)), f
+    finally:
+        dist.destroy_process_group()
+
+
 def test_config2_knobs_parity(docker):
     """c2 knobs (rigid 10, frag 10, 3 restarts, K=100) on two c1-distribution ligands."""
     w = W.config(2)
