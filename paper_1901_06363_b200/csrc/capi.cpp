@@ -939,15 +939,17 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   pr.final_pose = keep_pose ? static_cast<double*>(take(8 * pose_elems)) : nullptr;
 
   // Chunk plan: a small head chunk (its host prep is the only part nothing
-  // overlaps), then chunks growing geometrically by 1.5x: host prep runs
-  // ~1.7x faster than the GPU docks, so each chunk is prepared before the
-  // GPU drains the previous ones, and few launch tails remain (c1: 19.36 ms
-  // vs 19.85 with 15 equal chunks; tools/e2e_plan_ab.sh).  GD_E2E_GROWTH<=1
-  // selects the equal split into GD_E2E_CHUNKS parts.
+  // overlaps), then chunks growing geometrically by 1.6x: host prep runs
+  // faster than the GPU docks, so each chunk is prepared before the GPU
+  // drains the previous ones, and few launch tails remain (c1: 19.36 ms vs
+  // 19.85 with 15 equal chunks at r2a; 18.11 vs 18.24 at 1.5x on the r2b
+  // kernels, 1.7x / 2.0x worse again as the last chunk grows;
+  // tools/e2e_plan_ab.sh).  GD_E2E_GROWTH<=1 selects the equal split into
+  // GD_E2E_CHUNKS parts.
   std::vector<int> bounds{0};
   static const int kHead = static_cast<int>(env_double("GD_E2E_HEAD", 256));
   static const int kParts = static_cast<int>(env_double("GD_E2E_CHUNKS", 15));
-  static const double kGrowth = env_double("GD_E2E_GROWTH", 1.5);
+  static const double kGrowth = env_double("GD_E2E_GROWTH", 1.6);
   if (L > 2048 && kGrowth > 1.0) {
     bounds.push_back(kHead);
     double sz = kHead;
