@@ -21,6 +21,9 @@ namespace {
 #ifndef GD_RIGID_MLP
 #define GD_RIGID_MLP 2   // atoms whose nearest-point lookups are in flight together
 #endif
+#ifndef GD_RIGID_RSMEM
+#define GD_RIGID_RSMEM 1 // the orientation matrix re-read from shared memory per atom group (c1 rigid 2.96 -> 2.91 ms, c2 20.9 -> 19.9)
+#endif
 constexpr int kRigidThreads = 256;
 
 // Score of orientation s: rotate every atom (E3) and fold the overlap terms
@@ -30,12 +33,26 @@ template <bool On>
 __device__ __forceinline__ double score_orientation(const DockParams& p, int s, int n,
                                                    const double* vx, const double* vy,
                                                    const double* vz, Work<On>& wk) {
+#if GD_RIGID_RSMEM
+  // The thread's column of a [9][256] shared table: 18 registers free for
+  // the lookups, at 9 shared loads per atom group.
+  __shared__ double Rs[9 * kRigidThreads];
+  volatile double* Rv = Rs + threadIdx.x;
+#pragma unroll
+  for (int r = 0; r < 9; ++r) Rv[r * kRigidThreads] = __ldg(p.orient_R + 9 * s + r);
+#else
   double R[9];
 #pragma unroll
   for (int r = 0; r < 9; ++r) R[r] = __ldg(p.orient_R + 9 * s + r);
+#endif
   double sum = 0.0;
   int i = 0;
   for (; i + GD_RIGID_MLP - 1 < n; i += GD_RIGID_MLP) {
+#if GD_RIGID_RSMEM
+    double R[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) R[r] = Rv[r * kRigidThreads];
+#endif
     double x[GD_RIGID_MLP], y[GD_RIGID_MLP], z[GD_RIGID_MLP], mm[GD_RIGID_MLP];
 #pragma unroll
     for (int r = 0; r < GD_RIGID_MLP; ++r)
@@ -46,6 +63,11 @@ __device__ __forceinline__ double score_orientation(const DockParams& p, int s, 
     for (int r = 0; r < GD_RIGID_MLP; ++r) sum = dadd(sum, fmax(kMinDistanceSq, mm[r]));
   }
   for (; i < n; ++i) {
+#if GD_RIGID_RSMEM
+    double R[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) R[r] = Rv[r * kRigidThreads];
+#endif
     double x, y, z;
     rigid_apply(R, p.cx, p.cy, p.cz, vx[i], vy[i], vz[i], x, y, z);
     wk.add(kXform, 1);

@@ -6,10 +6,11 @@ import subprocess
 import sys
 
 kern = sys.argv[1] if len(sys.argv) > 1 else "flex_chain_kernelILb0ELi6ELi12E"
+src = "paper_1901_06363_b200/csrc/" + ("rigid.cu" if "rigid" in kern else "flex.cu")
 extra = sys.argv[2:]
 subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-fmad=false",
                 "-lineinfo", "-cubin", "-Iinclude", "-Ipaper_1901_06363_b200/csrc", *extra,
-                "paper_1901_06363_b200/csrc/flex.cu", "-o", "/tmp/spills.cubin"], check=True)
+                src, "-o", "/tmp/spills.cubin"], check=True)
 sass = subprocess.run(["nvdisasm", "--print-line-info", "/tmp/spills.cubin"], capture_output=True,
                       text=True).stdout.splitlines()
 on, cur, res, tot = False, None, collections.Counter(), 0
