@@ -159,7 +159,7 @@ struct gd_ctx {
   // Pocket.
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels], vox_counts, vox_doff;
+  DevBuf pts, tiles, vox_off[kGridLevels], vox_pts[kGridLevels], vox_counts, vox_doff, vox_keep;
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
@@ -364,11 +364,55 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   ctx->centre[2] = sz / n;
   ctx->P = n;
 
+  // Device copy of the points in Morton order (10 bits per axis over the
+  // bounding box): every use is a minimum over points, so the order is
+  // free, and 32-point tiles become spatially compact for the culled index
+  // build (pocket_index.cu), which gets their outward-rounded fp32 boxes.
+  std::vector<std::pair<uint32_t, int32_t>> key(n);
+  auto spread = [](uint32_t x) {  // 10 bits -> every third bit
+    x &= 0x3ff;
+    x = (x | (x << 16)) & 0x030000ff;
+    x = (x | (x << 8)) & 0x0300f00f;
+    x = (x | (x << 4)) & 0x030c30c3;
+    x = (x | (x << 2)) & 0x09249249;
+    return x;
+  };
+  for (int32_t j = 0; j < n; ++j) {
+    uint32_t c[3];
+    for (int k = 0; k < 3; ++k) {
+      const double ext = hi[k] - lo[k];
+      c[k] = ext > 0 ? static_cast<uint32_t>(std::min(1023.0, (xyz[3 * j + k] - lo[k]) / ext * 1023.0)) : 0;
+    }
+    key[j] = {spread(c[0]) | (spread(c[1]) << 1) | (spread(c[2]) << 2), j};
+  }
+  std::sort(key.begin(), key.end());
   std::vector<double> padded(4 * static_cast<size_t>(n), 0.0);
-  for (int32_t j = 0; j < n; ++j)
-    for (int k = 0; k < 3; ++k) padded[4 * j + k] = xyz[3 * j + k];
+  for (int32_t q = 0; q < n; ++q)
+    for (int k = 0; k < 3; ++k) padded[4 * q + k] = xyz[3 * key[q].second + k];
   GD_CUDA(ctx, ctx->pts.ensure(padded.size() * sizeof(double)));
   GD_CUDA(ctx, cudaMemcpy(ctx->pts.ptr, padded.data(), padded.size() * sizeof(double),
+                          cudaMemcpyHostToDevice));
+  static const bool kCull = env_double("GD_VOXEL_CULL", 1) != 0;
+  const int n_tiles = kCull ? (n + 31) / 32 : 0;
+  std::vector<float> tbox(6 * static_cast<size_t>(std::max(n_tiles, 1)), 0.0f);
+  for (int t = 0; t < n_tiles; ++t) {
+    double blo[3], bhi[3];
+    for (int k = 0; k < 3; ++k) blo[k] = bhi[k] = padded[4 * (32 * t) + k];
+    for (int q = 32 * t; q < std::min(n, 32 * t + 32); ++q)
+      for (int k = 0; k < 3; ++k) {
+        blo[k] = std::min(blo[k], padded[4 * q + k]);
+        bhi[k] = std::max(bhi[k], padded[4 * q + k]);
+      }
+    for (int k = 0; k < 3; ++k) {
+      float fl = static_cast<float>(blo[k]), fh = static_cast<float>(bhi[k]);
+      if (static_cast<double>(fl) > blo[k]) fl = std::nextafter(fl, -INFINITY);
+      if (static_cast<double>(fh) < bhi[k]) fh = std::nextafter(fh, INFINITY);
+      tbox[6 * t + k] = fl;
+      tbox[6 * t + 3 + k] = fh;
+    }
+  }
+  GD_CUDA(ctx, ctx->tiles.ensure(tbox.size() * sizeof(float)));
+  GD_CUDA(ctx, cudaMemcpy(ctx->tiles.ptr, tbox.data(), tbox.size() * sizeof(float),
                           cudaMemcpyHostToDevice));
 
   // Two grid levels over the pocket bounding box: a fine near field (voxel
@@ -409,8 +453,15 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     const int nv = g.dim_x * g.dim_y * g.dim_z;
     DevBuf& counts = ctx->vox_counts;
     GD_CUDA(ctx, counts.ensure(sizeof(int32_t) * nv));
+    int32_t* keep = nullptr;  // the count pass's first 8 candidates per voxel
+    if (n_tiles > 0) {
+      GD_CUDA(ctx, ctx->vox_keep.ensure(sizeof(int32_t) * 8 * static_cast<size_t>(nv)));
+      keep = ctx->vox_keep.as<int32_t>();
+    }
     GD_CUDA(ctx, static_cast<cudaError_t>(launch_voxel_count(ctx->pts.as<double>(), n, g,
-                                                             counts.as<int32_t>(), ctx->stream)));
+                                                             counts.as<int32_t>(),
+                                                             ctx->tiles.as<float>(), n_tiles, keep,
+                                                             ctx->stream)));
     std::vector<int32_t> cnt(nv);
     GD_CUDA(ctx, cudaMemcpyAsync(cnt.data(), counts.ptr, sizeof(int32_t) * nv,
                                  cudaMemcpyDeviceToHost, ctx->stream));
@@ -436,7 +487,8 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     GD_CUDA(ctx, static_cast<cudaError_t>(
                      launch_voxel_fill(ctx->pts.as<double>(), n, g, doff.as<int32_t>(),
                                        ctx->vox_off[L].as<double>(), ctx->vox_pts[L].as<double>(),
-                                       ctx->stream)));
+                                       ctx->tiles.as<float>(), n_tiles, counts.as<int32_t>(),
+                                       keep, ctx->stream)));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     ctx->grid[L] = g;
     ctx->n_cand += total;

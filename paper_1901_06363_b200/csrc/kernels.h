@@ -140,8 +140,15 @@ struct VoxelGrid {
 // voxel's record and its candidates past the inline ones at the
 // host-scanned list offsets (sum over earlier voxels of
 // max(count - kVoxInline, 0)).
-int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, void* stream);
+// tbox [nt][6] (lo xyz, hi xyz; fp32, outward-rounded) are the bounding
+// boxes of the Morton-ordered points' 32-point tiles: with nt > 0 the build
+// culls tiles per 4x4x8 voxel brick (pocket_index.cu); nt = 0 scans all.
+// keep [nv][8] (nullable): the count pass stores each voxel's first 8
+// candidates there and the fill pass copies them instead of recomputing.
+int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, const float* tbox,
+                       int nt, int32_t* keep, void* stream);
 int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
-                      double* lst, void* stream);
+                      double* lst, const float* tbox, int nt, const int32_t* counts,
+                      const int32_t* keep, void* stream);
 
 }  // namespace gdb200

@@ -149,12 +149,220 @@ __device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, b
   return kept;
 }
 
+// Culled build (pockets up to kMaxTiles x 32 points).  The host stores the
+// points in Morton order, so 32-point tiles are spatially compact, with
+// outward-rounded fp32 bounding boxes.  A CTA owns a 4 x 4 x 8 brick of
+// voxels, ranks the tiles by their distance to the brick and walks them
+// nearest first:
+//   pass 1 stops once the next tile is farther than every voxel's current
+//   U (no point beyond can lower a U: maxdist >= mindist; and any U is a
+//   valid bound, so culling here can only lengthen lists);
+//   pass 2 stops once the next tile is beyond every voxel's limit plus a
+//   pad far above fp32 rounding, so no point the exact rule keeps is
+//   skipped.
+// Lists are the same as the full scan's up to the centre-nearest choice and
+// an upper bound U that may only be larger, i.e. exact.
+constexpr int kTilePts = 32;
+constexpr int kMaxTiles = 512;
+constexpr int kGroupTiles = 8;  // tiles staged per round (256 points)
+constexpr int kBrickX = 4, kBrickY = 4, kBrickZ = 8;
+static_assert(kBrickX * kBrickY * kBrickZ == kBuildThreads, "one voxel per thread");
+
+struct BrickScratch {
+  float dB[kMaxTiles];    // squared distance brick -> tile box (shrunk: a lower bound)
+  short ord[kMaxTiles];   // tiles by ascending dB
+  int bound;              // CTA max of a per-voxel bound (float bits, >= 0)
+};
+
+__device__ __forceinline__ float box_gap(float alo, float ahi, float blo, float bhi) {
+  return fmaxf(0.0f, fmaxf(alo - bhi, blo - ahi));
+}
+
+// The voxel of this thread in brick `b` (x-major voxel numbering).
+__device__ __forceinline__ bool brick_voxel(const VoxelGrid& g, int b, int& ix, int& iy, int& iz) {
+  const int nby = (g.dim_y + kBrickY - 1) / kBrickY, nbz = (g.dim_z + kBrickZ - 1) / kBrickZ;
+  const int bx = b / (nby * nbz), by = (b / nbz) % nby, bz = b % nbz;
+  const int t = threadIdx.x;
+  ix = bx * kBrickX + t / (kBrickY * kBrickZ);
+  iy = by * kBrickY + (t / kBrickZ) % kBrickY;
+  iz = bz * kBrickZ + t % kBrickZ;
+  return ix < g.dim_x && iy < g.dim_y && iz < g.dim_z;
+}
+
+__device__ int voxel_list_culled(const double* pts, int P, const VoxelGrid& g, int b, int ix,
+                                 int iy, int iz, bool active, int* cand, float4* tile,
+                                 const float* tbox, int nt, BrickScratch& sc) {
+  const double bl[3] = {g.lo_x + ix * g.h - kVoxEps, g.lo_y + iy * g.h - kVoxEps,
+                        g.lo_z + iz * g.h - kVoxEps};
+  const double bh[3] = {bl[0] + g.h + 2 * kVoxEps, bl[1] + g.h + 2 * kVoxEps,
+                        bl[2] + g.h + 2 * kVoxEps};
+  const float lx = static_cast<float>(bl[0]), ly = static_cast<float>(bl[1]),
+              lz = static_cast<float>(bl[2]);
+  const float hx = static_cast<float>(bh[0]), hy = static_cast<float>(bh[1]),
+              hz = static_cast<float>(bh[2]);
+  const float cx = 0.5f * (lx + hx), cy = 0.5f * (ly + hy), cz = 0.5f * (lz + hz);
+  // The brick's box (all its voxel boxes, grid-clipped or not: a superset
+  // only lowers dB), shrunk by a hair so dB stays a lower bound.
+  const int nby = (g.dim_y + kBrickY - 1) / kBrickY, nbz = (g.dim_z + kBrickZ - 1) / kBrickZ;
+  const int bx = b / (nby * nbz), by = (b / nbz) % nby, bz = b % nbz;
+  const float pad = 1e-3f;
+  const float Bl[3] = {static_cast<float>(g.lo_x + bx * kBrickX * g.h) - pad,
+                       static_cast<float>(g.lo_y + by * kBrickY * g.h) - pad,
+                       static_cast<float>(g.lo_z + bz * kBrickZ * g.h) - pad};
+  const float Bh[3] = {static_cast<float>(g.lo_x + (bx + 1) * kBrickX * g.h) + pad,
+                       static_cast<float>(g.lo_y + (by + 1) * kBrickY * g.h) + pad,
+                       static_cast<float>(g.lo_z + (bz + 1) * kBrickZ * g.h) + pad};
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {
+    const float* q = tbox + 6 * t;
+    const float gx = box_gap(Bl[0], Bh[0], q[0], q[3]);
+    const float gy = box_gap(Bl[1], Bh[1], q[1], q[4]);
+    const float gz = box_gap(Bl[2], Bh[2], q[2], q[5]);
+    sc.dB[t] = gx * gx + gy * gy + gz * gz;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nt; t += blockDim.x) {  // rank sort (distinct by index)
+    const float d = sc.dB[t];
+    int r = 0;
+    for (int u = 0; u < nt; ++u) {
+      const float e = sc.dB[u];
+      r += (e < d) || (e == d && u < t);
+    }
+    sc.ord[r] = static_cast<short>(t);
+  }
+  __syncthreads();
+  // Stages sorted tiles [k0, k0 + kGroupTiles) into `tile` (w = the point's
+  // index bits); returns the number of points staged.
+  // Staged tile g occupies tile[g * kTilePts, + size); the stage holds
+  // min(kGroupTiles, nt - k0) tiles.
+  auto stage = [&](int k0) {
+    __syncthreads();
+    for (int k = k0; k < min(nt, k0 + kGroupTiles); ++k) {
+      const int t = sc.ord[k];
+      const int cnt = min(kTilePts, P - t * kTilePts);
+      for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const double* q = pts + 4 * static_cast<size_t>(t * kTilePts + i);
+        tile[(k - k0) * kTilePts + i] =
+            make_float4(static_cast<float>(q[0]), static_cast<float>(q[1]), static_cast<float>(q[2]),
+                        __int_as_float(t * kTilePts + i));
+      }
+    }
+    __syncthreads();
+    return min(kGroupTiles, nt - k0);
+  };
+  // Squared gap between this voxel's box and a tile's box (a lower bound on
+  // the squared distance from the voxel to any of the tile's points).
+  auto vgap2 = [&](int t) {
+    const float* q = tbox + 6 * t;
+    const float gx = box_gap(lx, hx, q[0], q[3]);
+    const float gy = box_gap(ly, hy, q[1], q[4]);
+    const float gz = box_gap(lz, hz, q[2], q[5]);
+    return gx * gx + gy * gy + gz * gz;
+  };
+  auto cta_max = [&](float x) {  // max over active threads (x >= 0)
+    __syncthreads();
+    if (threadIdx.x == 0) sc.bound = 0;
+    __syncthreads();
+    if (active) atomicMax(&sc.bound, __float_as_int(x));
+    __syncthreads();
+    return __int_as_float(sc.bound);
+  };
+  // Pass 1 (fp32): U and the point nearest the box centre, nearest tiles first.
+  float U = 3.0e38f, dc = 3.0e38f;
+  int jc = 0;
+  float Umax = 3.0e38f;
+  for (int k0 = 0; k0 < nt; k0 += kGroupTiles) {
+    if (sc.dB[sc.ord[k0]] > Umax) break;  // uniform: every later tile is farther
+    const int ng = stage(k0);
+    for (int gt = 0; gt < ng && active; ++gt) {
+      const int t = sc.ord[k0 + gt];
+      if (vgap2(t) > U) continue;  // none of its points can lower this U
+      const int cnt = min(kTilePts, P - t * kTilePts);
+      for (int i = gt * kTilePts; i < gt * kTilePts + cnt; ++i) {
+        const float4 q = tile[i];
+        const float fx = fmaxf(fabsf(q.x - lx), fabsf(q.x - hx));
+        const float fy = fmaxf(fabsf(q.y - ly), fabsf(q.y - hy));
+        const float fz = fmaxf(fabsf(q.z - lz), fabsf(q.z - hz));
+        U = fminf(U, fx * fx + fy * fy + fz * fz);
+        const float d = (q.x - cx) * (q.x - cx) + (q.y - cy) * (q.y - cy) + (q.z - cz) * (q.z - cz);
+        if (d < dc) {
+          dc = d;
+          jc = __float_as_int(q.w);
+        }
+      }
+    }
+    Umax = cta_max(U);
+  }
+  const float lim = U * (1.0f + kPassRel) + kPassAbs;
+  const float cut = cta_max(lim) * (1.0f + kPassRel) + 1e-2f;
+  const P3 C = ldp(pts, active ? jc : 0);
+  // Pass 2: every tile that can hold a point within some voxel's limit.
+  int k = 0;
+  bool over = false;
+  for (int k0 = 0; k0 < nt; k0 += kGroupTiles) {
+    if (sc.dB[sc.ord[k0]] > cut) break;  // uniform
+    const int ng = stage(k0);
+    if (!active || over) continue;
+    const float vcut = lim * (1.0f + kPassRel) + 1e-2f;
+    for (int gt = 0; gt < ng && !over; ++gt) {
+      const int t = sc.ord[k0 + gt];
+      if (vgap2(t) > vcut) continue;  // every point of it fails the test below
+      const int cnt = min(kTilePts, P - t * kTilePts);
+      for (int i = gt * kTilePts; i < gt * kTilePts + cnt; ++i) {
+        const float4 q = tile[i];
+        const float nx = fmaxf(0.0f, fmaxf(lx - q.x, q.x - hx));
+        const float ny = fmaxf(0.0f, fmaxf(ly - q.y, q.y - hy));
+        const float nz = fmaxf(0.0f, fmaxf(lz - q.z, q.z - hz));
+        if (nx * nx + ny * ny + nz * nz > lim) continue;
+        const int j = __float_as_int(q.w);
+        const P3 Q = ldp(pts, j);
+        if (dominates(C, Q, bl, bh)) continue;
+        if (k >= kVoxMaxCand) {
+          over = true;
+          break;
+        }
+        cand[k++] = j;
+      }
+    }
+  }
+  if (!active) return 0;
+  if (over) return -1;
+  int kept = 0;  // pass 3 (exact): full dominance pruning among the survivors
+  for (int a = 0; a < k; ++a) {
+    const P3 A = ldp(pts, cand[a]);
+    bool dominated = false;
+    for (int c = 0; c < k && !dominated; ++c)
+      if (c != a) dominated = dominates(ldp(pts, cand[c]), A, bl, bh);
+    if (!dominated) cand[kept++] = cand[a];
+  }
+  return kept;
+}
+
+// Culled builds keep each voxel's first kKeep candidates (point indices)
+// in `keep` [nv][kKeep], so the fill pass copies instead of recomputing
+// (a CTA recomputes only if one of its voxels has more).
+constexpr int kKeep = 8;
+
 __global__ void __launch_bounds__(kBuildThreads) voxel_count_kernel(const double* pts, int P,
-                                                                    VoxelGrid g, int32_t* counts) {
+                                                                    VoxelGrid g, int32_t* counts,
+                                                                    const float* tbox, int nt,
+                                                                    int32_t* keep) {
   __shared__ float4 tile[kTile];
+  __shared__ BrickScratch sc;
+  int cand[kVoxMaxCand];
+  if (nt > 0) {
+    int ix, iy, iz;
+    const bool in = brick_voxel(g, blockIdx.x, ix, iy, iz);
+    const int k = voxel_list_culled(pts, P, g, blockIdx.x, ix, iy, iz, in, cand, tile, tbox, nt, sc);
+    if (in) {
+      const int v = (ix * g.dim_y + iy) * g.dim_z + iz;
+      counts[v] = k < 0 ? P : k;
+      if (keep != nullptr)
+        for (int a = 0; a < min(max(k, 0), kKeep); ++a) keep[kKeep * static_cast<size_t>(v) + a] = cand[a];
+    }
+    return;
+  }
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   const int nv = g.dim_x * g.dim_y * g.dim_z;
-  int cand[kVoxMaxCand];
   const int k = voxel_list(pts, P, g, min(v, nv - 1), v < nv, cand, tile);
   if (v < nv) counts[v] = k < 0 ? P : k;  // overflow: keep every point (exact, rare)
 }
@@ -162,13 +370,33 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_count_kernel(const double
 __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double* pts, int P,
                                                                    VoxelGrid g,
                                                                    const int32_t* offsets,
-                                                                   double* rec, double* lst) {
+                                                                   double* rec, double* lst,
+                                                                   const float* tbox, int nt,
+                                                                   const int32_t* counts,
+                                                                   const int32_t* keep) {
   __shared__ float4 tile[kTile];
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  const int nv = g.dim_x * g.dim_y * g.dim_z;
+  __shared__ BrickScratch sc;
   int cand[kVoxMaxCand];
-  const int k = voxel_list(pts, P, g, min(v, nv - 1), v < nv, cand, tile);
-  if (v >= nv) return;
+  int v, k;
+  if (nt > 0) {
+    int ix, iy, iz;
+    const bool in = brick_voxel(g, blockIdx.x, ix, iy, iz);
+    v = in ? (ix * g.dim_y + iy) * g.dim_z + iz : 0;
+    const int c = in ? counts[v] : 0;
+    if (keep != nullptr && !__syncthreads_or(c > kKeep)) {  // uniform: copy the kept lists
+      if (!in) return;
+      k = c;
+      for (int a = 0; a < k; ++a) cand[a] = keep[kKeep * static_cast<size_t>(v) + a];
+    } else {
+      k = voxel_list_culled(pts, P, g, blockIdx.x, ix, iy, iz, in, cand, tile, tbox, nt, sc);
+      if (!in) return;
+    }
+  } else {
+    v = blockIdx.x * blockDim.x + threadIdx.x;
+    const int nv = g.dim_x * g.dim_y * g.dim_z;
+    k = voxel_list(pts, P, g, min(v, nv - 1), v < nv, cand, tile);
+    if (v >= nv) return;
+  }
   const int len = k < 0 ? P : k;  // >= 1: the nearest point always survives
   const int start = offsets[v];
   double* r = rec + kRecDoubles * static_cast<size_t>(v);
@@ -250,20 +478,29 @@ int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int
   return cudaGetLastError();
 }
 
-int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, void* stream) {
+static unsigned build_blocks(const VoxelGrid& g, int nt) {
+  if (nt > 0)
+    return static_cast<unsigned>(((g.dim_x + kBrickX - 1) / kBrickX) *
+                                 ((g.dim_y + kBrickY - 1) / kBrickY) *
+                                 ((g.dim_z + kBrickZ - 1) / kBrickZ));
   const int nv = g.dim_x * g.dim_y * g.dim_z;
-  const int bt = 128;
-  voxel_count_kernel<<<(nv + bt - 1) / bt, bt, 0, static_cast<cudaStream_t>(stream)>>>(pts, P, g,
-                                                                                      counts);
+  return static_cast<unsigned>((nv + kBuildThreads - 1) / kBuildThreads);
+}
+
+int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, const float* tbox,
+                       int nt, int32_t* keep, void* stream) {
+  if (nt > kMaxTiles) nt = 0;  // too many tiles for the brick scratch: full scan
+  voxel_count_kernel<<<build_blocks(g, nt), kBuildThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      pts, P, g, counts, tbox, nt, keep);
   return cudaGetLastError();
 }
 
 int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
-                      double* lst, void* stream) {
-  const int nv = g.dim_x * g.dim_y * g.dim_z;
-  const int bt = 128;
-  voxel_fill_kernel<<<(nv + bt - 1) / bt, bt, 0, static_cast<cudaStream_t>(stream)>>>(
-      pts, P, g, offsets, rec, lst);
+                      double* lst, const float* tbox, int nt, const int32_t* counts,
+                      const int32_t* keep, void* stream) {
+  if (nt > kMaxTiles) nt = 0;
+  voxel_fill_kernel<<<build_blocks(g, nt), kBuildThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      pts, P, g, offsets, rec, lst, tbox, nt, counts, keep);
   return cudaGetLastError();
 }
 

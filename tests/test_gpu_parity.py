@@ -248,6 +248,34 @@ def test_overlap_score_kats(docker):
     assert docker.overlap_scores(np.array([[0.0, 0.0, 2.0]]))[0] == 1.0
 
 
+@pytest.mark.parametrize("which", ["c1", "c3-largest", "c3-smallest"])
+def test_index_minimum_equals_full_scan_on_dense_queries(docker, which):
+    """The (culled, brick-built) voxel index returns the full scan's fp64
+    minimum for 300k single-atom queries: uniform over both grid levels and
+    beyond them, plus points clustered on the pocket lattice's Voronoi
+    boundaries (ties).  One-atom score = 1 / max(1e-12, min d^2), so equal
+    scores are equal minima."""
+    if which == "c1":
+        pocket = W.config(1).pocket()
+    else:
+        w3 = W.config(3)
+        pockets = sorted((W.pocket_of(w3, i) for i in range(16)), key=len)
+        pocket = pockets[-1] if which == "c3-largest" else pockets[0]
+    docker.set_pocket(pocket)
+    rng = np.random.default_rng(11)
+    lo, hi = pocket.min(axis=0), pocket.max(axis=0)
+    far = rng.uniform(lo - 36.0, hi + 36.0, size=(100000, 3))
+    near = rng.uniform(lo - 3.5, hi + 3.5, size=(100000, 3))
+    # Half-integer offsets from lattice points: equidistant from neighbours.
+    base = pocket[rng.integers(0, len(pocket), 100000)]
+    ties = base + rng.choice([-0.5, 0.0, 0.5], size=(100000, 3)) + rng.normal(0, 1e-9, (100000, 3))
+    q = np.concatenate([far, near, ties])[:, None, :]
+    idx = docker.overlap_scores(q)
+    brute = docker.overlap_scores(q, brute=True)
+    bad = np.flatnonzero(idx != brute)
+    assert bad.size == 0, (bad[:5], q[bad[:5], 0])
+
+
 def test_overlap_scores_random_poses_exact(docker):
     """Index vs brute vs oracle on random poses, including far-away atoms."""
     O = _oracle()
