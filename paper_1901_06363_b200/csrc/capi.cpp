@@ -159,7 +159,8 @@ struct gd_ctx {
   // Pocket.
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, tiles, vox_off[kGridLevels], vox_pts[kGridLevels], vox_counts, vox_doff, vox_keep;
+  DevBuf pts, tiles, vox_off[kGridLevels], vox_pts[kGridLevels], vox_counts, vox_doff, vox_keep,
+      vox_scan;
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
@@ -462,28 +463,24 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
                                                              counts.as<int32_t>(),
                                                              ctx->tiles.as<float>(), n_tiles, keep,
                                                              ctx->stream)));
-    std::vector<int32_t> cnt(nv);
-    GD_CUDA(ctx, cudaMemcpyAsync(cnt.data(), counts.ptr, sizeof(int32_t) * nv,
-                                 cudaMemcpyDeviceToHost, ctx->stream));
-    GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    // Each voxel's first kVoxInline candidates live in its record; the list
-    // holds the rest, offsets = exclusive scan of max(count - kVoxInline, 0).
-    std::vector<int32_t> off(nv, 0);
-    int64_t total = 0, listed = 0;
-    int32_t mx = 0;
-    for (int c = 0; c < nv; ++c) {
-      off[c] = static_cast<int32_t>(listed);
-      listed += std::max(cnt[c] - kVoxInline, 0);
-      total += cnt[c];
-      mx = std::max(mx, cnt[c]);
-      if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
-    }
+    // List offsets (exclusive scan of max(count - kVoxInline, 0)) and the
+    // totals on the device; only the three totals come back.
     DevBuf& doff = ctx->vox_doff;
     GD_CUDA(ctx, doff.ensure(sizeof(int32_t) * nv));
+    GD_CUDA(ctx, ctx->vox_scan.ensure(static_cast<size_t>(list_offsets_scratch_bytes(nv)) + 64));
+    long long* dtot = reinterpret_cast<long long*>(static_cast<unsigned char*>(ctx->vox_scan.ptr) +
+                                                   list_offsets_scratch_bytes(nv));
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_list_offsets(counts.as<int32_t>(), nv,
+                                                              doff.as<int32_t>(), ctx->vox_scan.ptr,
+                                                              dtot, ctx->stream)));
+    long long tot[3];
+    GD_CUDA(ctx, cudaMemcpyAsync(tot, dtot, sizeof tot, cudaMemcpyDeviceToHost, ctx->stream));
+    GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+    const int64_t listed = tot[0], total = tot[1];
+    const int32_t mx = static_cast<int32_t>(tot[2]);
+    if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
     GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
     GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
-    GD_CUDA(ctx, cudaMemcpyAsync(doff.ptr, off.data(), sizeof(int32_t) * nv, cudaMemcpyHostToDevice,
-                                 ctx->stream));
     GD_CUDA(ctx, static_cast<cudaError_t>(
                      launch_voxel_fill(ctx->pts.as<double>(), n, g, doff.as<int32_t>(),
                                        ctx->vox_off[L].as<double>(), ctx->vox_pts[L].as<double>(),
@@ -644,20 +641,37 @@ static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
     m.words = p.words;
     ctx->status_host[l] = p.status;
     reinterpret_cast<int32_t*>(ctx->pin[kStatus])[l] = p.status;
-    ctx->errors[l] = p.error;
+    if (!p.error.empty()) ctx->errors[l] = p.error;
     if (p.status != 0) continue;
-    std::copy(p.far_mask.begin(), p.far_mask.end(), hfar + run.wo);
-    std::copy(p.frag_mask.begin(), p.frag_mask.end(), hfm + run.mo);
-    for (int f = 0; f < p.nfrag(); ++f) {
-      hax[run.fo + f] = p.frag_axis[f];
-      han[run.fo + f] = p.frag_anchor[f];
-      hrel[run.fo + f] = p.frag_rel[f];
-    }
     run.wo += p.far_mask.size();
     run.mo += p.frag_mask.size();
     run.fo += p.nfrag();
     chunk_max_n = std::max(chunk_max_n, m.n);
     cost[e] = static_cast<double>(m.n) * (4.0 + m.nfrag);
+  }
+  // The descriptors into the pinned arena at the offsets just assigned:
+  // the bulk of the pack, on the workers for large chunks.
+  auto pack = [&](int e0, int e1) {
+    for (int e = e0; e < e1; ++e) {
+      const PreparedLigand& p = prep[e];
+      if (p.status != 0) continue;
+      const LigMeta& m = meta[c0 + e];
+      std::copy(p.far_mask.begin(), p.far_mask.end(), hfar + m.far_off);
+      std::copy(p.frag_mask.begin(), p.frag_mask.end(), hfm + m.fmask_off);
+      for (int f = 0; f < p.nfrag(); ++f) {
+        hax[m.frag_off + f] = p.frag_axis[f];
+        han[m.frag_off + f] = p.frag_anchor[f];
+        hrel[m.frag_off + f] = p.frag_rel[f];
+      }
+    }
+  };
+  if (cnt < 64 || !ctx->pool) {
+    pack(0, cnt);
+  } else {
+    std::atomic<int> nxt{0};
+    ctx->pool->run([&] {
+      for (int e; (e = nxt.fetch_add(32)) < cnt;) pack(e, std::min(cnt, e + 32));
+    });
   }
   // Longest-processing-time-first CTA order within the chunk.
   std::vector<int32_t> idx(cnt);

@@ -150,5 +150,11 @@ int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, c
 int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
                       double* lst, const float* tbox, int nt, const int32_t* counts,
                       const int32_t* keep, void* stream);
+// offsets[v] = exclusive prefix of max(counts - kVoxInline, 0) over voxels;
+// totals[3] (device) = {listed entries, candidates, max count}; `scratch`
+// holds list_offsets_scratch_bytes(nv).
+int list_offsets_scratch_bytes(int nv);
+int launch_list_offsets(const int32_t* counts, int nv, int32_t* offsets, void* scratch,
+                        long long* totals, void* stream);
 
 }  // namespace gdb200

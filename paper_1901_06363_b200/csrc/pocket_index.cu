@@ -414,6 +414,99 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double*
   }
 }
 
+// List offsets on the device: offsets[v] = sum over earlier voxels of
+// max(count - kVoxInline, 0); totals = {listed entries, candidates, max
+// count}.  Three passes over 1024-voxel blocks (block sums, one-block scan
+// of the sums, block-local scans), so the build needs no host round trip of
+// the counts.
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ long long block_sum_ll(long long x, long long* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+  __syncthreads();
+  long long t = 0;
+  for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
+__global__ void __launch_bounds__(kScanBlock) list_block_sums(const int32_t* counts, int nv,
+                                                              long long* bsum, long long* bcand,
+                                                              int* bmax) {
+  __shared__ long long red[kScanBlock / 32];
+  __shared__ int mx;
+  const int v = blockIdx.x * kScanBlock + threadIdx.x;
+  const int c = v < nv ? counts[v] : 0;
+  if (threadIdx.x == 0) mx = 0;
+  __syncthreads();
+  atomicMax(&mx, c);
+  const long long l = block_sum_ll(max(c - kVoxInline, 0), red);
+  const long long t = block_sum_ll(c, red);
+  if (threadIdx.x == 0) {
+    bsum[blockIdx.x] = l;
+    bcand[blockIdx.x] = t;
+    bmax[blockIdx.x] = mx;
+  }
+}
+
+// One block: exclusive scan of the block sums in place, and the totals.
+__global__ void __launch_bounds__(kScanBlock) list_scan_sums(long long* bsum, const long long* bcand,
+                                                             const int* bmax, int nb,
+                                                             long long* totals) {
+  __shared__ long long part[kScanBlock];
+  __shared__ long long red[kScanBlock / 32];
+  __shared__ int mx;
+  const int per = (nb + kScanBlock - 1) / kScanBlock;  // consecutive sums per thread
+  const int b0 = threadIdx.x * per;
+  long long s = 0, cand = 0;
+  int m = 0;
+  for (int b = b0; b < min(nb, b0 + per); ++b) {
+    s += bsum[b];
+    cand += bcand[b];
+    m = max(m, bmax[b]);
+  }
+  if (threadIdx.x == 0) mx = 0;
+  part[threadIdx.x] = s;
+  __syncthreads();
+  atomicMax(&mx, m);
+  for (int o = 1; o < kScanBlock; o <<= 1) {  // inclusive Hillis-Steele scan
+    const long long y = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  long long run = part[threadIdx.x] - s;  // exclusive base of this thread's run
+  for (int b = b0; b < min(nb, b0 + per); ++b) {
+    const long long x = bsum[b];
+    bsum[b] = run;
+    run += x;
+  }
+  const long long tc = block_sum_ll(cand, red);
+  if (threadIdx.x == kScanBlock - 1) totals[0] = part[kScanBlock - 1];
+  if (threadIdx.x == 0) {
+    totals[1] = tc;
+    totals[2] = mx;
+  }
+}
+
+__global__ void __launch_bounds__(kScanBlock) list_apply(const int32_t* counts, int nv,
+                                                         const long long* bsum, int32_t* offsets) {
+  __shared__ long long part[kScanBlock];
+  const int v = blockIdx.x * kScanBlock + threadIdx.x;
+  const long long x = v < nv ? max(counts[v] - kVoxInline, 0) : 0;
+  part[threadIdx.x] = x;
+  __syncthreads();
+  for (int o = 1; o < kScanBlock; o <<= 1) {
+    const long long y = threadIdx.x >= o ? part[threadIdx.x - o] : 0;
+    __syncthreads();
+    part[threadIdx.x] += y;
+    __syncthreads();
+  }
+  if (v < nv) offsets[v] = static_cast<int32_t>(bsum[blockIdx.x] + part[threadIdx.x] - x);
+}
+
 // FP64 peak probe: 8 independent chains per thread of a DMUL and a DADD
 // (no FMA: the hot path's recipe forbids it), 2 ops per step per chain.
 __global__ void fp64_probe_kernel(double* sink, int iters) {
@@ -501,6 +594,24 @@ int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offs
   if (nt > kMaxTiles) nt = 0;
   voxel_fill_kernel<<<build_blocks(g, nt), kBuildThreads, 0, static_cast<cudaStream_t>(stream)>>>(
       pts, P, g, offsets, rec, lst, tbox, nt, counts, keep);
+  return cudaGetLastError();
+}
+
+int list_offsets_scratch_bytes(int nv) {
+  const int nb = (nv + kScanBlock - 1) / kScanBlock;
+  return 3 * 8 * nb + 64;
+}
+
+int launch_list_offsets(const int32_t* counts, int nv, int32_t* offsets, void* scratch,
+                        long long* totals, void* stream) {
+  const int nb = (nv + kScanBlock - 1) / kScanBlock;
+  auto* bsum = static_cast<long long*>(scratch);
+  long long* bcand = bsum + nb;
+  int* bmax = reinterpret_cast<int*>(bcand + nb);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  list_block_sums<<<nb, kScanBlock, 0, st>>>(counts, nv, bsum, bcand, bmax);
+  list_scan_sums<<<1, kScanBlock, 0, st>>>(bsum, bcand, bmax, nb, totals);
+  list_apply<<<nb, kScanBlock, 0, st>>>(counts, nv, bsum, offsets);
   return cudaGetLastError();
 }
 

@@ -248,7 +248,7 @@ def test_overlap_score_kats(docker):
     assert docker.overlap_scores(np.array([[0.0, 0.0, 2.0]]))[0] == 1.0
 
 
-@pytest.mark.parametrize("which", ["c1", "c3-largest", "c3-smallest"])
+@pytest.mark.parametrize("which", ["c1", "c3-largest", "c3-smallest", "20k-points"])
 def test_index_minimum_equals_full_scan_on_dense_queries(docker, which):
     """The (culled, brick-built) voxel index returns the full scan's fp64
     minimum for 300k single-atom queries: uniform over both grid levels and
@@ -257,6 +257,10 @@ def test_index_minimum_equals_full_scan_on_dense_queries(docker, which):
     scores are equal minima."""
     if which == "c1":
         pocket = W.config(1).pocket()
+    elif which == "20k-points":  # beyond the culled build's 16,384 points: full-scan build
+        g = np.mgrid[-21:22, -18:19, -15:16].reshape(3, -1).T.astype(float)
+        pocket = g[(g[:, 0] / 21.0) ** 2 + (g[:, 1] / 18.0) ** 2 + (g[:, 2] / 15.0) ** 2 <= 1.0]
+        assert len(pocket) > 16384
     else:
         w3 = W.config(3)
         pockets = sorted((W.pocket_of(w3, i) for i in range(16)), key=len)
