@@ -5,6 +5,7 @@
 // launches (rigid_topk_kernel, flex_kernel).  No CPU fallback exists: every
 // score comes from the kernels in kernels.cu.
 #include <cuda_runtime.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <atomic>
@@ -88,6 +89,22 @@ double env_double(const char* name, double dflt) {
 }  // namespace
 
 namespace {
+
+// Host threads for one context: GD_HOST_THREADS, else the CPUs this process
+// may run on divided among the node's ranks (LOCAL_WORLD_SIZE, set by
+// torchrun), so one-process-per-GPU runs do not oversubscribe the host.
+static int host_threads() {
+  if (const char* e = std::getenv("GD_HOST_THREADS")) {
+    const int v = std::atoi(e);
+    if (v > 0) return v;
+  }
+  int cpus = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  cpu_set_t set;
+  if (sched_getaffinity(0, sizeof set, &set) == 0) cpus = std::max(1, CPU_COUNT(&set));
+  int ranks = 1;
+  if (const char* e = std::getenv("LOCAL_WORLD_SIZE")) ranks = std::max(1, std::atoi(e));
+  return std::max(1, cpus / ranks);
+}
 
 // Persistent host workers for ligand preprocessing: run(fn) executes fn on
 // every worker and on the caller and returns when all have finished (fn
@@ -606,10 +623,7 @@ static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
   if (cnt < 64) {
     work();
   } else {
-    if (!ctx->pool) {
-      const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
-      ctx->pool = std::make_unique<WorkerPool>(hw - 1);
-    }
+    if (!ctx->pool) ctx->pool = std::make_unique<WorkerPool>(host_threads() - 1);
     ctx->pool->run(work);
   }
 
