@@ -15,11 +15,14 @@
 namespace gdb200 {
 namespace {
 
+// With the orientation matrix in shared memory (GD_RIGID_RSMEM), one lookup
+// in flight at 6 CTAs per SM (40 registers) beats two at 5 (r2g: c1 rigid
+// 2.91 -> 2.78 ms, c2 19.8 -> 18.1 ms; 7 CTAs spill).
 #ifndef GD_RIGID_MINB
-#define GD_RIGID_MINB 5  // resident CTAs per SM the register budget targets
+#define GD_RIGID_MINB 6  // resident CTAs per SM the register budget targets
 #endif
 #ifndef GD_RIGID_MLP
-#define GD_RIGID_MLP 2   // atoms whose nearest-point lookups are in flight together
+#define GD_RIGID_MLP 1   // atoms whose nearest-point lookups are in flight together
 #endif
 #ifndef GD_RIGID_RSMEM
 #define GD_RIGID_RSMEM 1 // the orientation matrix re-read from shared memory per atom group (c1 rigid 2.96 -> 2.91 ms, c2 20.9 -> 19.9)
