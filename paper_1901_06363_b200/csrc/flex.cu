@@ -196,12 +196,30 @@ __device__ __forceinline__ void bump_item(const WarpMem& s, const DockParams& p,
 // Query phase: lanes over (live candidate, fragment atom), two items per
 // lane per iteration (t, t + 32) so both nearest-point lookups are in flight;
 // candidate c's term of atom i lands in v[c * n + i].
+#ifndef GD_QUERY_MLP
+#define GD_QUERY_MLP 1       // lookups in flight per lane in the query phase (1 or 2; r2h: 1 wins, c1 flex 13.63 -> 12.36 ms)
+#endif
 template <bool On>
 __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& p, const Axis& X,
                                             int n, int nf, unsigned live, int a0, int da, int nb,
                                             int lane, Work<On>& wk) {
   const int tq = nb * nf;
   const float rnf = 1.0f / static_cast<float>(nf);
+#if GD_QUERY_MLP == 1
+  for (int t = lane; t < tq; t += 32) {
+    const int c = qdiv(t, rnf);
+    if (!((live >> c) & 1u)) continue;
+    const int i = s.fidx[t - c * nf];
+    const int ac = a0 + c * da;
+    const double cs = __ldg(p.cos_deg + ac), sn = __ldg(p.sin_deg + ac);
+    double x, y, z;
+    const PT q = s.pt[i];
+    rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
+    wk.add(kRot, 1);
+    s.v[c * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+  }
+  return;
+#endif
   for (int t = lane; t < tq; t += 64) {
     const int c0 = qdiv(t, rnf);
     const int t1 = t + 32 < tq ? t + 32 : t;
