@@ -874,9 +874,11 @@ size_t flex_smem_bytes(const DockParams& p) {
 int flex_batch(const DockParams& p) {
   if (GD_FLEX_BATCH) return GD_FLEX_BATCH;
   const int c = std::max(1, 360 / p.hp - 1);
-  const int batches = (c + 7) / 8;
-  const int b = (c + batches - 1) / batches;
-  return b <= 4 ? 4 : b <= 6 ? 6 : 8;
+  if (c <= 8) return c <= 4 ? 4 : c <= 6 ? 6 : 8;  // one batch
+  // Several batches: at most 6 candidates each (r2h, one lookup per lane:
+  // c2's 35 candidates 59.1 ms in 6-batches vs 60.8 in 8-batches).
+  const int batches = (c + 5) / 6;
+  return (c + batches - 1) / batches <= 4 ? 4 : 6;
 }
 
 int max_smem_optin() {
@@ -963,8 +965,12 @@ int launch_flex(const DockParams& p, void* stream) {
 int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
                     uint8_t* valid, void* stream) {
   if (n_items == 0) return cudaSuccess;
+#ifndef GD_PROFILE_BATCH
+#define GD_PROFILE_BATCH 8
+#endif
   // 359 candidates per fragment: the wide batch.
-  return launch_profiles_b<8>(p, items, n_items, scores, valid, static_cast<cudaStream_t>(stream));
+  return launch_profiles_b<GD_PROFILE_BATCH>(p, items, n_items, scores, valid,
+                                             static_cast<cudaStream_t>(stream));
 }
 
 int launch_finalize(const DockParams& p, void* stream) {
