@@ -37,9 +37,10 @@ namespace gdb200 {
 namespace {
 
 // CTA shape: W chains (warps) per CTA, 24 / W CTAs per SM (the register
-// budget: 65536 / (24 * 32) = 85 registers).  12-chain CTAs for batches of
-// up to 6 candidates (c1: 16.09 ms vs 16.57 with 4), 4-chain CTAs for 8-
-// candidate batches, whose larger v rows fit better (c2: 74.3 vs 75.0 ms).
+// budget: 65536 / (24 * 32) = 85 registers).  8-chain CTAs for batches of
+// up to 6 candidates (r2k: c1 12.28 vs 12.36 ms with 12, c2 flex 58.6 vs
+// 59.1), 4-chain CTAs for 8-candidate batches, whose larger v rows fit
+// better.
 #ifndef GD_FLEX_RESIDENT
 #define GD_FLEX_RESIDENT 24  // warps per SM the register budget targets
 #endif
@@ -68,13 +69,14 @@ namespace {
 #define GD_AXIS_SMEM 1       // the step's rotation axis read from the warp's shared slot
 #endif
 #ifndef GD_META_RELOAD
-#define GD_META_RELOAD 1     // ligand descriptor fields re-read from global when used
+#define GD_META_RELOAD 0     // 1: ligand descriptor fields re-read from global when used (r2b's
+                             // win; after r2h's query change 0 is 0.4% faster)
 #endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
 #ifndef GD_FLEX_WARPS6
-#define GD_FLEX_WARPS6 12    // chains per CTA for batches of up to 6 candidates
+#define GD_FLEX_WARPS6 8    // chains per CTA for batches of up to 6 candidates
 #endif
 template <int B>
 constexpr int warps_for() {
