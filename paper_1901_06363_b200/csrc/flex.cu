@@ -62,6 +62,14 @@ namespace {
 #else
 #define GD_BOUND(cond) ((void)0)
 #endif
+#ifndef GD_PAIRMAJOR_MIN
+#define GD_PAIRMAJOR_MIN 16  // surviving pairs from which bump checks go pair-major (r2l: 16
+                             // beats 32 by 0.3-0.5% on c1/c2; 8 and 1 lose)
+#endif
+#ifndef GD_FOLD_UNROLL
+#define GD_FOLD_UNROLL 4
+#endif
+constexpr int kFoldUnroll = GD_FOLD_UNROLL;
 #ifndef GD_BUMP_SHARE
 #define GD_BUMP_SHARE 1      // pair-major: share found bumps across the warp per pair chunk
 #endif
@@ -255,14 +263,14 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
   ck.mark(kPhDecide);
   const unsigned zero = (a0 == 0) ? 1u : 0u;  // only c = 0 can be angle 0
   unsigned bl = 0;
-  // Pair-major when the pairs fill the warp and the batch is at most 6
-  // candidates (measured: c1 16.57 vs 16.84 ms; at 8 candidates the serial
+  // Pair-major when there are at least GD_PAIRMAJOR_MIN pairs and the batch
+  // is at most 6 candidates (measured: c1 16.57 vs 16.84 ms; at 8 candidates the serial
   // per-lane candidate loop loses, c2 76.3 vs 74.1): lane per surviving pair, the
   // angle-independent part of the moving atom's rotation once, then every
   // candidate angle (cos/sin from the candidate's lane); same expressions as
   // rodrigues, so the same bits.  Fewer pairs: lanes over (candidate, pair)
   // items, so candidates share the warp instead of leaving lanes idle.
-  if (GD_BUMP_PAIRMAJOR && np >= 32 && nb <= 6) {
+  if (GD_BUMP_PAIRMAJOR && np >= GD_PAIRMAJOR_MIN && nb <= 6) {
     const int ac = a0 + min(lane, nb - 1) * da;
     const double cs_l = __ldg(p.cos_deg + ac), sn_l = __ldg(p.sin_deg + ac);
     for (int t0 = 0; t0 < np; t0 += 32) {
@@ -310,7 +318,7 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
   if (lane < nb && ((live >> lane) & 1u)) {
     double sum = pre;
     const double* vc = s.v + lane * n;
-#pragma unroll 4
+#pragma unroll kFoldUnroll
     for (int i = first; i < n; ++i) sum = dadd(sum, vc[i]);
     score = __ddiv_rn(static_cast<double>(n), sum);
     wk.add(kTerms, n);
