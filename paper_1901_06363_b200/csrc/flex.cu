@@ -86,9 +86,12 @@ constexpr int kFoldUnroll = GD_FOLD_UNROLL;
 #ifndef GD_FLEX_WARPS6
 #define GD_FLEX_WARPS6 8    // chains per CTA for batches of up to 6 candidates
 #endif
+#ifndef GD_FLEX_WARPS8
+#define GD_FLEX_WARPS8 4     // chains per CTA for 8-candidate batches
+#endif
 template <int B>
 constexpr int warps_for() {
-  return B == 8 ? 4 : GD_FLEX_WARPS6;
+  return B == 8 ? GD_FLEX_WARPS8 : GD_FLEX_WARPS6;
 }
 constexpr unsigned kFull = 0xffffffffu;
 
