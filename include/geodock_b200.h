@@ -209,6 +209,15 @@ int gd_detect_peaks(const double* scores, const uint8_t* valid, double* delta_ov
 int gd_tile_hit_probability(const int32_t* best_peak_widths, int64_t n, const int32_t* tiles,
                             int32_t n_tiles, double* probability, double* eval_count);
 
+/* Why ligand `ligand` (batch position) of the last gd_upload / gd_dock_batch
+ * was skipped with GD_LIG_INVALID: the reference's Ligand validation text
+ * (molecule.hpp:66-115) with the batch position as the ligand id, e.g.
+ * "ligand '17': duplicate bond", or this path's size limit "ligand '17':
+ * more than 256 atoms is not supported".  Empty for accepted ligands;
+ * GD_LIG_DEGENERATE means the reference's "rotate_fragment: degenerate
+ * rotation axis" (geometry.hpp:168). */
+int gd_ligand_error(const gd_ctx* ctx, int32_t ligand, char* msg, size_t msg_len);
+
 /* Device-resident results of the last gd_dock_resident (valid until the
  * next dock call): [n_ligands*top_k] in final order.  Lets a multi-GPU host
  * gather per-ligand top-K tables over NCCL without a host round trip. */

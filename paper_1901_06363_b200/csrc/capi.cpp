@@ -434,7 +434,7 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
                           cudaMemcpyHostToDevice));
 
   // Two grid levels over the pocket bounding box: a fine near field (voxel
-  // 0.5 A, margin 4 A) and a coarse far field (2 A, margin 32 A); queries
+  // 0.2 A, margin 3 A) and a coarse far field (0.75 A, margin 32 A); queries
   // beyond both fall back to the exact full scan.
   PocketView& v = ctx->view;
   v.pts = ctx->pts.as<double>();
@@ -487,7 +487,7 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     GD_CUDA(ctx, ctx->vox_scan.ensure(static_cast<size_t>(list_offsets_scratch_bytes(nv)) + 64));
     long long* dtot = reinterpret_cast<long long*>(static_cast<unsigned char*>(ctx->vox_scan.ptr) +
                                                    list_offsets_scratch_bytes(nv));
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_list_offsets(counts.as<int32_t>(), nv,
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_list_offsets(counts.as<int32_t>(), nv, n, n,
                                                               doff.as<int32_t>(), ctx->vox_scan.ptr,
                                                               dtot, ctx->stream)));
     long long tot[3];
@@ -498,6 +498,9 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
     GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
     GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
+    // List head: the whole pocket, the list of every overflow voxel.
+    GD_CUDA(ctx, cudaMemcpyAsync(ctx->vox_pts[L].ptr, ctx->pts.ptr, sizeof(double) * 4 * n,
+                                 cudaMemcpyDeviceToDevice, ctx->stream));
     GD_CUDA(ctx, static_cast<cudaError_t>(
                      launch_voxel_fill(ctx->pts.as<double>(), n, g, doff.as<int32_t>(),
                                        ctx->vox_off[L].as<double>(), ctx->vox_pts[L].as<double>(),
@@ -591,7 +594,9 @@ static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
   }
   ctx->errors.assign(L, std::string());
   ctx->status_host.assign(L, 0);
-  ctx->atom_off.assign(b->atom_offsets, b->atom_offsets + L + 1);
+  // An empty batch may pass null offset arrays (nothing is read from them).
+  if (L > 0) ctx->atom_off.assign(b->atom_offsets, b->atom_offsets + L + 1);
+  else ctx->atom_off.assign(1, 0);
   ctx->n_lig = L;
   ctx->total_atoms = A;
   ctx->max_n = 1;
@@ -608,6 +613,8 @@ static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
 static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Running& run,
                        int& chunk_max_n) {
   const int cnt = c1 - c0;
+  chunk_max_n = 1;
+  if (cnt <= 0) return;
   std::vector<PreparedLigand> prep(cnt);
   std::atomic<int> next{0};
   auto work = [&] {
@@ -841,7 +848,8 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockPara
   p.counters = nullptr;
   if (k->flags & GD_FLAG_COUNT_WORK) {
     GD_CUDA(ctx, ctx->counters.ensure(sizeof(unsigned long long) * kCounterSlots));
-    GD_CUDA(ctx, cudaMemset(ctx->counters.ptr, 0, sizeof(unsigned long long) * kCounterSlots));
+    GD_CUDA(ctx, cudaMemsetAsync(ctx->counters.ptr, 0, sizeof(unsigned long long) * kCounterSlots,
+                                 ctx->stream));
     p.counters = ctx->counters.as<unsigned long long>();
   }
   ctx->counted = p.counters != nullptr;
@@ -1278,6 +1286,16 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores,
   if (n_items > 0) {
     cudaEventElapsedTime(&ctx->timing.flex_ms, ctx->ev[2], ctx->ev[3]);
     cudaEventElapsedTime(&ctx->timing.total_ms, ctx->ev[2], ctx->ev[4]);
+  }
+  return GD_OK;
+}
+
+extern "C" int gd_ligand_error(const gd_ctx* ctx, int32_t ligand, char* msg, size_t msg_len) {
+  if (ctx == nullptr || ligand < 0 || ligand >= static_cast<int32_t>(ctx->errors.size()))
+    return GD_ERR_INVALID;
+  if (msg && msg_len) {
+    std::strncpy(msg, ctx->errors[ligand].c_str(), msg_len - 1);
+    msg[msg_len - 1] = 0;
   }
   return GD_OK;
 }

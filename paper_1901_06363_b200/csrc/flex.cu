@@ -49,6 +49,8 @@ namespace {
 #ifndef GD_FLEX_BATCH
 #define GD_FLEX_BATCH 0
 #endif
+static_assert(GD_FLEX_BATCH == 0 || GD_FLEX_BATCH == 4 || GD_FLEX_BATCH == 6 || GD_FLEX_BATCH == 8,
+              "instantiated batch sizes: 4, 6, 8");
 #ifndef GD_BUMP_PAIRMAJOR
 #define GD_BUMP_PAIRMAJOR 1  // bump checks pair-major (0: (candidate, pair) items)
 #endif
@@ -543,6 +545,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
 template <bool On, int B, int kWarps = warps_for<B>()>
 __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     flex_chain_kernel(DockParams p) {
+  static_assert(B >= 1 && B <= 8, "batch_max reduces over an 8-lane butterfly");
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.k_slots;
@@ -759,6 +762,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
 template <bool On, int B, int kWarps = warps_for<B>()>
 __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     profile_kernel(DockParams p, const int32_t* items, int n_items, double* scores, uint8_t* valid) {
+  static_assert(B >= 1 && B <= 8, "batch_max reduces over an 8-lane butterfly");
   extern __shared__ __align__(16) unsigned char smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kWarps + warp;
@@ -968,9 +972,6 @@ int launch_flex(const DockParams& p, void* stream) {
   switch (flex_batch(p)) {
     case 8: return launch_flex_b<8>(p, chains, s);
     case 6: return launch_flex_b<6>(p, chains, s);
-#if GD_FLEX_BATCH == 12
-    case 12: return launch_flex_b<12>(p, chains, s);  // A/B builds
-#endif
     default: return launch_flex_b<4>(p, chains, s);
   }
 }

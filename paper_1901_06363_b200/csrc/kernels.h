@@ -136,10 +136,10 @@ struct VoxelGrid {
   double lo_x, lo_y, lo_z, h;
   int32_t dim_x, dim_y, dim_z;
 };
-// counts[v] = candidates of voxel v (>= 1); the fill pass writes each
-// voxel's record and its candidates past the inline ones at the
-// host-scanned list offsets (sum over earlier voxels of
-// max(count - kVoxInline, 0)).
+// counts[v] = candidates of voxel v (>= 1), or -1 when more than 1,024
+// survive (the voxel then scans the whole pocket, held once at the head of
+// the list array); the fill pass writes each voxel's record and its
+// candidates past the inline ones at the device-scanned list offsets.
 // tbox [nt][6] (lo xyz, hi xyz; fp32, outward-rounded) are the bounding
 // boxes of the Morton-ordered points' 32-point tiles: with nt > 0 the build
 // culls tiles per 4x4x8 voxel brick (pocket_index.cu); nt = 0 scans all.
@@ -150,11 +150,12 @@ int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, c
 int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
                       double* lst, const float* tbox, int nt, const int32_t* counts,
                       const int32_t* keep, void* stream);
-// offsets[v] = exclusive prefix of max(counts - kVoxInline, 0) over voxels;
-// totals[3] (device) = {listed entries, candidates, max count}; `scratch`
-// holds list_offsets_scratch_bytes(nv).
+// offsets[v] = base + exclusive prefix of max(counts - kVoxInline, 0) over
+// voxels (the first `base` = P list records hold the whole pocket for
+// overflow voxels); totals[3] (device) = {listed entries incl. base,
+// candidates, max count}; `scratch` holds list_offsets_scratch_bytes(nv).
 int list_offsets_scratch_bytes(int nv);
-int launch_list_offsets(const int32_t* counts, int nv, int32_t* offsets, void* scratch,
-                        long long* totals, void* stream);
+int launch_list_offsets(const int32_t* counts, int nv, int P, long long base, int32_t* offsets,
+                        void* scratch, long long* totals, void* stream);
 
 }  // namespace gdb200

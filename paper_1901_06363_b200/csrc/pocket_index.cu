@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_count_kernel(const double
     const int k = voxel_list_culled(pts, P, g, blockIdx.x, ix, iy, iz, in, cand, tile, tbox, nt, sc);
     if (in) {
       const int v = (ix * g.dim_y + iy) * g.dim_z + iz;
-      counts[v] = k < 0 ? P : k;
+      counts[v] = k;  // -1: overflow (the voxel scans the whole pocket, see fill)
       if (keep != nullptr)
         for (int a = 0; a < min(max(k, 0), kKeep); ++a) keep[kKeep * static_cast<size_t>(v) + a] = cand[a];
     }
@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_count_kernel(const double
   const int v = blockIdx.x * blockDim.x + threadIdx.x;
   const int nv = g.dim_x * g.dim_y * g.dim_z;
   const int k = voxel_list(pts, P, g, min(v, nv - 1), v < nv, cand, tile);
-  if (v < nv) counts[v] = k < 0 ? P : k;  // overflow: keep every point (exact, rare)
+  if (v < nv) counts[v] = k;  // -1: overflow (the voxel scans the whole pocket, see fill)
 }
 
 __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double* pts, int P,
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double*
     const bool in = brick_voxel(g, blockIdx.x, ix, iy, iz);
     v = in ? (ix * g.dim_y + iy) * g.dim_z + iz : 0;
     const int c = in ? counts[v] : 0;
-    if (keep != nullptr && !__syncthreads_or(c > kKeep)) {  // uniform: copy the kept lists
+    if (keep != nullptr && !__syncthreads_or(c > kKeep || c < 0)) {  // uniform: copy the kept lists
       if (!in) return;
       k = c;
       for (int a = 0; a < k; ++a) cand[a] = keep[kKeep * static_cast<size_t>(v) + a];
@@ -397,8 +397,13 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double*
     k = voxel_list(pts, P, g, min(v, nv - 1), v < nv, cand, tile);
     if (v >= nv) return;
   }
+  // Overflow (more than kVoxMaxCand survivors, e.g. inside a hollow shell
+  // pocket where no surface point dominates another): the voxel's list is
+  // the whole pocket, which the list array holds once at its head (records
+  // [0, P), copied by the host), so the record is {start 1, count P, point
+  // 0 inline} and costs no list memory.
   const int len = k < 0 ? P : k;  // >= 1: the nearest point always survives
-  const int start = offsets[v];
+  const int start = k < 0 ? 1 : offsets[v];
   double* r = rec + kRecDoubles * static_cast<size_t>(v);
   reinterpret_cast<int2*>(r)[0] = make_int2(start, len);
   for (int q = 0; q < kVoxInline; ++q) {
@@ -407,9 +412,10 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double*
     for (int c = 0; c < 3; ++c) r[1 + 3 * q + c] = pts[4 * j + c];
   }
   if (kRecDoubles == 8) r[7] = 0.0;
+  if (k < 0) return;
   double* out = lst + 4 * static_cast<size_t>(start);
   for (int a = kVoxInline; a < len; ++a) {
-    const int j = k < 0 ? a : cand[a];
+    const int j = cand[a];
     for (int c = 0; c < 4; ++c) out[4 * (a - kVoxInline) + c] = pts[4 * j + c];
   }
 }
@@ -432,17 +438,18 @@ __device__ __forceinline__ long long block_sum_ll(long long x, long long* red) {
   return t;
 }
 
-__global__ void __launch_bounds__(kScanBlock) list_block_sums(const int32_t* counts, int nv,
+__global__ void __launch_bounds__(kScanBlock) list_block_sums(const int32_t* counts, int nv, int P,
                                                               long long* bsum, long long* bcand,
                                                               int* bmax) {
   __shared__ long long red[kScanBlock / 32];
   __shared__ int mx;
   const int v = blockIdx.x * kScanBlock + threadIdx.x;
-  const int c = v < nv ? counts[v] : 0;
+  const int raw = v < nv ? counts[v] : 0;
+  const int c = raw < 0 ? P : raw;  // overflow voxels list the shared whole-pocket head
   if (threadIdx.x == 0) mx = 0;
   __syncthreads();
   atomicMax(&mx, c);
-  const long long l = block_sum_ll(max(c - kVoxInline, 0), red);
+  const long long l = block_sum_ll(max(raw - kVoxInline, 0), red);
   const long long t = block_sum_ll(c, red);
   if (threadIdx.x == 0) {
     bsum[blockIdx.x] = l;
@@ -453,7 +460,7 @@ __global__ void __launch_bounds__(kScanBlock) list_block_sums(const int32_t* cou
 
 // One block: exclusive scan of the block sums in place, and the totals.
 __global__ void __launch_bounds__(kScanBlock) list_scan_sums(long long* bsum, const long long* bcand,
-                                                             const int* bmax, int nb,
+                                                             const int* bmax, int nb, long long base,
                                                              long long* totals) {
   __shared__ long long part[kScanBlock];
   __shared__ long long red[kScanBlock / 32];
@@ -477,14 +484,14 @@ __global__ void __launch_bounds__(kScanBlock) list_scan_sums(long long* bsum, co
     part[threadIdx.x] += y;
     __syncthreads();
   }
-  long long run = part[threadIdx.x] - s;  // exclusive base of this thread's run
+  long long run = base + part[threadIdx.x] - s;  // exclusive base of this thread's run
   for (int b = b0; b < min(nb, b0 + per); ++b) {
     const long long x = bsum[b];
     bsum[b] = run;
     run += x;
   }
   const long long tc = block_sum_ll(cand, red);
-  if (threadIdx.x == kScanBlock - 1) totals[0] = part[kScanBlock - 1];
+  if (threadIdx.x == kScanBlock - 1) totals[0] = base + part[kScanBlock - 1];
   if (threadIdx.x == 0) {
     totals[1] = tc;
     totals[2] = mx;
@@ -602,15 +609,15 @@ int list_offsets_scratch_bytes(int nv) {
   return 3 * 8 * nb + 64;
 }
 
-int launch_list_offsets(const int32_t* counts, int nv, int32_t* offsets, void* scratch,
-                        long long* totals, void* stream) {
+int launch_list_offsets(const int32_t* counts, int nv, int P, long long base, int32_t* offsets,
+                        void* scratch, long long* totals, void* stream) {
   const int nb = (nv + kScanBlock - 1) / kScanBlock;
   auto* bsum = static_cast<long long*>(scratch);
   long long* bcand = bsum + nb;
   int* bmax = reinterpret_cast<int*>(bcand + nb);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  list_block_sums<<<nb, kScanBlock, 0, st>>>(counts, nv, bsum, bcand, bmax);
-  list_scan_sums<<<1, kScanBlock, 0, st>>>(bsum, bcand, bmax, nb, totals);
+  list_block_sums<<<nb, kScanBlock, 0, st>>>(counts, nv, P, bsum, bcand, bmax);
+  list_scan_sums<<<1, kScanBlock, 0, st>>>(bsum, bcand, bmax, nb, base, totals);
   list_apply<<<nb, kScanBlock, 0, st>>>(counts, nv, bsum, offsets);
   return cudaGetLastError();
 }

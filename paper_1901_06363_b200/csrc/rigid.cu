@@ -177,8 +177,8 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_top32_kernel(DockPara
     if (half > 1) __syncthreads();
   }
   if (warp == 0 && lane < K) {
-    p.seed_slot[l * p.top_k + lane] = list.i;
-    p.seed_score[l * p.top_k + lane] = list.k;
+    p.seed_slot[static_cast<size_t>(l) * p.top_k + lane] = list.i;
+    p.seed_score[static_cast<size_t>(l) * p.top_k + lane] = list.k;
   }
   if (threadIdx.x == 0) p.k_eff[l] = K;
   publish(wk, p.counters, 0);
@@ -290,8 +290,8 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_topk_kernel(DockParam
     ns = ts;
   }
   for (int r = threadIdx.x; r < K; r += BT) {
-    p.seed_slot[l * p.top_k + r] = ls[r];
-    p.seed_score[l * p.top_k + r] = lk[r];
+    p.seed_slot[static_cast<size_t>(l) * p.top_k + r] = ls[r];
+    p.seed_score[static_cast<size_t>(l) * p.top_k + r] = lk[r];
   }
   if (threadIdx.x == 0) p.k_eff[l] = K;
   publish(wk, p.counters, 0);

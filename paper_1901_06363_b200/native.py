@@ -114,6 +114,7 @@ SIGNATURES = {
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.c_int64]),
     "gd_device_results": (C.c_int, [C.c_void_p, C.POINTER(gd_device_result)]),
+    "gd_ligand_error": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t]),
     "gd_fp64_peak": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "gd_overlap_score_batch": (C.c_int, [C.c_void_p, _f64p, C.c_int32, C.c_int32, C.c_uint32,
                                          _f64p]),

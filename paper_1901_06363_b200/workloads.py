@@ -82,3 +82,9 @@ def pocket_of(w: Workload, p: int) -> np.ndarray:
     """Pocket p of a multi-pocket workload (configs 3/4)."""
     a, b, c = w.pockets[p] if w.pockets else w.pocket_axes
     return synth_pocket(a, b, c, w.spacing, w.rough_max, w.seed + 1000 + p)
+
+
+def synth_pocket_unrough(w: Workload, p: int) -> np.ndarray:
+    """Pocket p before its roughness mask (to report the removed fraction)."""
+    a, b, c = w.pockets[p] if w.pockets else w.pocket_axes
+    return synth_pocket(a, b, c, w.spacing, 0.0, w.seed + 1000 + p)

@@ -1,0 +1,133 @@
+"""Parity at every BASELINE configuration's own scale (north_star: "for every
+config, the selected pose indices and ordering of each ligand's top-K match
+the CPU oracle exactly").
+
+The checker is the reference itself: its headers compiled from
+/root/reference into oracle/_ref (PocketIndex, fp64, 16 host threads),
+driven through oracle/ref_harness.cpp's rigid sweep + top-K + restart
+chains of the reference match_probes_shape (kernel.hpp:205-248).  Where
+oracle/_ref is absent the plain-C restatement stands in.
+
+* c2: 200 ligands at rigid 10, fragment 10, 3 restarts, K = 100 (22,104
+  orientations through the rank-merge top-K, 35-candidate fragment
+  searches in 6-batches).
+* c3: all 16 pockets (1 A lattice, semi-axes U(5,12) A, roughness mask)
+  x 64 ligands each; the smallest, largest and roughest pockets are named
+  in the test ids.
+* c4: every one of the 180 knob points (rigid {10,15,20,30,45} x fragment
+  {10,20,30,60} x restarts {1,2,3} x K {10,30,100}) on 4 ligands, the
+  points spread over c4's four pockets.
+
+Bar: bit-exact top-K orientation indices, order, seed ranks, rigid and
+final scores, evaluation and feasibility-check counters and final poses.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+from paper_1901_06363_b200 import Knobs, workloads as W
+from gd_test_helpers import assert_same_result
+
+pytestmark = pytest.mark.gpu
+
+
+def _cpu(batch, pocket, knobs, poses=True):
+    from oracle import oracle_py as O
+    impl = "ref" if O.have_ref() else "oracle"
+    return O.dock_batch(batch, pocket, knobs, nthreads=O.threads(), keep_poses=poses, impl=impl)
+
+
+def test_config2_200_ligands(docker):
+    w = W.config(2)
+    pocket = w.pocket()
+    batch = w.ligands(range(200))
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, w.knobs, keep_poses=True)
+    assert (got.status == 0).all() and (got.k_eff == 100).all()
+    want = _cpu(batch, pocket, w.knobs)
+    assert_same_result(got, want, ctx="c2 x200: ")
+
+
+def _c3_pockets():
+    w = W.config(3)
+    pockets = [W.pocket_of(w, p) for p in range(16)]
+    full = [len(W.synth_pocket_unrough(w, p)) for p in range(16)]
+    rough = [1.0 - len(pk) / f for pk, f in zip(pockets, full)]
+    sizes = [len(pk) for pk in pockets]
+    tags = {}
+    tags[int(np.argmin(sizes))] = "smallest"
+    tags[int(np.argmax(sizes))] = "largest"
+    tags[int(np.argmax(rough))] = tags.get(int(np.argmax(rough)), "") + "roughest"
+    ids = [f"p{p}-P{sizes[p]}-rough{100 * rough[p]:.0f}pct" + (f"-{tags[p]}" if p in tags else "")
+           for p in range(16)]
+    return w, pockets, ids
+
+
+_C3 = None
+
+
+def _c3():
+    global _C3
+    if _C3 is None:
+        _C3 = _c3_pockets()
+    return _C3
+
+
+@pytest.mark.parametrize("p", range(16), ids=lambda p: f"pocket{p}")
+def test_config3_every_pocket(docker, p):
+    w, pockets, ids = _c3()
+    pocket = pockets[p]
+    batch = w.ligands(range(64 * p, 64 * p + 64), pocket.mean(axis=0))
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, w.knobs, keep_poses=True)
+    assert (got.status == 0).all()
+    want = _cpu(batch, pocket, w.knobs)
+    assert_same_result(got, want, ctx=f"c3 {ids[p]}: ")
+
+
+C4_GRID = list(itertools.product([10, 15, 20, 30, 45], [10, 20, 30, 60], [1, 2, 3], [10, 30, 100]))
+
+
+def test_config4_grid_is_complete():
+    assert len(C4_GRID) == 180
+
+
+@pytest.mark.parametrize("point", range(len(C4_GRID)),
+                         ids=lambda i: "r{}-f{}-x{}-k{}".format(*C4_GRID[i]))
+def test_config4_every_knob_point(docker, point):
+    w = W.config(4)
+    g = C4_GRID[point]
+    pocket = W.pocket_of(w, point % 4)
+    batch = w.ligands(range(4 * point, 4 * point + 4), pocket.mean(axis=0))
+    knobs = Knobs.baseline(*g)
+    docker.set_pocket(pocket)
+    got = docker.dock(batch, knobs, keep_poses=True)
+    assert (got.status == 0).all()
+    want = _cpu(batch, pocket, knobs)
+    assert_same_result(got, want, ctx=f"c4 {g}: ")
+
+
+def test_hollow_shell_pocket_overflow_voxels(docker):
+    """A hollow spherical shell: from the centre no surface point dominates
+    another, so interior voxels keep more than 1,024 candidates.  Those
+    voxels scan the whole pocket (held once at the head of the list array)
+    instead of listing it per voxel; minima stay exact and the index stays
+    small."""
+    g = np.mgrid[-12:13, -12:13, -12:13].reshape(3, -1).T.astype(np.float64)
+    r = np.linalg.norm(g, axis=1)
+    shell = g[(r >= 10.5) & (r < 11.5)]
+    assert len(shell) > 1024
+    docker.set_pocket(shell)
+    info = docker.pocket_info()
+    # Without the shared head every overflow voxel would list the whole shell.
+    assert info["max_candidates"] == len(shell)
+    rng = np.random.default_rng(7)
+    poses = rng.uniform(-13.0, 13.0, size=(512, 24, 3))
+    poses[:128] *= 0.05  # deep inside: the overflow voxels
+    a = docker.overlap_scores(poses)
+    b = docker.overlap_scores(poses, brute=True)
+    assert np.array_equal(a, b)
+    from oracle import oracle_py as O
+    want = np.array([O.overlap_score(q, shell) for q in poses[:64]])
+    assert np.array_equal(a[:64], want)
