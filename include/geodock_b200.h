@@ -121,7 +121,9 @@ const char* gd_version(void);
 /* Stages the pocket in HBM and builds the exact voxel nearest-point index.
  * Replaces geodock::Pocket(id, points) validation (molecule.hpp:152-157)
  * and PocketIndex(pocket) (geometry.hpp:49-65).  Also fixes the rigid-sweep
- * centre c = (sum_j P_j)/P, summed in index order (E1). */
+ * centre c = (sum_j P_j)/P, summed in index order (E1).  The
+ * context caches the last GD_POCKET_CACHE (env, default 16) pockets by
+ * their coordinates: re-staging one of them is a lookup, not a rebuild. */
 int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n_points);
 /* Centre and index statistics of the staged pocket. */
 int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[3], double* voxel,
@@ -144,6 +146,41 @@ int gd_upload(gd_ctx* ctx, const gd_ligand_batch* batch);
 int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs);
 int gd_download(gd_ctx* ctx, gd_result* result);
 int gd_last_timing(const gd_ctx* ctx, gd_timing* out);
+
+/* ---- multi-device dispatch ------------------------------------------------- */
+/* One process driving several GPUs: a gd_ctx, a host thread and its streams
+ * per device.  gd_multi_dock_batch cuts the batch into chunks of equal
+ * estimated cost (n (N_orient + K reps (1 + 2R 360/hp)) per ligand, about
+ * four per device) that the device threads pull from a shared cursor --
+ * the reference screen's work queue (screening.hpp:96-178) with GPUs as the
+ * workers -- and writes every chunk's results into the caller's arrays at
+ * the chunk's global offsets.  Results are bit-identical to gd_dock_batch
+ * on one context, for any device count.  The same device may be listed
+ * twice (two contexts on one GPU).  Host preprocessing threads are shared
+ * out: each context gets host CPUs / devices. */
+typedef struct gd_multi gd_multi;
+typedef struct {
+  int64_t ligands;  /* ligands docked by this device in the last call */
+  int64_t chunks;   /* chunks it pulled */
+  float busy_ms;    /* host wall time inside its gd_dock_batch calls */
+} gd_multi_stats;
+/* devices[n_devices] (CUDA ordinals), or devices == NULL: the first
+ * n_devices visible GPUs (n_devices <= 0: all of them). */
+int gd_multi_create(const int32_t* devices, int32_t n_devices, gd_multi** out);
+int gd_multi_destroy(gd_multi* m);
+const char* gd_multi_last_error(const gd_multi* m);  /* NULL m: gd_multi_create's */
+int32_t gd_multi_size(const gd_multi* m);
+/* Context i (for the fine-grained and diagnostic entry points); owned by m. */
+gd_ctx* gd_multi_context(gd_multi* m, int32_t i);
+/* gd_set_pocket on every device, in parallel. */
+int gd_multi_set_pocket(gd_multi* m, const double* xyz, int32_t n_points);
+/* gd_dock_batch over every device (same arguments and result layout). */
+int gd_multi_dock_batch(gd_multi* m, const gd_ligand_batch* batch, const gd_knobs* knobs,
+                        gd_result* result);
+/* gd_ligand_error for the last gd_multi_dock_batch, by batch position. */
+int gd_multi_ligand_error(const gd_multi* m, int32_t ligand, char* msg, size_t msg_len);
+/* Per-device statistics of the last gd_multi_dock_batch: out[min(cap, size)]. */
+int gd_multi_last_stats(const gd_multi* m, gd_multi_stats* out, int32_t cap);
 
 /* ---- planner (host) ------------------------------------------------------ */
 /* The seven interaction features (perf_model.hpp:36-47) of one dataset
@@ -257,6 +294,60 @@ int gd_l2_gather_peak(gd_ctx* ctx, double* gbs);
  * each, xyz pose-major [n_poses*n_atoms*3]. */
 int gd_overlap_score_batch(gd_ctx* ctx, const double* xyz, int32_t n_atoms, int32_t n_poses,
                            uint32_t flags, double* out_scores);
+
+/* One caller-given fragment per ligand of a batch (reference Fragment,
+ * molecule.hpp:177-185): membership[atom_offsets[l] + i] = 1 when atom i of
+ * ligand l is in its fragment (Fragment::membership; the fragment's atoms
+ * are the set members in ascending order, Fragment::atom_indices), and the
+ * rotation axis runs from axis_atom[l] (the bond endpoint inside the
+ * fragment) to anchor_atom[l] (the endpoint on the other side). */
+typedef struct {
+  const uint8_t* membership; /* [total_atoms] */
+  const int32_t* axis_atom;  /* [n_ligands] ligand-local atom index */
+  const int32_t* anchor_atom;/* [n_ligands] ligand-local atom index */
+} gd_fragment_set;
+
+/* The fine-grained entry points below stage `batch` (replacing any staged
+ * batch: gd_rotation_profiles needs a fresh gd_upload afterwards), validate
+ * and preprocess every ligand as the batch path does, and run one warp per
+ * ligand on that ligand's pose (batch xyz) and fragment.  Per-ligand
+ * outcomes land in status[L] (GD_LIG_OK, GD_LIG_INVALID with the text in
+ * gd_ligand_error, GD_LIG_DEGENERATE for "rotate_fragment: degenerate
+ * rotation axis", geometry.hpp:168).  A fragment with an axis/anchor atom
+ * out of range, axis == anchor, or holding no atom or every atom fails the
+ * call with GD_ERR_INVALID. */
+
+/* optimize_fragment_flat (kernel.hpp:125-143; refined == 0, `step` must
+ * divide 360: "optimize_fragment_flat: step must divide 360") or
+ * optimize_fragment_refined (kernel.hpp:150-198; refined != 0, step = the
+ * high-precision step, "optimize_fragment_refined: step must divide 360")
+ * of each ligand's fragment against the staged pocket.  entry_score
+ * (nullable [L]; NaN = not given) is the refined search's optional entry
+ * score.  Out [L]: FragmentSearchResult {best_angle, best_score} and the
+ * SearchCounters {evaluations, feasibility_checks} (kernel.hpp:77-85);
+ * out_pose [total_atoms*3]: the pose committed to the best angle
+ * (commit_angle, kernel.hpp:115-117).  Bit-identical to the reference. */
+int gd_optimize_fragment_batch(gd_ctx* ctx, const gd_ligand_batch* batch,
+                               const gd_fragment_set* fragments, int32_t step, int32_t refined,
+                               const double* entry_score, int32_t* best_angle, double* best_score,
+                               int64_t* evaluations, int64_t* feasibility_checks,
+                               double* out_pose, int32_t* status);
+
+/* rotate_fragment_into / rotate_fragment (geometry.hpp:161-193): each
+ * ligand's pose with its fragment rotated by angles_deg[l] degrees (any
+ * double; cos/sin from the host libm exactly as the reference evaluates
+ * them; angle 0 is an exact copy) into out_pose [total_atoms*3].  Needs no
+ * pocket. */
+int gd_rotate_fragment_batch(gd_ctx* ctx, const gd_ligand_batch* batch,
+                             const gd_fragment_set* fragments, const double* angles_deg,
+                             double* out_pose, int32_t* status);
+
+/* check_bumps (geometry.hpp:199-213) of each ligand's pose against its
+ * fragment: feasible[l] = 0 iff a fragment atom i and a non-fragment atom j
+ * at capped graph distance >= 4 sit closer than 0.8 (r_i + r_j).  Needs no
+ * pocket. */
+int gd_check_bumps_batch(gd_ctx* ctx, const gd_ligand_batch* batch,
+                         const gd_fragment_set* fragments, uint8_t* feasible, int32_t* status);
 
 /* ---- host helpers (no device work) --------------------------------------- */
 /* optimal_tile_size (kernel.hpp:62-75); returns -1 when step < 1. */

@@ -193,6 +193,34 @@ def optimize_fragment(xyz, radii, bonds, rot, pocket, f: int, step: int, refined
     return ang.value, sc.value, ev.value, ck.value, out
 
 
+def ref_optimize_fragment(xyz, radii, bonds, rot, pocket, f: int, step: int,
+                          refined: bool = False, pose=None, entry_score=None):
+    """The reference's optimize_fragment_flat / _refined (kernel.hpp:125-198)
+    on fragment f: (best_angle, best_score, evals, checks, committed pose)."""
+    h = ref()
+    h.gdref_optimize_fragment.argtypes = [C.c_int, _f64p, _f64p, C.c_int, _i32p, _u8p, _f64p,
+                                          C.c_int, _f64p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_double, _f64p, C.POINTER(C.c_int), _f64p, _i64p,
+                                          _i64p]
+    x = np.ascontiguousarray(xyz, dtype=np.float64)
+    r = np.ascontiguousarray(radii, dtype=np.float64)
+    b = np.ascontiguousarray(bonds, dtype=np.int32).reshape(-1, 2)
+    ro = np.ascontiguousarray(rot, dtype=np.uint8)
+    pk = np.ascontiguousarray(pocket, dtype=np.float64)
+    p = x if pose is None else np.ascontiguousarray(pose, dtype=np.float64)
+    out = np.zeros_like(x)
+    ang, sc, ev, ck = C.c_int(), C.c_double(), C.c_longlong(), C.c_longlong()
+    rc = h.gdref_optimize_fragment(len(x), _p(x, _f64p), _p(r, _f64p), len(b), _p(b, _i32p),
+                                   _p(ro, _u8p), _p(pk, _f64p), len(pk), _p(p, _f64p), f,
+                                   int(refined), step, int(entry_score is not None),
+                                   0.0 if entry_score is None else float(entry_score),
+                                   _p(out, _f64p), C.byref(ang), C.byref(sc), C.byref(ev),
+                                   C.byref(ck))
+    if rc:
+        raise RuntimeError(h.gdref_last_error().decode())
+    return ang.value, sc.value, ev.value, ck.value, out
+
+
 def rotate_fragment(xyz, radii, bonds, rot, pose, f: int, angle: float, impl: str = "oracle"):
     """(rotated pose, feasible) for fragment f (rotamer f//2; left if f even)."""
     x = np.ascontiguousarray(xyz, dtype=np.float64)

@@ -143,6 +143,46 @@ extern "C" int gdref_rotate_fragment(int n, const double* xyz, const double* rad
   }
 }
 
+// optimize_fragment_flat / optimize_fragment_refined (kernel.hpp:125-198)
+// on fragment f (rotamer f/2, left if even) from `pose`, with the
+// reference's SearchCounters and optional entry score (has_entry).
+extern "C" int gdref_optimize_fragment(int n, const double* xyz, const double* radii, int nb,
+                                       const int32_t* bonds, const uint8_t* rot,
+                                       const double* pocket, int P, const double* pose, int f,
+                                       int refined, int step, int has_entry, double entry_score,
+                                       double* pose_out, int* best_angle, double* best_score,
+                                       long long* evals, long long* checks) {
+  try {
+    const geodock::Ligand lig = make_ligand("L", n, xyz, radii, nb, bonds, rot);
+    const geodock::Pocket pk = make_pocket(pocket, P);
+    const auto rots = geodock::find_rotamers(lig);
+    if (f < 0 || f >= 2 * static_cast<int>(rots.size())) throw geodock::Error("no such fragment");
+    const auto frags = geodock::grow_fragments(lig, rots[f / 2]);
+    const geodock::Fragment& fr = (f % 2 == 0) ? frags.first : frags.second;
+    geodock::Pose p;
+    for (int i = 0; i < n; ++i) p.positions.push_back({pose[3 * i], pose[3 * i + 1], pose[3 * i + 2]});
+    geodock::SearchCounters c;
+    const geodock::FragmentSearchResult r =
+        refined ? geodock::optimize_fragment_refined(
+                      p, lig, fr, pk, step, &c,
+                      has_entry ? std::optional<double>(entry_score) : std::nullopt)
+                : geodock::optimize_fragment_flat(p, lig, fr, pk, step, &c);
+    for (int i = 0; i < n; ++i) {
+      pose_out[3 * i] = p.positions[i].x;
+      pose_out[3 * i + 1] = p.positions[i].y;
+      pose_out[3 * i + 2] = p.positions[i].z;
+    }
+    *best_angle = r.best_angle;
+    *best_score = r.best_score;
+    *evals = c.evaluations;
+    *checks = c.feasibility_checks;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
 // Reference generator (synthetic.hpp:71-188) for fixture datasets, sizes
 // first: call with null outputs to get counts.
 extern "C" int gdref_generate_synthetic(int count, uint64_t seed, int atom_lo, int atom_hi,

@@ -14,6 +14,7 @@ from .native import (  # noqa: F401
     GeoDockError,
     Knobs,
     LigandBatch,
+    MultiDocker,
     optimal_tile_size,
     orientations,
     synth_ligands,

@@ -163,8 +163,27 @@ class WorkerPool {
 
 }  // namespace
 
+// One staged pocket: its points (Morton order) and exact voxel index in
+// HBM, plus the host copy that identifies it.  A context keeps up to
+// GD_POCKET_CACHE (default 16) of them, so screens that alternate pockets
+// (config 3's 16 pockets, the drop-in's Pocket objects) re-stage a pocket
+// by lookup instead of rebuilding its index.
+struct PocketSlot {
+  std::vector<double> host;  // caller's xyz, the identity key
+  uint64_t hash = 0;
+  uint64_t last_use = 0;
+  int32_t P = 0;
+  double centre[3] = {0, 0, 0};
+  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels];
+  VoxelGrid grid[kGridLevels] = {};
+  int64_t n_cand = 0;
+  int32_t max_cand = 0;
+  PocketView view{};
+};
+
 struct gd_ctx {
   int device = 0;
+  int pool_threads = 0;  // host preprocessing threads (0: host_threads())
   cudaStream_t own_stream = nullptr;
   std::vector<cudaStream_t> aux_streams;  // further streams of the pipelined gd_dock_batch
   cudaStream_t stream = nullptr;
@@ -173,15 +192,17 @@ struct gd_ctx {
   std::vector<cudaEvent_t> chunk_ev;       // one per pipelined chunk (no timing)
   std::unique_ptr<WorkerPool> pool;        // host preprocessing workers
 
-  // Pocket.
+  // Pocket: the active slot and its mirrors (P == 0: none staged), the
+  // slot cache, and the index build's scratch.
+  std::vector<std::unique_ptr<PocketSlot>> slots;
+  uint64_t use_clock = 0;
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, tiles, vox_off[kGridLevels], vox_pts[kGridLevels], vox_counts, vox_doff, vox_keep,
-      vox_scan;
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
   PocketView view{};
+  DevBuf tiles, vox_counts, vox_doff, vox_keep, vox_scan;
 
   DevBuf cos_t, sin_t;
   int orient_step = -1;
@@ -365,6 +386,42 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   for (int32_t j = 0; j < 3 * n; ++j)
     if (!std::isfinite(xyz[j])) return ctx->fail(GD_ERR_INVALID, "pocket: non-finite point");
   GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  // Cache lookup: FNV-1a of the coordinate bytes, confirmed by comparison.
+  uint64_t hash = 1469598103934665603ull;
+  {
+    const unsigned char* b = reinterpret_cast<const unsigned char*>(xyz);
+    for (size_t i = 0; i < sizeof(double) * 3 * static_cast<size_t>(n); ++i)
+      hash = (hash ^ b[i]) * 1099511628211ull;
+  }
+  auto activate = [ctx](PocketSlot& sl) {
+    sl.last_use = ++ctx->use_clock;
+    ctx->P = sl.P;
+    for (int k = 0; k < 3; ++k) ctx->centre[k] = sl.centre[k];
+    for (int L = 0; L < kGridLevels; ++L) ctx->grid[L] = sl.grid[L];
+    ctx->n_cand = sl.n_cand;
+    ctx->max_cand = sl.max_cand;
+    ctx->view = sl.view;
+  };
+  for (auto& sl : ctx->slots)
+    if (sl->P == n && sl->hash == hash &&
+        std::memcmp(sl->host.data(), xyz, sizeof(double) * 3 * static_cast<size_t>(n)) == 0) {
+      activate(*sl);
+      return GD_OK;
+    }
+  static const size_t kCache = static_cast<size_t>(std::max(1.0, env_double("GD_POCKET_CACHE", 16)));
+  PocketSlot* slot = nullptr;
+  if (ctx->slots.size() < kCache) {
+    ctx->slots.push_back(std::make_unique<PocketSlot>());
+    slot = ctx->slots.back().get();
+  } else {  // least recently used
+    slot = std::min_element(ctx->slots.begin(), ctx->slots.end(), [](const auto& a, const auto& b) {
+             return a->last_use < b->last_use;
+           })->get();
+  }
+  slot->P = 0;  // invalid until the build completes
+  slot->hash = hash;
+  slot->host.assign(xyz, xyz + 3 * static_cast<size_t>(n));
+  ctx->P = 0;
   // E1: centre = (sum_j P_j) / P, summed in index order.
   double sx = 0.0, sy = 0.0, sz = 0.0, lo[3], hi[3];
   for (int k = 0; k < 3; ++k) lo[k] = hi[k] = xyz[k];
@@ -377,10 +434,9 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
       hi[k] = std::max(hi[k], xyz[3 * j + k]);
     }
   }
-  ctx->centre[0] = sx / n;
-  ctx->centre[1] = sy / n;
-  ctx->centre[2] = sz / n;
-  ctx->P = n;
+  slot->centre[0] = sx / n;
+  slot->centre[1] = sy / n;
+  slot->centre[2] = sz / n;
 
   // Device copy of the points in Morton order (10 bits per axis over the
   // bounding box): every use is a minimum over points, so the order is
@@ -407,8 +463,8 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   std::vector<double> padded(4 * static_cast<size_t>(n), 0.0);
   for (int32_t q = 0; q < n; ++q)
     for (int k = 0; k < 3; ++k) padded[4 * q + k] = xyz[3 * key[q].second + k];
-  GD_CUDA(ctx, ctx->pts.ensure(padded.size() * sizeof(double)));
-  GD_CUDA(ctx, cudaMemcpy(ctx->pts.ptr, padded.data(), padded.size() * sizeof(double),
+  GD_CUDA(ctx, slot->pts.ensure(padded.size() * sizeof(double)));
+  GD_CUDA(ctx, cudaMemcpy(slot->pts.ptr, padded.data(), padded.size() * sizeof(double),
                           cudaMemcpyHostToDevice));
   static const bool kCull = env_double("GD_VOXEL_CULL", 1) != 0;
   const int n_tiles = kCull ? (n + 31) / 32 : 0;
@@ -436,12 +492,12 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   // Two grid levels over the pocket bounding box: a fine near field (voxel
   // 0.2 A, margin 3 A) and a coarse far field (0.75 A, margin 32 A); queries
   // beyond both fall back to the exact full scan.
-  PocketView& v = ctx->view;
-  v.pts = ctx->pts.as<double>();
+  PocketView& v = slot->view;
+  v.pts = slot->pts.as<double>();
   v.P = n;
   v.use_index = 1;
-  ctx->n_cand = 0;
-  ctx->max_cand = 0;
+  slot->n_cand = 0;
+  slot->max_cand = 0;
   // Edges/margins from A/B on config 1 (profiles/r1_voxel_ab.md, DESIGN
   // §10): 0.2 A fine / 0.75 A far-field voxels.  A level whose grid would
   // exceed kMaxVoxels grows its edge (x1.25 steps) until it fits, so both
@@ -476,7 +532,7 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
       GD_CUDA(ctx, ctx->vox_keep.ensure(sizeof(int32_t) * 8 * static_cast<size_t>(nv)));
       keep = ctx->vox_keep.as<int32_t>();
     }
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_voxel_count(ctx->pts.as<double>(), n, g,
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_voxel_count(slot->pts.as<double>(), n, g,
                                                              counts.as<int32_t>(),
                                                              ctx->tiles.as<float>(), n_tiles, keep,
                                                              ctx->stream)));
@@ -496,23 +552,23 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     const int64_t listed = tot[0], total = tot[1];
     const int32_t mx = static_cast<int32_t>(tot[2]);
     if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
-    GD_CUDA(ctx, ctx->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
-    GD_CUDA(ctx, ctx->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
+    GD_CUDA(ctx, slot->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
+    GD_CUDA(ctx, slot->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
     // List head: the whole pocket, the list of every overflow voxel.
-    GD_CUDA(ctx, cudaMemcpyAsync(ctx->vox_pts[L].ptr, ctx->pts.ptr, sizeof(double) * 4 * n,
+    GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_pts[L].ptr, slot->pts.ptr, sizeof(double) * 4 * n,
                                  cudaMemcpyDeviceToDevice, ctx->stream));
     GD_CUDA(ctx, static_cast<cudaError_t>(
-                     launch_voxel_fill(ctx->pts.as<double>(), n, g, doff.as<int32_t>(),
-                                       ctx->vox_off[L].as<double>(), ctx->vox_pts[L].as<double>(),
+                     launch_voxel_fill(slot->pts.as<double>(), n, g, doff.as<int32_t>(),
+                                       slot->vox_off[L].as<double>(), slot->vox_pts[L].as<double>(),
                                        ctx->tiles.as<float>(), n_tiles, counts.as<int32_t>(),
                                        keep, ctx->stream)));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
-    ctx->grid[L] = g;
-    ctx->n_cand += total;
-    ctx->max_cand = std::max(ctx->max_cand, mx);
+    slot->grid[L] = g;
+    slot->n_cand += total;
+    slot->max_cand = std::max(slot->max_cand, mx);
     GridLevel& gl = v.lv[L];
-    gl.rec = ctx->vox_off[L].as<double>();
-    gl.lst = ctx->vox_pts[L].as<double>();
+    gl.rec = slot->vox_off[L].as<double>();
+    gl.lst = slot->vox_pts[L].as<double>();
     gl.lo_x = g.lo_x;
     gl.lo_y = g.lo_y;
     gl.lo_z = g.lo_z;
@@ -521,6 +577,8 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     gl.dim_y = g.dim_y;
     gl.dim_z = g.dim_z;
   }
+  slot->P = n;
+  activate(*slot);
   return GD_OK;
 }
 
@@ -630,7 +688,8 @@ static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
   if (cnt < 64) {
     work();
   } else {
-    if (!ctx->pool) ctx->pool = std::make_unique<WorkerPool>(host_threads() - 1);
+    if (!ctx->pool)
+      ctx->pool = std::make_unique<WorkerPool>((ctx->pool_threads > 0 ? ctx->pool_threads : host_threads()) - 1);
     ctx->pool->run(work);
   }
 
@@ -1179,6 +1238,241 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   return GD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Fine-grained drop-in entry points: every ligand of `b` with one
+// caller-given fragment (the device descriptors carry it as the ligand's
+// only fragment: nfrag 1 at frag_off l).
+// ---------------------------------------------------------------------------
+static int stage_fragments(gd_ctx* ctx, const gd_ligand_batch* b, const gd_fragment_set* fs,
+                           const char* who, DockParams& p) {
+  if (b == nullptr || fs == nullptr || b->n_ligands < 0 ||
+      (b->n_ligands > 0 && (!b->atom_offsets || !b->xyz || !b->radii || !b->bond_offsets ||
+                            !fs->membership || !fs->axis_atom || !fs->anchor_atom ||
+                            (b->bond_offsets[b->n_ligands] > 0 && (!b->bonds || !b->bond_rotatable)))))
+    return ctx->fail(GD_ERR_INVALID, std::string(who) + ": invalid ligand batch or fragments");
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  const int L = b->n_ligands;
+  for (int l = 0; l < L; ++l) {
+    const int a0 = b->atom_offsets[l], n = b->atom_offsets[l + 1] - a0;
+    if (n < 0 || b->bond_offsets[l + 1] < b->bond_offsets[l])
+      return ctx->fail(GD_ERR_INVALID, std::string(who) + ": offsets not ascending");
+    const int ax = fs->axis_atom[l], an = fs->anchor_atom[l];
+    if (ax < 0 || ax >= n || an < 0 || an >= n || ax == an)
+      return ctx->fail(GD_ERR_INVALID, std::string(who) + ": fragment axis/anchor atom out of range");
+    int nf = 0;
+    for (int i = 0; i < n; ++i) nf += fs->membership[a0 + i] != 0;
+    if (nf < 1 || nf >= n)
+      return ctx->fail(GD_ERR_INVALID, std::string(who) + ": fragment must hold 1..n-1 atoms");
+  }
+  std::vector<PreparedLigand> prep(L);
+  std::atomic<int> next{0};
+  auto work = [&] {
+    for (int l; (l = next.fetch_add(1)) < L;) {
+      const int a0 = b->atom_offsets[l], b0 = b->bond_offsets[l];
+      prep[l] = prepare_ligand(std::to_string(l), b->atom_offsets[l + 1] - a0, b->xyz + 3 * a0,
+                               b->radii + a0, b->bond_offsets[l + 1] - b0, b->bonds + 2 * b0,
+                               b->bond_rotatable + b0);
+    }
+  };
+  if (L < 64) {
+    work();
+  } else {
+    if (!ctx->pool)
+      ctx->pool = std::make_unique<WorkerPool>((ctx->pool_threads > 0 ? ctx->pool_threads : host_threads()) - 1);
+    ctx->pool->run(work);
+  }
+  const int A = L > 0 ? b->atom_offsets[L] : 0;
+  std::vector<LigMeta> meta(std::max(L, 1));
+  std::vector<uint64_t> far, fmask;
+  std::vector<int32_t> fax(std::max(L, 1)), fan(std::max(L, 1)), stat(std::max(L, 1), 0);
+  std::vector<double> frel(std::max(L, 1));
+  ctx->errors.assign(L, std::string());
+  ctx->status_host.assign(L, 0);
+  int max_n = 1;
+  for (int l = 0; l < L; ++l) {
+    const PreparedLigand& q = prep[l];
+    const int a0 = b->atom_offsets[l], n = b->atom_offsets[l + 1] - a0;
+    LigMeta& m = meta[l];
+    m.atom_off = a0;
+    m.n = n;
+    m.status = q.status;
+    m.frag_off = l;
+    m.nfrag = q.status == 0 ? 1 : 0;
+    m.far_off = static_cast<int32_t>(far.size());
+    m.fmask_off = static_cast<int32_t>(fmask.size());
+    m.words = q.words;
+    stat[l] = q.status;
+    ctx->status_host[l] = q.status;
+    ctx->errors[l] = q.error;
+    fax[l] = fs->axis_atom[l];
+    fan[l] = fs->anchor_atom[l];
+    frel[l] = 0.0;
+    if (q.status != 0) continue;
+    far.insert(far.end(), q.far_mask.begin(), q.far_mask.end());
+    int nf = 0;
+    for (int w = 0; w < q.words; ++w) {
+      uint64_t word = 0;
+      for (int i = 64 * w; i < std::min(n, 64 * w + 64); ++i)
+        if (fs->membership[a0 + i]) word |= 1ull << (i - 64 * w);
+      nf += __builtin_popcountll(word);
+      fmask.push_back(word);
+    }
+    frel[l] = static_cast<double>(nf) / n;
+    max_n = std::max(max_n, n);
+  }
+  auto up = [&](DevBuf& d, const void* src, size_t bytes) -> int {
+    GD_CUDA(ctx, d.ensure(std::max<size_t>(bytes, 8)));
+    if (bytes) GD_CUDA(ctx, cudaMemcpyAsync(d.ptr, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    return GD_OK;
+  };
+  int rc;
+  if ((rc = up(ctx->meta, meta.data(), sizeof(LigMeta) * L))) return rc;
+  if ((rc = up(ctx->xyz, b->xyz, sizeof(double) * 3 * A))) return rc;
+  if ((rc = up(ctx->radii, b->radii, sizeof(double) * A))) return rc;
+  if ((rc = up(ctx->far, far.data(), sizeof(uint64_t) * far.size()))) return rc;
+  if ((rc = up(ctx->fmask, fmask.data(), sizeof(uint64_t) * fmask.size()))) return rc;
+  if ((rc = up(ctx->fax, fax.data(), sizeof(int32_t) * L))) return rc;
+  if ((rc = up(ctx->fan, fan.data(), sizeof(int32_t) * L))) return rc;
+  if ((rc = up(ctx->frel, frel.data(), sizeof(double) * L))) return rc;
+  if ((rc = up(ctx->o_status, stat.data(), sizeof(int32_t) * L))) return rc;
+  // The staged descriptors now hold one caller fragment per ligand, not a
+  // dockable batch.
+  ctx->staged = false;
+  ctx->have_result = false;
+  ctx->n_lig = L;
+  ctx->total_atoms = A;
+  ctx->max_n = max_n;
+  if (L > 0) ctx->atom_off.assign(b->atom_offsets, b->atom_offsets + L + 1);
+  else ctx->atom_off.assign(1, 0);
+  p = DockParams{};
+  p.n_lig = L;
+  p.meta = ctx->meta.as<LigMeta>();
+  p.xyz = ctx->xyz.as<double>();
+  p.radii = ctx->radii.as<double>();
+  p.far_mask = ctx->far.as<uint64_t>();
+  p.frag_mask = ctx->fmask.as<uint64_t>();
+  p.frag_axis = ctx->fax.as<int32_t>();
+  p.frag_anchor = ctx->fan.as<int32_t>();
+  p.frag_rel = ctx->frel.as<double>();
+  p.pocket = ctx->view;
+  p.cos_deg = ctx->cos_t.as<double>();
+  p.sin_deg = ctx->sin_t.as<double>();
+  p.max_n = max_n;
+  p.max_pairs = std::max(1, max_n * max_n / 4);
+  p.status = ctx->o_status.as<int32_t>();
+  p.reps = 1;
+  return GD_OK;
+}
+
+static int fetch(gd_ctx* ctx, void* dst, const DevBuf& src, size_t bytes) {
+  if (dst == nullptr || bytes == 0) return GD_OK;
+  return ctx->cuda(cudaMemcpyAsync(dst, src.ptr, bytes, cudaMemcpyDeviceToHost, ctx->stream), "d2h");
+}
+
+extern "C" int gd_optimize_fragment_batch(gd_ctx* ctx, const gd_ligand_batch* batch,
+                                          const gd_fragment_set* fragments, int32_t step,
+                                          int32_t refined, const double* entry_score,
+                                          int32_t* best_angle, double* best_score,
+                                          int64_t* evaluations, int64_t* feasibility_checks,
+                                          double* out_pose, int32_t* status) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  const char* who = refined ? "optimize_fragment_refined" : "optimize_fragment_flat";
+  if (step < 1 || 360 % step != 0) return ctx->fail(GD_ERR_INVALID, std::string(who) + ": step must divide 360");
+  if (ctx->P == 0) return ctx->fail(GD_ERR_NO_POCKET, std::string(who) + ": no pocket staged (gd_set_pocket)");
+  DockParams p;
+  int rc = stage_fragments(ctx, batch, fragments, who, p);
+  if (rc != GD_OK) return rc;
+  const int L = p.n_lig;
+  const size_t A = static_cast<size_t>(ctx->total_atoms);
+  p.hp = step;
+  p.lp = step;
+  p.refine = refined ? 1 : 0;
+  p.tile = gd_optimal_tile_size(step);
+  GD_CUDA(ctx, ctx->st_final.ensure(sizeof(double) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->st_evals.ensure(sizeof(int64_t) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->st_checks.ensure(sizeof(int64_t) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->o_orient.ensure(sizeof(int32_t) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->seed_score.ensure(sizeof(double) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->o_pose.ensure(sizeof(double) * 3 * std::max<size_t>(A, 1)));
+  if (entry_score && L > 0)
+    GD_CUDA(ctx, cudaMemcpyAsync(ctx->seed_score.ptr, entry_score, sizeof(double) * L,
+                                 cudaMemcpyHostToDevice, ctx->stream));
+  FragmentIO io{};
+  io.refined = refined ? 1 : 0;
+  io.entry_score = entry_score ? ctx->seed_score.as<double>() : nullptr;
+  io.best_angle = ctx->o_orient.as<int32_t>();
+  io.best_score = ctx->st_final.as<double>();
+  io.evaluations = ctx->st_evals.as<int64_t>();
+  io.checks = ctx->st_checks.as<int64_t>();
+  io.pose = ctx->o_pose.as<double>();
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_fragment_search(p, io, ctx->stream)));
+  if ((rc = fetch(ctx, best_angle, ctx->o_orient, sizeof(int32_t) * L))) return rc;
+  if ((rc = fetch(ctx, best_score, ctx->st_final, sizeof(double) * L))) return rc;
+  if ((rc = fetch(ctx, evaluations, ctx->st_evals, sizeof(int64_t) * L))) return rc;
+  if ((rc = fetch(ctx, feasibility_checks, ctx->st_checks, sizeof(int64_t) * L))) return rc;
+  if ((rc = fetch(ctx, out_pose, ctx->o_pose, sizeof(double) * 3 * A))) return rc;
+  if ((rc = fetch(ctx, status, ctx->o_status, sizeof(int32_t) * L))) return rc;
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  ctx->timing = gd_timing{};
+  ctx->timing.launches = L > 0 ? 1 : 0;
+  return GD_OK;
+}
+
+extern "C" int gd_rotate_fragment_batch(gd_ctx* ctx, const gd_ligand_batch* batch,
+                                        const gd_fragment_set* fragments, const double* angles_deg,
+                                        double* out_pose, int32_t* status) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  if (batch && batch->n_ligands > 0 && (angles_deg == nullptr || out_pose == nullptr))
+    return ctx->fail(GD_ERR_INVALID, "rotate_fragment: null angles or output");
+  DockParams p;
+  int rc = stage_fragments(ctx, batch, fragments, "rotate_fragment", p);
+  if (rc != GD_OK) return rc;
+  const int L = p.n_lig;
+  const size_t A = static_cast<size_t>(ctx->total_atoms);
+  // cos/sin of angle * (pi/180) from the host libm (geometry.hpp:176-178).
+  std::vector<double> cs(std::max(L, 1)), sn(std::max(L, 1));
+  std::vector<uint8_t> zero(std::max(L, 1));
+  for (int l = 0; l < L; ++l) {
+    zero[l] = angles_deg[l] == 0.0;
+    trig_of(angles_deg[l], cs[l], sn[l]);
+  }
+  GD_CUDA(ctx, ctx->st_final.ensure(sizeof(double) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->seed_score.ensure(sizeof(double) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->o_orient.ensure(sizeof(int32_t) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->o_pose.ensure(sizeof(double) * 3 * std::max<size_t>(A, 1)));
+  if (L > 0) {
+    GD_CUDA(ctx, cudaMemcpyAsync(ctx->st_final.ptr, cs.data(), sizeof(double) * L, cudaMemcpyHostToDevice, ctx->stream));
+    GD_CUDA(ctx, cudaMemcpyAsync(ctx->seed_score.ptr, sn.data(), sizeof(double) * L, cudaMemcpyHostToDevice, ctx->stream));
+    GD_CUDA(ctx, cudaMemcpyAsync(ctx->o_orient.ptr, zero.data(), L, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_fragment_rotate(
+                   p, ctx->st_final.as<double>(), ctx->seed_score.as<double>(),
+                   static_cast<const uint8_t*>(ctx->o_orient.ptr), ctx->o_pose.as<double>(), ctx->stream)));
+  if ((rc = fetch(ctx, out_pose, ctx->o_pose, sizeof(double) * 3 * A))) return rc;
+  if ((rc = fetch(ctx, status, ctx->o_status, sizeof(int32_t) * L))) return rc;
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}
+
+extern "C" int gd_check_bumps_batch(gd_ctx* ctx, const gd_ligand_batch* batch,
+                                    const gd_fragment_set* fragments, uint8_t* feasible,
+                                    int32_t* status) {
+  if (ctx == nullptr) return GD_ERR_INVALID;
+  if (batch && batch->n_ligands > 0 && feasible == nullptr)
+    return ctx->fail(GD_ERR_INVALID, "check_bumps: null output");
+  DockParams p;
+  int rc = stage_fragments(ctx, batch, fragments, "check_bumps", p);
+  if (rc != GD_OK) return rc;
+  const int L = p.n_lig;
+  GD_CUDA(ctx, ctx->o_orient.ensure(sizeof(int32_t) * std::max(L, 1)));
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_fragment_bumps(
+                   p, static_cast<uint8_t*>(ctx->o_orient.ptr), ctx->stream)));
+  if (L > 0) GD_CUDA(ctx, cudaMemcpyAsync(feasible, ctx->o_orient.ptr, L, cudaMemcpyDeviceToHost, ctx->stream));
+  if ((rc = fetch(ctx, status, ctx->o_status, sizeof(int32_t) * L))) return rc;
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}
+
 extern "C" int gd_ligand_graph(int32_t n_atoms, const double* xyz, const double* radii,
                                int32_t n_bonds, const int32_t* bonds, const uint8_t* rotatable,
                                int32_t* n_rotamers, int32_t* rotamer_bonds, uint8_t* membership,
@@ -1406,5 +1700,259 @@ extern "C" int gd_overlap_score_batch(gd_ctx* ctx, const double* xyz, int32_t n_
   GD_CUDA(ctx, cudaMemcpyAsync(out, dout.ptr, sizeof(double) * n_poses, cudaMemcpyDeviceToHost,
                                ctx->stream));
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  return GD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-device dispatch (gd_multi_*): one gd_ctx, host thread and set of
+// streams per device; a batch is cut into cost-weighted chunks that the
+// device threads pull from a shared atomic cursor (the GPU analogue of the
+// reference screen's bounded work queue, screening.hpp:96-178), each chunk
+// docked by the pipelined single-device path and its results written
+// straight into the caller's arrays at the chunk's global offsets.
+// ---------------------------------------------------------------------------
+struct gd_multi {
+  std::vector<gd_ctx*> ctx;
+  std::vector<std::thread> th;
+  std::mutex mu;
+  std::condition_variable cv, done;
+  const std::function<void(int)>* job = nullptr;
+  int gen = 0, busy = 0;
+  bool stop = false;
+  std::string err;
+  std::vector<gd_multi_stats> stats;
+  std::vector<std::pair<int, std::string>> lig_errors;  // last call: (global position, text)
+
+  void loop(int d) {
+    int seen = 0;
+    for (;;) {
+      const std::function<void(int)>* j;
+      {
+        std::unique_lock<std::mutex> g(mu);
+        cv.wait(g, [&] { return stop || gen != seen; });
+        if (stop) return;
+        seen = gen;
+        j = job;
+      }
+      (*j)(d);
+      std::lock_guard<std::mutex> g(mu);
+      if (--busy == 0) done.notify_one();
+    }
+  }
+  // Runs fn(d) on every device thread; returns when all have finished.
+  void run(const std::function<void(int)>& fn) {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      job = &fn;
+      busy = static_cast<int>(th.size());
+      ++gen;
+    }
+    cv.notify_all();
+    std::unique_lock<std::mutex> g(mu);
+    done.wait(g, [&] { return busy == 0; });
+  }
+  ~gd_multi() {
+    {
+      std::lock_guard<std::mutex> g(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    for (auto& t : th) t.join();
+    for (gd_ctx* c : ctx) gd_destroy(c);
+  }
+};
+
+namespace {
+thread_local std::string g_multi_create_error;
+}
+
+extern "C" int gd_multi_create(const int32_t* devices, int32_t n_devices, gd_multi** out) {
+  if (out == nullptr) {
+    g_multi_create_error = "gd_multi_create: null output pointer";
+    return GD_ERR_INVALID;
+  }
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    g_multi_create_error = "gd_multi_create: no CUDA device";
+    return GD_ERR_CUDA;
+  }
+  std::vector<int> devs;
+  if (devices != nullptr) {
+    if (n_devices < 1) {
+      g_multi_create_error = "gd_multi_create: empty device list";
+      return GD_ERR_INVALID;
+    }
+    devs.assign(devices, devices + n_devices);
+  } else {
+    const int k = n_devices > 0 ? std::min<int>(n_devices, count) : count;
+    for (int d = 0; d < k; ++d) devs.push_back(d);
+  }
+  auto m = std::make_unique<gd_multi>();
+  // The host cores are shared by the device threads' preprocessing pools.
+  const int per = std::max(1, host_threads() / static_cast<int>(devs.size()));
+  for (int d : devs) {
+    gd_ctx* c = nullptr;
+    const int rc = gd_create(d, &c);
+    if (rc != GD_OK) {
+      g_multi_create_error = std::string("gd_multi_create: ") + gd_last_error(nullptr);
+      return rc;
+    }
+    c->pool_threads = per;
+    m->ctx.push_back(c);
+  }
+  m->stats.assign(devs.size(), gd_multi_stats{});
+  for (size_t d = 0; d < devs.size(); ++d) m->th.emplace_back([p = m.get(), d] { p->loop(static_cast<int>(d)); });
+  *out = m.release();
+  return GD_OK;
+}
+
+extern "C" int gd_multi_destroy(gd_multi* m) {
+  delete m;
+  return GD_OK;
+}
+
+extern "C" const char* gd_multi_last_error(const gd_multi* m) {
+  return m ? m->err.c_str() : g_multi_create_error.c_str();
+}
+
+extern "C" int32_t gd_multi_size(const gd_multi* m) { return m ? static_cast<int32_t>(m->ctx.size()) : 0; }
+
+extern "C" gd_ctx* gd_multi_context(gd_multi* m, int32_t i) {
+  return (m && i >= 0 && i < static_cast<int32_t>(m->ctx.size())) ? m->ctx[i] : nullptr;
+}
+
+extern "C" int gd_multi_set_pocket(gd_multi* m, const double* xyz, int32_t n_points) {
+  if (m == nullptr) return GD_ERR_INVALID;
+  std::vector<int> rc(m->ctx.size(), GD_OK);
+  m->run([&](int d) { rc[d] = gd_set_pocket(m->ctx[d], xyz, n_points); });
+  for (size_t d = 0; d < rc.size(); ++d)
+    if (rc[d] != GD_OK) {
+      m->err = m->ctx[d]->err;
+      return rc[d];
+    }
+  return GD_OK;
+}
+
+extern "C" int gd_multi_dock_batch(gd_multi* m, const gd_ligand_batch* b, const gd_knobs* k,
+                                   gd_result* r) {
+  if (m == nullptr) return GD_ERR_INVALID;
+  auto fail = [&](int code, const std::string& msg) {
+    m->err = msg;
+    return code;
+  };
+  if (r == nullptr) return fail(GD_ERR_INVALID, "gd_dock_batch: null result");
+  if (k == nullptr) return fail(GD_ERR_INVALID, "knob config: null");
+  char msg[128];
+  if (gd_validate_knobs(k, msg, sizeof msg) != GD_OK) return fail(GD_ERR_INVALID, msg);
+  if (b == nullptr || b->n_ligands < 0 ||
+      (b->n_ligands > 0 && (!b->atom_offsets || !b->xyz || !b->radii || !b->bond_offsets ||
+                            (b->bond_offsets[b->n_ligands] > 0 && (!b->bonds || !b->bond_rotatable)))))
+    return fail(GD_ERR_INVALID, "gd_upload: invalid ligand batch");
+  const int L = b->n_ligands;
+  const int D = static_cast<int>(m->ctx.size());
+  for (auto& st : m->stats) st = gd_multi_stats{};
+  const bool rigid = k->rigid_step > 0;
+  const int K = rigid ? k->top_k : 1;
+  // Cost per ligand ~ rigid atom-orientations + restart chains' rotated
+  // atoms: n (N_orient + K reps (1 + 2R (360/hp))).
+  const int32_t n_orient = rigid ? gd_orientations(k->rigid_step, nullptr, nullptr, 0) : 0;
+  std::vector<double> cost(L);
+  double total = 0.0;
+  for (int l = 0; l < L; ++l) {
+    const int n = b->atom_offsets[l + 1] - b->atom_offsets[l];
+    int R = 0;
+    for (int e = b->bond_offsets[l]; e < b->bond_offsets[l + 1]; ++e) R += b->bond_rotatable[e] != 0;
+    const double keff = rigid ? std::min(K, std::max<int32_t>(n_orient, 1)) : 1;
+    cost[l] = std::max(n, 1) * (n_orient + keff * k->repetitions * (1.0 + 2.0 * R * (360.0 / k->high_precision_step)));
+    total += cost[l];
+  }
+  // Chunks: ~4 per device of equal cost (at least 256 ligands), so the
+  // cursor balances the ~10x cost spread of BASELINE ligands while each
+  // chunk stays large enough for the single-device pipeline.
+  std::vector<int> bounds{0};
+  if (L > 0) {
+    const int per_dev_chunks = static_cast<int>(env_double("GD_MULTI_CHUNKS", 4));
+    const double target = total / std::max(1, D * per_dev_chunks);
+    double acc = 0.0;
+    for (int l = 0; l < L; ++l) {
+      acc += cost[l];
+      if ((acc >= target && l + 1 - bounds.back() >= 256) || l + 1 == L) {
+        bounds.push_back(l + 1);
+        acc = 0.0;
+      }
+    }
+  }
+  const int chunks = static_cast<int>(bounds.size()) - 1;
+  std::atomic<int> cursor{0};
+  std::vector<int> rc(D, GD_OK);
+  std::vector<std::string> errs(D);
+  std::vector<std::vector<std::pair<int, std::string>>> lerr(D);
+  m->lig_errors.clear();
+  m->run([&](int d) {
+    gd_ctx* c = m->ctx[d];
+    std::vector<int32_t> ao, bo;
+    for (int ci; (ci = cursor.fetch_add(1)) < chunks;) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const int c0 = bounds[ci], c1 = bounds[ci + 1];
+      const int a0 = b->atom_offsets[c0], e0 = b->bond_offsets[c0];
+      ao.resize(c1 - c0 + 1);
+      bo.resize(c1 - c0 + 1);
+      for (int l = c0; l <= c1; ++l) {
+        ao[l - c0] = b->atom_offsets[l] - a0;
+        bo[l - c0] = b->bond_offsets[l] - e0;
+      }
+      const gd_ligand_batch sub{c1 - c0, ao.data(), b->xyz + 3 * static_cast<size_t>(a0),
+                                b->radii + a0, bo.data(), b->bonds ? b->bonds + 2 * static_cast<size_t>(e0) : nullptr,
+                                b->bond_rotatable ? b->bond_rotatable + e0 : nullptr};
+      const size_t s0 = static_cast<size_t>(c0) * K;
+      auto off = [](auto* p, size_t o) { return p ? p + o : nullptr; };
+      gd_result sr{off(r->orientation, s0), off(r->seed_rank, s0), off(r->rigid_score, s0),
+                   off(r->final_score, s0), off(r->evaluations, s0), off(r->feasibility_checks, s0),
+                   off(r->final_pose, 3 * static_cast<size_t>(K) * a0), off(r->k_eff, c0),
+                   off(r->poses_scored, c0), off(r->status, c0)};
+      const int e = gd_dock_batch(c, &sub, k, &sr);
+      if (e != GD_OK) {
+        rc[d] = e;
+        errs[d] = c->err;
+        cursor.store(chunks);  // stop handing out work
+        return;
+      }
+      // Validation texts, re-keyed from chunk to batch positions.
+      for (int l = 0; l < c1 - c0; ++l)
+        if (!c->errors[l].empty()) {
+          std::string t = c->errors[l];
+          const std::string pre = "ligand '" + std::to_string(l) + "': ";
+          if (t.rfind(pre, 0) == 0) t = "ligand '" + std::to_string(c0 + l) + "': " + t.substr(pre.size());
+          lerr[d].emplace_back(c0 + l, std::move(t));
+        }
+      gd_multi_stats& st = m->stats[d];
+      st.ligands += c1 - c0;
+      st.chunks += 1;
+      st.busy_ms += std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  });
+  for (int d = 0; d < D; ++d)
+    if (rc[d] != GD_OK) return fail(rc[d], errs[d]);
+  for (auto& v : lerr) m->lig_errors.insert(m->lig_errors.end(), v.begin(), v.end());
+  std::sort(m->lig_errors.begin(), m->lig_errors.end());
+  return GD_OK;
+}
+
+extern "C" int gd_multi_ligand_error(const gd_multi* m, int32_t ligand, char* msg, size_t msg_len) {
+  if (m == nullptr || ligand < 0) return GD_ERR_INVALID;
+  const auto it = std::lower_bound(m->lig_errors.begin(), m->lig_errors.end(),
+                                   std::make_pair(static_cast<int>(ligand), std::string()));
+  const bool hit = it != m->lig_errors.end() && it->first == ligand;
+  if (msg && msg_len) {
+    std::strncpy(msg, hit ? it->second.c_str() : "", msg_len - 1);
+    msg[msg_len - 1] = 0;
+  }
+  return GD_OK;
+}
+
+extern "C" int gd_multi_last_stats(const gd_multi* m, gd_multi_stats* out, int32_t cap) {
+  if (m == nullptr || out == nullptr) return GD_ERR_INVALID;
+  for (int32_t d = 0; d < std::min<int32_t>(cap, static_cast<int32_t>(m->stats.size())); ++d) out[d] = m->stats[d];
   return GD_OK;
 }

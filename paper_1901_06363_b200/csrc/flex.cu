@@ -542,6 +542,97 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   return true;
 }
 
+// One fragment search from the committed pose, whose score is `cur`:
+// optimize_fragment_flat (kernel.hpp:125-143) with `step`, or
+// optimize_fragment_refined (:150-198) with high-precision step `step`, tile
+// p.tile and the entry score `entry` (the reference's optional entry_score;
+// the chains pass cur).  Returns the winning angle and score warp-uniformly
+// and the CandidateEvaluator tallies (evaluations, feasibility checks).
+template <bool On, int B, class CK>
+__device__ __forceinline__ void search_fragment(const WarpMem& s, const DockParams& p, const Axis& X,
+                                                int n, int nf, int np, int first, double pre,
+                                                double cur, double entry, int step, bool refined,
+                                                int lane, int& best_a, double& best, int& evals,
+                                                int& checks, Work<On>& wk, CK& ck) {
+  best_a = 0;
+  best = cur;
+  if (!refined) {
+    // optimize_fragment_flat (kernel.hpp:125-143).
+    const int A = 360 / step;
+    int nfeas = 0;
+    for (int kb = 0; kb < A - 1; kb += B) {
+      const int nb = min(B, A - 1 - kb);
+      const int a0 = (kb + 1) * step;
+      double sc;
+      unsigned bumped;
+      eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, step, nb, lane, sc, bumped, wk, ck);
+      int c;
+      const double v = batch_max(sc, bumped, nb, lane, c);
+      nfeas += __popc(~bumped & ((1u << nb) - 1u));
+      if (c >= 0 && v > best) {
+        best = v;
+        best_a = a0 + c * step;
+      }
+    }
+    evals = 1 + nfeas;
+    checks = A;
+    return;
+  }
+  // optimize_fragment_refined (kernel.hpp:150-198).
+  const int T = p.tile, tc = 360 / T;
+  bool have = false;
+  int wt = -1;
+  double ws = 0.0;
+  int nfeas = 0;
+  best = 0.0;
+  for (int kb = 0; kb < tc; kb += B) {
+    const int nb = min(B, tc - kb);
+    const int a0 = kb * T + T / 2;
+    double sc;
+    unsigned bumped;
+    eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, T, nb, lane, sc, bumped, wk, ck);
+    int c;
+    const double v = batch_max(sc, bumped, nb, lane, c);
+    nfeas += __popc(~bumped & ((1u << nb) - 1u));
+    if (c >= 0 && (!have || v > best)) {
+      best = v;
+      best_a = a0 + c * T;
+      have = true;
+    }
+    if (c >= 0 && (wt < 0 || v > ws)) {
+      wt = kb + c;
+      ws = v;
+    }
+  }
+  checks = tc;
+  if (wt >= 0) {
+    int cnt2 = 0;
+    while ((cnt2 + 1) * step <= T) ++cnt2;
+    for (int kb = 0; kb < cnt2; kb += B) {
+      const int nb = min(B, cnt2 - kb);
+      const int a0 = wt * T + kb * step;
+      double sc;
+      unsigned bumped;
+      eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, step, nb, lane, sc, bumped, wk, ck);
+      int c;
+      const double v = batch_max(sc, bumped, nb, lane, c);
+      nfeas += __popc(~bumped & ((1u << nb) - 1u));
+      if (c >= 0 && (!have || v > best)) {
+        best = v;
+        best_a = a0 + c * step;
+        have = true;
+      }
+    }
+    checks += cnt2;
+  }
+  checks += 1;  // entry-pose comparison (kernel.hpp:192-194)
+  if (!have || entry > best) {
+    best = entry;
+    best_a = 0;
+  }
+  evals = nfeas;
+}
+
 template <bool On, int B, int kWarps = warps_for<B>()>
 __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     flex_chain_kernel(DockParams p) {
@@ -641,79 +732,10 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
 
       int best_a = 0;
       double best = cur;
-      if (!refined) {
-        // optimize_fragment_flat (kernel.hpp:125-143).
-        int nfeas = 0;
-        for (int kb = 0; kb < A - 1; kb += B) {
-          const int nb = min(B, A - 1 - kb);
-          const int a0 = (kb + 1) * step;
-          double sc;
-          unsigned bumped;
-          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, step, nb, lane, sc, bumped, wk, ck);
-          int c;
-          const double v = batch_max(sc, bumped, nb, lane, c);
-          nfeas += __popc(~bumped & ((1u << nb) - 1u));
-          if (c >= 0 && v > best) {
-            best = v;
-            best_a = a0 + c * step;
-          }
-        }
-        tally(1 + nfeas, A);
-      } else {
-        // optimize_fragment_refined (kernel.hpp:150-198).
-        const int T = p.tile, tc = 360 / T;
-        bool have = false;
-        int wt = -1;
-        double ws = 0.0;
-        int nfeas = 0;
-        best = 0.0;
-        for (int kb = 0; kb < tc; kb += B) {
-          const int nb = min(B, tc - kb);
-          const int a0 = kb * T + T / 2;
-          double sc;
-          unsigned bumped;
-          eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, T, nb, lane, sc, bumped, wk, ck);
-          int c;
-          const double v = batch_max(sc, bumped, nb, lane, c);
-          nfeas += __popc(~bumped & ((1u << nb) - 1u));
-          if (c >= 0 && (!have || v > best)) {
-            best = v;
-            best_a = a0 + c * T;
-            have = true;
-          }
-          if (c >= 0 && (wt < 0 || v > ws)) {
-            wt = kb + c;
-            ws = v;
-          }
-        }
-        tally(0, tc);
-        if (wt >= 0) {
-          int cnt2 = 0;
-          while ((cnt2 + 1) * p.hp <= T) ++cnt2;
-          for (int kb = 0; kb < cnt2; kb += B) {
-            const int nb = min(B, cnt2 - kb);
-            const int a0 = wt * T + kb * p.hp;
-            double sc;
-            unsigned bumped;
-            eval_batch(s, p, X, n, nf, np, first, pre, cur, a0, p.hp, nb, lane, sc, bumped, wk, ck);
-            int c;
-            const double v = batch_max(sc, bumped, nb, lane, c);
-            nfeas += __popc(~bumped & ((1u << nb) - 1u));
-            if (c >= 0 && (!have || v > best)) {
-              best = v;
-              best_a = a0 + c * p.hp;
-              have = true;
-            }
-          }
-          tally(0, cnt2);
-        }
-        tally(0, 1);  // entry-pose comparison (kernel.hpp:192-194)
-        if (!have || cur > best) {
-          best = cur;
-          best_a = 0;
-        }
-        tally(nfeas, 0);
-      }
+      int evals = 0, checks = 0;
+      search_fragment<On, B>(s, p, X, n, nf, np, first, pre, cur, cur, step, refined, lane, best_a,
+                             best, evals, checks, wk, ck);
+      tally(evals, checks);
       ck.mark(kPhDecide);
       // commit_angle (kernel.hpp:115-117): a fresh rotation of the entry pose,
       // bit-identical to the scored candidate; refresh the fragment's terms.
@@ -835,6 +857,162 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     }
   }
   publish_warp(wk, p.counters, 8, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Fine-grained drop-in entry points (gd_optimize_fragment_batch,
+// gd_rotate_fragment_batch, gd_check_bumps_batch): one warp per ligand of
+// the staged batch, each ligand carrying exactly one caller-given fragment
+// (meta.nfrag == 1 at frag_off == l).
+// ---------------------------------------------------------------------------
+
+// optimize_fragment_flat / optimize_fragment_refined (kernel.hpp:125-198)
+// from the ligand's staged pose: the same setup, candidate evaluator and
+// decisions as a chain's fragment step, then commit_angle (:115-117).
+template <bool On, int B, int kWarps = warps_for<B>()>
+__global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
+    fragment_search_kernel(DockParams p, FragmentIO io) {
+  static_assert(B >= 1 && B <= 8, "batch_max reduces over an 8-lane butterfly");
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int l = blockIdx.x * kWarps + warp;
+  if (l >= p.n_lig) return;
+  const LigMeta m = p.meta[l];
+  if (m.status != 0) return;
+  const int n = m.n, W = m.words;
+  const WarpMem s =
+      carve<B>(smem + warp * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W,
+               p.max_pairs);
+  Work<On> wk;
+  Clocks<false> ck;
+  for (int i = lane; i < n; i += 32) s.radius[i] = __ldg(p.radii + m.atom_off + i);
+  for (int i = lane; i < n * W; i += 32) s.far[i] = __ldg(p.far_mask + m.far_off + i);
+  for (int i = lane; i < n; i += 32) {
+    const double* q = p.xyz + 3 * (m.atom_off + i);
+    s.pt[i] = PT{q[0], q[1], q[2], fmax(kMinDistanceSq, min_dist_sq(p.pocket, q[0], q[1], q[2], wk))};
+  }
+  __syncwarp();
+  double cur = 0.0;
+  if (lane == 0) {
+    double sum = 0.0;
+    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt[i].t);
+    cur = __ddiv_rn(static_cast<double>(n), sum);
+  }
+  cur = __shfl_sync(kFull, cur, 0);
+  const double given = io.entry_score ? io.entry_score[l] : cur;
+  const double entry = given == given ? given : cur;  // NaN: not given
+  const bool refined = io.refined != 0;
+  const int step = p.hp;
+  int best_a = 0, evals = 1, checks = 1;
+  double best = cur;
+  if (refined || step != 360) {  // flat at 360: angle 0 alone, no rotation
+    StepInfo st;
+    int left_np = -1;
+    const uint64_t fm_word = lane < W ? __ldg(p.frag_mask + m.fmask_off + lane) : 0ull;
+    if (!setup_step<B>(s, p, m, 0, __ldg(p.frag_axis + l), __ldg(p.frag_anchor + l), fm_word, lane,
+                       left_np, st, ck)) {
+      if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
+      return;
+    }
+    search_fragment<On, B>(s, p, st.X, n, st.nf, st.np, st.first, st.pre, cur, entry, step, refined,
+                           lane, best_a, best, evals, checks, wk, ck);
+    if (best_a != 0) {  // commit_angle: rotate the fragment by the winning angle
+      const double cs = __ldg(p.cos_deg + best_a), sn = __ldg(p.sin_deg + best_a);
+      const double omc = dsub(1.0, cs);
+      for (int sl = lane; sl < st.nf; sl += 32) {
+        const int i = s.fidx[sl];
+        const PT q = s.pt[i];
+        double qx, qy, qz;
+        rodrigues(st.X, cs, sn, omc, q.x, q.y, q.z, qx, qy, qz);
+        s.pt[i] = PT{qx, qy, qz, 0.0};
+      }
+    }
+    __syncwarp();
+  }
+  for (int i = lane; i < n; i += 32) {
+    const PT q = s.pt[i];
+    double* d = io.pose + 3 * (static_cast<size_t>(m.atom_off) + i);
+    d[0] = q.x;
+    d[1] = q.y;
+    d[2] = q.z;
+  }
+  if (lane == 0) {
+    io.best_angle[l] = best_a;
+    io.best_score[l] = best;
+    io.evaluations[l] = evals;
+    io.checks[l] = checks;
+  }
+  publish_warp(wk, p.counters, 8, lane);
+}
+
+// rotate_fragment_into (geometry.hpp:161-186): the axis from the staged
+// pose (degenerate below 1e-9 A, checked before the angle-0 shortcut), then
+// every fragment atom rotated by the ligand's angle (host cos/sin of
+// angle * (pi/180), as the reference computes them) and the rest copied.
+__global__ void __launch_bounds__(256) fragment_rotate_kernel(DockParams p, const double* cs_in,
+                                                               const double* sn_in,
+                                                               const uint8_t* is_zero,
+                                                               double* out) {
+  const int lane = threadIdx.x & 31;
+  const int l = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (l >= p.n_lig) return;
+  const LigMeta m = p.meta[l];
+  if (m.status != 0) return;
+  const double* xyz = p.xyz + 3 * static_cast<size_t>(m.atom_off);
+  const int ia = __ldg(p.frag_axis + l), ib = __ldg(p.frag_anchor + l);
+  const double ox = xyz[3 * ia], oy = xyz[3 * ia + 1], oz = xyz[3 * ia + 2];
+  const double ax = dsub(xyz[3 * ib], ox), ay = dsub(xyz[3 * ib + 1], oy), az = dsub(xyz[3 * ib + 2], oz);
+  const double len = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
+  if (len < kMinAxisLength) {
+    if (lane == 0) p.status[l] = 3;
+    return;
+  }
+  const Axis X{ox, oy, oz, __ddiv_rn(ax, len), __ddiv_rn(ay, len), __ddiv_rn(az, len)};
+  const bool zero = is_zero[l] != 0;
+  const double cs = cs_in[l], sn = sn_in[l], omc = dsub(1.0, cs);
+  const uint64_t* fm = p.frag_mask + m.fmask_off;
+  double* o = out + 3 * static_cast<size_t>(m.atom_off);
+  for (int i = lane; i < m.n; i += 32) {
+    double x = xyz[3 * i], y = xyz[3 * i + 1], z = xyz[3 * i + 2];
+    if (!zero && ((fm[i >> 6] >> (i & 63)) & 1ull)) rodrigues(X, cs, sn, omc, x, y, z, x, y, z);
+    o[3 * i] = x;
+    o[3 * i + 1] = y;
+    o[3 * i + 2] = z;
+  }
+}
+
+// check_bumps (geometry.hpp:199-213) of the staged pose against the
+// ligand's fragment: lanes over fragment atoms i, each scanning its
+// partners j outside the fragment at capped graph distance >= 4.
+__global__ void __launch_bounds__(256) fragment_bumps_kernel(DockParams p, uint8_t* feasible) {
+  const int lane = threadIdx.x & 31;
+  const int l = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (l >= p.n_lig) return;
+  const LigMeta m = p.meta[l];
+  if (m.status != 0) return;
+  const double* xyz = p.xyz + 3 * static_cast<size_t>(m.atom_off);
+  const double* rad = p.radii + m.atom_off;
+  const uint64_t* fm = p.frag_mask + m.fmask_off;
+  const uint64_t* far = p.far_mask + m.far_off;
+  bool bump = false;
+  for (int i = lane; i < m.n && !bump; i += 32) {
+    if (!((fm[i >> 6] >> (i & 63)) & 1ull)) continue;
+    for (int w = 0; w < m.words && !bump; ++w) {
+      uint64_t bits = far[static_cast<size_t>(i) * m.words + w] & ~fm[w];
+      while (bits) {
+        const int j = 64 * w + __ffsll(static_cast<long long>(bits)) - 1;
+        bits &= bits - 1;
+        const double cut = dmul(kBumpScale, dadd(rad[i], rad[j]));
+        if (dist_sq(xyz[3 * i], xyz[3 * i + 1], xyz[3 * i + 2], xyz[3 * j], xyz[3 * j + 1],
+                    xyz[3 * j + 2]) < dmul(cut, cut)) {
+          bump = true;
+          break;
+        }
+      }
+    }
+  }
+  bump = __any_sync(kFull, bump);
+  if (lane == 0) feasible[l] = bump ? 0 : 1;
 }
 
 // (E7) final order: (final score desc, seed rank asc), one rank per thread;
@@ -985,6 +1163,40 @@ int launch_profiles(const DockParams& p, const int32_t* items, int n_items, doub
   // 359 candidates per fragment: the wide batch.
   return launch_profiles_b<GD_PROFILE_BATCH>(p, items, n_items, scores, valid,
                                              static_cast<cudaStream_t>(stream));
+}
+
+template <int B, int W>
+int launch_fragment_search_bw(const DockParams& p, const FragmentIO& io, cudaStream_t stream) {
+  const size_t smem = flex_smem_bytes<B, W>(p);
+  auto kernel = p.counters ? fragment_search_kernel<true, B, W> : fragment_search_kernel<false, B, W>;
+  cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem));
+  if (e != cudaSuccess) return e;
+  kernel<<<(p.n_lig + W - 1) / W, W * 32, smem, stream>>>(p, io);
+  return cudaGetLastError();
+}
+
+int launch_fragment_search(const DockParams& p, const FragmentIO& io, void* stream) {
+  if (p.n_lig == 0) return cudaSuccess;
+  const auto s = static_cast<cudaStream_t>(stream);
+  if (flex_smem_bytes<8, 4>(p) <= static_cast<size_t>(max_smem_optin()))
+    return launch_fragment_search_bw<8, 4>(p, io, s);
+  return launch_fragment_search_bw<8, 1>(p, io, s);
+}
+
+int launch_fragment_rotate(const DockParams& p, const double* cs, const double* sn,
+                           const uint8_t* is_zero, double* out, void* stream) {
+  if (p.n_lig == 0) return cudaSuccess;
+  fragment_rotate_kernel<<<(p.n_lig + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      p, cs, sn, is_zero, out);
+  return cudaGetLastError();
+}
+
+int launch_fragment_bumps(const DockParams& p, uint8_t* feasible, void* stream) {
+  if (p.n_lig == 0) return cudaSuccess;
+  fragment_bumps_kernel<<<(p.n_lig + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(p,
+                                                                                         feasible);
+  return cudaGetLastError();
 }
 
 int launch_finalize(const DockParams& p, void* stream) {

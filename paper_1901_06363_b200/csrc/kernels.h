@@ -126,6 +126,22 @@ int launch_flex(const DockParams& p, void* stream);
 // ([2*n_items] ligand, fragment), 360 scores + validity flags per item.
 int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
                     uint8_t* valid, void* stream);
+// Fine-grained drop-in kernels over a staged batch whose ligand l carries
+// one caller-given fragment (meta.nfrag == 1, frag_off == l).  Search:
+// p.hp = step, p.tile = optimal_tile_size(step).
+struct FragmentIO {
+  int32_t refined;             // 0: optimize_fragment_flat, 1: _refined
+  const double* entry_score;   // nullable [L]; NaN = not given
+  int32_t* best_angle;         // [L]
+  double* best_score;          // [L]
+  int64_t* evaluations;        // [L]
+  int64_t* checks;             // [L]
+  double* pose;                // [3*atoms] committed poses
+};
+int launch_fragment_search(const DockParams& p, const FragmentIO& io, void* stream);
+int launch_fragment_rotate(const DockParams& p, const double* cs, const double* sn,
+                           const uint8_t* is_zero, double* out, void* stream);
+int launch_fragment_bumps(const DockParams& p, uint8_t* feasible, void* stream);
 // E7 final ordering + poses scored, one CTA per ligand.
 int launch_finalize(const DockParams& p, void* stream);
 int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int n_poses,

@@ -17,6 +17,12 @@ __attribute__((noinline)) double libm_sin(double x) { return std::sin(x); }
 
 }  // namespace
 
+void trig_of(double angle_deg, double& c, double& s) {
+  const double theta = angle_deg * (kPi / 180.0);
+  c = libm_cos(theta);
+  s = libm_sin(theta);
+}
+
 void trig_tables(std::vector<double>& cos_deg, std::vector<double>& sin_deg) {
   cos_deg.resize(360);
   sin_deg.resize(360);

@@ -11,6 +11,9 @@ namespace gdb200 {
 // (reference geometry.hpp:176-178).  Uploaded so the device never calls its
 // own (differently rounded) cos/sin.
 void trig_tables(std::vector<double>& cos_deg, std::vector<double>& sin_deg);
+// The same for any angle: c = std::cos(angle * (pi/180)), s = std::sin(...)
+// (geometry.hpp:176-178), for rotate_fragment's arbitrary double angles.
+void trig_of(double angle_deg, double& c, double& s);
 
 // Distinct orientations of the rigid Euler grid with step s (divisor of
 // 360): (alpha, beta, gamma) = (i, j, k) * s, linear index (i*m + j)*m + k,

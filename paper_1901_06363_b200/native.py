@@ -59,6 +59,10 @@ class gd_device_result(C.Structure):
                 ("n_ligands", C.c_int32), ("top_k", C.c_int32)]
 
 
+class gd_fragment_set(C.Structure):
+    _fields_ = [("membership", _u8p), ("axis_atom", _i32p), ("anchor_atom", _i32p)]
+
+
 class _CudaArray:
     """__cuda_array_interface__ view of a device buffer owned by the library
     (lets torch wrap it without a copy, e.g. for an NCCL all-gather)."""
@@ -75,6 +79,10 @@ class gd_timing(C.Structure):
                 ("launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("host_prep_ms", C.c_float), ("host_pack_ms", C.c_float),
                 ("host_post_ms", C.c_float)]
+
+
+class gd_multi_stats(C.Structure):
+    _fields_ = [("ligands", C.c_int64), ("chunks", C.c_int64), ("busy_ms", C.c_float)]
 
 
 # Every symbol include/geodock_b200.h declares, with its ctypes signature.
@@ -115,6 +123,23 @@ SIGNATURES = {
                                        C.POINTER(C.c_int32), C.c_int64]),
     "gd_device_results": (C.c_int, [C.c_void_p, C.POINTER(gd_device_result)]),
     "gd_ligand_error": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t]),
+    "gd_multi_create": (C.c_int, [_i32p, C.c_int32, C.POINTER(C.c_void_p)]),
+    "gd_multi_destroy": (C.c_int, [C.c_void_p]),
+    "gd_multi_last_error": (C.c_char_p, [C.c_void_p]),
+    "gd_multi_size": (C.c_int32, [C.c_void_p]),
+    "gd_multi_context": (C.c_void_p, [C.c_void_p, C.c_int32]),
+    "gd_multi_set_pocket": (C.c_int, [C.c_void_p, _f64p, C.c_int32]),
+    "gd_multi_dock_batch": (C.c_int, [C.c_void_p, C.POINTER(gd_ligand_batch), C.POINTER(gd_knobs),
+                                      C.POINTER(gd_result)]),
+    "gd_multi_last_stats": (C.c_int, [C.c_void_p, C.POINTER(gd_multi_stats), C.c_int32]),
+    "gd_multi_ligand_error": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t]),
+    "gd_optimize_fragment_batch": (C.c_int, [C.c_void_p, C.POINTER(gd_ligand_batch),
+                                             C.POINTER(gd_fragment_set), C.c_int32, C.c_int32,
+                                             _f64p, _i32p, _f64p, _i64p, _i64p, _f64p, _i32p]),
+    "gd_rotate_fragment_batch": (C.c_int, [C.c_void_p, C.POINTER(gd_ligand_batch),
+                                           C.POINTER(gd_fragment_set), _f64p, _f64p, _i32p]),
+    "gd_check_bumps_batch": (C.c_int, [C.c_void_p, C.POINTER(gd_ligand_batch),
+                                       C.POINTER(gd_fragment_set), _u8p, _i32p]),
     "gd_fp64_peak": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "gd_overlap_score_batch": (C.c_int, [C.c_void_p, _f64p, C.c_int32, C.c_int32, C.c_uint32,
                                          _f64p]),
@@ -442,6 +467,64 @@ class Docker:
         return Profiles(buf.scores[:F], buf.valid[:F].view(bool), buf.rel[:F], buf.offs[:L + 1],
                         buf.status[:L])
 
+    # -- fine-grained drop-in entry points (one caller fragment per ligand) --
+    @staticmethod
+    def _fragset(batch: LigandBatch, membership, axis, anchor):
+        mem = np.ascontiguousarray(membership, dtype=np.uint8).reshape(-1)
+        ax = np.ascontiguousarray(np.atleast_1d(axis), dtype=np.int32)
+        an = np.ascontiguousarray(np.atleast_1d(anchor), dtype=np.int32)
+        assert len(mem) == batch.atom_offsets[-1] and len(ax) == len(an) == batch.n_ligands
+        keep = (mem, ax, an)
+        return gd_fragment_set(_p(mem, _u8p), _p(ax, _i32p), _p(an, _i32p)), keep
+
+    def optimize_fragment(self, batch: LigandBatch, membership, axis, anchor, step: int,
+                          refined: bool = False, entry_score=None) -> dict:
+        """gd_optimize_fragment_batch: optimize_fragment_flat/_refined
+        (kernel.hpp:125-198) of each ligand's fragment from its pose."""
+        L, A = batch.n_ligands, int(batch.atom_offsets[-1])
+        fs, keep = self._fragset(batch, membership, axis, anchor)
+        out = {"best_angle": np.zeros(L, np.int32), "best_score": np.zeros(L),
+               "evaluations": np.zeros(L, np.int64), "feasibility_checks": np.zeros(L, np.int64),
+               "pose": np.zeros((A, 3)), "status": np.zeros(L, np.int32)}
+        es = None if entry_score is None else np.ascontiguousarray(entry_score, dtype=np.float64)
+        b = batch.c_struct()
+        self._check(self._lib.gd_optimize_fragment_batch(
+            self._h, C.byref(b), C.byref(fs), step, int(bool(refined)), _p(es, _f64p),
+            _p(out["best_angle"], _i32p), _p(out["best_score"], _f64p),
+            _p(out["evaluations"], _i64p), _p(out["feasibility_checks"], _i64p),
+            _p(out["pose"], _f64p), _p(out["status"], _i32p)))
+        self._batch = None
+        return out
+
+    def rotate_fragment(self, batch: LigandBatch, membership, axis, anchor, angles):
+        """gd_rotate_fragment_batch (rotate_fragment_into, geometry.hpp:161-186)."""
+        L, A = batch.n_ligands, int(batch.atom_offsets[-1])
+        fs, keep = self._fragset(batch, membership, axis, anchor)
+        ang = np.ascontiguousarray(np.atleast_1d(angles), dtype=np.float64)
+        pose, status = np.zeros((A, 3)), np.zeros(L, np.int32)
+        b = batch.c_struct()
+        self._check(self._lib.gd_rotate_fragment_batch(self._h, C.byref(b), C.byref(fs),
+                                                       _p(ang, _f64p), _p(pose, _f64p),
+                                                       _p(status, _i32p)))
+        self._batch = None
+        return pose, status
+
+    def check_bumps(self, batch: LigandBatch, membership, axis, anchor):
+        """gd_check_bumps_batch (check_bumps, geometry.hpp:199-213)."""
+        L = batch.n_ligands
+        fs, keep = self._fragset(batch, membership, axis, anchor)
+        feas, status = np.zeros(L, np.uint8), np.zeros(L, np.int32)
+        b = batch.c_struct()
+        self._check(self._lib.gd_check_bumps_batch(self._h, C.byref(b), C.byref(fs),
+                                                   _p(feas, _u8p), _p(status, _i32p)))
+        self._batch = None
+        return feas.astype(bool), status
+
+    def ligand_error(self, l: int) -> str:
+        buf = C.create_string_buffer(512)
+        self._check(self._lib.gd_ligand_error(self._h, l, buf, 512))
+        return buf.value.decode()
+
     def l2_gather_peak_gbs(self) -> float:
         g = C.c_double()
         self._check(self._lib.gd_l2_gather_peak(self._h, C.byref(g)))
@@ -467,6 +550,62 @@ class Docker:
             self._h, _p(p, _f64p), p.shape[1], p.shape[0],
             GD_FLAG_BRUTE_FORCE if brute else 0, _p(out, _f64p)))
         return out
+
+
+class MultiDocker:
+    """gd_multi: one process, several GPUs (or several contexts on one GPU),
+    cost-weighted chunks pulled from a shared cursor."""
+
+    def __init__(self, devices=None, n_devices: int = 0):
+        self._lib = lib()
+        h = C.c_void_p()
+        if devices is not None:
+            dv = np.ascontiguousarray(devices, dtype=np.int32)
+            rc = self._lib.gd_multi_create(_p(dv, _i32p), len(dv), C.byref(h))
+        else:
+            rc = self._lib.gd_multi_create(None, n_devices, C.byref(h))
+        if rc != GD_OK:
+            raise GeoDockError(rc, self._lib.gd_multi_last_error(None).decode())
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.gd_multi_destroy(self._h)
+            self._h = None
+
+    __del__ = close
+
+    def _check(self, rc: int):
+        if rc != GD_OK:
+            raise GeoDockError(rc, self._lib.gd_multi_last_error(self._h).decode())
+
+    @property
+    def size(self) -> int:
+        return int(self._lib.gd_multi_size(self._h))
+
+    def set_pocket(self, xyz: np.ndarray):
+        pts = np.ascontiguousarray(xyz, dtype=np.float64).reshape(-1, 3)
+        self._check(self._lib.gd_multi_set_pocket(self._h, _p(pts, _f64p), len(pts)))
+
+    def dock(self, batch: LigandBatch, knobs: Knobs, keep_poses: bool = False,
+             out: "DockResult | None" = None) -> DockResult:
+        K = knobs.slots
+        A = int(batch.atom_offsets[-1])
+        res = out if out is not None and out.fits(batch.n_ligands, K, A, keep_poses) \
+            else DockResult.empty(batch.n_ligands, K, A, keep_poses)
+        b, k, r = batch.c_struct(), knobs.c_struct(), res.c_struct()
+        self._check(self._lib.gd_multi_dock_batch(self._h, C.byref(b), C.byref(k), C.byref(r)))
+        return res
+
+    def ligand_error(self, l: int) -> str:
+        buf = C.create_string_buffer(512)
+        self._check(self._lib.gd_multi_ligand_error(self._h, l, buf, 512))
+        return buf.value.decode()
+
+    def stats(self) -> list:
+        out = (gd_multi_stats * self.size)()
+        self._check(self._lib.gd_multi_last_stats(self._h, out, self.size))
+        return [{"ligands": s.ligands, "chunks": s.chunks, "busy_ms": s.busy_ms} for s in out]
 
 
 # ---------------------------------------------------------------------------

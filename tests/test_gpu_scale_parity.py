@@ -109,15 +109,15 @@ def test_config4_every_knob_point(docker, point):
 
 
 def test_hollow_shell_pocket_overflow_voxels(docker):
-    """A hollow spherical shell: from the centre no surface point dominates
+    """A hollow spherical shell: near the centre no surface point dominates
     another, so interior voxels keep more than 1,024 candidates.  Those
     voxels scan the whole pocket (held once at the head of the list array)
     instead of listing it per voxel; minima stay exact and the index stays
     small."""
-    g = np.mgrid[-12:13, -12:13, -12:13].reshape(3, -1).T.astype(np.float64)
-    r = np.linalg.norm(g, axis=1)
-    shell = g[(r >= 10.5) & (r < 11.5)]
-    assert len(shell) > 1024
+    m = 1500  # Fibonacci sphere of radius 8 A: equidistant from the centre
+    k = np.arange(m) + 0.5
+    phi, th = np.arccos(1 - 2 * k / m), np.pi * (1 + 5 ** 0.5) * k
+    shell = 8.0 * np.stack([np.cos(th) * np.sin(phi), np.sin(th) * np.sin(phi), np.cos(phi)], 1)
     docker.set_pocket(shell)
     info = docker.pocket_info()
     # Without the shared head every overflow voxel would list the whole shell.
