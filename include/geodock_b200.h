@@ -268,10 +268,12 @@ typedef struct {
 } gd_device_result;
 int gd_device_results(const gd_ctx* ctx, gd_device_result* out);
 /* Exact work executed by the last call made with GD_FLAG_COUNT_WORK:
- * out[0..6] rigid kernel, out[8..14] flex kernel, each {point pairs, rotated
- * atoms, bump pairs, nearest-point queries, score-sum terms, candidate
- * evaluations, rigid-transformed atoms}.  DESIGN.md §4 turns them into FLOPs. */
-int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]);
+ * out[0..11] rigid kernel, out[16..27] flex kernel, each {fp64: point pairs,
+ * rotated atoms, bump pairs, nearest-point queries, score-sum terms,
+ * candidate evaluations, rigid-transformed atoms; fp32 screen: point pairs,
+ * rotated (or rigid-transformed) atoms, bump pairs, queries; candidates
+ * resolved exactly}.  DESIGN.md §4 turns them into FLOPs. */
+int gd_work_counters(const gd_ctx* ctx, uint64_t out[32]);
 /* Diagnostic: SM clock cycles the flex kernel's warps spent per phase in
  * the last GD_FLAG_COUNT_WORK call, summed over warps: out[0] chain start,
  * [1] step setup (axis, fragment list, prefix), [2] bump-pair prefilter,

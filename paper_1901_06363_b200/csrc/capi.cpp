@@ -174,7 +174,7 @@ struct PocketSlot {
   uint64_t last_use = 0;
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels];
+  DevBuf pts, pts32, vox_rec[kGridLevels], vox_lst[kGridLevels], vox_big[kGridLevels];
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
@@ -466,6 +466,20 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   GD_CUDA(ctx, slot->pts.ensure(padded.size() * sizeof(double)));
   GD_CUDA(ctx, cudaMemcpy(slot->pts.ptr, padded.data(), padded.size() * sizeof(double),
                           cudaMemcpyHostToDevice));
+  // fp32 copy with point indices: the fp32 screen's brute-force scan and
+  // the head of every level's list array (the overflow voxels' list).
+  std::vector<float> p32(4 * static_cast<size_t>(n));
+  double pmax = 0.0;
+  for (int32_t q = 0; q < n; ++q) {
+    for (int k = 0; k < 3; ++k) {
+      p32[4 * q + k] = static_cast<float>(padded[4 * q + k]);
+      pmax = std::max(pmax, std::fabs(padded[4 * q + k]));
+    }
+    uint32_t idx = static_cast<uint32_t>(q);
+    std::memcpy(&p32[4 * q + 3], &idx, 4);
+  }
+  GD_CUDA(ctx, slot->pts32.ensure(p32.size() * sizeof(float)));
+  GD_CUDA(ctx, cudaMemcpy(slot->pts32.ptr, p32.data(), p32.size() * sizeof(float), cudaMemcpyHostToDevice));
   static const bool kCull = env_double("GD_VOXEL_CULL", 1) != 0;
   const int n_tiles = kCull ? (n + 31) / 32 : 0;
   std::vector<float> tbox(6 * static_cast<size_t>(std::max(n_tiles, 1)), 0.0f);
@@ -494,8 +508,11 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   // beyond both fall back to the exact full scan.
   PocketView& v = slot->view;
   v.pts = slot->pts.as<double>();
+  v.pts32 = slot->pts32.as<float>();
   v.P = n;
   v.use_index = 1;
+  constexpr double kU = 1.0 / 16777216.0;  // fp32 unit roundoff 2^-24
+  double eloc = 0.0;  // fp32 voxel-locate misplacement, worst level
   slot->n_cand = 0;
   slot->max_cand = 0;
   // Edges/margins from A/B on config 1 (profiles/r1_voxel_ab.md, DESIGN
@@ -551,15 +568,18 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     const int64_t listed = tot[0], total = tot[1];
     const int32_t mx = static_cast<int32_t>(tot[2]);
-    if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
-    GD_CUDA(ctx, slot->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
-    GD_CUDA(ctx, slot->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
+    if (listed >= static_cast<int64_t>(kPayloadMask))
+      return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
+    GD_CUDA(ctx, slot->vox_rec[L].ensure(sizeof(float) * 4 * static_cast<size_t>(nv)));
+    GD_CUDA(ctx, slot->vox_big[L].ensure(sizeof(int32_t) * static_cast<size_t>(nv)));
+    GD_CUDA(ctx, slot->vox_lst[L].ensure(sizeof(float) * 4 * std::max<int64_t>(listed, 1)));
     // List head: the whole pocket, the list of every overflow voxel.
-    GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_pts[L].ptr, slot->pts.ptr, sizeof(double) * 4 * n,
+    GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_lst[L].ptr, slot->pts32.ptr, sizeof(float) * 4 * n,
                                  cudaMemcpyDeviceToDevice, ctx->stream));
     GD_CUDA(ctx, static_cast<cudaError_t>(
                      launch_voxel_fill(slot->pts.as<double>(), n, g, doff.as<int32_t>(),
-                                       slot->vox_off[L].as<double>(), slot->vox_pts[L].as<double>(),
+                                       slot->vox_rec[L].as<float>(), slot->vox_lst[L].as<float>(),
+                                       slot->vox_big[L].as<int32_t>(),
                                        ctx->tiles.as<float>(), n_tiles, counts.as<int32_t>(),
                                        keep, ctx->stream)));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -567,16 +587,29 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     slot->n_cand += total;
     slot->max_cand = std::max(slot->max_cand, mx);
     GridLevel& gl = v.lv[L];
-    gl.rec = slot->vox_off[L].as<double>();
-    gl.lst = slot->vox_pts[L].as<double>();
+    gl.rec = slot->vox_rec[L].as<float>();
+    gl.lst = slot->vox_lst[L].as<float>();
+    gl.big = slot->vox_big[L].as<int32_t>();
     gl.lo_x = g.lo_x;
     gl.lo_y = g.lo_y;
     gl.lo_z = g.lo_z;
     gl.inv_h = 1.0 / g.h;
+    gl.flo_x = static_cast<float>(g.lo_x);
+    gl.flo_y = static_cast<float>(g.lo_y);
+    gl.flo_z = static_cast<float>(g.lo_z);
+    gl.finv_h = static_cast<float>(gl.inv_h);
     gl.dim_x = g.dim_x;
     gl.dim_y = g.dim_y;
     gl.dim_z = g.dim_z;
+    // fp32 locate: (x - flo) * finv_h misplaces a point by at most a few
+    // roundings of the origin and the in-grid offset, per axis.
+    const double lomax = std::max({std::fabs(g.lo_x), std::fabs(g.lo_y), std::fabs(g.lo_z)});
+    const double ext = g.h * std::max({g.dim_x, g.dim_y, g.dim_z});
+    eloc = std::max(eloc, 8.0 * kU * std::sqrt(3.0) * (lomax + 2.0 * ext));
   }
+  // Screen distance error of the pocket side: fp32 point rounding plus
+  // twice the misplacement (the fp32 screen).
+  v.eps = static_cast<float>(1.01 * (std::sqrt(3.0) * kU * pmax + 2.0 * eloc));
   slot->P = n;
   activate(*slot);
   return GD_OK;
@@ -1605,10 +1638,10 @@ extern "C" int gd_device_results(const gd_ctx* ctx, gd_device_result* out) {
   return GD_OK;
 }
 
-extern "C" int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]) {
+extern "C" int gd_work_counters(const gd_ctx* ctx, uint64_t out[32]) {
   if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
   if (!ctx->counted) return GD_ERR_INVALID;
-  if (cudaMemcpy(out, ctx->counters.ptr, sizeof(uint64_t) * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (cudaMemcpy(out, ctx->counters.ptr, sizeof(uint64_t) * 32, cudaMemcpyDeviceToHost) != cudaSuccess)
     return GD_ERR_CUDA;
   return GD_OK;
 }

@@ -208,19 +208,16 @@ __device__ __forceinline__ void bump_item(const WarpMem& s, const DockParams& p,
   if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < dmul(cut, cut)) bl |= 1u << c;
 }
 
-// Query phase: lanes over (live candidate, fragment atom), two items per
-// lane per iteration (t, t + 32) so both nearest-point lookups are in flight;
-// candidate c's term of atom i lands in v[c * n + i].
-#ifndef GD_QUERY_MLP
-#define GD_QUERY_MLP 1       // lookups in flight per lane in the query phase (1 or 2; r2h: 1 wins, c1 flex 13.63 -> 12.36 ms)
-#endif
+// Query phase: lanes over (live candidate, fragment atom), one exact
+// nearest-point lookup per lane per iteration (r2h: beats two in flight
+// once registers were cut); candidate c's term of atom i lands in
+// v[c * n + i].
 template <bool On>
 __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& p, const Axis& X,
                                             int n, int nf, unsigned live, int a0, int da, int nb,
                                             int lane, Work<On>& wk) {
   const int tq = nb * nf;
   const float rnf = 1.0f / static_cast<float>(nf);
-#if GD_QUERY_MLP == 1
   for (int t = lane; t < tq; t += 32) {
     const int c = qdiv(t, rnf);
     if (!((live >> c) & 1u)) continue;
@@ -232,27 +229,6 @@ __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& 
     rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
     wk.add(kRot, 1);
     s.v[c * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
-  }
-  return;
-#endif
-  for (int t = lane; t < tq; t += 64) {
-    const int c0 = qdiv(t, rnf);
-    const int t1 = t + 32 < tq ? t + 32 : t;
-    const int c1 = qdiv(t1, rnf);
-    const bool l0 = (live >> c0) & 1u, l1 = t1 != t && ((live >> c1) & 1u);
-    if (!l0 && !l1) continue;
-    const int i0 = s.fidx[t - c0 * nf], i1 = s.fidx[t1 - c1 * nf];
-    const int a0c = a0 + c0 * da, a1c = a0 + c1 * da;
-    const double cs0 = __ldg(p.cos_deg + a0c), sn0 = __ldg(p.sin_deg + a0c);
-    const double cs1 = __ldg(p.cos_deg + a1c), sn1 = __ldg(p.sin_deg + a1c);
-    double x0, y0, z0, x1, y1, z1, m0, m1;
-    const PT q0 = s.pt[i0], q1 = s.pt[i1];
-    rodrigues(X, cs0, sn0, dsub(1.0, cs0), q0.x, q0.y, q0.z, x0, y0, z0);
-    rodrigues(X, cs1, sn1, dsub(1.0, cs1), q1.x, q1.y, q1.z, x1, y1, z1);
-    wk.add(kRot, 2);
-    min_dist_sq2(p.pocket, x0, y0, z0, x1, y1, z1, m0, m1, wk);
-    if (l0) s.v[c0 * n + i0] = fmax(kMinDistanceSq, m0);
-    if (l1) s.v[c1 * n + i1] = fmax(kMinDistanceSq, m1);
   }
 }
 
@@ -770,7 +746,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       dst[3 * i + 2] = q.z;
     }
   }
-  publish_warp(wk, p.counters, 8, lane);
+  publish_warp(wk, p.counters, kFlexWorkBase, lane);
   ck.publish(p.counters, lane);
 }
 
@@ -826,7 +802,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       out[a] = 0.0;
       vout[a] = 0;
     }
-    publish_warp(wk, p.counters, 8, lane);
+    publish_warp(wk, p.counters, kFlexWorkBase, lane);
     return;
   }
   bool b0 = false;
@@ -856,7 +832,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       out[a0 + lane] = ok ? sc : 0.0;
     }
   }
-  publish_warp(wk, p.counters, 8, lane);
+  publish_warp(wk, p.counters, kFlexWorkBase, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -942,7 +918,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     io.evaluations[l] = evals;
     io.checks[l] = checks;
   }
-  publish_warp(wk, p.counters, 8, lane);
+  publish_warp(wk, p.counters, kFlexWorkBase, lane);
 }
 
 // rotate_fragment_into (geometry.hpp:161-186): the axis from the staged

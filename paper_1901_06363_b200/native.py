@@ -25,7 +25,8 @@ GD_LIG_DEGENERATE = 3
 GD_FLAG_BRUTE_FORCE = 1
 GD_FLAG_KEEP_POSES = 2
 GD_FLAG_COUNT_WORK = 4
-WORK_FIELDS = ["pairs", "rotated", "bump_pairs", "queries", "sum_terms", "evaluations", "xform"]
+WORK_FIELDS = ["pairs", "rotated", "bump_pairs", "queries", "sum_terms", "evaluations", "xform",
+               "pairs32", "rotated32", "bump_pairs32", "queries32", "exact_resolved"]
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -436,9 +437,10 @@ class Docker:
 
     def work_counters(self) -> dict:
         """Executed work of the last call made with GD_FLAG_COUNT_WORK."""
-        out = (C.c_uint64 * 16)()
+        out = (C.c_uint64 * 32)()
         self._check(self._lib.gd_work_counters(self._h, out))
-        return {"rigid": dict(zip(WORK_FIELDS, out[0:7])), "flex": dict(zip(WORK_FIELDS, out[8:15]))}
+        n = len(WORK_FIELDS)
+        return {"rigid": dict(zip(WORK_FIELDS, out[0:n])), "flex": dict(zip(WORK_FIELDS, out[16:16 + n]))}
 
     def phase_clocks(self) -> list:
         """Flex-kernel SM cycles per phase (GD_PHASE_CLOCKS builds; zeros otherwise)."""
