@@ -9,10 +9,12 @@
  * geodock::screen, geodock::overlap_score, ...), including its exception
  * messages; bindings for other hosts (ctypes, cgo, JNI) bind this file.
  *
- * Numerics: every score, coordinate and decision is computed in fp64 with
- * the reference's exact expression trees (no FMA contraction, atom-order
- * sums, host-built trig tables), so results are bit-identical to the
- * reference CPU path.  See DESIGN.md.
+ * Numerics: every reported score, coordinate and every decision equals the
+ * reference CPU path bit for bit.  Candidates are screened in fp32 with
+ * rigorous error bounds; whatever the bounds cannot decide, and every
+ * committed pose and reported score, is computed in fp64 with the
+ * reference's exact expression trees (no FMA contraction, atom-order sums,
+ * host-built trig tables).  See DESIGN.md.
  *
  * Threading: one gd_ctx per device, not thread-safe per context.
  */
@@ -43,6 +45,8 @@ extern "C" {
 #define GD_FLAG_BRUTE_FORCE 1u /* scan every pocket point instead of the voxel index */
 #define GD_FLAG_KEEP_POSES 2u  /* gd_dock_resident: keep final poses for gd_download */
 #define GD_FLAG_COUNT_WORK 4u  /* count executed work (gd_work_counters) */
+#define GD_FLAG_EXACT_FP64 8u  /* no fp32 screens: every candidate in the fp64 recipe
+                                  (same results; for A/B and as a parity cross-check) */
 
 typedef struct gd_ctx gd_ctx;
 

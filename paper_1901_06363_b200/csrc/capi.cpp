@@ -204,7 +204,7 @@ struct gd_ctx {
   PocketView view{};
   DevBuf tiles, vox_counts, vox_doff, vox_keep, vox_scan;
 
-  DevBuf cos_t, sin_t;
+  DevBuf cos_t, sin_t, cos32_t, sin32_t;
   int orient_step = -1;
   int32_t n_orient = 0;
   std::vector<int32_t> orient_idx_host;
@@ -286,6 +286,15 @@ extern "C" int gd_create(int device, gd_ctx** out) {
   ctx->stream = ctx->own_stream;
   std::vector<double> c, s;
   trig_tables(c, s);
+  std::vector<float> c32(c.begin(), c.end()), s32(s.begin(), s.end());
+  if (ctx->cos32_t.ensure(360 * sizeof(float)) != cudaSuccess ||
+      ctx->sin32_t.ensure(360 * sizeof(float)) != cudaSuccess ||
+      cudaMemcpy(ctx->cos32_t.ptr, c32.data(), 360 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemcpy(ctx->sin32_t.ptr, s32.data(), 360 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
+    g_create_error = "gd_create: trig table upload failed";
+    delete ctx;
+    return GD_ERR_CUDA;
+  }
   if (ctx->cos_t.ensure(360 * sizeof(double)) != cudaSuccess ||
       ctx->sin_t.ensure(360 * sizeof(double)) != cudaSuccess ||
       cudaMemcpy(ctx->cos_t.ptr, c.data(), 360 * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -912,10 +921,13 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockPara
   p.orient_R = ctx->orient_R.as<double>();
   p.cos_deg = ctx->cos_t.as<double>();
   p.sin_deg = ctx->sin_t.as<double>();
+  p.cos32 = ctx->cos32_t.as<float>();
+  p.sin32 = ctx->sin32_t.as<float>();
   p.hp = k->high_precision_step;
   p.lp = k->low_precision_step;
   p.reps = k->repetitions;
   p.refine = k->enable_refinement ? 1 : 0;
+  p.screen = (k->flags & GD_FLAG_EXACT_FP64) ? 0 : 1;
   p.tile = gd_optimal_tile_size(k->high_precision_step);
   p.threshold = k->threshold;
   p.top_k = K;
@@ -1390,6 +1402,8 @@ static int stage_fragments(gd_ctx* ctx, const gd_ligand_batch* b, const gd_fragm
   p.pocket = ctx->view;
   p.cos_deg = ctx->cos_t.as<double>();
   p.sin_deg = ctx->sin_t.as<double>();
+  p.cos32 = ctx->cos32_t.as<float>();
+  p.sin32 = ctx->sin32_t.as<float>();
   p.max_n = max_n;
   p.max_pairs = std::max(1, max_n * max_n / 4);
   p.status = ctx->o_status.as<int32_t>();
@@ -1581,6 +1595,8 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores,
     p.pocket.use_index = (flags & GD_FLAG_BRUTE_FORCE) ? 0 : ctx->view.use_index;
     p.cos_deg = ctx->cos_t.as<double>();
     p.sin_deg = ctx->sin_t.as<double>();
+    p.cos32 = ctx->cos32_t.as<float>();
+    p.sin32 = ctx->sin32_t.as<float>();
     p.max_n = ctx->max_n;
     p.max_pairs = std::max(1, ctx->max_n * ctx->max_n / 4);
     p.status = ctx->o_status.as<int32_t>();

@@ -86,6 +86,9 @@ struct DockParams {
   const double* orient_R;  // [n_orient*9] row-major
   const double* cos_deg;   // [360] std::cos(a * (pi/180)) from the host libm
   const double* sin_deg;   // [360]
+  const float* cos32;      // [360] the same rounded to fp32 (the screens)
+  const float* sin32;      // [360]
+  int32_t screen;          // 1: fp32 screens with exact resolution; 0: fp64 throughout
 
   // Knobs (kernel.hpp:21-26) + batch knobs.
   int32_t hp, lp, reps, refine, tile;

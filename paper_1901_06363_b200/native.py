@@ -25,6 +25,7 @@ GD_LIG_DEGENERATE = 3
 GD_FLAG_BRUTE_FORCE = 1
 GD_FLAG_KEEP_POSES = 2
 GD_FLAG_COUNT_WORK = 4
+GD_FLAG_EXACT_FP64 = 8
 WORK_FIELDS = ["pairs", "rotated", "bump_pairs", "queries", "sum_terms", "evaluations", "xform",
                "pairs32", "rotated32", "bump_pairs32", "queries32", "exact_resolved"]
 
