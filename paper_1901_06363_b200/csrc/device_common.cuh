@@ -181,9 +181,13 @@ __device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, do
       }
       const float* l = g.lst + 4 * static_cast<size_t>(hw & kPayloadMask);
       double m = __longlong_as_double(0x7ff0000000000000ll);
-      for (int k = 0; k < cnt; ++k) {
-        const P3 p = ldp<GD_LST_NA>(pk.pts, static_cast<int>(ldw(l + 4 * k)));
-        m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+      for (int k = 0; k < cnt; k += 2) {  // two candidates per round in flight
+        const bool two = k + 1 < cnt;
+        const uint32_t i0 = ldw(l + 4 * k), i1 = two ? ldw(l + 4 * (k + 1)) : i0;
+        const P3 p0 = ldp<GD_LST_NA>(pk.pts, static_cast<int>(i0));
+        const P3 p1 = ldp<GD_LST_NA>(pk.pts, static_cast<int>(i1));
+        m = fmin(m, dist_sq(x, y, z, p0.x, p0.y, p0.z));
+        m = fmin(m, dist_sq(x, y, z, p1.x, p1.y, p1.z));
       }
       return m;
     }
@@ -198,37 +202,77 @@ __device__ __noinline__ float min_d2_brute_f32(const float* pts32, int P, float 
   return m;
 }
 
-// fp32 screen query: min over the candidate list of the voxel containing
-// the fp32 point, located in fp32, of fp32 squared distances to the fp32
-// coordinates.  Within the error bound of screen_term_error() of the exact
-// minimum at the exact (fp64) position.
-template <bool On>
-__device__ __forceinline__ float min_d2_f32(const PocketView& pk, float x, float y, float z,
-                                            Work<On>& w) {
-  w.add(kQuery32, 1);
-  if (pk.use_index) {
+// fp32 screen queries, M at a time: min over the candidate list of the
+// voxel containing each fp32 point (located in fp32) of fp32 squared
+// distances to the fp32 coordinates; within the error bound the screens
+// derive (flex.cu: screen_scores) of the exact minimum at the exact (fp64)
+// position.  Latency-bound gathers, so everything is issued as early as
+// possible: the M record loads together, then the lists walked two
+// entries per query per round (2M loads in flight).
+template <int M, bool On>
+__device__ __forceinline__ void min_d2_f32(const PocketView& pk, const float* x, const float* y,
+                                           const float* z, float* m, Work<On>& w) {
+  w.add(kQuery32, M);
+  int lv[M], vox[M];
 #pragma unroll
-    for (int L = 0; L < kGridLevels; ++L) {
-      const GridLevel& g = pk.lv[L];
-      const int v = voxel_of(g, (x - g.flo_x) * g.finv_h, (y - g.flo_y) * g.finv_h,
-                             (z - g.flo_z) * g.finv_h);
-      if (v < 0) continue;
-      const F4 r = ld128(g.rec + 4 * static_cast<size_t>(v));
-      float m = d2f(x, y, z, r);
-      const int cf = static_cast<int>(r.w >> kCountShift);
-      if (cf != 1) {
-        const int cnt = cf ? cf : __ldg(g.big + v);
-        const float* l = g.lst + 4 * static_cast<size_t>(r.w & kPayloadMask);
-        for (int k = 1; k < cnt; ++k) m = fminf(m, d2f(x, y, z, ld128(l + 4 * k)));
-        w.add(kPairs32, cnt);
-      } else {
-        w.add(kPairs32, 1);
+  for (int r = 0; r < M; ++r) {
+    lv[r] = -1;
+    vox[r] = 0;
+    if (pk.use_index) {
+#pragma unroll
+      for (int L = kGridLevels - 1; L >= 0; --L) {  // the finest level containing the point wins
+        const GridLevel& g = pk.lv[L];
+        const int v = voxel_of(g, (x[r] - g.flo_x) * g.finv_h, (y[r] - g.flo_y) * g.finv_h,
+                               (z[r] - g.flo_z) * g.finv_h);
+        if (v >= 0) {
+          lv[r] = L;
+          vox[r] = v;
+        }
       }
-      return m;
     }
   }
-  w.add(kPairs32, pk.P);
-  return min_d2_brute_f32(pk.pts32, pk.P, x, y, z);
+  F4 rec[M];
+  const float* lst[M];
+  int cnt[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    const GridLevel& g = pk.lv[lv[r] > 0 ? 1 : 0];
+    rec[r] = lv[r] >= 0 ? ld128(g.rec + 4 * static_cast<size_t>(vox[r])) : F4{0.f, 0.f, 0.f, 1u << kCountShift};
+    lst[r] = g.lst;
+  }
+  int most = 1;
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    const GridLevel& g = pk.lv[lv[r] > 0 ? 1 : 0];
+    const int cf = static_cast<int>(rec[r].w >> kCountShift);
+    cnt[r] = cf ? cf : __ldg(g.big + vox[r]);
+    lst[r] += 4 * static_cast<size_t>(rec[r].w & kPayloadMask);
+    m[r] = d2f(x[r], y[r], z[r], rec[r]);
+    w.add(kPairs32, lv[r] >= 0 ? cnt[r] : 0);
+    most = max(most, cnt[r]);
+  }
+#if GD_WHATIF_NOLIST
+  most = 1;  // timing experiment only: wrong minima
+#endif
+  for (int k = 1; k < most; k += 2) {
+    F4 e0[M], e1[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      if (k < cnt[r]) e0[r] = ld128(lst[r] + 4 * k);
+      if (k + 1 < cnt[r]) e1[r] = ld128(lst[r] + 4 * (k + 1));
+    }
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      if (k < cnt[r]) m[r] = fminf(m[r], d2f(x[r], y[r], z[r], e0[r]));
+      if (k + 1 < cnt[r]) m[r] = fminf(m[r], d2f(x[r], y[r], z[r], e1[r]));
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < M; ++r)
+    if (lv[r] < 0) {  // beyond both grids: the whole pocket
+      w.add(kPairs32, pk.P);
+      m[r] = min_d2_brute_f32(pk.pts32, pk.P, x[r], y[r], z[r]);
+    }
 }
 
 // Rodrigues rotation of one atom (geometry.hpp:182-184):

@@ -82,6 +82,9 @@ constexpr int kFoldUnroll = GD_FOLD_UNROLL;
 #define GD_META_RELOAD 0     // 1: ligand descriptor fields re-read from global when used (r2b's
                              // win; after r2h's query change 0 is 0.4% faster)
 #endif
+#ifndef GD_SCREEN_MLP
+#define GD_SCREEN_MLP 1      // fp32 screen queries in flight per lane
+#endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
@@ -174,7 +177,7 @@ __device__ __forceinline__ int qdiv(int t, float rcp) {
 // Per-phase SM-clock attribution of a chain (diagnostic builds only; the
 // disabled form compiles to nothing).
 enum Phase { kPhInit, kPhSetup, kPhPrefilter, kPhPrefill, kPhBump, kPhQuery, kPhFold, kPhDecide,
-             kPhCommit, kPhases };
+             kPhCommit, kPhBound, kPhases };
 template <bool On>
 struct Clocks {
   long long last;
@@ -702,7 +705,7 @@ __device__ __forceinline__ void turn32(const Screen& sc, const float4& v, float 
 // The reference's bump rule for one pair at one angle, in fp64
 // (geometry.hpp:182-184, :199-213): the rare re-check of a pair whose fp32
 // distance falls inside the error band.
-__device__ __noinline__ bool exact_bump(const WarpMem& s, const DockParams& p, int i, int j, int a) {
+__device__ __forceinline__ bool exact_bump(const WarpMem& s, const DockParams& p, int i, int j, int a) {
   const Axis& X = *s.ax;
   const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
   const PT ai = s.pt[i], aj = s.pt[j];
@@ -780,25 +783,46 @@ __device__ __forceinline__ unsigned screen_bumps(const WarpMem& s, const DockPar
 // D = distance error dq: |t32 - t64| <= 8u t + D (t + 1) + D^2 (the list
 // of the voxel holding the fp32 point gives its exact nearest distance;
 // distances are 1-Lipschitz in the point; 2 sqrt(t) D <= D (t + 1)).
-template <bool On>
+template <bool On, class CK>
 __device__ __forceinline__ void screen_scores(const WarpMem& s, const DockParams& p, const Screen& sc,
                                               int n, int nf, unsigned live, int nb, int lane,
-                                              double& lo, double& hi, Work<On>& wk) {
+                                              double& lo, double& hi, Work<On>& wk, CK& ck) {
   float* tq = reinterpret_cast<float*>(s.v);
   const int tot = nb * nf;
   const float rnf = 1.0f / static_cast<float>(nf);
-  for (int t = lane; t < tot; t += 32) {
-    const int c = qdiv(t, rnf);
-    if (!((live >> c) & 1u)) continue;
-    const int sl = t - c * nf;
-    const int a = s.ang[c];
-    const float cs = __ldg(p.cos32 + a), sn = __ldg(p.sin32 + a);
-    float rx, ry, rz;
-    turn32(sc, s.vf[s.fidx[sl]], cs, sn, 1.0f - cs, rx, ry, rz);
-    wk.add(kRot32, 1);
-    tq[t] = fmaxf(1e-12f, min_d2_f32(p.pocket, sc.ox + rx, sc.oy + ry, sc.oz + rz, wk));
+  // GD_SCREEN_MLP items per lane per round, their lookups in flight together.
+  constexpr int M = GD_SCREEN_MLP;
+  for (int t0 = lane; t0 < tot; t0 += 32 * M) {
+    float qx[M], qy[M], qz[M], m[M];
+    bool act[M];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      const int t = t0 + 32 * r;
+      const int c = qdiv(min(t, tot - 1), rnf);
+      act[r] = t < tot && ((live >> c) & 1u);
+      const int sl = min(t, tot - 1) - c * nf;
+      const int a = s.ang[c];
+      const float cs = __ldg(p.cos32 + a), sn = __ldg(p.sin32 + a);
+      float rx, ry, rz;
+      turn32(sc, s.vf[s.fidx[sl]], cs, sn, 1.0f - cs, rx, ry, rz);
+      qx[r] = sc.ox + rx;
+      qy[r] = sc.oy + ry;
+      qz[r] = sc.oz + rz;
+    }
+    bool any = false;
+#pragma unroll
+    for (int r = 0; r < M; ++r) any |= act[r];
+    if (!any) continue;
+    min_d2_f32<M>(p.pocket, qx, qy, qz, m, wk);
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+      if (act[r]) {
+        tq[t0 + 32 * r] = fmaxf(1e-12f, m[r]);
+        wk.add(kRot32, 1);
+      }
   }
   __syncwarp();
+  ck.mark(kPhQuery);
   lo = hi = -kInfinity;
   if (lane < nb && ((live >> lane) & 1u)) {
     float a = 0.0f;
@@ -862,6 +886,7 @@ __device__ __forceinline__ void search_flat_screened(const WarpMem& s, const Doc
                                                      int& best_a, double& best, bool& exact_after,
                                                      int& evals, int& checks, Work<On>& wk, CK& ck) {
   const Screen sc = screen_setup(s, p, X, n, lane);
+  ck.mark(kPhPrefill);
   const int A = 360 / step;
   double L = cur;  // best lower bound so far (the committed pose: exact)
   int ns = 0, nfeas = 0;
@@ -875,8 +900,8 @@ __device__ __forceinline__ void search_flat_screened(const WarpMem& s, const Doc
     nfeas += __popc(live);
     ck.mark(kPhBump);
     double lo, hi;
-    screen_scores(s, p, sc, n, nf, live, nb, lane, lo, hi, wk);
-    ck.mark(kPhQuery);
+    screen_scores(s, p, sc, n, nf, live, nb, lane, lo, hi, wk, ck);
+    ck.mark(kPhBound);
     L = fmax(L, warp_max(lo));
     // Drop survivors the new bound rules out, then add this batch's.
     const bool keep = lane < ns && s.sv[lane].hi >= L;

@@ -6,6 +6,6 @@ for v in "$@"; do
     echo "variant $v BUILD FAILED" >> gpurun_out/ab_defs.log; continue
   fi
   echo "variant $v" >> gpurun_out/ab_defs.log
-  timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e >> gpurun_out/ab_defs.log 2>&1
+  timeout 300 python tools/quick_bench.py --configs ${AB_CONFIGS:-1 2} >> gpurun_out/ab_defs.log 2>&1
 done
 python paper_1901_06363_b200/build.py --force > /dev/null 2>&1

@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--configs", type=int, nargs="+", default=[1, 2])
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--count", action="store_true")
+    ap.add_argument("--exact", action="store_true", help="GD_FLAG_EXACT_FP64: no fp32 screens")
     a = ap.parse_args()
     d = Docker(0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -32,11 +33,14 @@ def main():
         batch = w.ligands()
         d.set_pocket(pocket)
         d.upload(batch)
+        from paper_1901_06363_b200 import Knobs
+        from paper_1901_06363_b200.native import GD_FLAG_EXACT_FP64
+        knobs = Knobs(**{**w.knobs.__dict__, "flags": GD_FLAG_EXACT_FP64 if a.exact else 0})
         rows = []
         for r in range(a.reps + 2):
             flush.random_()
             torch.cuda.synchronize()
-            d.dock_resident(w.knobs)
+            d.dock_resident(knobs)
             t = d.timing()
             if r >= 2:
                 rows.append((t["rigid_ms"], t["flex_ms"], t["total_ms"]))
@@ -44,8 +48,7 @@ def main():
         out = {"config": c, "rigid_ms": med[0], "flex_ms": med[1], "total_ms": med[2],
                "ligands_per_s": batch.n_ligands / (med[2] * 1e-3)}
         if a.count:
-            from paper_1901_06363_b200 import Knobs
-            k = Knobs(**{**w.knobs.__dict__, "flags": GD_FLAG_COUNT_WORK})
+            k = Knobs(**{**knobs.__dict__, "flags": knobs.flags | GD_FLAG_COUNT_WORK})
             d.dock_resident(k)
             out["work"] = d.work_counters()
         print(json.dumps(out), flush=True)
