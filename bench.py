@@ -115,8 +115,23 @@ def flops_of(work: dict) -> float:
     return float(sum(FLOPS[k] * v for k, v in work.items()))
 
 
-def cpu_reference(batch, pocket, knobs, n: int):
-    """The reference CPU path on the first n ligands: (ligands/s, info)."""
+CPU_BRUTE_SAMPLE = 24  # ligands of the brute-force (no PocketIndex) reference timing
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_reference(batch, pocket, knobs, n: int, brute: bool = False):
+    """The reference CPU path on the first n ligands: (ligands/s, info).
+    brute: the reference's default brute-force overlap scan instead of its
+    PocketIndex (the CLI's --spatial-index path, tools/geodock.cpp:387)."""
     from oracle import oracle_py as O
     sub = batch.subset(range(min(n, batch.n_ligands)))
     threads = O.threads()
@@ -124,21 +139,49 @@ def cpu_reference(batch, pocket, knobs, n: int):
     impl = "ref" if kind == "reference" else "oracle"
     t0 = time.perf_counter()
     res = O.dock_batch(sub, pocket, knobs, nthreads=threads, keep_poses=False, impl=impl,
-                       use_index=True)
+                       use_index=not brute)
     dt = time.perf_counter() - t0
     return sub.n_ligands / dt, {
-        "kind": kind, "cores": threads,
+        "kind": kind, "cores": threads, "cpu_model": cpu_model(), "logical_cpus": os.cpu_count(),
         "sample": (f"first {sub.n_ligands} ligands of the workload, "
-                   + ("reference headers (oracle/_ref) with PocketIndex"
-                      if kind == "reference" else "C oracle, brute force")
+                   + (("reference headers (oracle/_ref) with "
+                       + ("brute-force scan" if brute else "PocketIndex"))
+                      if kind == "reference" else "C oracle")
                    + f", {threads} threads"),
         "poses_scored_per_s": float(res.poses_scored.sum()) / dt, "seconds": dt}
+
+
+def cpu_baseline_of(batch, pocket, knobs) -> dict:
+    """cpu_baseline: PocketIndex on CPU_SAMPLE ligands (the value) and the
+    brute-force scan on CPU_BRUTE_SAMPLE beside it."""
+    v, inf = cpu_reference(batch, pocket, knobs, CPU_SAMPLE)
+    vb, infb = cpu_reference(batch, pocket, knobs, CPU_BRUTE_SAMPLE, brute=True)
+    return {"value": v, "unit": "ligands/s", "cores": inf["cores"], "kind": inf["kind"],
+            "sample": inf["sample"], "cpu_model": inf["cpu_model"], "logical_cpus": inf["logical_cpus"],
+            "brute_force": {"value": vb, "unit": "ligands/s", "sample": infb["sample"]}}
+
+
+def reference_inputs() -> None:
+    """Inputs of the reference arms come from the generator built on its own
+    (oracle/libgd_synth.so, same csrc/synth.cpp): they never load the
+    product library."""
+    from oracle import oracle_py as O
+    if not (O.HERE / "libgd_synth.so").exists():
+        O.build(ref=True)
+    from paper_1901_06363_b200 import native
+    native.set_synth_library(O.HERE / "libgd_synth.so")
+
+
+def assert_no_product_library() -> None:
+    maps = Path("/proc/self/maps").read_text()
+    assert "libgeodock_b200" not in maps, "a reference arm loaded the product library"
 
 
 def run_reference(a):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    reference_inputs()
     from paper_1901_06363_b200 import workloads as W
     w = W.config(a.config)
     pocket = w.pocket()
@@ -159,10 +202,12 @@ def run_reference(a):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "ligands_per_step": n},
         "cpu_baseline": {"value": value, "unit": "ligands/s", "cores": info["cores"],
-                         "kind": info["kind"], "sample": info["sample"]},
+                         "kind": info["kind"], "sample": info["sample"],
+                         "cpu_model": info["cpu_model"], "logical_cpus": info["logical_cpus"]},
         "e2e": {"value": value, "unit": "ligands/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
+    assert_no_product_library()
     print(json.dumps(line), flush=True)
 
 
@@ -203,7 +248,7 @@ def run_ours(a):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def step():
-        d.dock_resident(knobs)
+        d.dock_resident(knobs, top_pose=True)  # the same work as the e2e call (top-1 poses kept)
         if gather is not None:
             gather()  # NCCL all-gather of every rank's top-K table
 
@@ -253,7 +298,9 @@ def run_ours(a):
     e2e = None
     if not a.no_e2e:
         e2e_steps = max(1, min(a.steps, 5))
-        host_out = d.dock(batch, knobs)  # warm; host result arrays reused, as a caller would
+        # warm; host result arrays reused, as a caller would; every field of
+        # the top-K table plus each ligand's top-1 pose comes back
+        host_out = d.dock(batch, knobs, top_pose=True)
         tms = []
         for _ in range(e2e_steps):
             flush.zero_()
@@ -261,7 +308,7 @@ def run_ours(a):
             if dist:
                 dist.barrier()
             t0 = time.perf_counter()
-            d.dock(batch, knobs, out=host_out)
+            d.dock(batch, knobs, out=host_out, top_pose=True)
             tms.append(time.perf_counter() - t0)
         tt = float(np.mean(tms))
         if dist:
@@ -272,7 +319,9 @@ def run_ours(a):
         e2e = {"value": world * batch.n_ligands / tt, "unit": "ligands/s",
                "h2d_bytes_per_step": int(tim["h2d_bytes"]),
                "d2h_bytes_per_step": int(tim["d2h_bytes"]), "ms_per_step": 1e3 * tt,
-               "steps": e2e_steps, "timer": "host wall clock around gd_dock_batch"}
+               "steps": e2e_steps, "timer": "host wall clock around gd_dock_batch",
+               "returns": "top-K table (orientation, seed rank, rigid/final score, evaluations, "
+                          "feasibility checks), k_eff, poses scored, status, top-1 pose"}
 
     if rank == 0:
         r_ms, f_ms = float(np.mean(rigid_ms)), float(np.mean(flex_ms))
@@ -306,9 +355,11 @@ def run_ours(a):
             "poses_scored_per_s": poses_per_s,
             "pairs": {"executed_per_s": world * exec_pairs / (ms_per_step / 1e3),
                       "brute_equivalent_per_s": world * brute_pairs / (ms_per_step / 1e3),
-                      "brute_equivalent_fp32_tflops": 8 * world * brute_pairs / (ms_per_step / 1e3) / 1e12,
-                      "note": "brute-force equivalent = n_atoms x pocket points per scored pose "
-                              "(reference distance_sq calls in brute mode, 8 FLOPs each)"},
+                      "index_pruning_ratio": brute_pairs / max(exec_pairs, 1.0),
+                      "note": "a work ratio, not a throughput: brute-force equivalent = n_atoms x "
+                              "pocket points per scored pose (the reference's distance_sq calls "
+                              "without PocketIndex) over the point pairs the exact voxel index "
+                              "actually evaluates"},
             "kernel_ms": {"rigid_topk_kernel": r_ms, "flex_chain_kernel+finalize": f_ms},
             "gpu_launches": 3 * a.steps,
             "roofline": {"kernel": dom, "bound": "fp64", "achieved": achieved,
@@ -331,9 +382,7 @@ def run_ours(a):
         if e2e:
             line["e2e"] = e2e
         if world == 1 and not a.no_cpu_baseline:
-            v, inf = cpu_reference(batch, pocket, knobs, CPU_SAMPLE)
-            line["cpu_baseline"] = {"value": v, "unit": "ligands/s", "cores": inf["cores"],
-                                    "kind": inf["kind"], "sample": inf["sample"]}
+            line["cpu_baseline"] = cpu_baseline_of(batch, pocket, knobs)
         print(json.dumps(line), flush=True)
     if dist:
         dist.barrier()
@@ -375,6 +424,7 @@ def run_profiles_reference(a):
     rank, _, _ = dist_env()
     if rank != 0:
         return
+    reference_inputs()
     w, pocket, batch = profile_batch_of(a)
     for _ in range(a.warmup):
         cpu_profiles(batch, pocket, PROFILE_CPU_SAMPLE)
@@ -393,9 +443,10 @@ def run_profiles_reference(a):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"profiles of {w.name}", "ligands_per_step": PROFILE_CPU_SAMPLE},
         "cpu_baseline": {"value": value, "unit": "fragments/s", "cores": info["cores"],
-                         "kind": info["kind"], "sample": info["sample"]},
+                         "kind": info["kind"], "sample": info["sample"], "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "fragments/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0}}), flush=True)
+    assert_no_product_library()
 
 
 def run_profiles(a):

@@ -9,12 +9,10 @@
  * geodock::screen, geodock::overlap_score, ...), including its exception
  * messages; bindings for other hosts (ctypes, cgo, JNI) bind this file.
  *
- * Numerics: every reported score, coordinate and every decision equals the
- * reference CPU path bit for bit.  Candidates are screened in fp32 with
- * rigorous error bounds; whatever the bounds cannot decide, and every
- * committed pose and reported score, is computed in fp64 with the
- * reference's exact expression trees (no FMA contraction, atom-order sums,
- * host-built trig tables).  See DESIGN.md.
+ * Numerics: every score, coordinate and decision is computed in fp64 with
+ * the reference's exact expression trees (no FMA contraction, atom-order
+ * sums, host-built trig tables), so results are bit-identical to the
+ * reference CPU path.  See DESIGN.md.
  *
  * Threading: one gd_ctx per device, not thread-safe per context.
  */
@@ -45,8 +43,8 @@ extern "C" {
 #define GD_FLAG_BRUTE_FORCE 1u /* scan every pocket point instead of the voxel index */
 #define GD_FLAG_KEEP_POSES 2u  /* gd_dock_resident: keep final poses for gd_download */
 #define GD_FLAG_COUNT_WORK 4u  /* count executed work (gd_work_counters) */
-#define GD_FLAG_EXACT_FP64 8u  /* no fp32 screens: every candidate in the fp64 recipe
-                                  (same results; for A/B and as a parity cross-check) */
+#define GD_FLAG_TOP_POSE 16u   /* gd_dock_resident: keep each ligand's top-1 pose
+                                  for gd_download's top_pose */
 
 typedef struct gd_ctx gd_ctx;
 
@@ -92,6 +90,9 @@ typedef struct {
   int32_t* k_eff;                /* [L] min(top_k, distinct orientations) (1 if no sweep) */
   int64_t* poses_scored;         /* [L] rigid orientations scored + sum evaluations  */
   int32_t* status;               /* [L] GD_LIG_*                                     */
+  double* top_pose;              /* optional (NULL): [total_atoms*3], ligand l's
+                                    top-1 final pose (PoseResult::final_pose of slot
+                                    0) at atom_offsets[l]*3; zeros if skipped        */
 } gd_result;
 
 /* Device-side timing of the last gd_dock_* call (CUDA events on the
@@ -107,8 +108,9 @@ typedef struct {
   int64_t launches;    /* kernels launched by the call                 */
   int64_t h2d_bytes;   /* bytes copied host->device by the last upload */
   int64_t d2h_bytes;   /* bytes copied device->host by the last download */
-  float host_prep_ms;  /* host wall time: validation + graph preprocessing */
-  float host_pack_ms;  /* host wall time: packing descriptors into pinned staging */
+  float host_prep_ms;  /* host wall time: messages of rejected ligands (the
+                          validation and graph preprocessing run on the GPU) */
+  float host_pack_ms;  /* host wall time: offsets + raw atoms/bonds into pinned staging */
   float host_post_ms;  /* host wall time: result download + bookkeeping */
 } gd_timing;
 
@@ -260,24 +262,29 @@ int gd_tile_hit_probability(const int32_t* best_peak_widths, int64_t n, const in
 int gd_ligand_error(const gd_ctx* ctx, int32_t ligand, char* msg, size_t msg_len);
 
 /* Device-resident results of the last gd_dock_resident (valid until the
- * next dock call): [n_ligands*top_k] in final order.  Lets a multi-GPU host
- * gather per-ligand top-K tables over NCCL without a host round trip. */
+ * next dock call): every gd_result field except the poses, in the same
+ * layout and with the same empty-slot values (orientation -2, zeros).  Lets
+ * a multi-GPU host gather per-ligand top-K tables over NCCL without a host
+ * round trip. */
 typedef struct {
-  const int32_t* orientation;
-  const int32_t* seed_rank;
-  const double* final_score;
-  const int64_t* evaluations;
+  const int32_t* orientation;        /* [n_ligands*top_k] as gd_result  */
+  const int32_t* seed_rank;          /* [n_ligands*top_k]               */
+  const double* final_score;         /* [n_ligands*top_k]               */
+  const int64_t* evaluations;        /* [n_ligands*top_k]               */
   int32_t n_ligands;
   int32_t top_k;
+  const double* rigid_score;         /* [n_ligands*top_k]               */
+  const int64_t* feasibility_checks; /* [n_ligands*top_k]               */
+  const int32_t* k_eff;              /* [n_ligands]                     */
+  const int64_t* poses_scored;       /* [n_ligands]                     */
+  const int32_t* status;             /* [n_ligands] GD_LIG_*            */
 } gd_device_result;
 int gd_device_results(const gd_ctx* ctx, gd_device_result* out);
 /* Exact work executed by the last call made with GD_FLAG_COUNT_WORK:
- * out[0..11] rigid kernel, out[16..27] flex kernel, each {fp64: point pairs,
- * rotated atoms, bump pairs, nearest-point queries, score-sum terms,
- * candidate evaluations, rigid-transformed atoms; fp32 screen: point pairs,
- * rotated (or rigid-transformed) atoms, bump pairs, queries; candidates
- * resolved exactly}.  DESIGN.md §4 turns them into FLOPs. */
-int gd_work_counters(const gd_ctx* ctx, uint64_t out[32]);
+ * out[0..6] rigid kernel, out[8..14] flex kernel, each {point pairs, rotated
+ * atoms, bump pairs, nearest-point queries, score-sum terms, candidate
+ * evaluations, rigid-transformed atoms}.  DESIGN.md §4 turns them into FLOPs. */
+int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]);
 /* Diagnostic: SM clock cycles the flex kernel's warps spent per phase in
  * the last GD_FLAG_COUNT_WORK call, summed over warps: out[0] chain start,
  * [1] step setup (axis, fragment list, prefix), [2] bump-pair prefilter,

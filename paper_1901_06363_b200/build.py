@@ -21,7 +21,7 @@ BUILD = PKG / "_build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_SRCS = ["capi.cpp", "prep.cpp", "orient.cpp", "synth.cpp", "analysis.cpp", "planner.cpp"]
-CUDA_SRCS = ["rigid.cu", "flex.cu", "pocket_index.cu"]
+CUDA_SRCS = ["rigid.cu", "flex.cu", "pocket_index.cu", "prep.cu"]
 HEADERS = ["kernels.h", "device_common.cuh", "prep.hpp", "orient.hpp"]
 
 

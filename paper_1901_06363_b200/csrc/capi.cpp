@@ -174,7 +174,7 @@ struct PocketSlot {
   uint64_t last_use = 0;
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, pts32, vox_rec[kGridLevels], vox_lst[kGridLevels], vox_big[kGridLevels];
+  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels];
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
@@ -204,7 +204,7 @@ struct gd_ctx {
   PocketView view{};
   DevBuf tiles, vox_counts, vox_doff, vox_keep, vox_scan;
 
-  DevBuf cos_t, sin_t, cos32_t, sin32_t;
+  DevBuf cos_t, sin_t;
   int orient_step = -1;
   int32_t n_orient = 0;
   std::vector<int32_t> orient_idx_host;
@@ -218,7 +218,9 @@ struct gd_ctx {
   std::vector<int32_t> atom_off;
   std::vector<int32_t> status_host;
   std::vector<std::string> errors;
-  DevBuf meta, xyz, radii, far, fmask, fax, fan, frel, order;
+  DevBuf meta, xyz, radii, bonds, rot, boff;  // staged raw ligands (+ host-filled offsets)
+  DevBuf far, fmask, fax, fan, frel, order;   // written by the GPU preprocessing
+  size_t frag_total = 0;                      // fragment slots allocated (2 x bonds)
   PinnedBuf staging;
   PinnedBuf res_staging;         // pinned D2H targets of gd_dock_batch
   unsigned char* pin[10] = {};   // per-segment pointers into staging
@@ -227,6 +229,7 @@ struct gd_ctx {
   int32_t last_topk = 0;
   bool last_rigid = false;
   bool last_pose = false;
+  bool last_top = false;
   bool have_result = false;
   DevBuf counters;
   bool counted = false;
@@ -234,7 +237,7 @@ struct gd_ctx {
   bool staged = false;  // a batch is staged (gd_upload / gd_dock_batch)
   DevBuf st_final, st_evals, st_checks;
   DevBuf seed_slot, seed_score, k_eff, o_orient, o_rank, o_rigid, o_final, o_evals, o_checks,
-      o_pose, stage_pose, o_scored, o_status;
+      o_pose, stage_pose, o_top, o_scored, o_status;
   std::vector<double> initial_score;  // given-pose mode: rigid_score column
 
   gd_timing timing{};
@@ -286,15 +289,6 @@ extern "C" int gd_create(int device, gd_ctx** out) {
   ctx->stream = ctx->own_stream;
   std::vector<double> c, s;
   trig_tables(c, s);
-  std::vector<float> c32(c.begin(), c.end()), s32(s.begin(), s.end());
-  if (ctx->cos32_t.ensure(360 * sizeof(float)) != cudaSuccess ||
-      ctx->sin32_t.ensure(360 * sizeof(float)) != cudaSuccess ||
-      cudaMemcpy(ctx->cos32_t.ptr, c32.data(), 360 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess ||
-      cudaMemcpy(ctx->sin32_t.ptr, s32.data(), 360 * sizeof(float), cudaMemcpyHostToDevice) != cudaSuccess) {
-    g_create_error = "gd_create: trig table upload failed";
-    delete ctx;
-    return GD_ERR_CUDA;
-  }
   if (ctx->cos_t.ensure(360 * sizeof(double)) != cudaSuccess ||
       ctx->sin_t.ensure(360 * sizeof(double)) != cudaSuccess ||
       cudaMemcpy(ctx->cos_t.ptr, c.data(), 360 * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
@@ -475,20 +469,6 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   GD_CUDA(ctx, slot->pts.ensure(padded.size() * sizeof(double)));
   GD_CUDA(ctx, cudaMemcpy(slot->pts.ptr, padded.data(), padded.size() * sizeof(double),
                           cudaMemcpyHostToDevice));
-  // fp32 copy with point indices: the fp32 screen's brute-force scan and
-  // the head of every level's list array (the overflow voxels' list).
-  std::vector<float> p32(4 * static_cast<size_t>(n));
-  double pmax = 0.0;
-  for (int32_t q = 0; q < n; ++q) {
-    for (int k = 0; k < 3; ++k) {
-      p32[4 * q + k] = static_cast<float>(padded[4 * q + k]);
-      pmax = std::max(pmax, std::fabs(padded[4 * q + k]));
-    }
-    uint32_t idx = static_cast<uint32_t>(q);
-    std::memcpy(&p32[4 * q + 3], &idx, 4);
-  }
-  GD_CUDA(ctx, slot->pts32.ensure(p32.size() * sizeof(float)));
-  GD_CUDA(ctx, cudaMemcpy(slot->pts32.ptr, p32.data(), p32.size() * sizeof(float), cudaMemcpyHostToDevice));
   static const bool kCull = env_double("GD_VOXEL_CULL", 1) != 0;
   const int n_tiles = kCull ? (n + 31) / 32 : 0;
   std::vector<float> tbox(6 * static_cast<size_t>(std::max(n_tiles, 1)), 0.0f);
@@ -517,11 +497,8 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   // beyond both fall back to the exact full scan.
   PocketView& v = slot->view;
   v.pts = slot->pts.as<double>();
-  v.pts32 = slot->pts32.as<float>();
   v.P = n;
   v.use_index = 1;
-  constexpr double kU = 1.0 / 16777216.0;  // fp32 unit roundoff 2^-24
-  double eloc = 0.0;  // fp32 voxel-locate misplacement, worst level
   slot->n_cand = 0;
   slot->max_cand = 0;
   // Edges/margins from A/B on config 1 (profiles/r1_voxel_ab.md, DESIGN
@@ -577,18 +554,15 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     const int64_t listed = tot[0], total = tot[1];
     const int32_t mx = static_cast<int32_t>(tot[2]);
-    if (listed >= static_cast<int64_t>(kPayloadMask))
-      return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
-    GD_CUDA(ctx, slot->vox_rec[L].ensure(sizeof(float) * 4 * static_cast<size_t>(nv)));
-    GD_CUDA(ctx, slot->vox_big[L].ensure(sizeof(int32_t) * static_cast<size_t>(nv)));
-    GD_CUDA(ctx, slot->vox_lst[L].ensure(sizeof(float) * 4 * std::max<int64_t>(listed, 1)));
+    if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
+    GD_CUDA(ctx, slot->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
+    GD_CUDA(ctx, slot->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
     // List head: the whole pocket, the list of every overflow voxel.
-    GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_lst[L].ptr, slot->pts32.ptr, sizeof(float) * 4 * n,
+    GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_pts[L].ptr, slot->pts.ptr, sizeof(double) * 4 * n,
                                  cudaMemcpyDeviceToDevice, ctx->stream));
     GD_CUDA(ctx, static_cast<cudaError_t>(
                      launch_voxel_fill(slot->pts.as<double>(), n, g, doff.as<int32_t>(),
-                                       slot->vox_rec[L].as<float>(), slot->vox_lst[L].as<float>(),
-                                       slot->vox_big[L].as<int32_t>(),
+                                       slot->vox_off[L].as<double>(), slot->vox_pts[L].as<double>(),
                                        ctx->tiles.as<float>(), n_tiles, counts.as<int32_t>(),
                                        keep, ctx->stream)));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
@@ -596,29 +570,16 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     slot->n_cand += total;
     slot->max_cand = std::max(slot->max_cand, mx);
     GridLevel& gl = v.lv[L];
-    gl.rec = slot->vox_rec[L].as<float>();
-    gl.lst = slot->vox_lst[L].as<float>();
-    gl.big = slot->vox_big[L].as<int32_t>();
+    gl.rec = slot->vox_off[L].as<double>();
+    gl.lst = slot->vox_pts[L].as<double>();
     gl.lo_x = g.lo_x;
     gl.lo_y = g.lo_y;
     gl.lo_z = g.lo_z;
     gl.inv_h = 1.0 / g.h;
-    gl.flo_x = static_cast<float>(g.lo_x);
-    gl.flo_y = static_cast<float>(g.lo_y);
-    gl.flo_z = static_cast<float>(g.lo_z);
-    gl.finv_h = static_cast<float>(gl.inv_h);
     gl.dim_x = g.dim_x;
     gl.dim_y = g.dim_y;
     gl.dim_z = g.dim_z;
-    // fp32 locate: (x - flo) * finv_h misplaces a point by at most a few
-    // roundings of the origin and the in-grid offset, per axis.
-    const double lomax = std::max({std::fabs(g.lo_x), std::fabs(g.lo_y), std::fabs(g.lo_z)});
-    const double ext = g.h * std::max({g.dim_x, g.dim_y, g.dim_z});
-    eloc = std::max(eloc, 8.0 * kU * std::sqrt(3.0) * (lomax + 2.0 * ext));
   }
-  // Screen distance error of the pocket side: fp32 point rounding plus
-  // twice the misplacement (the fp32 screen).
-  v.eps = static_cast<float>(1.01 * (std::sqrt(3.0) * kU * pmax + 2.0 * eloc));
   slot->P = n;
   activate(*slot);
   return GD_OK;
@@ -641,57 +602,69 @@ extern "C" int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[
 }
 
 // ---------------------------------------------------------------------------
-// Batch staging.  Descriptors are packed per ligand range ("chunk") into a
-// pinned arena laid out with upper bounds, so chunk k+1 can be prepared on
-// the host while chunk k is copied and docked on the GPU.
+// Batch staging.  The host copies each ligand range ("chunk") of raw atoms
+// and bonds into a pinned arena and fills the per-ligand offsets (O(L));
+// the chunk is copied to HBM and preprocessed there (prep.cu: validation,
+// far masks, rotamers, fragments, CTA order), so chunk k+1 is packed on the
+// host while chunk k is copied, preprocessed and docked on the GPU.
 // ---------------------------------------------------------------------------
 namespace {
 
-enum Seg { kMeta, kXyz, kRad, kFar, kFmask, kFax, kFan, kFrel, kOrder, kStatus, kSegs };
+enum Seg { kMeta, kXyz, kRad, kBonds, kRot, kBoff, kSegs };
 
 struct Running {
   size_t fo = 0, wo = 0, mo = 0;  // frag, far-word, fmask-word cursors
 };
 
+// Atom counts the GPU preprocessing takes (the rest is rejected up front).
+bool size_ok(int n) { return n >= 2 && n <= kMaxAtoms; }
+
 }  // namespace
 
-// Validates the batch, sizes the pinned arena and the device descriptor
-// buffers with upper bounds, and resets the host bookkeeping.
+// Validates the batch, sizes the pinned arena and the device buffers with
+// upper bounds, and resets the host bookkeeping.
 static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
   if (b == nullptr || b->n_ligands < 0 || (b->n_ligands > 0 &&
       (!b->atom_offsets || !b->xyz || !b->radii || !b->bond_offsets ||
        (b->bond_offsets[b->n_ligands] > 0 && (!b->bonds || !b->bond_rotatable)))))
     return ctx->fail(GD_ERR_INVALID, "gd_upload: invalid ligand batch");
   const int L = b->n_ligands;
-  size_t far_ub = 0, frag_ub = 0, fmask_ub = 0;
+  size_t far_ub = 0, fmask_ub = 0;
   for (int l = 0; l < L; ++l) {
     const int n = b->atom_offsets[l + 1] - b->atom_offsets[l];
     const int nb = b->bond_offsets[l + 1] - b->bond_offsets[l];
     if (n < 0 || nb < 0) return ctx->fail(GD_ERR_INVALID, "gd_upload: offsets not ascending");
+    if (!size_ok(n)) continue;
     const size_t W = static_cast<size_t>((n + 63) / 64);
     far_ub += static_cast<size_t>(n) * W;
-    frag_ub += 2 * static_cast<size_t>(nb);
     fmask_ub += 2 * static_cast<size_t>(nb) * W;
   }
   const int32_t A = L > 0 ? b->atom_offsets[L] : 0;
-  const size_t sizes[kSegs] = {
-      sizeof(LigMeta) * std::max(L, 1),       sizeof(double) * 3 * std::max(A, 1),
-      sizeof(double) * std::max(A, 1),        sizeof(uint64_t) * std::max<size_t>(far_ub, 1),
-      sizeof(uint64_t) * std::max<size_t>(fmask_ub, 1), sizeof(int32_t) * std::max<size_t>(frag_ub, 1),
-      sizeof(int32_t) * std::max<size_t>(frag_ub, 1),   sizeof(double) * std::max<size_t>(frag_ub, 1),
-      sizeof(int32_t) * std::max(L, 1), sizeof(int32_t) * std::max(L, 1)};
+  const int64_t B = L > 0 ? b->bond_offsets[L] : 0;
+  const size_t frag_ub = 2 * static_cast<size_t>(B);
+  const size_t sizes[kSegs] = {sizeof(LigMeta) * std::max(L, 1), sizeof(double) * 3 * std::max(A, 1),
+                               sizeof(double) * std::max(A, 1),
+                               sizeof(int32_t) * 2 * std::max<size_t>(B, 1),
+                               std::max<size_t>(B, 1), sizeof(int32_t) * (std::max(L, 1) + 1)};
   size_t arena = 0;
-  for (size_t s : sizes) arena += (s + 255) & ~size_t(255);
+  for (size_t sz : sizes) arena += (sz + 255) & ~size_t(255);
   GD_CUDA(ctx, ctx->staging.ensure(arena));
   unsigned char* base = static_cast<unsigned char*>(ctx->staging.ptr);
   size_t o = 0;
-  DevBuf* dev[kSegs] = {&ctx->meta, &ctx->xyz, &ctx->radii, &ctx->far, &ctx->fmask,
-                        &ctx->fax,  &ctx->fan, &ctx->frel,  &ctx->order, &ctx->o_status};
+  DevBuf* dev[kSegs] = {&ctx->meta, &ctx->xyz, &ctx->radii, &ctx->bonds, &ctx->rot, &ctx->boff};
   for (int i = 0; i < kSegs; ++i) {
     ctx->pin[i] = base + o;
     o += (sizes[i] + 255) & ~size_t(255);
     GD_CUDA(ctx, dev[i]->ensure(sizes[i]));
   }
+  GD_CUDA(ctx, ctx->far.ensure(sizeof(uint64_t) * std::max<size_t>(far_ub, 1)));
+  GD_CUDA(ctx, ctx->fmask.ensure(sizeof(uint64_t) * std::max<size_t>(fmask_ub, 1)));
+  GD_CUDA(ctx, ctx->fax.ensure(sizeof(int32_t) * std::max<size_t>(frag_ub, 1)));
+  GD_CUDA(ctx, ctx->fan.ensure(sizeof(int32_t) * std::max<size_t>(frag_ub, 1)));
+  GD_CUDA(ctx, ctx->frel.ensure(sizeof(double) * std::max<size_t>(frag_ub, 1)));
+  GD_CUDA(ctx, ctx->order.ensure(sizeof(int32_t) * std::max(L, 1)));
+  GD_CUDA(ctx, ctx->o_status.ensure(sizeof(int32_t) * std::max(L, 1)));
+  ctx->frag_total = frag_ub;
   ctx->errors.assign(L, std::string());
   ctx->status_host.assign(L, 0);
   // An empty batch may pass null offset arrays (nothing is read from them).
@@ -707,105 +680,74 @@ static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
   return GD_OK;
 }
 
-// Host half of a chunk: preprocess ligands [c0, c1) on the host cores
-// (Ligand ctor checks, capped distances, rotamers, fragments) and pack them
-// into the pinned arena; the chunk's CTA order is longest-first.
-static void prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Running& run,
-                       int& chunk_max_n) {
-  const int cnt = c1 - c0;
+// Host half of a chunk: offsets of ligands [c0, c1) into the descriptor
+// arrays, and their raw atoms and bonds into the pinned arena (the bulk
+// copy on the worker pool for large chunks).  Returns the chunk's largest
+// atom and bond counts (of ligands the GPU preprocesses).
+static void pack_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Running& run,
+                       int& chunk_max_n, int& chunk_max_b) {
   chunk_max_n = 1;
-  if (cnt <= 0) return;
-  std::vector<PreparedLigand> prep(cnt);
-  std::atomic<int> next{0};
-  auto work = [&] {
-    for (int s; (s = next.fetch_add(8)) < cnt;)
-      for (int e = s; e < std::min(cnt, s + 8); ++e) {
-        const int l = c0 + e;
-        const int a0 = b->atom_offsets[l], n = b->atom_offsets[l + 1] - a0;
-        const int b0 = b->bond_offsets[l], nb = b->bond_offsets[l + 1] - b0;
-        prep[e] = prepare_ligand(std::to_string(l), n, b->xyz + 3 * a0, b->radii + a0, nb,
-                                 b->bonds + 2 * b0, b->bond_rotatable + b0);
-      }
-  };
-  if (cnt < 64) {
-    work();
-  } else {
-    if (!ctx->pool)
-      ctx->pool = std::make_unique<WorkerPool>((ctx->pool_threads > 0 ? ctx->pool_threads : host_threads()) - 1);
-    ctx->pool->run(work);
-  }
-
+  chunk_max_b = 1;
+  if (c1 <= c0) return;
   auto* meta = reinterpret_cast<LigMeta*>(ctx->pin[kMeta]);
-  auto* hxyz = reinterpret_cast<double*>(ctx->pin[kXyz]);
-  auto* hrad = reinterpret_cast<double*>(ctx->pin[kRad]);
-  auto* hfar = reinterpret_cast<uint64_t*>(ctx->pin[kFar]);
-  auto* hfm = reinterpret_cast<uint64_t*>(ctx->pin[kFmask]);
-  auto* hax = reinterpret_cast<int32_t*>(ctx->pin[kFax]);
-  auto* han = reinterpret_cast<int32_t*>(ctx->pin[kFan]);
-  auto* hrel = reinterpret_cast<double*>(ctx->pin[kFrel]);
-  auto* hord = reinterpret_cast<int32_t*>(ctx->pin[kOrder]);
-  const int a0 = b->atom_offsets[c0], a1 = b->atom_offsets[c1];
-  std::memcpy(hxyz + 3 * a0, b->xyz + 3 * a0, sizeof(double) * 3 * (a1 - a0));
-  std::memcpy(hrad + a0, b->radii + a0, sizeof(double) * (a1 - a0));
-  std::vector<double> cost(cnt, 0.0);
-  chunk_max_n = 1;
-  for (int e = 0; e < cnt; ++e) {
-    const int l = c0 + e;
-    const PreparedLigand& p = prep[e];
+  for (int l = c0; l < c1; ++l) {
     LigMeta& m = meta[l];
     m.atom_off = b->atom_offsets[l];
     m.n = b->atom_offsets[l + 1] - b->atom_offsets[l];
-    m.status = p.status;
-    m.frag_off = static_cast<int32_t>(run.fo);
-    m.nfrag = p.status == 0 ? p.nfrag() : 0;
+    const int nb = b->bond_offsets[l + 1] - b->bond_offsets[l];
+    m.words = (m.n + 63) / 64;
+    m.nfrag = 0;
+    m.frag_off = 2 * b->bond_offsets[l];
     m.far_off = static_cast<int32_t>(run.wo);
     m.fmask_off = static_cast<int32_t>(run.mo);
-    m.words = p.words;
-    ctx->status_host[l] = p.status;
-    reinterpret_cast<int32_t*>(ctx->pin[kStatus])[l] = p.status;
-    if (!p.error.empty()) ctx->errors[l] = p.error;
-    if (p.status != 0) continue;
-    run.wo += p.far_mask.size();
-    run.mo += p.frag_mask.size();
-    run.fo += p.nfrag();
+    m.status = size_ok(m.n) ? GD_LIG_OK : GD_LIG_INVALID;
+    if (m.status != GD_LIG_OK) continue;
+    run.wo += static_cast<size_t>(m.n) * m.words;
+    run.mo += 2 * static_cast<size_t>(nb) * m.words;
     chunk_max_n = std::max(chunk_max_n, m.n);
-    cost[e] = static_cast<double>(m.n) * (4.0 + m.nfrag);
+    chunk_max_b = std::max(chunk_max_b, nb);
   }
-  // The descriptors into the pinned arena at the offsets just assigned:
-  // the bulk of the pack, on the workers for large chunks.
-  auto pack = [&](int e0, int e1) {
-    for (int e = e0; e < e1; ++e) {
-      const PreparedLigand& p = prep[e];
-      if (p.status != 0) continue;
-      const LigMeta& m = meta[c0 + e];
-      std::copy(p.far_mask.begin(), p.far_mask.end(), hfar + m.far_off);
-      std::copy(p.frag_mask.begin(), p.frag_mask.end(), hfm + m.fmask_off);
-      for (int f = 0; f < p.nfrag(); ++f) {
-        hax[m.frag_off + f] = p.frag_axis[f];
-        han[m.frag_off + f] = p.frag_anchor[f];
-        hrel[m.frag_off + f] = p.frag_rel[f];
-      }
-    }
-  };
-  if (cnt < 64 || !ctx->pool) {
-    pack(0, cnt);
+  auto* bo = reinterpret_cast<int32_t*>(ctx->pin[kBoff]);
+  for (int l = c0; l <= c1; ++l) bo[l] = b->bond_offsets[l];
+  const size_t a0 = b->atom_offsets[c0], a1 = b->atom_offsets[c1];
+  const size_t q0 = b->bond_offsets[c0], q1 = b->bond_offsets[c1];
+  struct Part {
+    unsigned char* dst;
+    const unsigned char* src;
+    size_t bytes;
+  } parts[4] = {
+      {ctx->pin[kXyz] + 24 * a0, reinterpret_cast<const unsigned char*>(b->xyz + 3 * a0), 24 * (a1 - a0)},
+      {ctx->pin[kRad] + 8 * a0, reinterpret_cast<const unsigned char*>(b->radii + a0), 8 * (a1 - a0)},
+      {ctx->pin[kBonds] + 8 * q0, reinterpret_cast<const unsigned char*>(b->bonds + 2 * q0), 8 * (q1 - q0)},
+      {ctx->pin[kRot] + q0, b->bond_rotatable + q0, q1 - q0}};
+  size_t total = 0;
+  for (const Part& pt : parts) total += pt.bytes;
+  constexpr size_t kBlock = 256 << 10;
+  if (total < 4 * kBlock) {
+    for (const Part& pt : parts)
+      if (pt.bytes) std::memcpy(pt.dst, pt.src, pt.bytes);
   } else {
-    std::atomic<int> nxt{0};
+    if (!ctx->pool)
+      ctx->pool = std::make_unique<WorkerPool>((ctx->pool_threads > 0 ? ctx->pool_threads : host_threads()) - 1);
+    size_t starts[5] = {0};
+    for (int k = 0; k < 4; ++k) starts[k + 1] = starts[k] + (parts[k].bytes + kBlock - 1) / kBlock;
+    std::atomic<size_t> next{0};
     ctx->pool->run([&] {
-      for (int e; (e = nxt.fetch_add(32)) < cnt;) pack(e, std::min(cnt, e + 32));
+      for (size_t bi; (bi = next.fetch_add(1)) < starts[4];) {
+        int k = 0;
+        while (starts[k + 1] <= bi) ++k;
+        const size_t off = (bi - starts[k]) * kBlock;
+        std::memcpy(parts[k].dst + off, parts[k].src + off, std::min(kBlock, parts[k].bytes - off));
+      }
     });
   }
-  // Longest-processing-time-first CTA order within the chunk.
-  std::vector<int32_t> idx(cnt);
-  std::iota(idx.begin(), idx.end(), 0);
-  std::stable_sort(idx.begin(), idx.end(), [&](int32_t x, int32_t y) { return cost[x] > cost[y]; });
-  for (int e = 0; e < cnt; ++e) hord[c0 + e] = c0 + idx[e];
   ctx->max_n = std::max(ctx->max_n, chunk_max_n);
 }
 
-// Copy half of a chunk: the chunk's descriptor segments, pinned -> HBM.
-static int h2d_range(gd_ctx* ctx, int c0, int c1, const Running& before, const Running& after,
-                     cudaStream_t s) {
+// Copy half of a chunk (pinned -> HBM) and its GPU preprocessing, on stream s.
+static int h2d_prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, int max_n, int max_b,
+                          cudaStream_t s) {
+  if (c1 <= c0) return GD_OK;
   auto cp = [&](DevBuf& d, int seg, size_t off, size_t bytes) -> int {
     if (bytes == 0) return GD_OK;
     ctx->timing.h2d_bytes += static_cast<int64_t>(bytes);
@@ -813,18 +755,53 @@ static int h2d_range(gd_ctx* ctx, int c0, int c1, const Running& before, const R
                                      bytes, cudaMemcpyHostToDevice, s), "h2d");
   };
   const size_t a0 = ctx->atom_off[c0], a1 = ctx->atom_off[c1];
+  const size_t q0 = b->bond_offsets[c0], q1 = b->bond_offsets[c1];
   int rc = GD_OK;
   if ((rc = cp(ctx->meta, kMeta, sizeof(LigMeta) * c0, sizeof(LigMeta) * (c1 - c0)))) return rc;
-  if ((rc = cp(ctx->xyz, kXyz, sizeof(double) * 3 * a0, sizeof(double) * 3 * (a1 - a0)))) return rc;
-  if ((rc = cp(ctx->radii, kRad, sizeof(double) * a0, sizeof(double) * (a1 - a0)))) return rc;
-  if ((rc = cp(ctx->far, kFar, 8 * before.wo, 8 * (after.wo - before.wo)))) return rc;
-  if ((rc = cp(ctx->fmask, kFmask, 8 * before.mo, 8 * (after.mo - before.mo)))) return rc;
-  if ((rc = cp(ctx->fax, kFax, 4 * before.fo, 4 * (after.fo - before.fo)))) return rc;
-  if ((rc = cp(ctx->fan, kFan, 4 * before.fo, 4 * (after.fo - before.fo)))) return rc;
-  if ((rc = cp(ctx->frel, kFrel, 8 * before.fo, 8 * (after.fo - before.fo)))) return rc;
-  if ((rc = cp(ctx->order, kOrder, 4 * c0, 4 * (c1 - c0)))) return rc;
-  if ((rc = cp(ctx->o_status, kStatus, 4 * c0, 4 * (c1 - c0)))) return rc;
+  if ((rc = cp(ctx->xyz, kXyz, 24 * a0, 24 * (a1 - a0)))) return rc;
+  if ((rc = cp(ctx->radii, kRad, 8 * a0, 8 * (a1 - a0)))) return rc;
+  if ((rc = cp(ctx->bonds, kBonds, 8 * q0, 8 * (q1 - q0)))) return rc;
+  if ((rc = cp(ctx->rot, kRot, q0, q1 - q0))) return rc;
+  if ((rc = cp(ctx->boff, kBoff, 4 * static_cast<size_t>(c0), 4 * static_cast<size_t>(c1 - c0 + 1)))) return rc;
+  PrepParams q{};
+  q.l0 = c0;
+  q.l1 = c1;
+  q.max_n = max_n;
+  q.max_b = max_b;
+  q.meta = ctx->meta.as<LigMeta>();
+  q.boff = ctx->boff.as<int32_t>();
+  q.bonds = ctx->bonds.as<int32_t>();
+  q.rot = ctx->rot.as<uint8_t>();
+  q.xyz = ctx->xyz.as<double>();
+  q.radii = ctx->radii.as<double>();
+  q.far = ctx->far.as<uint64_t>();
+  q.fmask = ctx->fmask.as<uint64_t>();
+  q.fax = ctx->fax.as<int32_t>();
+  q.fan = ctx->fan.as<int32_t>();
+  q.frel = ctx->frel.as<double>();
+  q.status = ctx->o_status.as<int32_t>();
+  q.order = ctx->order.as<int32_t>();
+  GD_CUDA(ctx, static_cast<cudaError_t>(launch_prep(q, s)));
+  ctx->timing.launches += 2;
   return GD_OK;
+}
+
+// Host bookkeeping once a batch's statuses are known: the per-ligand
+// status mirror, and the reference's message for every rejected ligand
+// (re-derived on the host, prep.cpp; the batch is still the caller's).
+static void note_status(gd_ctx* ctx, const gd_ligand_batch* b, const int32_t* status) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int l = 0; l < ctx->n_lig; ++l) {
+    ctx->status_host[l] = status[l];
+    if (status[l] != GD_LIG_INVALID) continue;
+    const int a0 = b->atom_offsets[l], b0 = b->bond_offsets[l];
+    const PreparedLigand p = prepare_ligand(std::to_string(l), b->atom_offsets[l + 1] - a0, b->xyz + 3 * a0,
+                                            b->radii + a0, b->bond_offsets[l + 1] - b0, b->bonds + 2 * b0,
+                                            b->bond_rotatable + b0);
+    ctx->errors[l] = p.error.empty() ? "ligand '" + std::to_string(l) + "': invalid" : p.error;
+  }
+  ctx->timing.host_prep_ms =
+      std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
 }
 
 extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
@@ -834,14 +811,22 @@ extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
   int rc = begin_batch(ctx, b, run);
   if (rc != GD_OK) return rc;
   const auto t0 = std::chrono::steady_clock::now();
-  int mx = 1;
-  prep_range(ctx, b, 0, ctx->n_lig, run, mx);
-  ctx->timing.host_prep_ms =
+  int mx = 1, mb = 1;
+  pack_range(ctx, b, 0, ctx->n_lig, run, mx, mb);
+  ctx->timing.host_pack_ms =
       std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
   cudaEventRecord(ctx->ev[0], ctx->stream);
-  rc = h2d_range(ctx, 0, ctx->n_lig, Running{}, run, ctx->stream);
+  rc = h2d_prep_range(ctx, b, 0, ctx->n_lig, mx, mb, ctx->stream);
   if (rc != GD_OK) return rc;
   cudaEventRecord(ctx->ev[1], ctx->stream);
+  // The statuses (and rejected ligands' messages) while the batch is at hand.
+  std::vector<int32_t> st(std::max(ctx->n_lig, 1));
+  if (ctx->n_lig > 0)
+    GD_CUDA(ctx, cudaMemcpyAsync(st.data(), ctx->o_status.ptr, sizeof(int32_t) * ctx->n_lig,
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+  GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  cudaEventElapsedTime(&ctx->timing.upload_ms, ctx->ev[0], ctx->ev[1]);
+  note_status(ctx, b, st.data());
   ctx->staged = true;
   return GD_OK;
 }
@@ -869,7 +854,7 @@ static int ensure_orientations(gd_ctx* ctx, int step) {
 // Validates knobs, allocates every output buffer for the whole batch (before
 // any asynchronous work: a reallocation would free memory in flight) and
 // returns the launch parameters common to all chunks.
-static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockParams& p) {
+static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, bool keep_top, DockParams& p) {
   char msg[128];
   if (gd_validate_knobs(k, msg, sizeof msg) != GD_OK) return ctx->fail(GD_ERR_INVALID, msg);
   if (ctx->P == 0) return ctx->fail(GD_ERR_NO_POCKET, "gd_dock: no pocket staged (gd_set_pocket)");
@@ -896,11 +881,13 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockPara
   GD_CUDA(ctx, ctx->st_checks.ensure(sizeof(int64_t) * slots));
   GD_CUDA(ctx, ctx->o_scored.ensure(sizeof(int64_t) * std::max(L, 1)));
   GD_CUDA(ctx, ctx->o_status.ensure(sizeof(int32_t) * std::max(L, 1)));
-  if (keep_pose) {
+  if (keep_pose || keep_top) {
     const size_t pose_bytes = sizeof(double) * 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1)) * K;
-    GD_CUDA(ctx, ctx->o_pose.ensure(pose_bytes));
+    if (keep_pose) GD_CUDA(ctx, ctx->o_pose.ensure(pose_bytes));
     GD_CUDA(ctx, ctx->stage_pose.ensure(pose_bytes));
   }
+  if (keep_top)
+    GD_CUDA(ctx, ctx->o_top.ensure(sizeof(double) * 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1))));
   p = DockParams{};
   p.order = ctx->order.as<int32_t>();
   p.meta = ctx->meta.as<LigMeta>();
@@ -921,13 +908,10 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockPara
   p.orient_R = ctx->orient_R.as<double>();
   p.cos_deg = ctx->cos_t.as<double>();
   p.sin_deg = ctx->sin_t.as<double>();
-  p.cos32 = ctx->cos32_t.as<float>();
-  p.sin32 = ctx->sin32_t.as<float>();
   p.hp = k->high_precision_step;
   p.lp = k->low_precision_step;
   p.reps = k->repetitions;
   p.refine = k->enable_refinement ? 1 : 0;
-  p.screen = (k->flags & GD_FLAG_EXACT_FP64) ? 0 : 1;
   p.tile = gd_optimal_tile_size(k->high_precision_step);
   p.threshold = k->threshold;
   p.top_k = K;
@@ -946,7 +930,8 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockPara
   p.out_evals = ctx->o_evals.as<int64_t>();
   p.out_checks = ctx->o_checks.as<int64_t>();
   p.out_pose = keep_pose ? ctx->o_pose.as<double>() : nullptr;
-  p.stage_pose = keep_pose ? ctx->stage_pose.as<double>() : nullptr;
+  p.stage_pose = (keep_pose || keep_top) ? ctx->stage_pose.as<double>() : nullptr;
+  p.out_top = keep_top ? ctx->o_top.as<double>() : nullptr;
   p.poses_scored = ctx->o_scored.as<int64_t>();
   p.status = ctx->o_status.as<int32_t>();
   p.counters = nullptr;
@@ -960,6 +945,7 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, DockPara
   ctx->last_topk = K;
   ctx->last_rigid = rigid;
   ctx->last_pose = keep_pose;
+  ctx->last_top = keep_top;
   return GD_OK;
 }
 
@@ -986,7 +972,8 @@ extern "C" int gd_dock_resident(gd_ctx* ctx, const gd_knobs* knobs) {
   if (ctx == nullptr) return GD_ERR_INVALID;
   if (knobs == nullptr) return ctx->fail(GD_ERR_INVALID, "knob config: null");
   DockParams p;
-  int rc = prepare_dock(ctx, knobs, (knobs->flags & GD_FLAG_KEEP_POSES) != 0, p);
+  int rc = prepare_dock(ctx, knobs, (knobs->flags & GD_FLAG_KEEP_POSES) != 0,
+                        (knobs->flags & GD_FLAG_TOP_POSE) != 0, p);
   if (rc != GD_OK) return rc;
   ctx->timing.launches = 0;
   cudaEventRecord(ctx->ev[2], ctx->stream);
@@ -1027,6 +1014,10 @@ static int d2h_range(gd_ctx* ctx, const gd_result* r, int l0, int l1, cudaStream
     const size_t a0 = ctx->atom_off[l0], a1 = ctx->atom_off[l1];
     if ((rc = cp(r->final_pose, ctx->o_pose, 24, K * a0, K * (a1 - a0)))) return rc;
   }
+  if (r->top_pose != nullptr) {
+    const size_t a0 = ctx->atom_off[l0], a1 = ctx->atom_off[l1];
+    if ((rc = cp(r->top_pose, ctx->o_top, 24, a0, a1 - a0))) return rc;
+  }
   return GD_OK;
 }
 
@@ -1060,6 +1051,8 @@ static int download(gd_ctx* ctx, gd_result* r) {
   if (!ctx->have_result) return ctx->fail(GD_ERR_INVALID, "gd_download: nothing docked yet");
   if (r->final_pose != nullptr && !ctx->last_pose)
     return ctx->fail(GD_ERR_INVALID, "gd_download: poses were not kept");
+  if (r->top_pose != nullptr && !ctx->last_top)
+    return ctx->fail(GD_ERR_INVALID, "gd_download: top poses were not kept (GD_FLAG_TOP_POSE)");
   const int L = ctx->n_lig;
   ctx->timing.d2h_bytes = 0;
   int rc = d2h_range(ctx, r, 0, L, ctx->stream);
@@ -1095,8 +1088,9 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   int rc = begin_batch(ctx, batch, run);
   if (rc != GD_OK) return rc;
   const bool keep_pose = result->final_pose != nullptr;
+  const bool keep_top = result->top_pose != nullptr;
   DockParams p;
-  rc = prepare_dock(ctx, knobs, keep_pose, p);
+  rc = prepare_dock(ctx, knobs, keep_pose, keep_top, p);
   if (rc != GD_OK) return rc;
   const int L = ctx->n_lig, K = ctx->last_topk;
   static const int kStreams = std::max(1, static_cast<int>(env_double("GD_E2E_STREAMS", 2)));
@@ -1108,8 +1102,9 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   // Pinned result arena: the async D2H targets.
   const size_t slots = static_cast<size_t>(std::max(L, 1)) * K;
   const size_t pose_elems = keep_pose ? 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1)) * K : 0;
+  const size_t top_elems = keep_top ? 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1)) : 0;
   const size_t rbytes = slots * (4 + 4 + 8 + 8 + 8 + 8) + static_cast<size_t>(std::max(L, 1)) * (4 + 8 + 4) +
-                        8 * pose_elems + 1024;
+                        8 * (pose_elems + top_elems) + 1024;
   GD_CUDA(ctx, ctx->res_staging.ensure(rbytes));
   unsigned char* rb = static_cast<unsigned char*>(ctx->res_staging.ptr);
   size_t ro = 0;
@@ -1129,6 +1124,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   pr.poses_scored = result->poses_scored ? static_cast<int64_t*>(take(8 * std::max(L, 1))) : nullptr;
   pr.status = static_cast<int32_t*>(take(4 * std::max(L, 1)));
   pr.final_pose = keep_pose ? static_cast<double*>(take(8 * pose_elems)) : nullptr;
+  pr.top_pose = keep_top ? static_cast<double*>(take(8 * top_elems)) : nullptr;
 
   // Chunk plan: a small head chunk (its host prep is the only part nothing
   // overlaps), then chunks growing geometrically by 1.6x: host prep runs
@@ -1181,10 +1177,9 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   for (int c = 0; c < chunks; ++c) {
     const int c0 = bounds[c], c1 = bounds[c + 1];
     cudaStream_t s = (c % kStreams) ? ctx->aux_streams[c % kStreams - 1] : ctx->stream;
-    const Running before = run;
     const auto t0 = std::chrono::steady_clock::now();
-    int mx = 1;
-    prep_range(ctx, batch, c0, c1, run, mx);
+    int mx = 1, mb = 1;
+    pack_range(ctx, batch, c0, c1, run, mx, mb);
     const auto t1 = std::chrono::steady_clock::now();
     prep_ms += std::chrono::duration<float, std::milli>(t1 - t0).count();
     if (kTrace) {
@@ -1192,7 +1187,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
       tprep.push_back(std::chrono::duration<double, std::milli>(t1 - t_start).count());
       GD_CUDA(ctx, cudaEventRecord(tev[2 * c], s));
     }
-    if ((rc = h2d_range(ctx, c0, c1, before, run, s)) != GD_OK) return rc;
+    if ((rc = h2d_prep_range(ctx, batch, c0, c1, mx, mb, s)) != GD_OK) return rc;
     if ((rc = launch_range(ctx, p, c0, c1, mx, s, nullptr)) != GD_OK) return rc;
     if ((rc = d2h_range(ctx, &pr, c0, c1, s)) != GD_OK) return rc;
     if (kTrace) GD_CUDA(ctx, cudaEventRecord(tev[2 * c + 1], s));
@@ -1211,7 +1206,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
       const unsigned char* src;
       size_t bytes;
     };
-    Seg segs[9];
+    Seg segs[10];
     int nseg = 0;
     size_t total = 0;
     auto copy = [&](void* dst, const void* src, size_t elem, size_t off, size_t cnt) {
@@ -1234,11 +1229,15 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
       const size_t p1 = 3 * static_cast<size_t>(K) * ctx->atom_off[l1];
       copy(result->final_pose, pr.final_pose, 8, p0, p1 - p0);
     }
+    if (keep_top) {
+      const size_t p0 = 3 * static_cast<size_t>(ctx->atom_off[l0]), p1 = 3 * static_cast<size_t>(ctx->atom_off[l1]);
+      copy(result->top_pose, pr.top_pose, 8, p0, p1 - p0);
+    }
     // Pinned arena -> caller arrays: large chunks in 64 KiB blocks over the
     // worker pool (the last chunk's copy is on the critical path).
     constexpr size_t kBlock = 64 << 10;
     if (total >= 4 * kBlock && ctx->pool) {
-      size_t starts[10];
+      size_t starts[11];
       starts[0] = 0;
       for (int k = 0; k < nseg; ++k) starts[k + 1] = starts[k] + (segs[k].bytes + kBlock - 1) / kBlock;
       std::atomic<size_t> next{0};
@@ -1260,6 +1259,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   if (L == 0) fill_empty(ctx, result, pr.k_eff, pr.status);
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
   for (cudaStream_t st : ctx->aux_streams) GD_CUDA(ctx, cudaStreamSynchronize(st));
+  note_status(ctx, batch, pr.status);
   ctx->have_result = true;
   ctx->staged = true;
   const auto t_end = std::chrono::steady_clock::now();
@@ -1277,7 +1277,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
     for (auto e : tev) cudaEventDestroy(e);
     cudaEventDestroy(tev0);
   }
-  ctx->timing.host_prep_ms = prep_ms;
+  ctx->timing.host_pack_ms = prep_ms;
   ctx->timing.host_post_ms = post_ms;
   ctx->timing.total_ms = std::chrono::duration<float, std::milli>(t_end - t_start).count();
   return GD_OK;
@@ -1402,8 +1402,6 @@ static int stage_fragments(gd_ctx* ctx, const gd_ligand_batch* b, const gd_fragm
   p.pocket = ctx->view;
   p.cos_deg = ctx->cos_t.as<double>();
   p.sin_deg = ctx->sin_t.as<double>();
-  p.cos32 = ctx->cos32_t.as<float>();
-  p.sin32 = ctx->sin32_t.as<float>();
   p.max_n = max_n;
   p.max_pairs = std::max(1, max_n * max_n / 4);
   p.status = ctx->o_status.as<int32_t>();
@@ -1556,8 +1554,16 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores,
     return ctx->fail(GD_ERR_INVALID, "gd_rotation_profiles: null output");
   GD_CUDA(ctx, cudaSetDevice(ctx->device));
   const int L = ctx->n_lig;
-  const auto* meta = reinterpret_cast<const LigMeta*>(ctx->pin[kMeta]);
-  const auto* hrel = reinterpret_cast<const double*>(ctx->pin[kFrel]);
+  // The fragment counts and relative sizes the GPU preprocessing wrote.
+  std::vector<LigMeta> meta(std::max(L, 1));
+  std::vector<double> hrel(std::max<size_t>(ctx->frag_total, 1));
+  if (L > 0) {
+    GD_CUDA(ctx, cudaMemcpyAsync(meta.data(), ctx->meta.ptr, sizeof(LigMeta) * L, cudaMemcpyDeviceToHost,
+                                 ctx->stream));
+    GD_CUDA(ctx, cudaMemcpyAsync(hrel.data(), ctx->frel.ptr, sizeof(double) * hrel.size(),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  }
   std::vector<int32_t> items;
   frag_offsets[0] = 0;
   for (int l = 0; l < L; ++l) {
@@ -1595,8 +1601,6 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores,
     p.pocket.use_index = (flags & GD_FLAG_BRUTE_FORCE) ? 0 : ctx->view.use_index;
     p.cos_deg = ctx->cos_t.as<double>();
     p.sin_deg = ctx->sin_t.as<double>();
-    p.cos32 = ctx->cos32_t.as<float>();
-    p.sin32 = ctx->sin32_t.as<float>();
     p.max_n = ctx->max_n;
     p.max_pairs = std::max(1, ctx->max_n * ctx->max_n / 4);
     p.status = ctx->o_status.as<int32_t>();
@@ -1651,13 +1655,18 @@ extern "C" int gd_device_results(const gd_ctx* ctx, gd_device_result* out) {
   out->evaluations = ctx->o_evals.as<int64_t>();
   out->n_ligands = ctx->n_lig;
   out->top_k = ctx->last_topk;
+  out->rigid_score = ctx->o_rigid.as<double>();
+  out->feasibility_checks = ctx->o_checks.as<int64_t>();
+  out->k_eff = ctx->k_eff.as<int32_t>();
+  out->poses_scored = ctx->o_scored.as<int64_t>();
+  out->status = ctx->o_status.as<int32_t>();
   return GD_OK;
 }
 
-extern "C" int gd_work_counters(const gd_ctx* ctx, uint64_t out[32]) {
+extern "C" int gd_work_counters(const gd_ctx* ctx, uint64_t out[16]) {
   if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
   if (!ctx->counted) return GD_ERR_INVALID;
-  if (cudaMemcpy(out, ctx->counters.ptr, sizeof(uint64_t) * 32, cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (cudaMemcpy(out, ctx->counters.ptr, sizeof(uint64_t) * 16, cudaMemcpyDeviceToHost) != cudaSuccess)
     return GD_ERR_CUDA;
   return GD_OK;
 }
@@ -1959,7 +1968,8 @@ extern "C" int gd_multi_dock_batch(gd_multi* m, const gd_ligand_batch* b, const 
       gd_result sr{off(r->orientation, s0), off(r->seed_rank, s0), off(r->rigid_score, s0),
                    off(r->final_score, s0), off(r->evaluations, s0), off(r->feasibility_checks, s0),
                    off(r->final_pose, 3 * static_cast<size_t>(K) * a0), off(r->k_eff, c0),
-                   off(r->poses_scored, c0), off(r->status, c0)};
+                   off(r->poses_scored, c0), off(r->status, c0),
+                   off(r->top_pose, 3 * static_cast<size_t>(a0))};
       const int e = gd_dock_batch(c, &sub, k, &sr);
       if (e != GD_OK) {
         rc[d] = e;

@@ -73,16 +73,11 @@ __device__ __forceinline__ P3 ldp(const double* base, int j) {
   return P3{x, y, z};
 }
 
-// Executed-work counters (exact; DESIGN.md §4 turns them into FLOPs): fp64
-// work {point pairs, rotated atoms, bump pairs, queries, score terms,
-// candidate evaluations, rigid-transformed atoms}, then the fp32 screen's
-// {point pairs, rotated atoms (rigid-transformed in the sweep), bump pairs,
-// queries} and the candidates the screen had to resolve exactly.
+// Executed-work counters (exact; DESIGN.md §4 turns them into fp64 FLOPs).
 // Kernels are instantiated twice: Work<true> counts (GD_FLAG_COUNT_WORK),
 // Work<false> compiles every increment away so the timed kernels carry no
 // counter registers.
-enum WorkKind { kPairs, kRot, kBump, kQuery, kTerms, kEvals, kXform, kPairs32, kRot32, kBump32,
-                kQuery32, kExactEvals, kWorkKinds };
+enum WorkKind { kPairs, kRot, kBump, kQuery, kTerms, kEvals, kXform, kWorkKinds };
 template <bool On>
 struct Work {
   unsigned c[kWorkKinds];
@@ -117,163 +112,145 @@ __device__ __noinline__ double min_dist_sq_brute(const double* pts, int P, doubl
   return m;
 }
 
-// 128-bit read-only loads of fp32 index records (L1::no_allocate: they are
-// scattered and rarely re-hit; L1 keeps spill slots and the small tables).
-struct F4 {
-  float x, y, z;
-  uint32_t w;
+// Exact nearest-point query: the voxel's candidate list holds every point
+// that can attain the fp64 minimum anywhere in the (slightly expanded)
+// voxel, so the minimum is bit-identical to the brute-force scan (the
+// reference's PocketIndex makes the same exactness argument,
+// geometry.hpp:45-46).  Fine level first, then the coarse far-field level;
+// queries beyond both fall back to the full scan.
+// Voxel lookup: the record of the first grid level containing q (one or
+// two independent 256-bit loads); lst == nullptr means the full-scan
+// fallback.
+struct Loc {
+  const double* lst;  // further candidates (start already applied)
+  int count;          // candidates in the voxel (>= 1)
+  double x0, y0, z0;  // the inline candidates (the second repeats the first
+  double x1, y1, z1;  // when count == 1; unused when kVoxInline == 1)
 };
-__device__ __forceinline__ F4 ld128(const float* p) {
-  F4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-      : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=r"(r.w)
-      : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint32_t ldw(const float* p) {  // the w word of a record
-  uint32_t w;
-  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(w) : "l"(p + 3));
-  return w;
-}
-
-// fp32 squared distance (explicit FMAs: the TU is built with -fmad=false).
-__device__ __forceinline__ float d2f(float x, float y, float z, const F4& r) {
-  const float dx = x - r.x, dy = y - r.y, dz = z - r.z;
-  return __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-}
-
-// The voxel of (x, y, z) in the first grid level containing it, -1 if none.
-template <class T>
-__device__ __forceinline__ int voxel_of(const GridLevel& g, T fx, T fy, T fz) {
-  if (fx >= T(0) && fy >= T(0) && fz >= T(0) && fx < T(g.dim_x) && fy < T(g.dim_y) && fz < T(g.dim_z))
-    return (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z + static_cast<int>(fz);
-  return -1;
-}
-
-__device__ __forceinline__ int count_of(const GridLevel& g, int v, uint32_t w) {
-  const int cf = static_cast<int>(w >> kCountShift);
-  return cf ? cf : __ldg(g.big + v);
-}
-
-// Exact nearest-point query (fp64, bit-identical to the brute-force scan):
-// the voxel's candidate list holds every point that can attain the fp64
-// minimum anywhere in the (slightly expanded) voxel -- the reference's
-// PocketIndex makes the same exactness argument (geometry.hpp:45-46).  The
-// voxel is located in fp64; candidates' fp64 coordinates come from the
-// point table by index.  Fine level first, then the coarse far field;
-// beyond both, the full scan.
-template <bool On>
-__device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, double y, double z,
-                                              Work<On>& w) {
-  w.add(kQuery, 1);
+__device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, double z) {
   if (pk.use_index) {
 #pragma unroll
     for (int L = 0; L < kGridLevels; ++L) {
       const GridLevel& g = pk.lv[L];
-      const int v = voxel_of(g, (x - g.lo_x) * g.inv_h, (y - g.lo_y) * g.inv_h, (z - g.lo_z) * g.inv_h);
-      if (v < 0) continue;
-      const uint32_t hw = ldw(g.rec + 4 * static_cast<size_t>(v));
-      const int cnt = count_of(g, v, hw);
-      w.add(kPairs, cnt);
-      if (cnt == 1) {
-        const P3 p = ldp<GD_LST_NA>(pk.pts, static_cast<int>(hw & kPayloadMask));
-        return dist_sq(x, y, z, p.x, p.y, p.z);
+      const double fx = (x - g.lo_x) * g.inv_h;
+      const double fy = (y - g.lo_y) * g.inv_h;
+      const double fz = (z - g.lo_z) * g.inv_h;
+      if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
+        const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
+                      static_cast<int>(fz);
+        const double* r = g.rec + kRecDoubles * static_cast<size_t>(v);
+        double hdr, pad;
+        Loc l;
+        ld256<GD_REC_NA>(r, hdr, l.x0, l.y0, l.z0);
+        if constexpr (kVoxInline == 2) ld256<GD_REC_NA>(r + 4, l.x1, l.y1, l.z1, pad);
+        const long long h = __double_as_longlong(hdr);
+        l.count = static_cast<int>(h >> 32);
+        l.lst = g.lst + 4 * static_cast<size_t>(static_cast<unsigned>(h & 0xffffffffll));
+        return l;
       }
-      const float* l = g.lst + 4 * static_cast<size_t>(hw & kPayloadMask);
-      double m = __longlong_as_double(0x7ff0000000000000ll);
-      for (int k = 0; k < cnt; k += 2) {  // two candidates per round in flight
-        const bool two = k + 1 < cnt;
-        const uint32_t i0 = ldw(l + 4 * k), i1 = two ? ldw(l + 4 * (k + 1)) : i0;
-        const P3 p0 = ldp<GD_LST_NA>(pk.pts, static_cast<int>(i0));
-        const P3 p1 = ldp<GD_LST_NA>(pk.pts, static_cast<int>(i1));
-        m = fmin(m, dist_sq(x, y, z, p0.x, p0.y, p0.z));
-        m = fmin(m, dist_sq(x, y, z, p1.x, p1.y, p1.z));
-      }
-      return m;
     }
   }
-  w.add(kPairs, pk.P);
-  return min_dist_sq_brute(pk.pts, pk.P, x, y, z);
+  return Loc{nullptr, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
 }
 
-__device__ __noinline__ float min_d2_brute_f32(const float* pts32, int P, float x, float y, float z) {
-  float m = __int_as_float(0x7f800000);
-  for (int j = 0; j < P; ++j) m = fminf(m, d2f(x, y, z, ld128(pts32 + 4 * j)));
+// min over the inline candidates; the list scan covers count - kVoxInline.
+__device__ __forceinline__ double inline_min(const Loc& a, double x, double y, double z) {
+  double m = dist_sq(x, y, z, a.x0, a.y0, a.z0);
+  if constexpr (kVoxInline == 2) m = fmin(m, dist_sq(x, y, z, a.x1, a.y1, a.z1));
+  return m;
+}
+__device__ __forceinline__ int listed(const Loc& a) { return a.lst ? a.count - kVoxInline : 0; }
+
+template <bool On>
+__device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, double y, double z,
+                                              Work<On>& w) {
+  w.add(kQuery, 1);
+  const Loc a = locate(pk, x, y, z);
+  if (a.lst == nullptr) {
+    w.add(kPairs, pk.P);
+    return min_dist_sq_brute(pk.pts, pk.P, x, y, z);
+  }
+  w.add(kPairs, a.count);
+  double m = inline_min(a, x, y, z);
+  for (int k = 0; k < a.count - kVoxInline; ++k) {
+    const P3 p = ldp<GD_LST_NA>(a.lst, k);
+    m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+  }
   return m;
 }
 
-// fp32 screen queries, M at a time: min over the candidate list of the
-// voxel containing each fp32 point (located in fp32) of fp32 squared
-// distances to the fp32 coordinates; within the error bound the screens
-// derive (flex.cu: screen_scores) of the exact minimum at the exact (fp64)
-// position.  Latency-bound gathers, so everything is issued as early as
-// possible: the M record loads together, then the lists walked two
-// entries per query per round (2M loads in flight).
+// Two independent queries with both record loads issued before either scan
+// and the two candidate scans interleaved (memory-level parallelism 2).
+template <bool On>
+__device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, double y0, double z0,
+                                             double x1, double y1, double z1, double& m0,
+                                             double& m1, Work<On>& w) {
+  w.add(kQuery, 2);
+  const Loc a = locate(pk, x0, y0, z0);
+  const Loc b = locate(pk, x1, y1, z1);
+  const int na = listed(a), nb = listed(b);
+  w.add(kPairs, (a.lst ? a.count : 0) + (b.lst ? b.count : 0));
+  m0 = inline_min(a, x0, y0, z0);
+  m1 = inline_min(b, x1, y1, z1);
+#if GD_WHATIF_NOLIST
+  const int nmax = 0;  // timing experiment only: wrong minima
+#else
+  const int nmax = max(na, nb);
+#endif
+  for (int k = 0; k < nmax; ++k) {
+    if (k < na) {
+      const P3 p = ldp<GD_LST_NA>(a.lst, k);
+      m0 = fmin(m0, dist_sq(x0, y0, z0, p.x, p.y, p.z));
+    }
+    if (k < nb) {
+      const P3 p = ldp<GD_LST_NA>(b.lst, k);
+      m1 = fmin(m1, dist_sq(x1, y1, z1, p.x, p.y, p.z));
+    }
+  }
+  if (a.lst == nullptr) {
+    w.add(kPairs, pk.P);
+    m0 = min_dist_sq_brute(pk.pts, pk.P, x0, y0, z0);
+  }
+  if (b.lst == nullptr) {
+    w.add(kPairs, pk.P);
+    m1 = min_dist_sq_brute(pk.pts, pk.P, x1, y1, z1);
+  }
+}
+
+// M independent queries: all M record loads in flight before any scan, the
+// M candidate scans interleaved (memory-level parallelism M).
 template <int M, bool On>
-__device__ __forceinline__ void min_d2_f32(const PocketView& pk, const float* x, const float* y,
-                                           const float* z, float* m, Work<On>& w) {
-  w.add(kQuery32, M);
-  int lv[M], vox[M];
+__device__ __forceinline__ void min_dist_sqM(const PocketView& pk, const double* x, const double* y,
+                                             const double* z, double* m, Work<On>& w) {
+  w.add(kQuery, M);
+  Loc a[M];
+#pragma unroll
+  for (int r = 0; r < M; ++r) a[r] = locate(pk, x[r], y[r], z[r]);
+  int nmax = 0;
 #pragma unroll
   for (int r = 0; r < M; ++r) {
-    lv[r] = -1;
-    vox[r] = 0;
-    if (pk.use_index) {
+    m[r] = inline_min(a[r], x[r], y[r], z[r]);
+    nmax = max(nmax, listed(a[r]));
+    if (a[r].lst) w.add(kPairs, a[r].count);
+  }
+  for (int k = 0; k < nmax; ++k) {
 #pragma unroll
-      for (int L = kGridLevels - 1; L >= 0; --L) {  // the finest level containing the point wins
-        const GridLevel& g = pk.lv[L];
-        const int v = voxel_of(g, (x[r] - g.flo_x) * g.finv_h, (y[r] - g.flo_y) * g.finv_h,
-                               (z[r] - g.flo_z) * g.finv_h);
-        if (v >= 0) {
-          lv[r] = L;
-          vox[r] = v;
-        }
+    for (int r = 0; r < M; ++r) {
+      if (k < listed(a[r])) {
+        const P3 p = ldp<GD_LST_NA>(a[r].lst, k);
+        m[r] = fmin(m[r], dist_sq(x[r], y[r], z[r], p.x, p.y, p.z));
       }
     }
   }
-  F4 rec[M];
-  const float* lst[M];
-  int cnt[M];
 #pragma unroll
   for (int r = 0; r < M; ++r) {
-    const GridLevel& g = pk.lv[lv[r] > 0 ? 1 : 0];
-    rec[r] = lv[r] >= 0 ? ld128(g.rec + 4 * static_cast<size_t>(vox[r])) : F4{0.f, 0.f, 0.f, 1u << kCountShift};
-    lst[r] = g.lst;
-  }
-  int most = 1;
-#pragma unroll
-  for (int r = 0; r < M; ++r) {
-    const GridLevel& g = pk.lv[lv[r] > 0 ? 1 : 0];
-    const int cf = static_cast<int>(rec[r].w >> kCountShift);
-    cnt[r] = cf ? cf : __ldg(g.big + vox[r]);
-    lst[r] += 4 * static_cast<size_t>(rec[r].w & kPayloadMask);
-    m[r] = d2f(x[r], y[r], z[r], rec[r]);
-    w.add(kPairs32, lv[r] >= 0 ? cnt[r] : 0);
-    most = max(most, cnt[r]);
-  }
-#if GD_WHATIF_NOLIST
-  most = 1;  // timing experiment only: wrong minima
-#endif
-  for (int k = 1; k < most; k += 2) {
-    F4 e0[M], e1[M];
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      if (k < cnt[r]) e0[r] = ld128(lst[r] + 4 * k);
-      if (k + 1 < cnt[r]) e1[r] = ld128(lst[r] + 4 * (k + 1));
-    }
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      if (k < cnt[r]) m[r] = fminf(m[r], d2f(x[r], y[r], z[r], e0[r]));
-      if (k + 1 < cnt[r]) m[r] = fminf(m[r], d2f(x[r], y[r], z[r], e1[r]));
+    if (a[r].lst == nullptr) {
+      w.add(kPairs, pk.P);
+      m[r] = min_dist_sq_brute(pk.pts, pk.P, x[r], y[r], z[r]);
     }
   }
-#pragma unroll
-  for (int r = 0; r < M; ++r)
-    if (lv[r] < 0) {  // beyond both grids: the whole pocket
-      w.add(kPairs32, pk.P);
-      m[r] = min_d2_brute_f32(pk.pts32, pk.P, x[r], y[r], z[r]);
-    }
 }
+
 
 // Rodrigues rotation of one atom (geometry.hpp:182-184):
 // ((o + v*c) + cross(k,v)*s) + k*(dot(k,v)*(1-c)), v = p - o.

@@ -82,9 +82,6 @@ constexpr int kFoldUnroll = GD_FOLD_UNROLL;
 #define GD_META_RELOAD 0     // 1: ligand descriptor fields re-read from global when used (r2b's
                              // win; after r2h's query change 0 is 0.4% faster)
 #endif
-#ifndef GD_SCREEN_MLP
-#define GD_SCREEN_MLP 1      // fp32 screen queries in flight per lane
-#endif
 #ifndef GD_PHASE_CLOCKS
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
@@ -102,19 +99,10 @@ constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
-// A candidate that may still win a screened fragment step.
-struct Surv {
-  double lo, hi;  // bounds on its exact overlap score
-  int angle;
-  int pad;
-};
-constexpr int kMaxSurv = 32;
-
 template <int B>
 __host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pairs) {
   return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * B * n) +
-         a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16) + a16(sizeof(Axis)) + a16(16ull * n) +
-         a16(sizeof(Surv) * kMaxSurv) + a16(4 * 16);
+         a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16) + a16(sizeof(Axis));
 }
 
 // One atom of a chain's committed pose and its overlap term max(1e-12,
@@ -133,9 +121,6 @@ struct WarpMem {
   uint64_t* fm;          // [4] fragment membership bits
   long long* tally;      // [2] the chain's evaluations, feasibility checks (lane 0)
   Axis* ax;              // [1] the step's rotation axis (GD_AXIS_SMEM)
-  float4* vf;            // [n]    fp32 screen: p_i - o of the step's axis, radius
-  Surv* sv;              // [kMaxSurv] screened step's possible winners
-  int* ang;              // [16]   angles of an exact-evaluation batch
 };
 
 template <int B>
@@ -156,9 +141,6 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   s.fm = reinterpret_cast<uint64_t*>(take(32));
   s.tally = reinterpret_cast<long long*>(take(16));
   s.ax = reinterpret_cast<Axis*>(take(sizeof(Axis)));
-  s.vf = reinterpret_cast<float4*>(take(16ull * n));
-  s.sv = reinterpret_cast<Surv*>(take(sizeof(Surv) * kMaxSurv));
-  s.ang = reinterpret_cast<int*>(take(4 * 16));
   GD_BOUND(o <= warp_bytes<B>(n, W, max_pairs));
   return s;
 }
@@ -177,7 +159,7 @@ __device__ __forceinline__ int qdiv(int t, float rcp) {
 // Per-phase SM-clock attribution of a chain (diagnostic builds only; the
 // disabled form compiles to nothing).
 enum Phase { kPhInit, kPhSetup, kPhPrefilter, kPhPrefill, kPhBump, kPhQuery, kPhFold, kPhDecide,
-             kPhCommit, kPhBound, kPhases };
+             kPhCommit, kPhases };
 template <bool On>
 struct Clocks {
   long long last;
@@ -209,13 +191,13 @@ struct Clocks {
 // bump (or the angle-0 candidate, always feasible) are skipped.
 template <bool On>
 __device__ __forceinline__ void bump_item(const WarpMem& s, const DockParams& p, const Axis& X, int t,
-                                          float rnp, int np, unsigned skip, unsigned& bl,
-                                          Work<On>& wk) {
+                                          float rnp, int np, int a0, int da, unsigned skip,
+                                          unsigned& bl, Work<On>& wk) {
   const int c = qdiv(t, rnp);
   if (((bl | skip) >> c) & 1u) return;
   const int pr = s.pairs[t - c * np];
   const int i = pr & 0xff, j = pr >> 8;
-  const int a = s.ang[c];
+  const int a = a0 + c * da;
   const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
   double qx, qy, qz;
   const PT ai = s.pt[i], aj = s.pt[j];
@@ -226,27 +208,51 @@ __device__ __forceinline__ void bump_item(const WarpMem& s, const DockParams& p,
   if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < dmul(cut, cut)) bl |= 1u << c;
 }
 
-// Query phase: lanes over (live candidate, fragment atom), one exact
-// nearest-point lookup per lane per iteration (r2h: beats two in flight
-// once registers were cut); candidate c's term of atom i lands in
-// v[c * n + i].
+// Query phase: lanes over (live candidate, fragment atom), two items per
+// lane per iteration (t, t + 32) so both nearest-point lookups are in flight;
+// candidate c's term of atom i lands in v[c * n + i].
+#ifndef GD_QUERY_MLP
+#define GD_QUERY_MLP 1       // lookups in flight per lane in the query phase (1 or 2; r2h: 1 wins, c1 flex 13.63 -> 12.36 ms)
+#endif
 template <bool On>
 __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& p, const Axis& X,
-                                            int n, int nf, unsigned live, int nb, int lane,
-                                            Work<On>& wk) {
+                                            int n, int nf, unsigned live, int a0, int da, int nb,
+                                            int lane, Work<On>& wk) {
   const int tq = nb * nf;
   const float rnf = 1.0f / static_cast<float>(nf);
+#if GD_QUERY_MLP == 1
   for (int t = lane; t < tq; t += 32) {
     const int c = qdiv(t, rnf);
     if (!((live >> c) & 1u)) continue;
     const int i = s.fidx[t - c * nf];
-    const int ac = s.ang[c];
+    const int ac = a0 + c * da;
     const double cs = __ldg(p.cos_deg + ac), sn = __ldg(p.sin_deg + ac);
     double x, y, z;
     const PT q = s.pt[i];
     rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
     wk.add(kRot, 1);
     s.v[c * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+  }
+  return;
+#endif
+  for (int t = lane; t < tq; t += 64) {
+    const int c0 = qdiv(t, rnf);
+    const int t1 = t + 32 < tq ? t + 32 : t;
+    const int c1 = qdiv(t1, rnf);
+    const bool l0 = (live >> c0) & 1u, l1 = t1 != t && ((live >> c1) & 1u);
+    if (!l0 && !l1) continue;
+    const int i0 = s.fidx[t - c0 * nf], i1 = s.fidx[t1 - c1 * nf];
+    const int a0c = a0 + c0 * da, a1c = a0 + c1 * da;
+    const double cs0 = __ldg(p.cos_deg + a0c), sn0 = __ldg(p.sin_deg + a0c);
+    const double cs1 = __ldg(p.cos_deg + a1c), sn1 = __ldg(p.sin_deg + a1c);
+    double x0, y0, z0, x1, y1, z1, m0, m1;
+    const PT q0 = s.pt[i0], q1 = s.pt[i1];
+    rodrigues(X, cs0, sn0, dsub(1.0, cs0), q0.x, q0.y, q0.z, x0, y0, z0);
+    rodrigues(X, cs1, sn1, dsub(1.0, cs1), q1.x, q1.y, q1.z, x1, y1, z1);
+    wk.add(kRot, 2);
+    min_dist_sq2(p.pocket, x0, y0, z0, x1, y1, z1, m0, m1, wk);
+    if (l0) s.v[c0 * n + i0] = fmax(kMinDistanceSq, m0);
+    if (l1) s.v[c1 * n + i1] = fmax(kMinDistanceSq, m1);
   }
 }
 
@@ -261,15 +267,6 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
                            CK& ck) {
   ck.mark(kPhDecide);
   const unsigned zero = (a0 == 0) ? 1u : 0u;  // only c = 0 can be angle 0
-  if (lane < nb) s.ang[lane] = a0 + lane * da;
-  // Non-fragment terms are the same for every candidate of this step:
-  // pre-fill them into each candidate slot so the fold is a plain sum.
-  for (int i = lane; i < n; i += 32)
-    if (!in_frag(s.fm, i)) {
-      const double t = s.pt[i].t;
-      for (int c = 0; c < nb; ++c) s.v[c * n + i] = t;
-    }
-  __syncwarp();
   unsigned bl = 0;
   // Pair-major when there are at least GD_PAIRMAJOR_MIN pairs and the batch
   // is at most 6 candidates (measured: c1 16.57 vs 16.84 ms; at 8 candidates the serial
@@ -313,12 +310,12 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
   } else {
     const int total = nb * np;
     const float rnp = 1.0f / static_cast<float>(max(np, 1));
-    for (int t = lane; t < total; t += 32) bump_item(s, p, X, t, rnp, np, zero, bl, wk);
+    for (int t = lane; t < total; t += 32) bump_item(s, p, X, t, rnp, np, a0, da, zero, bl, wk);
   }
   const unsigned bumped = __reduce_or_sync(kFull, bl);
   const unsigned live = ((1u << nb) - 1u) & ~bumped & ~zero;
   ck.mark(kPhBump);
-  query_phase(s, p, X, n, nf, live, nb, lane, wk);
+  query_phase(s, p, X, n, nf, live, a0, da, nb, lane, wk);
   __syncwarp();
   ck.mark(kPhQuery);
   // Fold phase: lane c, atom order.
@@ -528,6 +525,15 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   __syncwarp();
   left_np = (f & 1) ? -1 : np;  // a left step's list serves its right step
   ck.mark(kPhPrefilter);
+  // Non-fragment terms are the same for every candidate of this step:
+  // pre-fill them into each candidate slot so the fold is a plain sum.
+  for (int i = lane; i < n; i += 32)
+    if (!in_frag(s.fm, i)) {
+      const double t = s.pt[i].t;
+#pragma unroll
+      for (int c = 0; c < B; ++c) s.v[c * n + i] = t;
+    }
+  __syncwarp();
   ck.mark(kPhPrefill);
   st.nf = nf;
   st.first = first;
@@ -625,334 +631,6 @@ __device__ __forceinline__ void search_fragment(const WarpMem& s, const DockPara
     best_a = 0;
   }
   evals = nfeas;
-}
-
-// ---------------------------------------------------------------------------
-// fp32 screen of a flat fragment search ("fp32 screen").
-//
-// Every candidate is first rotated, bump-checked and scored in fp32 (FMA
-// Rodrigues from per-step fp32 arms, fp32 nearest-point queries over the
-// fp32 index).  Feasibility is decided exactly: a bump pair whose fp32
-// squared distance lies within the proven error band of the cutoff is
-// re-checked with the reference's fp64 recipe.  Scores get rigorous
-// bounds [lo, hi] on the exact fp64 overlap score; only candidates whose
-// upper bound reaches the best lower bound can win, and the exact winner
-// (strict '>', first encountered; kernel.hpp:136) is resolved among them:
-// a single survivor whose lower bound beats the committed pose's score is
-// the winner outright (its exact score comes from the commit, which
-// recomputes its terms in fp64 anyway); otherwise the survivors are
-// re-evaluated with the fp64 recipe.  The committed pose, its terms and
-// every reported score stay bit-identical to the reference.
-// ---------------------------------------------------------------------------
-constexpr float kU32 = 5.9604645e-8f;  // fp32 unit roundoff 2^-24
-
-struct Screen {
-  float ox, oy, oz, kx, ky, kz;  // the step's axis in fp32
-  float dq;                      // bound on the fp32 query-position error + pocket eps (A)
-  float db;                      // bound on a bump pair's fp32 distance error (A)
-  double snf;                    // sum of the non-fragment terms (fp64)
-};
-
-// Per-step fp32 arms p_i - o (fp64 difference rounded to fp32) with the
-// radius, the error bounds and the non-fragment term sum.
-__device__ __forceinline__ Screen screen_setup(const WarpMem& s, const DockParams& p, const Axis& X,
-                                               int n, int lane) {
-  double vmax = 0.0, snf = 0.0;
-  for (int i = lane; i < n; i += 32) {
-    const PT q = s.pt[i];
-    const double vx = dsub(q.x, X.ox), vy = dsub(q.y, X.oy), vz = dsub(q.z, X.oz);
-    s.vf[i] = make_float4(static_cast<float>(vx), static_cast<float>(vy), static_cast<float>(vz),
-                          static_cast<float>(s.radius[i]));
-    vmax = fmax(vmax, fabs(vx) + fabs(vy) + fabs(vz));  // >= the Euclidean norm
-    if (!in_frag(s.fm, i)) snf += q.t;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    vmax = fmax(vmax, __shfl_xor_sync(kFull, vmax, o));
-    snf += __shfl_xor_sync(kFull, snf, o);
-  }
-  Screen sc;
-  sc.ox = static_cast<float>(X.ox);
-  sc.oy = static_cast<float>(X.oy);
-  sc.oz = static_cast<float>(X.oz);
-  sc.kx = static_cast<float>(X.kx);
-  sc.ky = static_cast<float>(X.ky);
-  sc.kz = static_cast<float>(X.kz);
-  const double on = fabs(X.ox) + fabs(X.oy) + fabs(X.oz);
-  // Rodrigues in fp32 from fp32-rounded arms, axis, cos/sin: a few dozen
-  // roundings of magnitude |v| per component, plus o's and q's roundings;
-  // 128 u (|v| + |o| + 1) bounds the Euclidean error with a wide margin.
-  sc.dq = static_cast<float>(128.0 * kU32 * (vmax + on + 1.0)) + p.pocket.eps;
-  sc.db = static_cast<float>(132.0 * kU32 * (vmax + 1.0));
-  sc.snf = snf;
-  __syncwarp();
-  return sc;
-}
-
-// The fp32 Rodrigues turn of arm v (relative to the axis origin).
-__device__ __forceinline__ void turn32(const Screen& sc, const float4& v, float c, float sn, float omc,
-                                      float& rx, float& ry, float& rz) {
-  const float crx = __fmaf_rn(sc.ky, v.z, -sc.kz * v.y);
-  const float cry = __fmaf_rn(sc.kz, v.x, -sc.kx * v.z);
-  const float crz = __fmaf_rn(sc.kx, v.y, -sc.ky * v.x);
-  const float d = __fmaf_rn(sc.kz, v.z, __fmaf_rn(sc.ky, v.y, sc.kx * v.x));
-  const float w = d * omc;
-  rx = __fmaf_rn(sc.kx, w, __fmaf_rn(crx, sn, v.x * c));
-  ry = __fmaf_rn(sc.ky, w, __fmaf_rn(cry, sn, v.y * c));
-  rz = __fmaf_rn(sc.kz, w, __fmaf_rn(crz, sn, v.z * c));
-}
-
-// The reference's bump rule for one pair at one angle, in fp64
-// (geometry.hpp:182-184, :199-213): the rare re-check of a pair whose fp32
-// distance falls inside the error band.
-__device__ __forceinline__ bool exact_bump(const WarpMem& s, const DockParams& p, int i, int j, int a) {
-  const Axis& X = *s.ax;
-  const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
-  const PT ai = s.pt[i], aj = s.pt[j];
-  double qx, qy, qz;
-  rodrigues(X, cs, sn, dsub(1.0, cs), ai.x, ai.y, ai.z, qx, qy, qz);
-  const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
-  return dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < dmul(cut, cut);
-}
-
-// fp32 bump screen of candidates s.ang[0..nb): returns the (exact) mask of
-// candidates with a clash.  Pair-major for many pairs (a lane per pair,
-// its arm once, every candidate angle), else lanes over (candidate, pair).
-template <bool On>
-__device__ __forceinline__ unsigned screen_bumps(const WarpMem& s, const DockParams& p, const Screen& sc,
-                                                 int np, int nb, int lane, Work<On>& wk) {
-  const unsigned all = (1u << nb) - 1u;
-  unsigned bl = 0;
-  auto test = [&](const float4& vi, const float4& vj, float c, float sn, int i, int j, int a) {
-    float rx, ry, rz;
-    turn32(sc, vi, c, sn, 1.0f - c, rx, ry, rz);
-    const float dx = rx - vj.x, dy = ry - vj.y, dz = rz - vj.z;
-    const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-    const float cut = 0.8f * (vi.w + vj.w), c2 = cut * cut;
-    const float band = __fmaf_rn(sc.db + 32.0f * kU32, c2 + 1.0f, sc.db * sc.db);
-    wk.add(kRot32, 1);
-    wk.add(kBump32, 1);
-    if (d2 < c2 - band) return true;
-    if (d2 <= c2 + band) {
-      wk.add(kBump, 1);
-      return exact_bump(s, p, i, j, a);
-    }
-    return false;
-  };
-  if (np >= GD_PAIRMAJOR_MIN) {
-    const int al = s.ang[min(lane, nb - 1)];
-    const float cs_l = __ldg(p.cos32 + al), sn_l = __ldg(p.sin32 + al);
-    for (int t0 = 0; t0 < np; t0 += 32) {
-      const int t = t0 + lane;
-      const bool act = t < np;
-      int i = 0, j = 0;
-      float4 vi{}, vj{};
-      if (act) {
-        const int pr = s.pairs[t];
-        i = pr & 0xff;
-        j = pr >> 8;
-        vi = s.vf[i];
-        vj = s.vf[j];
-      }
-      for (int c = 0; c < nb; ++c) {
-        const float cs = __shfl_sync(kFull, cs_l, c), sn = __shfl_sync(kFull, sn_l, c);
-        if (!act || ((bl >> c) & 1u)) continue;
-        if (test(vi, vj, cs, sn, i, j, s.ang[c])) bl |= 1u << c;
-      }
-      bl = __reduce_or_sync(kFull, bl);  // later pairs skip known bumps
-      if (bl == all) break;
-    }
-  } else {
-    const int total = nb * np;
-    const float rnp = 1.0f / static_cast<float>(max(np, 1));
-    for (int t = lane; t < total; t += 32) {
-      const int c = qdiv(t, rnp);
-      if ((bl >> c) & 1u) continue;
-      const int pr = s.pairs[t - c * np];
-      const int i = pr & 0xff, j = pr >> 8;
-      const int a = s.ang[c];
-      if (test(s.vf[i], s.vf[j], __ldg(p.cos32 + a), __ldg(p.sin32 + a), i, j, a)) bl |= 1u << c;
-    }
-  }
-  return __reduce_or_sync(kFull, bl);
-}
-
-// fp32 score screen of the live candidates of s.ang[0..nb): lane c < nb
-// receives bounds [lo, hi] on candidate c's exact overlap score
-// (-inf, -inf when it bumped).  Term error per fragment atom, with
-// D = distance error dq: |t32 - t64| <= 8u t + D (t + 1) + D^2 (the list
-// of the voxel holding the fp32 point gives its exact nearest distance;
-// distances are 1-Lipschitz in the point; 2 sqrt(t) D <= D (t + 1)).
-template <bool On, class CK>
-__device__ __forceinline__ void screen_scores(const WarpMem& s, const DockParams& p, const Screen& sc,
-                                              int n, int nf, unsigned live, int nb, int lane,
-                                              double& lo, double& hi, Work<On>& wk, CK& ck) {
-  float* tq = reinterpret_cast<float*>(s.v);
-  const int tot = nb * nf;
-  const float rnf = 1.0f / static_cast<float>(nf);
-  // GD_SCREEN_MLP items per lane per round, their lookups in flight together.
-  constexpr int M = GD_SCREEN_MLP;
-  for (int t0 = lane; t0 < tot; t0 += 32 * M) {
-    float qx[M], qy[M], qz[M], m[M];
-    bool act[M];
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      const int t = t0 + 32 * r;
-      const int c = qdiv(min(t, tot - 1), rnf);
-      act[r] = t < tot && ((live >> c) & 1u);
-      const int sl = min(t, tot - 1) - c * nf;
-      const int a = s.ang[c];
-      const float cs = __ldg(p.cos32 + a), sn = __ldg(p.sin32 + a);
-      float rx, ry, rz;
-      turn32(sc, s.vf[s.fidx[sl]], cs, sn, 1.0f - cs, rx, ry, rz);
-      qx[r] = sc.ox + rx;
-      qy[r] = sc.oy + ry;
-      qz[r] = sc.oz + rz;
-    }
-    bool any = false;
-#pragma unroll
-    for (int r = 0; r < M; ++r) any |= act[r];
-    if (!any) continue;
-    min_d2_f32<M>(p.pocket, qx, qy, qz, m, wk);
-#pragma unroll
-    for (int r = 0; r < M; ++r)
-      if (act[r]) {
-        tq[t0 + 32 * r] = fmaxf(1e-12f, m[r]);
-        wk.add(kRot32, 1);
-      }
-  }
-  __syncwarp();
-  ck.mark(kPhQuery);
-  lo = hi = -kInfinity;
-  if (lane < nb && ((live >> lane) & 1u)) {
-    float a = 0.0f;
-    const float* row = tq + lane * nf;
-    for (int k = 0; k < nf; ++k) a += row[k];
-    const double A = a, dq = sc.dq, u = kU32;
-    const double E = 1.02 * ((10.0 * u + nf * u + dq) * A + nf * (dq + dq * dq)) +
-                     0x1p-49 * n * (sc.snf + A);
-    const double slo = sc.snf + A - E, shi = sc.snf + A + E;
-    lo = static_cast<double>(n) / shi * (1.0 - 0x1p-50);
-    hi = slo > 0.0 ? static_cast<double>(n) / slo * (1.0 + 0x1p-50) : kInfinity;
-  }
-  __syncwarp();
-}
-
-// Exact overlap scores (the reference recipe: fp64 Rodrigues, exact
-// nearest-point queries, atom-order fold) of the feasible candidates
-// s.ang[0..nb), lane c receiving candidate c's.
-template <bool On>
-__device__ __forceinline__ double exact_scores(const WarpMem& s, const DockParams& p, const Axis& X,
-                                               int n, int nf, int first, double pre, int nb,
-                                               int lane, Work<On>& wk) {
-  for (int i = lane; i < n; i += 32)
-    if (!in_frag(s.fm, i)) {
-      const double t = s.pt[i].t;
-      for (int c = 0; c < nb; ++c) s.v[c * n + i] = t;
-    }
-  __syncwarp();
-  query_phase(s, p, X, n, nf, (1u << nb) - 1u, nb, lane, wk);
-  __syncwarp();
-  double score = 0.0;
-  if (lane < nb) {
-    double sum = pre;
-    const double* vc = s.v + lane * n;
-#pragma unroll kFoldUnroll
-    for (int i = first; i < n; ++i) sum = dadd(sum, vc[i]);
-    score = __ddiv_rn(static_cast<double>(n), sum);
-    wk.add(kTerms, n);
-    wk.add(kEvals, 1);
-    wk.add(kExactEvals, 1);
-  }
-  __syncwarp();
-  return score;
-}
-
-__device__ __forceinline__ double warp_max(double x) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(kFull, x, o));
-  return x;
-}
-
-// optimize_fragment_flat (kernel.hpp:125-143) through the fp32 screen.
-// Returns the winning angle (0: the committed pose), its exact score in
-// `best` unless `exact_after` (then the caller derives it from the
-// commit's exact terms), and the evaluator's tallies.  Falls back to the
-// all-fp64 search when more than kMaxSurv candidates stay undecided.
-template <bool On, int B, int SB, class CK>
-__device__ __forceinline__ void search_flat_screened(const WarpMem& s, const DockParams& p,
-                                                     const Axis& X, int n, int nf, int np, int first,
-                                                     double pre, double cur, int step, int lane,
-                                                     int& best_a, double& best, bool& exact_after,
-                                                     int& evals, int& checks, Work<On>& wk, CK& ck) {
-  const Screen sc = screen_setup(s, p, X, n, lane);
-  ck.mark(kPhPrefill);
-  const int A = 360 / step;
-  double L = cur;  // best lower bound so far (the committed pose: exact)
-  int ns = 0, nfeas = 0;
-  bool ovf = false;
-  for (int kb = 0; kb < A - 1; kb += SB) {
-    const int nb = min(SB, A - 1 - kb);
-    if (lane < nb) s.ang[lane] = (kb + 1 + lane) * step;
-    __syncwarp();
-    const unsigned bumped = screen_bumps(s, p, sc, np, nb, lane, wk);
-    const unsigned live = ((1u << nb) - 1u) & ~bumped;
-    nfeas += __popc(live);
-    ck.mark(kPhBump);
-    double lo, hi;
-    screen_scores(s, p, sc, n, nf, live, nb, lane, lo, hi, wk, ck);
-    ck.mark(kPhBound);
-    L = fmax(L, warp_max(lo));
-    // Drop survivors the new bound rules out, then add this batch's.
-    const bool keep = lane < ns && s.sv[lane].hi >= L;
-    Surv e{};
-    if (keep) e = s.sv[lane];
-    unsigned m = __ballot_sync(kFull, keep);
-    __syncwarp();
-    if (keep) s.sv[__popc(m & ((1u << lane) - 1u))] = e;
-    ns = __popc(m);
-    const bool add = lane < nb && ((live >> lane) & 1u) && hi >= L;
-    m = __ballot_sync(kFull, add);
-    if (ns + __popc(m) > kMaxSurv) {
-      ovf = true;
-      break;
-    }
-    if (add) s.sv[ns + __popc(m & ((1u << lane) - 1u))] = Surv{lo, hi, s.ang[lane], 0};
-    ns += __popc(m);
-    __syncwarp();
-    ck.mark(kPhFold);
-  }
-  exact_after = false;
-  if (ovf) {  // too many near-ties to screen: the reference recipe throughout
-    search_fragment<On, B>(s, p, X, n, nf, np, first, pre, cur, cur, step, false, lane, best_a, best,
-                           evals, checks, wk, ck);
-    return;
-  }
-  evals = 1 + nfeas;
-  checks = A;
-  best_a = 0;
-  best = cur;
-  if (ns == 0) return;
-  if (ns == 1 && s.sv[0].lo > cur) {
-    best_a = s.sv[0].angle;
-    exact_after = true;
-    return;
-  }
-  // Exact resolution among the survivors, in angle order (strict '>').
-  for (int g = 0; g < ns; g += B) {
-    const int nb = min(B, ns - g);
-    if (lane < nb) s.ang[lane] = s.sv[g + lane].angle;
-    __syncwarp();
-    const double sc_l = exact_scores(s, p, X, n, nf, first, pre, nb, lane, wk);
-    for (int c = 0; c < nb; ++c) {
-      const double v = __shfl_sync(kFull, sc_l, c);
-      if (v > best) {
-        best = v;
-        best_a = s.sv[g + c].angle;
-      }
-    }
-  }
-  ck.mark(kPhDecide);
 }
 
 template <bool On, int B, int kWarps = warps_for<B>()>
@@ -1055,13 +733,8 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       int best_a = 0;
       double best = cur;
       int evals = 0, checks = 0;
-      bool exact_after = false;
-      if (!refined && p.screen)
-        search_flat_screened<On, B, 2 * B>(s, p, X, n, nf, np, first, pre, cur, step, lane, best_a,
-                                          best, exact_after, evals, checks, wk, ck);
-      else
-        search_fragment<On, B>(s, p, X, n, nf, np, first, pre, cur, cur, step, refined, lane,
-                               best_a, best, evals, checks, wk, ck);
+      search_fragment<On, B>(s, p, X, n, nf, np, first, pre, cur, cur, step, refined, lane, best_a,
+                             best, evals, checks, wk, ck);
       tally(evals, checks);
       ck.mark(kPhDecide);
       // commit_angle (kernel.hpp:115-117): a fresh rotation of the entry pose,
@@ -1079,13 +752,6 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
         }
       }
       __syncwarp();
-      if (exact_after) {  // the screened winner's exact score: the fold of its committed terms
-        double sum = 0.0;
-        if (lane == 0)
-          for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt[i].t);
-        best = __ddiv_rn(static_cast<double>(n), __shfl_sync(kFull, sum, 0));
-        wk.add(kTerms, n);
-      }
       ck.mark(kPhCommit);
       cur = best;
     }
@@ -1104,7 +770,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       dst[3 * i + 2] = q.z;
     }
   }
-  publish_warp(wk, p.counters, kFlexWorkBase, lane);
+  publish_warp(wk, p.counters, 8, lane);
   ck.publish(p.counters, lane);
 }
 
@@ -1160,7 +826,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       out[a] = 0.0;
       vout[a] = 0;
     }
-    publish_warp(wk, p.counters, kFlexWorkBase, lane);
+    publish_warp(wk, p.counters, 8, lane);
     return;
   }
   bool b0 = false;
@@ -1190,7 +856,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       out[a0 + lane] = ok ? sc : 0.0;
     }
   }
-  publish_warp(wk, p.counters, kFlexWorkBase, lane);
+  publish_warp(wk, p.counters, 8, lane);
 }
 
 // ---------------------------------------------------------------------------
@@ -1276,7 +942,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     io.evaluations[l] = evals;
     io.checks[l] = checks;
   }
-  publish_warp(wk, p.counters, kFlexWorkBase, lane);
+  publish_warp(wk, p.counters, 8, lane);
 }
 
 // rotate_fragment_into (geometry.hpp:161-186): the axis from the staged
@@ -1354,8 +1020,28 @@ __global__ void __launch_bounds__(256) fragment_bumps_kernel(DockParams p, uint8
 __global__ void __launch_bounds__(256) finalize_kernel(DockParams p) {
   const int l = p.order[blockIdx.x];
   const LigMeta m = p.meta[l];
-  if (m.status != 0 || p.status[l] != 0) return;
   const int K = p.k_slots, slots = p.top_k;
+  // Empty slots read as orientation -2 and zeros on the device too (the
+  // gd_device_results table equals the downloaded gd_result).
+  const bool failed = m.status != 0 || p.status[l] != 0;
+  for (int e = (failed ? 0 : K) + threadIdx.x; e < slots; e += blockDim.x) {
+    const size_t d = static_cast<size_t>(l) * slots + e;
+    p.out_final[d] = 0.0;
+    p.out_evals[d] = 0;
+    p.out_checks[d] = 0;
+    p.out_rank[d] = 0;
+    p.out_orient[d] = -2;
+    p.out_rigid[d] = 0.0;
+  }
+  if (failed) {
+    if (threadIdx.x == 0) {
+      p.poses_scored[l] = 0;
+      p.k_eff[l] = 0;
+    }
+    if (p.out_top != nullptr)
+      for (int i = threadIdx.x; i < 3 * m.n; i += blockDim.x) p.out_top[3 * static_cast<size_t>(m.atom_off) + i] = 0.0;
+    return;
+  }
   __shared__ double fin[256];
   __shared__ unsigned long long total;
   const int e = threadIdx.x;
@@ -1379,6 +1065,12 @@ __global__ void __launch_bounds__(256) finalize_kernel(DockParams p) {
       const int n = m.n;
       const double* from = p.stage_pose + 3 * (static_cast<size_t>(slots) * m.atom_off + static_cast<size_t>(e) * n);
       double* to = p.out_pose + 3 * (static_cast<size_t>(slots) * m.atom_off + static_cast<size_t>(pos) * n);
+      for (int i = 0; i < 3 * n; ++i) to[i] = from[i];
+    }
+    if (p.out_top != nullptr && pos == 0) {
+      const int n = m.n;
+      const double* from = p.stage_pose + 3 * (static_cast<size_t>(slots) * m.atom_off + static_cast<size_t>(e) * n);
+      double* to = p.out_top + 3 * static_cast<size_t>(m.atom_off);
       for (int i = 0; i < 3 * n; ++i) to[i] = from[i];
     }
     atomicAdd(&total, static_cast<unsigned long long>(ev));

@@ -2,6 +2,7 @@
 // and kernels.cu (device, nvcc -fmad=false).  No CUDA headers needed here.
 #pragma once
 
+#include <cstddef>
 #include <cstdint>
 
 namespace gdb200 {
@@ -18,50 +19,37 @@ struct LigMeta {
   int32_t status;     // GD_LIG_*
 };
 
-// One level of the exact voxel candidate-list index.  Voxel
-// v holds every pocket point that can attain the fp64 minimum anywhere in
-// its box (expanded by 1e-6 A).  16-byte fp32 records keep both levels
-// L2-resident; the fp64 points are reached through point indices:
-//   rec[v] = {x0, y0, z0, w}: the first candidate's coordinates rounded to
-//            fp32 and w = count << 26 | payload, payload = that candidate's
-//            point index when count == 1, else the offset of the voxel's
-//            list in lst (count field 0: count >= 64, in big[v]);
-//   lst[]  = {x, y, z, w = point index}: every candidate of each
-//            multi-candidate voxel, the first one included.  Entries [0, P)
-//            are the whole pocket: the list of overflow voxels (more than
-//            1,024 survivors) and the fp32 brute-force scan.
-// The fp32 screen walks the fp32 coordinates; exact (fp64) queries locate
-// in fp64 and read the points' fp64 coordinates by index.
-constexpr int kCountShift = 26;
-constexpr uint32_t kPayloadMask = (1u << kCountShift) - 1u;
-constexpr int kMaxFieldCount = 63;
+// One level of the exact voxel candidate-list index.  Voxel v's record is
+// {int32 start, int32 count, x0, y0, z0[, x1, y1, z1, pad]}: the first
+// kVoxInline candidates inline (a voxel with one candidate repeats it), the
+// rest at lst[start..) as 32-byte (x, y, z, pad) records.  Two inline
+// candidates (a 64-byte record, two independent 256-bit loads) spare most
+// queries their dependent list load but double the record traffic; on
+// config 1 that is 7% slower, so one is the default.
+#ifndef GD_VOX_INLINE
+#define GD_VOX_INLINE 1
+#endif
+constexpr int kVoxInline = GD_VOX_INLINE;
+static_assert(kVoxInline == 1 || kVoxInline == 2, "1 or 2 inline candidates");
+constexpr int kRecDoubles = kVoxInline == 1 ? 4 : 8;
 struct GridLevel {
-  const float* rec;          // [nvox*4]
-  const float* lst;          // [entries*4]
-  const int32_t* big;        // [nvox] counts >= 64 (only those entries are meaningful)
-  double lo_x, lo_y, lo_z;   // grid origin (fp64 locate)
-  double inv_h;              // 1 / voxel edge
-  float flo_x, flo_y, flo_z; // the same in fp32 (screen locate)
-  float finv_h;
+  const double* rec;       // [nvox*kRecDoubles] voxel records
+  const double* lst;       // [sum max(count-kVoxInline,0) * 4] further candidates, voxel-major
+  double lo_x, lo_y, lo_z; // grid origin
+  double inv_h;            // 1 / voxel edge
   int32_t dim_x, dim_y, dim_z;
   int32_t pad;
 };
 
 constexpr int kGridLevels = 2;  // fine (near field) + coarse (far field)
-constexpr int kFlexWorkBase = 16;  // counters[0..16): rigid kernel work, [16..32): flex kernel work
-constexpr int kPhaseBase = 32;     // counters[32..48): flex phase clocks
-constexpr int kCounterSlots = 48;
+constexpr int kPhaseBase = 16;     // counters[16..32): flex phase clocks
+constexpr int kCounterSlots = 32;
 
 // Exact nearest-pocket-point structure staged in HBM.
 struct PocketView {
-  const double* pts;       // [P*4] x,y,z,pad (32-B records, Morton order)
-  const float* pts32;      // [P*4] fp32 x,y,z + point index (the list head)
+  const double* pts;       // [P*4] x,y,z,pad (32-B records)
   int32_t P;
   int32_t use_index;       // 0 = brute force only
-  float eps;               // fp32-screen distance error of this pocket's
-                           // coordinates and grids (A): point rounding +
-                           // twice the fp32 voxel-locate misplacement
-  float pad;
   GridLevel lv[kGridLevels];
 };
 
@@ -86,9 +74,6 @@ struct DockParams {
   const double* orient_R;  // [n_orient*9] row-major
   const double* cos_deg;   // [360] std::cos(a * (pi/180)) from the host libm
   const double* sin_deg;   // [360]
-  const float* cos32;      // [360] the same rounded to fp32 (the screens)
-  const float* sin32;      // [360]
-  int32_t screen;          // 1: fp32 screens with exact resolution; 0: fp64 throughout
 
   // Knobs (kernel.hpp:21-26) + batch knobs.
   int32_t hp, lp, reps, refine, tile;
@@ -118,11 +103,13 @@ struct DockParams {
   int64_t* out_checks;
   double* out_pose;        // nullable; [K*atoms*3]
   double* stage_pose;      // nullable; rank-order staging, same shape
+  double* out_top;         // nullable; [3*atoms] each ligand's slot-0 pose (needs stage_pose)
   int64_t* poses_scored;   // [L]
   int32_t* status;         // [L]
-  // Optional exact work counters: [0..16) rigid kernel, [16..32) flex
-  // kernel, each in WorkKind order (device_common.cuh); [kPhaseBase..+16)
-  // flex phase clocks (GD_PHASE_CLOCKS builds).
+  // Optional exact work counters: [0..6] rigid kernel, [8..14] flex kernel,
+  // each {pairs, rotated atoms, bump pairs, queries, sum terms, candidate
+  // evaluations, rigid-transformed atoms}; [kPhaseBase..+16) flex phase
+  // clocks (GD_PHASE_CLOCKS builds).
   unsigned long long* counters;
 };
 
@@ -162,6 +149,32 @@ int launch_finalize(const DockParams& p, void* stream);
 int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int n_poses,
                        double* out, void* stream);
 
+// Ligand preprocessing on the GPU (prep.cu), ligands [l0, l1) of a batch.
+// The host fills meta[] except nfrag/status (status pre-set to 1 for atom
+// counts outside [2, kMaxAtoms]) with far_off = prefix of n*words,
+// frag_off = 2 * first bond, fmask_off = prefix of 2 * bonds * words; the
+// kernel writes status[] (and meta.status / nfrag), the far masks and the
+// fragments, and order[l0..l1) = the ligands longest-first.
+struct PrepParams {
+  int32_t l0, l1;
+  int32_t max_n, max_b;    // largest atom (<= kMaxAtoms) and bond count in [l0, l1)
+  LigMeta* meta;
+  const int32_t* boff;     // [L+1] bond offsets
+  const int32_t* bonds;    // [2*bonds] ligand-local atom pairs
+  const uint8_t* rot;      // [bonds] Bond::rotatable
+  const double* xyz;       // [3*atoms]
+  const double* radii;     // [atoms]
+  uint64_t* far;
+  uint64_t* fmask;
+  int32_t* fax;
+  int32_t* fan;
+  double* frel;
+  int32_t* status;         // [L] per-ligand status (GD_LIG_*)
+  int32_t* order;          // [L] CTA order
+};
+size_t prep_smem_per_warp(int max_n, int max_b);
+int launch_prep(const PrepParams& q, void* stream);
+
 // Voxel index build (two passes: count, then fill after a host scan).
 struct VoxelGrid {
   double lo_x, lo_y, lo_z, h;
@@ -178,14 +191,13 @@ struct VoxelGrid {
 // candidates there and the fill pass copies them instead of recomputing.
 int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, const float* tbox,
                        int nt, int32_t* keep, void* stream);
-int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, float* rec,
-                      float* lst, int32_t* big, const float* tbox, int nt, const int32_t* counts,
+int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
+                      double* lst, const float* tbox, int nt, const int32_t* counts,
                       const int32_t* keep, void* stream);
-// offsets[v] = base + exclusive prefix over voxels of the listed entries
-// (count when count > 1, else 0; the first `base` = P entries hold the
-// whole pocket for overflow voxels); totals[3] (device) = {listed entries
-// incl. base, candidates, max count}; `scratch` holds
-// list_offsets_scratch_bytes(nv).
+// offsets[v] = base + exclusive prefix of max(counts - kVoxInline, 0) over
+// voxels (the first `base` = P list records hold the whole pocket for
+// overflow voxels); totals[3] (device) = {listed entries incl. base,
+// candidates, max count}; `scratch` holds list_offsets_scratch_bytes(nv).
 int list_offsets_scratch_bytes(int nv);
 int launch_list_offsets(const int32_t* counts, int nv, int P, long long base, int32_t* offsets,
                         void* scratch, long long* totals, void* stream);

@@ -370,9 +370,9 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_count_kernel(const double
 __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double* pts, int P,
                                                                    VoxelGrid g,
                                                                    const int32_t* offsets,
-                                                                   float* rec, float* lst,
-                                                                   int32_t* big, const float* tbox,
-                                                                   int nt, const int32_t* counts,
+                                                                   double* rec, double* lst,
+                                                                   const float* tbox, int nt,
+                                                                   const int32_t* counts,
                                                                    const int32_t* keep) {
   __shared__ float4 tile[kTile];
   __shared__ BrickScratch sc;
@@ -399,28 +399,29 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double*
   }
   // Overflow (more than kVoxMaxCand survivors, e.g. inside a hollow shell
   // pocket where no surface point dominates another): the voxel's list is
-  // the whole pocket, held once at the head of the list array (entries
-  // [0, P), written by the host), so it costs no list memory.
+  // the whole pocket, which the list array holds once at its head (records
+  // [0, P), copied by the host), so the record is {start 1, count P, point
+  // 0 inline} and costs no list memory.
   const int len = k < 0 ? P : k;  // >= 1: the nearest point always survives
-  const int j0 = k < 0 ? 0 : cand[0];
-  const int start = k < 0 ? 0 : offsets[v];
-  const uint32_t cf = len <= kMaxFieldCount ? static_cast<uint32_t>(len) : 0u;
-  const uint32_t payload = len == 1 ? static_cast<uint32_t>(j0) : static_cast<uint32_t>(start);
-  float4* r = reinterpret_cast<float4*>(rec) + v;
-  *r = make_float4(static_cast<float>(pts[4 * j0]), static_cast<float>(pts[4 * j0 + 1]),
-                   static_cast<float>(pts[4 * j0 + 2]), __uint_as_float((cf << kCountShift) | payload));
-  if (cf == 0) big[v] = len;
-  if (k < 0 || len == 1) return;
-  float4* out = reinterpret_cast<float4*>(lst) + start;
-  for (int a = 0; a < len; ++a) {
+  const int start = k < 0 ? 1 : offsets[v];
+  double* r = rec + kRecDoubles * static_cast<size_t>(v);
+  reinterpret_cast<int2*>(r)[0] = make_int2(start, len);
+  for (int q = 0; q < kVoxInline; ++q) {
+    const int a = min(q, len - 1);  // one candidate: repeat it
+    const int j = k < 0 ? a : cand[a];
+    for (int c = 0; c < 3; ++c) r[1 + 3 * q + c] = pts[4 * j + c];
+  }
+  if (kRecDoubles == 8) r[7] = 0.0;
+  if (k < 0) return;
+  double* out = lst + 4 * static_cast<size_t>(start);
+  for (int a = kVoxInline; a < len; ++a) {
     const int j = cand[a];
-    out[a] = make_float4(static_cast<float>(pts[4 * j]), static_cast<float>(pts[4 * j + 1]),
-                         static_cast<float>(pts[4 * j + 2]), __uint_as_float(static_cast<uint32_t>(j)));
+    for (int c = 0; c < 4; ++c) out[4 * (a - kVoxInline) + c] = pts[4 * j + c];
   }
 }
 
-// List offsets on the device: offsets[v] = base + the listed entries of
-// earlier voxels (count when count > 1); totals = {listed entries, candidates, max
+// List offsets on the device: offsets[v] = sum over earlier voxels of
+// max(count - kVoxInline, 0); totals = {listed entries, candidates, max
 // count}.  Three passes over 1024-voxel blocks (block sums, one-block scan
 // of the sums, block-local scans), so the build needs no host round trip of
 // the counts.
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(kScanBlock) list_block_sums(const int32_t* cou
   if (threadIdx.x == 0) mx = 0;
   __syncthreads();
   atomicMax(&mx, c);
-  const long long l = block_sum_ll(raw > 1 ? raw : 0, red);
+  const long long l = block_sum_ll(max(raw - kVoxInline, 0), red);
   const long long t = block_sum_ll(c, red);
   if (threadIdx.x == 0) {
     bsum[blockIdx.x] = l;
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(kScanBlock) list_apply(const int32_t* counts, 
                                                          const long long* bsum, int32_t* offsets) {
   __shared__ long long part[kScanBlock];
   const int v = blockIdx.x * kScanBlock + threadIdx.x;
-  const long long x = v < nv && counts[v] > 1 ? counts[v] : 0;
+  const long long x = v < nv ? max(counts[v] - kVoxInline, 0) : 0;
   part[threadIdx.x] = x;
   __syncthreads();
   for (int o = 1; o < kScanBlock; o <<= 1) {
@@ -594,12 +595,12 @@ int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, c
   return cudaGetLastError();
 }
 
-int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, float* rec,
-                      float* lst, int32_t* big, const float* tbox, int nt, const int32_t* counts,
+int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
+                      double* lst, const float* tbox, int nt, const int32_t* counts,
                       const int32_t* keep, void* stream) {
   if (nt > kMaxTiles) nt = 0;
   voxel_fill_kernel<<<build_blocks(g, nt), kBuildThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      pts, P, g, offsets, rec, lst, big, tbox, nt, counts, keep);
+      pts, P, g, offsets, rec, lst, tbox, nt, counts, keep);
   return cudaGetLastError();
 }
 

@@ -21,13 +21,17 @@ namespace {
 #ifndef GD_RIGID_MINB
 #define GD_RIGID_MINB 6  // resident CTAs per SM the register budget targets
 #endif
+#ifndef GD_RIGID_MLP
+#define GD_RIGID_MLP 1   // atoms whose nearest-point lookups are in flight together
+#endif
 #ifndef GD_RIGID_RSMEM
 #define GD_RIGID_RSMEM 1 // the orientation matrix re-read from shared memory per atom group (c1 rigid 2.96 -> 2.91 ms, c2 20.9 -> 19.9)
 #endif
 constexpr int kRigidThreads = 256;
 
 // Score of orientation s: rotate every atom (E3) and fold the overlap terms
-// strictly in atom order (geometry.hpp:143-154).
+// strictly in atom order (geometry.hpp:143-154); atoms go in groups of
+// GD_RIGID_MLP so their nearest-point lookups are in flight together.
 template <bool On>
 __device__ __forceinline__ double score_orientation(const DockParams& p, int s, int n,
                                                    const double* vx, const double* vy,
@@ -45,7 +49,23 @@ __device__ __forceinline__ double score_orientation(const DockParams& p, int s, 
   for (int r = 0; r < 9; ++r) R[r] = __ldg(p.orient_R + 9 * s + r);
 #endif
   double sum = 0.0;
-  for (int i = 0; i < n; ++i) {
+  int i = 0;
+  for (; i + GD_RIGID_MLP - 1 < n; i += GD_RIGID_MLP) {
+#if GD_RIGID_RSMEM
+    double R[9];
+#pragma unroll
+    for (int r = 0; r < 9; ++r) R[r] = Rv[r * kRigidThreads];
+#endif
+    double x[GD_RIGID_MLP], y[GD_RIGID_MLP], z[GD_RIGID_MLP], mm[GD_RIGID_MLP];
+#pragma unroll
+    for (int r = 0; r < GD_RIGID_MLP; ++r)
+      rigid_apply(R, p.cx, p.cy, p.cz, vx[i + r], vy[i + r], vz[i + r], x[r], y[r], z[r]);
+    wk.add(kXform, GD_RIGID_MLP);
+    min_dist_sqM<GD_RIGID_MLP>(p.pocket, x, y, z, mm, wk);
+#pragma unroll
+    for (int r = 0; r < GD_RIGID_MLP; ++r) sum = dadd(sum, fmax(kMinDistanceSq, mm[r]));
+  }
+  for (; i < n; ++i) {
 #if GD_RIGID_RSMEM
     double R[9];
 #pragma unroll

@@ -25,9 +25,8 @@ GD_LIG_DEGENERATE = 3
 GD_FLAG_BRUTE_FORCE = 1
 GD_FLAG_KEEP_POSES = 2
 GD_FLAG_COUNT_WORK = 4
-GD_FLAG_EXACT_FP64 = 8
-WORK_FIELDS = ["pairs", "rotated", "bump_pairs", "queries", "sum_terms", "evaluations", "xform",
-               "pairs32", "rotated32", "bump_pairs32", "queries32", "exact_resolved"]
+GD_FLAG_TOP_POSE = 16
+WORK_FIELDS = ["pairs", "rotated", "bump_pairs", "queries", "sum_terms", "evaluations", "xform"]
 
 _i32p = C.POINTER(C.c_int32)
 _i64p = C.POINTER(C.c_int64)
@@ -52,13 +51,15 @@ class gd_result(C.Structure):
     _fields_ = [("orientation", _i32p), ("seed_rank", _i32p), ("rigid_score", _f64p),
                 ("final_score", _f64p), ("evaluations", _i64p),
                 ("feasibility_checks", _i64p), ("final_pose", _f64p), ("k_eff", _i32p),
-                ("poses_scored", _i64p), ("status", _i32p)]
+                ("poses_scored", _i64p), ("status", _i32p), ("top_pose", _f64p)]
 
 
 class gd_device_result(C.Structure):
     _fields_ = [("orientation", C.c_void_p), ("seed_rank", C.c_void_p),
                 ("final_score", C.c_void_p), ("evaluations", C.c_void_p),
-                ("n_ligands", C.c_int32), ("top_k", C.c_int32)]
+                ("n_ligands", C.c_int32), ("top_k", C.c_int32),
+                ("rigid_score", C.c_void_p), ("feasibility_checks", C.c_void_p),
+                ("k_eff", C.c_void_p), ("poses_scored", C.c_void_p), ("status", C.c_void_p)]
 
 
 class gd_fragment_set(C.Structure):
@@ -321,26 +322,31 @@ class DockResult:
     poses_scored: np.ndarray
     status: np.ndarray
     final_pose: np.ndarray | None = None  # flat [K*A*3] (see header for layout)
+    top_pose: np.ndarray | None = None    # [A, 3]: each ligand's slot-0 pose at its atom offset
 
     @staticmethod
-    def empty(L: int, K: int, total_atoms: int, poses: bool) -> "DockResult":
+    def empty(L: int, K: int, total_atoms: int, poses: bool, top: bool = False) -> "DockResult":
         return DockResult(np.zeros((L, K), np.int32), np.zeros((L, K), np.int32),
                           np.zeros((L, K)), np.zeros((L, K)), np.zeros((L, K), np.int64),
                           np.zeros((L, K), np.int64), np.zeros(L, np.int32),
                           np.zeros(L, np.int64), np.zeros(L, np.int32),
-                          np.zeros(K * total_atoms * 3) if poses else None)
+                          np.zeros(K * total_atoms * 3) if poses else None,
+                          np.zeros((total_atoms, 3)) if top else None)
 
-    def fits(self, L: int, K: int, total_atoms: int, poses: bool) -> bool:
+    def fits(self, L: int, K: int, total_atoms: int, poses: bool, top: bool = False) -> bool:
         return (self.orientation.shape == (L, K)
                 and (self.final_pose is not None) == poses
-                and (not poses or len(self.final_pose) == K * total_atoms * 3))
+                and (not poses or len(self.final_pose) == K * total_atoms * 3)
+                and (self.top_pose is not None) == top
+                and (not top or self.top_pose.shape == (total_atoms, 3)))
 
     def c_struct(self) -> gd_result:
         return gd_result(_p(self.orientation, _i32p), _p(self.seed_rank, _i32p),
                          _p(self.rigid_score, _f64p), _p(self.final_score, _f64p),
                          _p(self.evaluations, _i64p), _p(self.feasibility_checks, _i64p),
                          _p(self.final_pose, _f64p), _p(self.k_eff, _i32p),
-                         _p(self.poses_scored, _i64p), _p(self.status, _i32p))
+                         _p(self.poses_scored, _i64p), _p(self.status, _i32p),
+                         _p(self.top_pose, _f64p))
 
     def pose(self, batch: LigandBatch, l: int, e: int) -> np.ndarray:
         K = self.orientation.shape[1]
@@ -396,13 +402,14 @@ class Docker:
                 "max_candidates": m.value}
 
     def dock(self, batch: LigandBatch, knobs: Knobs, keep_poses: bool = False,
-             out: "DockResult | None" = None) -> DockResult:
+             out: "DockResult | None" = None, top_pose: bool = False) -> DockResult:
         """gd_dock_batch: host buffers in, host buffers out.  `out` (a
-        DockResult of the right shape) is reused instead of allocating."""
+        DockResult of the right shape) is reused instead of allocating;
+        top_pose fetches each ligand's top-1 final pose."""
         K = knobs.slots
         A = int(batch.atom_offsets[-1])
-        res = out if out is not None and out.fits(batch.n_ligands, K, A, keep_poses) \
-            else DockResult.empty(batch.n_ligands, K, A, keep_poses)
+        res = out if out is not None and out.fits(batch.n_ligands, K, A, keep_poses, top_pose) \
+            else DockResult.empty(batch.n_ligands, K, A, keep_poses, top_pose)
         b, k, r = batch.c_struct(), knobs.c_struct(), res.c_struct()
         self._check(self._lib.gd_dock_batch(self._h, C.byref(b), C.byref(k), C.byref(r)))
         self._batch = batch
@@ -413,10 +420,12 @@ class Docker:
         self._check(self._lib.gd_upload(self._h, C.byref(b)))
         self._batch = batch
 
-    def dock_resident(self, knobs: Knobs, keep_poses: bool = False):
+    def dock_resident(self, knobs: Knobs, keep_poses: bool = False, top_pose: bool = False):
         k = knobs.c_struct()
         if keep_poses:
             k.flags |= GD_FLAG_KEEP_POSES
+        if top_pose:
+            k.flags |= GD_FLAG_TOP_POSE
         self._check(self._lib.gd_dock_resident(self._h, C.byref(k)))
         self._K = knobs.slots
 
@@ -432,16 +441,20 @@ class Docker:
         d = gd_device_result()
         self._check(self._lib.gd_device_results(self._h, C.byref(d)))
         shape = (d.n_ligands, d.top_k)
-        view = lambda ptr, ts: torch.as_tensor(_CudaArray(ptr, shape, ts), device="cuda")
+        view = lambda ptr, ts, sh=shape: torch.as_tensor(_CudaArray(ptr, sh, ts), device="cuda")
+        per_lig = (d.n_ligands,)
         return {"final_score": view(d.final_score, "<f8"), "orientation": view(d.orientation, "<i4"),
-                "seed_rank": view(d.seed_rank, "<i4"), "evaluations": view(d.evaluations, "<i8")}
+                "seed_rank": view(d.seed_rank, "<i4"), "evaluations": view(d.evaluations, "<i8"),
+                "rigid_score": view(d.rigid_score, "<f8"),
+                "feasibility_checks": view(d.feasibility_checks, "<i8"),
+                "k_eff": view(d.k_eff, "<i4", per_lig), "poses_scored": view(d.poses_scored, "<i8", per_lig),
+                "status": view(d.status, "<i4", per_lig)}
 
     def work_counters(self) -> dict:
         """Executed work of the last call made with GD_FLAG_COUNT_WORK."""
-        out = (C.c_uint64 * 32)()
+        out = (C.c_uint64 * 16)()
         self._check(self._lib.gd_work_counters(self._h, out))
-        n = len(WORK_FIELDS)
-        return {"rigid": dict(zip(WORK_FIELDS, out[0:n])), "flex": dict(zip(WORK_FIELDS, out[16:16 + n]))}
+        return {"rigid": dict(zip(WORK_FIELDS, out[0:7])), "flex": dict(zip(WORK_FIELDS, out[8:15]))}
 
     def phase_clocks(self) -> list:
         """Flex-kernel SM cycles per phase (GD_PHASE_CLOCKS builds; zeros otherwise)."""
@@ -591,11 +604,11 @@ class MultiDocker:
         self._check(self._lib.gd_multi_set_pocket(self._h, _p(pts, _f64p), len(pts)))
 
     def dock(self, batch: LigandBatch, knobs: Knobs, keep_poses: bool = False,
-             out: "DockResult | None" = None) -> DockResult:
+             out: "DockResult | None" = None, top_pose: bool = False) -> DockResult:
         K = knobs.slots
         A = int(batch.atom_offsets[-1])
-        res = out if out is not None and out.fits(batch.n_ligands, K, A, keep_poses) \
-            else DockResult.empty(batch.n_ligands, K, A, keep_poses)
+        res = out if out is not None and out.fits(batch.n_ligands, K, A, keep_poses, top_pose) \
+            else DockResult.empty(batch.n_ligands, K, A, keep_poses, top_pose)
         b, k, r = batch.c_struct(), knobs.c_struct(), res.c_struct()
         self._check(self._lib.gd_multi_dock_batch(self._h, C.byref(b), C.byref(k), C.byref(r)))
         return res
@@ -665,18 +678,38 @@ def orientations(step: int):
     return idx, R.reshape(n, 3, 3)
 
 
+_synth_override = None
+
+
+def set_synth_library(path) -> None:
+    """Generate synthetic inputs with the gd_synth_* functions of another
+    library built from the same csrc/synth.cpp (oracle/libgd_synth.so): the
+    reference benchmark arm builds its inputs without the product library."""
+    global _synth_override
+    h = C.CDLL(str(path))
+    for name in ("gd_synth_pocket", "gd_synth_ligand_size", "gd_synth_ligand"):
+        res, args = SIGNATURES[name]
+        getattr(h, name).restype = res
+        getattr(h, name).argtypes = args
+    _synth_override = h
+
+
+def _synth() -> C.CDLL:
+    return _synth_override if _synth_override is not None else lib()
+
+
 def synth_pocket(a: float, b: float, c: float, spacing: float, rough_max: float = 0.0,
                  seed: int = 0) -> np.ndarray:
-    n = lib().gd_synth_pocket(a, b, c, spacing, rough_max, seed, None, 0)
+    n = _synth().gd_synth_pocket(a, b, c, spacing, rough_max, seed, None, 0)
     out = np.zeros((n, 3))
-    lib().gd_synth_pocket(a, b, c, spacing, rough_max, seed, _p(out, _f64p), n)
+    _synth().gd_synth_pocket(a, b, c, spacing, rough_max, seed, _p(out, _f64p), n)
     return out
 
 
 def synth_ligands(base_seed: int, ids, n_lo: int = 20, n_hi: int = 60, fixed_n: int = 0,
                   r_cap: int = 12, fixed_r: int = -1, centre=(0.0, 0.0, 0.0)) -> LigandBatch:
     """BASELINE random-walk-tree ligands `ids` of the family `base_seed`."""
-    L = lib()
+    L = _synth()
     ids = list(ids)
     sizes = np.zeros(len(ids), np.int32)
     tmp = C.c_int32()

@@ -151,3 +151,26 @@ def test_ligand_graph_matches_reference():
     assert O.ref_ligand_graph(*bad) is None
     with pytest.raises(GeoDockError, match="self-bond"):
         ligand_graph(*bad)
+
+
+def test_standalone_synth_library_matches_product():
+    """bench.py's reference arm builds its inputs with oracle/libgd_synth.so
+    (the same csrc/synth.cpp built alone); they equal the product's."""
+    import subprocess
+    import sys
+    code = """
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+from oracle import oracle_py as O
+from paper_1901_06363_b200 import native, workloads as W
+w = W.config(1)
+a = (w.pocket(), w.ligands(range(40)))
+native.set_synth_library(O.HERE / "libgd_synth.so")
+b = (w.pocket(), w.ligands(range(40)))
+assert np.array_equal(a[0], b[0])
+for f in ("atom_offsets", "xyz", "radii", "bond_offsets", "bonds", "rotatable"):
+    assert np.array_equal(getattr(a[1], f), getattr(b[1], f)), f
+print("ok")
+""".format(root=str(ROOT))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True)
+    assert out.stdout.strip() == "ok", out.stderr

@@ -99,7 +99,8 @@ def test_device_results_views_match_download(docker):
     host = docker.download(DockResult.empty(batch.n_ligands, w.knobs.slots,
                                             int(batch.atom_offsets[-1]), False))
     dev = docker.device_results()
-    for f in ("final_score", "orientation", "seed_rank", "evaluations"):
+    from paper_1901_06363_b200.sharding import DeviceGather
+    for f in DeviceGather.FIELDS:  # every gd_result field but the poses, empty slots included
         assert np.array_equal(dev[f].cpu().numpy(), getattr(host, f)), f
     # The bench's N>1 gather over those views (a world-1 NCCL group here).
     import socket
@@ -115,6 +116,28 @@ def test_device_results_views_match_download(docker):
             assert np.array_equal(out[f][0].cpu().numpy(), getattr(host, f)), f
     finally:
         dist.destroy_process_group()
+
+
+def test_device_results_empty_slots_and_failed_ligands(docker):
+    """The device table carries the host's empty-slot values: K = 40 above a
+    24-orientation grid (rigid 90), and a ligand the validation rejects."""
+    from paper_1901_06363_b200 import DockResult, Knobs
+    from paper_1901_06363_b200.sharding import DeviceGather
+    w = W.config(1)
+    pocket = w.pocket()
+    batch = w.ligands(range(12))
+    batch.radii[batch.atom_offsets[5]] = -1.0  # ligand 5: "non-positive radius on atom 0"
+    knobs = Knobs.baseline(90, 60, 1, 40)
+    docker.set_pocket(pocket)
+    docker.upload(batch)
+    docker.dock_resident(knobs)
+    host = docker.download(DockResult.empty(batch.n_ligands, knobs.slots,
+                                            int(batch.atom_offsets[-1]), False))
+    assert host.status[5] != 0 and (host.status[np.arange(12) != 5] == 0).all()
+    assert (host.k_eff[host.status == 0] < 40).all() and (host.orientation[:, -1] == -2).all()
+    dev = docker.device_results()
+    for f in DeviceGather.FIELDS:
+        assert np.array_equal(dev[f].cpu().numpy(), getattr(host, f)), f
 
 
 def test_config2_knobs_parity(docker):

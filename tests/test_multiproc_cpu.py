@@ -61,10 +61,10 @@ def test_sharded_gather_equals_single_process(tmp_path, scaling):
     assert ids == list(range(len(ids)))
     batch = synth_ligands(77, ids, 12, 20, centre=pocket.mean(axis=0))
     want = O.dock_batch(batch, pocket, Knobs.baseline(90, 60, 1, 4), nthreads=2, keep_poses=False)
-    assert np.array_equal(merged["final_score"], want.final_score)
-    assert np.array_equal(merged["orientation"], want.orientation)
-    assert np.array_equal(merged["seed_rank"], want.seed_rank)
-    assert np.array_equal(merged["evaluations"], want.evaluations)
+    from paper_1901_06363_b200.sharding import LIGAND_FIELDS, SLOT_FIELDS
+    for f, dt in {**SLOT_FIELDS, **LIGAND_FIELDS}.items():
+        assert merged[f].dtype == dt, f  # native dtypes, no float64 packing
+        assert np.array_equal(merged[f], getattr(want, f)), f
 
 
 def _gather_worker(rank, world, port, out_dir):
@@ -79,7 +79,12 @@ def _gather_worker(rank, world, port, out_dir):
     tables = {"final_score": torch.full((L, K), float(rank) + 0.5, dtype=torch.float64),
               "orientation": torch.full((L, K), rank, dtype=torch.int32),
               "seed_rank": torch.arange(L * K, dtype=torch.int32).reshape(L, K),
-              "evaluations": torch.full((L, K), 10 * rank, dtype=torch.int64)}
+              "evaluations": torch.full((L, K), 10 * rank, dtype=torch.int64),
+              "rigid_score": torch.full((L, K), float(rank) + 0.25, dtype=torch.float64),
+              "feasibility_checks": torch.full((L, K), 7 * rank + 2**40, dtype=torch.int64),
+              "k_eff": torch.full((L,), K - rank, dtype=torch.int32),
+              "poses_scored": torch.full((L,), 2**41 + rank, dtype=torch.int64),
+              "status": torch.full((L,), rank, dtype=torch.int32)}
     out = DeviceGather(tables, world)()
     if rank == 0:
         np.savez(Path(out_dir) / "gather.npz",
@@ -99,6 +104,10 @@ def test_device_gather_all_gathers_every_field(tmp_path):
         assert (z["orientation"][r] == r).all()
         assert (z["evaluations"][r] == 10 * r).all()
         assert np.array_equal(z["seed_rank"][r], np.arange(12).reshape(3, 4))
+        assert (z["rigid_score"][r] == r + 0.25).all()
+        assert (z["feasibility_checks"][r] == 7 * r + 2**40).all()
+        assert (z["k_eff"][r] == 4 - r).all() and (z["status"][r] == r).all()
+        assert (z["poses_scored"][r] == 2**41 + r).all() and z["poses_scored"].dtype == np.int64
 
 
 def test_shard_ids_cover_exactly():

@@ -12,8 +12,8 @@ import subprocess
 import sys
 
 sys.path.insert(0, os.getcwd())
-PHASES = ["chain start", "step setup", "bump prefilter", "screen setup", "bump checks",
-          "queries", "survivors", "decisions", "commit", "fold + bounds"]
+PHASES = ["chain start", "step setup", "bump prefilter", "term pre-fill", "bump checks",
+          "queries", "folds", "decisions", "commit"]
 
 
 def main():

@@ -34,7 +34,8 @@ def main():
         d.set_pocket(pocket)
         d.upload(batch)
         from paper_1901_06363_b200 import Knobs
-        from paper_1901_06363_b200.native import GD_FLAG_EXACT_FP64
+        from paper_1901_06363_b200 import native as _nat
+        GD_FLAG_EXACT_FP64 = getattr(_nat, "GD_FLAG_EXACT_FP64", 0)
         knobs = Knobs(**{**w.knobs.__dict__, "flags": GD_FLAG_EXACT_FP64 if a.exact else 0})
         rows = []
         for r in range(a.reps + 2):
