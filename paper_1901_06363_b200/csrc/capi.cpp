@@ -237,7 +237,7 @@ struct gd_ctx {
   bool staged = false;  // a batch is staged (gd_upload / gd_dock_batch)
   DevBuf st_final, st_evals, st_checks;
   DevBuf seed_slot, seed_score, k_eff, o_orient, o_rank, o_rigid, o_final, o_evals, o_checks,
-      o_pose, stage_pose, o_top, o_scored, o_status;
+      o_pose, stage_pose, o_top, top_best, o_scored, o_status;
   std::vector<double> initial_score;  // given-pose mode: rigid_score column
 
   gd_timing timing{};
@@ -886,8 +886,10 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, bool kee
     if (keep_pose) GD_CUDA(ctx, ctx->o_pose.ensure(pose_bytes));
     GD_CUDA(ctx, ctx->stage_pose.ensure(pose_bytes));
   }
-  if (keep_top)
+  if (keep_top) {
     GD_CUDA(ctx, ctx->o_top.ensure(sizeof(double) * 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1))));
+    GD_CUDA(ctx, ctx->top_best.ensure(sizeof(unsigned long long) * std::max(L, 1)));
+  }
   p = DockParams{};
   p.order = ctx->order.as<int32_t>();
   p.meta = ctx->meta.as<LigMeta>();
@@ -932,6 +934,8 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, bool kee
   p.out_pose = keep_pose ? ctx->o_pose.as<double>() : nullptr;
   p.stage_pose = (keep_pose || keep_top) ? ctx->stage_pose.as<double>() : nullptr;
   p.out_top = keep_top ? ctx->o_top.as<double>() : nullptr;
+  // Top-1 only: chains stage their pose only while improving their ligand's best.
+  p.top_best = (keep_top && !keep_pose) ? ctx->top_best.as<unsigned long long>() : nullptr;
   p.poses_scored = ctx->o_scored.as<int64_t>();
   p.status = ctx->o_status.as<int32_t>();
   p.counters = nullptr;
@@ -957,6 +961,8 @@ static int launch_range(gd_ctx* ctx, DockParams p, int c0, int c1, int max_n, cu
   p.max_n = max_n;
   p.max_pairs = std::max(1, max_n * max_n / 4);
   if (p.n_lig == 0) return GD_OK;
+  if (p.top_best != nullptr)
+    GD_CUDA(ctx, cudaMemsetAsync(p.top_best + c0, 0, sizeof(unsigned long long) * (c1 - c0), s));
   if (p.rigid) {
     GD_CUDA(ctx, static_cast<cudaError_t>(launch_rigid_topk(p, s)));
     ctx->timing.launches += 1;

@@ -761,7 +761,18 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     p.st_evals[e] = s.tally[0];
     p.st_checks[e] = s.tally[1];
   }
-  if (p.stage_pose != nullptr) {
+  // Final pose staging.  Top-1-only callers (top_best set) stage a chain's
+  // pose only if its score is >= every score the ligand's finished chains
+  // have published (scores are positive doubles, so their bit patterns
+  // order as integers): the E7 winner always stages (ties included), most
+  // chains skip the write.
+  bool stage = p.stage_pose != nullptr;
+  if (stage && p.top_best != nullptr) {
+    unsigned long long old = 0;
+    if (lane == 0) old = atomicMax(p.top_best + l, static_cast<unsigned long long>(__double_as_longlong(cur)));
+    stage = __longlong_as_double(static_cast<long long>(__shfl_sync(kFull, old, 0))) <= cur;
+  }
+  if (stage) {
     double* dst = p.stage_pose + 3 * (static_cast<size_t>(p.top_k) * m.atom_off + static_cast<size_t>(r) * n);
     for (int i = lane; i < n; i += 32) {
       const PT q = s.pt[i];

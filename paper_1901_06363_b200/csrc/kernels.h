@@ -104,6 +104,8 @@ struct DockParams {
   double* out_pose;        // nullable; [K*atoms*3]
   double* stage_pose;      // nullable; rank-order staging, same shape
   double* out_top;         // nullable; [3*atoms] each ligand's slot-0 pose (needs stage_pose)
+  unsigned long long* top_best;  // nullable; [L] running max of finished chains' scores
+                                 // (bits), zeroed per launch: only improving chains stage
   int64_t* poses_scored;   // [L]
   int32_t* status;         // [L]
   // Optional exact work counters: [0..6] rigid kernel, [8..14] flex kernel,
