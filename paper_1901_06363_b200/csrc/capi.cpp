@@ -1099,7 +1099,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   rc = prepare_dock(ctx, knobs, keep_pose, keep_top, p);
   if (rc != GD_OK) return rc;
   const int L = ctx->n_lig, K = ctx->last_topk;
-  static const int kStreams = std::max(1, static_cast<int>(env_double("GD_E2E_STREAMS", 2)));
+  static const int kStreams = std::max(1, static_cast<int>(env_double("GD_E2E_STREAMS", 6)));
   while (static_cast<int>(ctx->aux_streams.size()) < kStreams - 1) {
     cudaStream_t st;
     GD_CUDA(ctx, cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -1132,18 +1132,18 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
   pr.final_pose = keep_pose ? static_cast<double*>(take(8 * pose_elems)) : nullptr;
   pr.top_pose = keep_top ? static_cast<double*>(take(8 * top_elems)) : nullptr;
 
-  // Chunk plan: a small head chunk (its host prep is the only part nothing
-  // overlaps), then chunks growing geometrically by 1.6x: host prep runs
-  // faster than the GPU docks, so each chunk is prepared before the GPU
-  // drains the previous ones, and few launch tails remain (c1: 19.36 ms vs
-  // 19.85 with 15 equal chunks at r2a; 18.11 vs 18.24 at 1.5x on the r2b
-  // kernels, 1.7x / 2.0x worse again as the last chunk grows;
-  // tools/e2e_plan_ab.sh).  GD_E2E_GROWTH<=1 selects the equal split into
-  // GD_E2E_CHUNKS parts.
+  // Chunk plan: a small head chunk (the only host packing nothing
+  // overlaps), then chunks growing geometrically by 1.3x, spread over six
+  // streams so each chunk's kernels start while earlier chunks' tails and
+  // copies drain.  Re-tuned once preprocessing moved to the GPU (r3b,
+  // tools/e2e_ab.py, c1 with top-1 poses: 2 streams / 1.6x 17.1-17.3 ms,
+  // 3 streams 16.3-16.4, 4 streams 16.2-16.3, 6 streams / 1.3x 16.15-16.18;
+  // mirrored "tapered" plans 16.5-17.7).  GD_E2E_GROWTH<=1 selects the equal
+  // split into GD_E2E_CHUNKS parts.
   std::vector<int> bounds{0};
   static const int kHead = static_cast<int>(env_double("GD_E2E_HEAD", 256));
   static const int kParts = static_cast<int>(env_double("GD_E2E_CHUNKS", 15));
-  static const double kGrowth = env_double("GD_E2E_GROWTH", 1.6);
+  static const double kGrowth = env_double("GD_E2E_GROWTH", 1.3);
   if (L > 2048 && kGrowth > 1.0) {
     bounds.push_back(kHead);
     double sz = kHead;
