@@ -683,11 +683,10 @@ static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
 // Host half of a chunk: offsets of ligands [c0, c1) into the descriptor
 // arrays, and their raw atoms and bonds into the pinned arena (the bulk
 // copy on the worker pool for large chunks).  Returns the chunk's largest
-// atom and bond counts (of ligands the GPU preprocesses).
+// atom count (of ligands the GPU preprocesses).
 static void pack_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Running& run,
-                       int& chunk_max_n, int& chunk_max_b) {
+                       int& chunk_max_n) {
   chunk_max_n = 1;
-  chunk_max_b = 1;
   if (c1 <= c0) return;
   auto* meta = reinterpret_cast<LigMeta*>(ctx->pin[kMeta]);
   for (int l = c0; l < c1; ++l) {
@@ -705,7 +704,6 @@ static void pack_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
     run.wo += static_cast<size_t>(m.n) * m.words;
     run.mo += 2 * static_cast<size_t>(nb) * m.words;
     chunk_max_n = std::max(chunk_max_n, m.n);
-    chunk_max_b = std::max(chunk_max_b, nb);
   }
   auto* bo = reinterpret_cast<int32_t*>(ctx->pin[kBoff]);
   for (int l = c0; l <= c1; ++l) bo[l] = b->bond_offsets[l];
@@ -745,7 +743,7 @@ static void pack_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
 }
 
 // Copy half of a chunk (pinned -> HBM) and its GPU preprocessing, on stream s.
-static int h2d_prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, int max_n, int max_b,
+static int h2d_prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, int max_n,
                           cudaStream_t s) {
   if (c1 <= c0) return GD_OK;
   auto cp = [&](DevBuf& d, int seg, size_t off, size_t bytes) -> int {
@@ -767,7 +765,6 @@ static int h2d_prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1,
   q.l0 = c0;
   q.l1 = c1;
   q.max_n = max_n;
-  q.max_b = max_b;
   q.meta = ctx->meta.as<LigMeta>();
   q.boff = ctx->boff.as<int32_t>();
   q.bonds = ctx->bonds.as<int32_t>();
@@ -811,12 +808,12 @@ extern "C" int gd_upload(gd_ctx* ctx, const gd_ligand_batch* b) {
   int rc = begin_batch(ctx, b, run);
   if (rc != GD_OK) return rc;
   const auto t0 = std::chrono::steady_clock::now();
-  int mx = 1, mb = 1;
-  pack_range(ctx, b, 0, ctx->n_lig, run, mx, mb);
+  int mx = 1;
+  pack_range(ctx, b, 0, ctx->n_lig, run, mx);
   ctx->timing.host_pack_ms =
       std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
   cudaEventRecord(ctx->ev[0], ctx->stream);
-  rc = h2d_prep_range(ctx, b, 0, ctx->n_lig, mx, mb, ctx->stream);
+  rc = h2d_prep_range(ctx, b, 0, ctx->n_lig, mx, ctx->stream);
   if (rc != GD_OK) return rc;
   cudaEventRecord(ctx->ev[1], ctx->stream);
   // The statuses (and rejected ligands' messages) while the batch is at hand.
@@ -1184,8 +1181,8 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
     const int c0 = bounds[c], c1 = bounds[c + 1];
     cudaStream_t s = (c % kStreams) ? ctx->aux_streams[c % kStreams - 1] : ctx->stream;
     const auto t0 = std::chrono::steady_clock::now();
-    int mx = 1, mb = 1;
-    pack_range(ctx, batch, c0, c1, run, mx, mb);
+    int mx = 1;
+    pack_range(ctx, batch, c0, c1, run, mx);
     const auto t1 = std::chrono::steady_clock::now();
     prep_ms += std::chrono::duration<float, std::milli>(t1 - t0).count();
     if (kTrace) {
@@ -1193,7 +1190,7 @@ extern "C" int gd_dock_batch(gd_ctx* ctx, const gd_ligand_batch* batch, const gd
       tprep.push_back(std::chrono::duration<double, std::milli>(t1 - t_start).count());
       GD_CUDA(ctx, cudaEventRecord(tev[2 * c], s));
     }
-    if ((rc = h2d_prep_range(ctx, batch, c0, c1, mx, mb, s)) != GD_OK) return rc;
+    if ((rc = h2d_prep_range(ctx, batch, c0, c1, mx, s)) != GD_OK) return rc;
     if ((rc = launch_range(ctx, p, c0, c1, mx, s, nullptr)) != GD_OK) return rc;
     if ((rc = d2h_range(ctx, &pr, c0, c1, s)) != GD_OK) return rc;
     if (kTrace) GD_CUDA(ctx, cudaEventRecord(tev[2 * c + 1], s));

@@ -159,7 +159,7 @@ int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int
 // fragments, and order[l0..l1) = the ligands longest-first.
 struct PrepParams {
   int32_t l0, l1;
-  int32_t max_n, max_b;    // largest atom (<= kMaxAtoms) and bond count in [l0, l1)
+  int32_t max_n;           // largest atom count (<= kMaxAtoms) in [l0, l1)
   LigMeta* meta;
   const int32_t* boff;     // [L+1] bond offsets
   const int32_t* bonds;    // [2*bonds] ligand-local atom pairs
@@ -174,7 +174,7 @@ struct PrepParams {
   int32_t* status;         // [L] per-ligand status (GD_LIG_*)
   int32_t* order;          // [L] CTA order
 };
-size_t prep_smem_per_warp(int max_n, int max_b);
+size_t prep_smem_per_warp(int max_n);
 int launch_prep(const PrepParams& q, void* stream);
 
 // Voxel index build (two passes: count, then fill after a host scan).

@@ -31,9 +31,11 @@ namespace {
 
 constexpr int kPrepWarps = 4;  // ligands per CTA
 
-__host__ __device__ __forceinline__ size_t smem_per_warp(int max_n, int max_b) {
+// Per warp: adjacency rows [max_n * Wm], left-fragment masks and keys of at
+// most max_n rotamers.
+__host__ __device__ __forceinline__ size_t smem_per_warp(int max_n) {
   const size_t Wm = (max_n + 63) / 64;
-  return ((8 * Wm * (max_n + max_b) + 4 * static_cast<size_t>(max_b)) + 15) & ~size_t(15);
+  return ((16 * Wm * max_n + 4 * static_cast<size_t>(max_n)) + 15) & ~size_t(15);
 }
 constexpr unsigned kAll = 0xffffffffu;
 
@@ -67,10 +69,10 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(PrepParams q) {
   const int n = m.n, W = m.words;
   const int b0 = q.boff[l], nb = q.boff[l + 1] - b0;
   const int Wm = (q.max_n + 63) / 64;
-  unsigned char* base = smem + warp * smem_per_warp(q.max_n, q.max_b);
+  unsigned char* base = smem + warp * smem_per_warp(q.max_n);
   uint64_t* adj = reinterpret_cast<uint64_t*>(base);                         // [max_n * Wm]
-  uint64_t* left = adj + static_cast<size_t>(q.max_n) * Wm;                 // [max_b * Wm]
-  int32_t* key = reinterpret_cast<int32_t*>(left + static_cast<size_t>(q.max_b) * Wm);  // [max_b]
+  uint64_t* left = adj + static_cast<size_t>(q.max_n) * Wm;                 // [max_n * Wm]
+  int32_t* key = reinterpret_cast<int32_t*>(left + static_cast<size_t>(q.max_n) * Wm);  // [max_n]
 
   // Ligand::validate (molecule.hpp:66-89): atoms.
   bool bad = false;
@@ -168,57 +170,66 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(PrepParams q) {
     }
   }
 
-  // Rotamers and their left fragments: a lane per rotatable bond.
-  for (int b = lane; b < nb; b += 32) {
-    key[b] = 0x7fffffff;
-    if (!q.rot[b0 + b]) continue;
-    const int a0 = q.bonds[2 * (b0 + b)], a1 = q.bonds[2 * (b0 + b) + 1];
-    const int lo = min(a0, a1), hi = max(a0, a1);
-    uint64_t vis[4] = {0, 0, 0, 0}, fr[4] = {0, 0, 0, 0};
-    vis[lo >> 6] = fr[lo >> 6] = 1ull << (lo & 63);
-    for (;;) {
-      uint64_t nx[4] = {0, 0, 0, 0};
-      for (int w = 0; w < W; ++w)
-        for (uint64_t bits = fr[w]; bits; bits &= bits - 1) {
-          const int a = 64 * w + __ffsll(static_cast<long long>(bits)) - 1;
-          for (int v = 0; v < W; ++v) {
-            uint64_t row = adj[a * W + v];
-            if (a == lo && v == (hi >> 6)) row &= ~(1ull << (hi & 63));  // the bond itself is cut
-            nx[v] |= row;
+  // Rotamers and their left fragments: a lane per rotatable bond, in rounds
+  // of 32; bridges (at most n - 1 in any graph) are appended to a compact
+  // list, so shared memory is sized by the atom count, not the bond count.
+  int nrot = 0;
+  for (int b0r = 0; b0r < nb; b0r += 32) {
+    const int b = b0r + lane;
+    bool bridge = false;
+    int kb = 0;
+    uint64_t vis[4] = {0, 0, 0, 0};
+    if (b < nb && q.rot[b0 + b]) {
+      const int a0 = q.bonds[2 * (b0 + b)], a1 = q.bonds[2 * (b0 + b) + 1];
+      const int lo = min(a0, a1), hi = max(a0, a1);
+      uint64_t fr[4] = {0, 0, 0, 0};
+      vis[lo >> 6] = fr[lo >> 6] = 1ull << (lo & 63);
+      for (;;) {
+        uint64_t nx[4] = {0, 0, 0, 0};
+        for (int w = 0; w < W; ++w)
+          for (uint64_t bits = fr[w]; bits; bits &= bits - 1) {
+            const int a = 64 * w + __ffsll(static_cast<long long>(bits)) - 1;
+            for (int v = 0; v < W; ++v) {
+              uint64_t row = adj[a * W + v];
+              if (a == lo && v == (hi >> 6)) row &= ~(1ull << (hi & 63));  // the bond itself is cut
+              nx[v] |= row;
+            }
           }
+        bool any = false;
+        for (int v = 0; v < W; ++v) {
+          nx[v] &= ~vis[v];
+          vis[v] |= nx[v];
+          fr[v] = nx[v];
+          any |= nx[v] != 0;
         }
-      bool any = false;
-      for (int v = 0; v < W; ++v) {
-        nx[v] &= ~vis[v];
-        vis[v] |= nx[v];
-        fr[v] = nx[v];
-        any |= nx[v] != 0;
+        if (!any) break;
       }
-      if (!any) break;
+      bridge = !has(vis, hi);  // in a ring: not a bridge, not a rotamer
+      kb = (lo << 8) | hi;
     }
-    if (has(vis, hi)) continue;  // in a ring: not a bridge, not a rotamer
-    key[b] = (lo << 8) | hi;
-    for (int v = 0; v < W; ++v) left[b * Wm + v] = vis[v];
+    const unsigned bal = __ballot_sync(kAll, bridge);
+    if (bridge) {
+      const int at = nrot + __popc(bal & ((1u << lane) - 1u));
+      key[at] = kb;
+      for (int v = 0; v < W; ++v) left[at * Wm + v] = vis[v];
+    }
+    nrot += __popc(bal);
   }
   __syncwarp();
-  int nrot = 0;
-  for (int b = lane; b < nb; b += 32) nrot += key[b] != 0x7fffffff;
-  nrot = __reduce_add_sync(kAll, nrot);
-  for (int b = lane; b < nb; b += 32) {
-    const int kb = key[b];
-    if (kb == 0x7fffffff) continue;
-    int r = 0;
-    for (int c = 0; c < nb; ++c) r += key[c] < kb;
+  for (int e = lane; e < nrot; e += 32) {
+    const int kb = key[e];
+    int r = 0;  // find_rotamers order: rank of the unique key (lo, hi)
+    for (int c = 0; c < nrot; ++c) r += key[c] < kb;
     const int lo = kb >> 8, hi = kb & 0xff;
     int size = 0;
-    for (int v = 0; v < W; ++v) size += __popcll(left[b * Wm + v]);
+    for (int v = 0; v < W; ++v) size += __popcll(left[e * Wm + v]);
     for (int side = 0; side < 2; ++side) {
       const int f = m.frag_off + 2 * r + side;
       uint64_t* fm = q.fmask + m.fmask_off + static_cast<size_t>(2 * r + side) * W;
       for (int v = 0; v < W; ++v) {
         const int bits = min(64, n - 64 * v);
         const uint64_t valid = bits == 64 ? ~0ull : ((1ull << bits) - 1ull);
-        fm[v] = side == 0 ? left[b * Wm + v] : (~left[b * Wm + v] & valid);
+        fm[v] = side == 0 ? left[e * Wm + v] : (~left[e * Wm + v] & valid);
       }
       const int sz = side == 0 ? size : n - size;
       q.frel[f] = __ddiv_rn(static_cast<double>(sz), static_cast<double>(n));
@@ -268,12 +279,12 @@ __global__ void __launch_bounds__(kOrderThreads) order_kernel(const LigMeta* met
 
 }  // namespace
 
-size_t prep_smem_per_warp(int max_n, int max_b) { return smem_per_warp(max_n, max_b); }
+size_t prep_smem_per_warp(int max_n) { return smem_per_warp(max_n); }
 
 int launch_prep(const PrepParams& q, void* stream) {
   const int cnt = q.l1 - q.l0;
   if (cnt <= 0) return 0;
-  const size_t smem = kPrepWarps * prep_smem_per_warp(q.max_n, q.max_b);
+  const size_t smem = kPrepWarps * prep_smem_per_warp(q.max_n);
   if (smem > 48 * 1024) {
     const cudaError_t e =
         cudaFuncSetAttribute(prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));

@@ -137,3 +137,31 @@ def test_top_pose_is_slot_zero_pose(docker):
         assert np.array_equal(mres.top_pose, want)
     finally:
         m.close()
+
+
+def test_bond_count_far_above_atom_count(docker):
+    """Shared memory is sized by atoms, not bonds: a 24-atom ligand with
+    every one of its 276 atom pairs bonded (all flagged rotatable, none a
+    bridge) docks with no rotamers, and one with each bond listed twice
+    (552 bonds) is rejected as a duplicate -- neither fails the batch."""
+    O = pytest.importorskip("oracle.oracle_py")
+    n = 24
+    pos = [[1.6 * np.cos(2 * np.pi * k / n) * (1 + 0.3 * (k % 3)), 1.6 * np.sin(2 * np.pi * k / n),
+            0.4 * (k % 5)] for k in range(n)]
+    pairs = [(a, b) for a in range(n) for b in range(a + 1, n)]
+    dense = Lig(pos, [(a, b, True) for a, b in pairs], radius=0.5)
+    dup = Lig(pos, [(a, b, True) for a, b in pairs] + [(b, a, False) for a, b in pairs], radius=0.5)
+    chain = Lig(_zigzag(8), [(i, i + 1, True) for i in range(7)])
+    batch = LigandBatch.from_parts([dense.args, dup.args, chain.args])
+    pocket = W.config(0).pocket()
+    c = pocket.mean(axis=0)
+    batch.xyz[:] += c - batch.xyz.mean(axis=0)
+    docker.set_pocket(pocket)
+    knobs = Knobs.baseline(90, 60, 1, 2)
+    got = docker.dock(batch, knobs, keep_poses=True)
+    assert list(got.status) == [0, 1, 0]
+    assert "duplicate bond" in docker.ligand_error(1)
+    keep = [0, 2]
+    want = O.dock_batch(batch.subset(keep), pocket, knobs, nthreads=1)
+    for f in ("final_score", "orientation", "evaluations", "feasibility_checks"):
+        assert np.array_equal(getattr(got, f)[keep], getattr(want, f)), f
