@@ -241,7 +241,13 @@ def run_ours(a):
     knobs = w.knobs
     K = knobs.slots
 
-    stream = torch.cuda.current_stream()
+    # A dedicated stream for everything in the timed loop (the flush, the
+    # events, the library's kernels): torch's default stream is handle 0,
+    # which gd_set_stream reads as "the context's own stream", so events on
+    # it would not order the kernels.
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    assert stream.cuda_stream != 0
     d = Docker(local)
     d.set_stream(stream.cuda_stream)
     d.set_pocket(pocket)
@@ -467,7 +473,8 @@ def run_profiles(a):
     from paper_1901_06363_b200 import Docker
     from paper_1901_06363_b200.native import GD_FLAG_COUNT_WORK
     w, pocket, batch = profile_batch_of(a)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # see run_ours
+    torch.cuda.set_stream(stream)
     d = Docker(local)
     d.set_stream(stream.cuda_stream)
     d.set_pocket(pocket)
