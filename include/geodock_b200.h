@@ -134,6 +134,17 @@ int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n_points);
 /* Centre and index statistics of the staged pocket. */
 int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[3], double* voxel,
                    int64_t* n_candidates, int32_t* max_candidates);
+/* Per level of the staged pocket's exact voxel index (0 = fine near field,
+ * 1 = coarse far field): grid dims, voxel edge (A), candidates, and the
+ * HBM bytes of its voxel records and candidate lists. */
+typedef struct {
+  int32_t dims[3];
+  double voxel;
+  int64_t candidates;
+  int64_t record_bytes;
+  int64_t list_bytes;
+} gd_index_level;
+int gd_pocket_index_stats(const gd_ctx* ctx, gd_index_level out[2]);
 
 /* ---- batch docking (the hot path) --------------------------------------- */
 /* Host buffers in, host buffers out: validate + preprocess (Ligand ctor,

@@ -178,6 +178,7 @@ struct PocketSlot {
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
+  gd_index_level stats[kGridLevels] = {};
   PocketView view{};
 };
 
@@ -567,6 +568,9 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
                                        keep, ctx->stream)));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     slot->grid[L] = g;
+    slot->stats[L] = gd_index_level{{g.dim_x, g.dim_y, g.dim_z}, g.h, total,
+                                    static_cast<int64_t>(sizeof(double) * kRecDoubles) * nv,
+                                    static_cast<int64_t>(sizeof(double) * 4) * std::max<int64_t>(listed, 1)};
     slot->n_cand += total;
     slot->max_cand = std::max(slot->max_cand, mx);
     GridLevel& gl = v.lv[L];
@@ -583,6 +587,16 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   slot->P = n;
   activate(*slot);
   return GD_OK;
+}
+
+extern "C" int gd_pocket_index_stats(const gd_ctx* ctx, gd_index_level out[2]) {
+  if (ctx == nullptr || ctx->P == 0 || out == nullptr) return GD_ERR_NO_POCKET;
+  for (const auto& sl : ctx->slots)
+    if (sl->last_use == ctx->use_clock) {  // the active slot
+      for (int L = 0; L < kGridLevels; ++L) out[L] = sl->stats[L];
+      return GD_OK;
+    }
+  return GD_ERR_NO_POCKET;
 }
 
 extern "C" int gd_pocket_info(const gd_ctx* ctx, double centre[3], int32_t dims[3], double* voxel,

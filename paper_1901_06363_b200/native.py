@@ -84,6 +84,11 @@ class gd_timing(C.Structure):
                 ("host_post_ms", C.c_float)]
 
 
+class gd_index_level(C.Structure):
+    _fields_ = [("dims", C.c_int32 * 3), ("voxel", C.c_double), ("candidates", C.c_int64),
+                ("record_bytes", C.c_int64), ("list_bytes", C.c_int64)]
+
+
 class gd_multi_stats(C.Structure):
     _fields_ = [("ligands", C.c_int64), ("chunks", C.c_int64), ("busy_ms", C.c_float)]
 
@@ -125,6 +130,7 @@ SIGNATURES = {
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.c_int64]),
     "gd_device_results": (C.c_int, [C.c_void_p, C.POINTER(gd_device_result)]),
+    "gd_pocket_index_stats": (C.c_int, [C.c_void_p, C.POINTER(gd_index_level)]),
     "gd_ligand_error": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t]),
     "gd_multi_create": (C.c_int, [_i32p, C.c_int32, C.POINTER(C.c_void_p)]),
     "gd_multi_destroy": (C.c_int, [C.c_void_p]),
@@ -398,8 +404,14 @@ class Docker:
         m = C.c_int32()
         self._check(self._lib.gd_pocket_info(self._h, _p(c, _f64p), _p(d, _i32p), C.byref(h),
                                              C.byref(n), C.byref(m)))
-        return {"centre": c, "dims": d, "voxel": h.value, "n_candidates": n.value,
-                "max_candidates": m.value}
+        out = {"centre": c, "dims": d, "voxel": h.value, "n_candidates": n.value,
+               "max_candidates": m.value}
+        lv = (gd_index_level * 2)()
+        self._check(self._lib.gd_pocket_index_stats(self._h, lv))
+        out["levels"] = [{"dims": list(x.dims), "voxel": x.voxel, "candidates": x.candidates,
+                          "record_bytes": x.record_bytes, "list_bytes": x.list_bytes} for x in lv]
+        out["index_bytes"] = sum(x.record_bytes + x.list_bytes for x in lv)
+        return out
 
     def dock(self, batch: LigandBatch, knobs: Knobs, keep_poses: bool = False,
              out: "DockResult | None" = None, top_pose: bool = False) -> DockResult:

@@ -48,6 +48,13 @@ def main():
         med = [statistics.median(x[i] for x in rows) for i in range(3)]
         out = {"config": c, "rigid_ms": med[0], "flex_ms": med[1], "total_ms": med[2],
                "ligands_per_s": batch.n_ligands / (med[2] * 1e-3)}
+        try:
+            info = d.pocket_info()
+            out["index_mb"] = info["index_bytes"] / 1e6
+            out["levels"] = [(x["voxel"], round(x["record_bytes"] / 1e6, 1), round(x["list_bytes"] / 1e6, 1))
+                             for x in info["levels"]]
+        except Exception:  # older trees (A/B) lack gd_pocket_index_stats
+            pass
         if a.count:
             k = Knobs(**{**knobs.__dict__, "flags": knobs.flags | GD_FLAG_COUNT_WORK})
             d.dock_resident(k)

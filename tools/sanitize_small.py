@@ -21,4 +21,13 @@ d.dock(b, Knobs(20, 45, 0.25, 2, True, 45, 40))
 big = synth_ligands(777, [0, 1], n_lo=150, n_hi=256, r_cap=12, centre=p1.mean(axis=0))
 d.dock(big, Knobs(90, 90, 0.0, 1, False, 90, 3), keep_poses=True)
 prof = d.rotation_profiles(b)
+# GPU preprocessing corner cases and the top-1 pose output.
+from paper_1901_06363_b200 import LigandBatch  # noqa: E402
+bad = b.subset(range(6))
+bad.radii[bad.atom_offsets[2]] = -1.0
+bad.bonds[bad.bond_offsets[4]] = [0, 0]
+d.dock(bad, w1.knobs, top_pose=True)
+d.dock(b, w1.knobs, top_pose=True)
+d.upload(b)
+d.dock_resident(w1.knobs, top_pose=True)
 print("sanitize run ok", len(prof.scores))
