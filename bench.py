@@ -259,6 +259,7 @@ def run_ours(a):
     work = d.work_counters()
     fp64_peak = d.fp64_peak_tflops()
     l2_peak = d.l2_gather_peak_gbs()
+    l2_at_occ = d.l2_gather_rate_gbs(24)  # the flex kernel's residency, one gather in flight per lane
 
     d.dock_resident(knobs)
     gather = DeviceGather(d.device_results(), world) if world > 1 else None
@@ -393,7 +394,14 @@ def run_ours(a):
                                    "peak": l2_peak, "unit": "GB/s",
                                    "frac": 32.0 * dom_work["pairs"] / (dom_ms / 1e3) / 1e9 / l2_peak,
                                    "peak_source": "measured random 32 B L1-bypassing gathers over "
-                                                  "an L2-resident 48 MB buffer (gd_l2_gather_peak)"},
+                                                  "an L2-resident 48 MB buffer (gd_l2_gather_peak)",
+                                   "latency_bound_at_residency": {
+                                       "gbs": l2_at_occ,
+                                       "frac": 32.0 * dom_work["pairs"] / (dom_ms / 1e3) / 1e9 / l2_at_occ,
+                                       "what": "the same gathers with one dependent load in flight per "
+                                               "lane at the flex kernel's 24 warps per SM "
+                                               "(gd_l2_gather_rate): the ceiling for lanes that each "
+                                               "wait on their own lookup"}},
             "clocks": clk,
         }
         if e2e:

@@ -312,6 +312,11 @@ int gd_fp64_peak(gd_ctx* ctx, double* tflops);
  * the access pattern of the voxel-index gathers; the denominator of the
  * L2-gather roofline. */
 int gd_l2_gather_peak(gd_ctx* ctx, double* gbs);
+/* Latency-bound counterpart (diagnostic): the same random 32-byte gathers
+ * with ONE dependent load in flight per thread and warps_per_sm resident
+ * warps per SM (e.g. the flex kernel's 24): what a kernel whose lanes each
+ * wait on their own gather can reach at that residency (GB/s). */
+int gd_l2_gather_rate(gd_ctx* ctx, int32_t warps_per_sm, double* gbs);
 
 /* ---- fine-grained kernels ------------------------------------------------ */
 /* overlap_score (geometry.hpp:140-155) of n_poses poses of n_atoms atoms

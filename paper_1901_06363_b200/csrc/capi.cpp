@@ -1748,6 +1748,33 @@ extern "C" int gd_l2_gather_peak(gd_ctx* ctx, double* gbs) {
   return GD_OK;
 }
 
+extern "C" int gd_l2_gather_rate(gd_ctx* ctx, int32_t warps_per_sm, double* gbs) {
+  if (ctx == nullptr || gbs == nullptr || warps_per_sm < 1) return GD_ERR_INVALID;
+  GD_CUDA(ctx, cudaSetDevice(ctx->device));
+  int sms = 0;
+  GD_CUDA(ctx, cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+  const unsigned long long n_rec = (48ull << 20) / 32;  // the same 48 MB L2-resident buffer
+  DevBuf buf, sink;
+  GD_CUDA(ctx, buf.ensure(32 * n_rec));
+  GD_CUDA(ctx, sink.ensure(64));
+  GD_CUDA(ctx, cudaMemsetAsync(buf.ptr, 0, 32 * n_rec, ctx->stream));
+  const int threads = 32 * std::min(warps_per_sm, 32), blocks = sms * ((warps_per_sm + 31) / 32);
+  const int iters = 1024;
+  float best = 1e30f;
+  for (int rep = 0; rep < 5; ++rep) {
+    GD_CUDA(ctx, cudaEventRecord(ctx->ev[0], ctx->stream));
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_l2_chase_probe(buf.as<double>(), n_rec, blocks, threads,
+                                                                 iters, sink.as<double>(), ctx->stream)));
+    GD_CUDA(ctx, cudaEventRecord(ctx->ev[1], ctx->stream));
+    GD_CUDA(ctx, cudaEventSynchronize(ctx->ev[1]));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->ev[0], ctx->ev[1]);
+    if (rep > 0) best = std::min(best, ms);
+  }
+  *gbs = 32.0 * static_cast<double>(blocks) * threads * iters / (best * 1e-3) / 1e9;
+  return GD_OK;
+}
+
 extern "C" int gd_last_timing(const gd_ctx* ctx, gd_timing* out) {
   if (ctx == nullptr || out == nullptr) return GD_ERR_INVALID;
   *out = ctx->timing;

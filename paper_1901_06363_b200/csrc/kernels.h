@@ -119,6 +119,8 @@ struct DockParams {
 int launch_fp64_probe(double* sink, int blocks, int threads, int iters, void* stream);
 // L2 gather probe: random 32-byte loads over an L2-resident buffer of n_rec
 // records; blocks * threads * iters * 4 loads.
+int launch_l2_chase_probe(const double* buf, unsigned long long n_rec, int blocks, int threads, int iters,
+                          double* sink, void* stream);
 int launch_l2_gather_probe(const double* buf, unsigned long long n_rec, int blocks, int threads,
                            int iters, double* sink, void* stream);
 

@@ -555,7 +555,32 @@ __global__ void l2_gather_probe_kernel(const double* buf, unsigned long long n_r
   if (acc == 12345.678) sink[0] = acc;  // keeps the loads live
 }
 
+// The same random 32-byte L1-bypassing gathers with one load in flight per
+// thread: each address depends on the previous load's value (the buffer is
+// zero, so the chain is real but the addresses stay random) -- the rate a
+// kernel with `threads` resident lanes each waiting on its own gather gets.
+__global__ void l2_chase_probe_kernel(const double* buf, unsigned long long n_rec, int iters, double* sink) {
+  unsigned long long h = (blockIdx.x * 0x9E3779B97F4A7C15ull) ^ (threadIdx.x * 0xBF58476D1CE4E5B9ull);
+  double acc = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    h ^= h >> 31;
+    h *= 0x94D049BB133111EBull;
+    h ^= h >> 29;
+    double x, y, z, w;
+    ld256<true>(buf + 4 * (h % n_rec), x, y, z, w);
+    h ^= static_cast<unsigned long long>(__double_as_longlong(x + w));
+    acc += y;
+  }
+  if (acc == 12345.678) sink[0] = acc;
+}
+
 }  // namespace
+
+int launch_l2_chase_probe(const double* buf, unsigned long long n_rec, int blocks, int threads, int iters,
+                          double* sink, void* stream) {
+  l2_chase_probe_kernel<<<blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(buf, n_rec, iters, sink);
+  return cudaGetLastError();
+}
 
 int launch_l2_gather_probe(const double* buf, unsigned long long n_rec, int blocks, int threads,
                            int iters, double* sink, void* stream) {

@@ -130,6 +130,7 @@ SIGNATURES = {
                                        C.POINTER(C.c_double), C.POINTER(C.c_int32),
                                        C.POINTER(C.c_int32), C.c_int64]),
     "gd_device_results": (C.c_int, [C.c_void_p, C.POINTER(gd_device_result)]),
+    "gd_l2_gather_rate": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double)]),
     "gd_pocket_index_stats": (C.c_int, [C.c_void_p, C.POINTER(gd_index_level)]),
     "gd_ligand_error": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t]),
     "gd_multi_create": (C.c_int, [_i32p, C.c_int32, C.POINTER(C.c_void_p)]),
@@ -556,6 +557,12 @@ class Docker:
     def l2_gather_peak_gbs(self) -> float:
         g = C.c_double()
         self._check(self._lib.gd_l2_gather_peak(self._h, C.byref(g)))
+        return g.value
+
+    def l2_gather_rate_gbs(self, warps_per_sm: int) -> float:
+        """gd_l2_gather_rate: one dependent random gather in flight per lane."""
+        g = C.c_double()
+        self._check(self._lib.gd_l2_gather_rate(self._h, warps_per_sm, C.byref(g)))
         return g.value
 
     def fp64_peak_tflops(self) -> float:
