@@ -102,7 +102,7 @@ __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~si
 template <int B>
 __host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pairs) {
   return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * B * n) +
-         a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16) + a16(sizeof(Axis));
+         a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16) + a16(sizeof(Axis)) + a16(8);
 }
 
 // One atom of a chain's committed pose and its overlap term max(1e-12,
@@ -121,6 +121,7 @@ struct WarpMem {
   uint64_t* fm;          // [4] fragment membership bits
   long long* tally;      // [2] the chain's evaluations, feasibility checks (lane 0)
   Axis* ax;              // [1] the step's rotation axis (GD_AXIS_SMEM)
+  uint8_t* lidx;         // [8] the batch's live candidates, ascending (GD_QUERY_LIVE)
 };
 
 template <int B>
@@ -141,6 +142,7 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   s.fm = reinterpret_cast<uint64_t*>(take(32));
   s.tally = reinterpret_cast<long long*>(take(16));
   s.ax = reinterpret_cast<Axis*>(take(sizeof(Axis)));
+  s.lidx = reinterpret_cast<uint8_t*>(take(8));
   GD_BOUND(o <= warp_bytes<B>(n, W, max_pairs));
   return s;
 }
@@ -211,6 +213,10 @@ __device__ __forceinline__ void bump_item(const WarpMem& s, const DockParams& p,
 // Query phase: lanes over (live candidate, fragment atom), two items per
 // lane per iteration (t, t + 32) so both nearest-point lookups are in flight;
 // candidate c's term of atom i lands in v[c * n + i].
+#ifndef GD_QUERY_LIVE
+#define GD_QUERY_LIVE 1      // query items over live candidates only, via a byte table (r3e: c1 flex
+                             // 12.22 -> 11.85 ms, c2 58.2 -> 56.6; the n-th-set-bit form lost at r2)
+#endif
 #ifndef GD_QUERY_MLP
 #define GD_QUERY_MLP 1       // lookups in flight per lane in the query phase (1 or 2; r2h: 1 wins, c1 flex 13.63 -> 12.36 ms)
 #endif
@@ -220,6 +226,26 @@ __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& 
                                             int lane, Work<On>& wk) {
   const int tq = nb * nf;
   const float rnf = 1.0f / static_cast<float>(nf);
+#if GD_QUERY_LIVE
+  // Items over the live candidates only (a bumped candidate's items would
+  // idle their lanes): the batch's live candidates in a byte table.
+  const int nl = __popc(live);
+  if (lane < nb && ((live >> lane) & 1u)) s.lidx[__popc(live & ((1u << lane) - 1u))] = static_cast<uint8_t>(lane);
+  __syncwarp();
+  for (int t = lane; t < nl * nf; t += 32) {
+    const int cl = qdiv(t, rnf);
+    const int c = s.lidx[cl];
+    const int i = s.fidx[t - cl * nf];
+    const int ac = a0 + c * da;
+    const double cs = __ldg(p.cos_deg + ac), sn = __ldg(p.sin_deg + ac);
+    double x, y, z;
+    const PT q = s.pt[i];
+    rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
+    wk.add(kRot, 1);
+    s.v[c * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+  }
+  return;
+#endif
 #if GD_QUERY_MLP == 1
   for (int t = lane; t < tq; t += 32) {
     const int c = qdiv(t, rnf);
