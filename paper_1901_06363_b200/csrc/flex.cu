@@ -568,6 +568,88 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   return true;
 }
 
+#ifndef GD_FLAT_LIVE
+#define GD_FLAT_LIVE 1       // flat searches: bump-check up to 32 candidates at once, then query
+                             // and fold only the live ones in batches of B
+#endif
+#ifndef GD_FLAT_LIVE_MINC
+#define GD_FLAT_LIVE_MINC 1  // ... for searches of at least this many candidates
+#endif
+#ifndef GD_GROUP_PAIRMAJOR_MIN
+#define GD_GROUP_PAIRMAJOR_MIN 64  // bump_group goes pair-major from this many surviving pairs ...
+#endif
+#ifndef GD_GROUP_PAIRMAJOR_MIN_WIDE
+#define GD_GROUP_PAIRMAJOR_MIN_WIDE 24  // ... or this many for groups of more than 16 candidates
+                                        // (r3e: c1 flex 11.65 ms at 64 / 12.22 at 16, c2 54.2 at 24 / 55.7 at 64)
+#endif
+
+// Bump checks of candidates angle(c) = a0 + c*da, c < nb <= 32 (check_bumps,
+// geometry.hpp:199-213): the mask of those that clash.  Pair-major over the
+// surviving pairs (each lane's pair rotated to every candidate angle,
+// found bumps shared across the warp) or, for few pairs, lanes over
+// (candidate, pair) items.
+template <bool On>
+__device__ __forceinline__ unsigned bump_group(const WarpMem& s, const DockParams& p, const Axis& X, int np,
+                                               int a0, int da, int nb, int lane, Work<On>& wk) {
+  const unsigned all = nb == 32 ? kFull : (1u << nb) - 1u;
+  unsigned bl = 0;
+  if (np >= (nb > 16 ? GD_GROUP_PAIRMAJOR_MIN_WIDE : GD_GROUP_PAIRMAJOR_MIN)) {
+    const int ac = a0 + min(lane, nb - 1) * da;
+    const double cs_l = __ldg(p.cos_deg + ac), sn_l = __ldg(p.sin_deg + ac);
+    for (int t0 = 0; t0 < np; t0 += 32) {
+      const int t = t0 + lane;
+      const bool act = t < np;
+      Arm r{};
+      PT aj{};
+      double cut2 = 0.0;
+      if (act) {
+        const int pr = s.pairs[t];
+        const int i = pr & 0xff, j = pr >> 8;
+        const PT ai = s.pt[i];
+        aj = s.pt[j];
+        r = arm_of(X, ai.x, ai.y, ai.z);
+        const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
+        cut2 = dmul(cut, cut);
+      }
+      for (int c = 0; c < nb; ++c) {
+        const double cs = __shfl_sync(kFull, cs_l, c), sn = __shfl_sync(kFull, sn_l, c);
+        if (!act || ((bl >> c) & 1u)) continue;
+        double qx, qy, qz;
+        turn(X, r, cs, sn, dsub(1.0, cs), qx, qy, qz);
+        wk.add(kRot, 1);
+        wk.add(kBump, 1);
+        if (dist_sq(qx, qy, qz, aj.x, aj.y, aj.z) < cut2) bl |= 1u << c;
+      }
+      bl = __reduce_or_sync(kFull, bl);  // later pairs skip known bumps
+      if (bl == all) break;              // every candidate has bumped
+    }
+  } else {
+    const int total = nb * np;
+    const float rnp = 1.0f / static_cast<float>(max(np, 1));
+    for (int t = lane; t < total; t += 32) bump_item(s, p, X, t, rnp, np, a0, da, 0u, bl, wk);
+  }
+  return __reduce_or_sync(kFull, bl) & all;
+}
+
+// Query phase over a batch of live candidates: slot k < nb is candidate
+// s.lidx[k] (angle a0 + lidx[k]*da); its terms land in row k of v.
+template <bool On>
+__device__ __forceinline__ void query_slots(const WarpMem& s, const DockParams& p, const Axis& X, int n,
+                                            int nf, int nb, int a0, int da, int lane, Work<On>& wk) {
+  const float rnf = 1.0f / static_cast<float>(nf);
+  for (int t = lane; t < nb * nf; t += 32) {
+    const int k = qdiv(t, rnf);
+    const int i = s.fidx[t - k * nf];
+    const int ac = a0 + s.lidx[k] * da;
+    const double cs = __ldg(p.cos_deg + ac), sn = __ldg(p.sin_deg + ac);
+    double x, y, z;
+    const PT q = s.pt[i];
+    rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
+    wk.add(kRot, 1);
+    s.v[k * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+  }
+}
+
 // One fragment search from the committed pose, whose score is `cur`:
 // optimize_fragment_flat (kernel.hpp:125-143) with `step`, or
 // optimize_fragment_refined (:150-198) with high-precision step `step`, tile
@@ -582,6 +664,57 @@ __device__ __forceinline__ void search_fragment(const WarpMem& s, const DockPara
                                                 int& checks, Work<On>& wk, CK& ck) {
   best_a = 0;
   best = cur;
+  if (!refined && GD_FLAT_LIVE && 360 / step - 1 >= GD_FLAT_LIVE_MINC) {
+    // optimize_fragment_flat (kernel.hpp:125-143): candidates c*step,
+    // c = 1..A-1, bump-checked 32 at a time, then the live ones queried and
+    // folded in batches of B in angle order -- the first-encountered
+    // maximum under strict '>' is the reference's choice whatever the
+    // batching.  Bumped candidates cost no query lanes and no fold.
+    const int A = 360 / step;
+    int nfeas = 0;
+    for (int g0 = 1; g0 < A; g0 += 32) {
+      const int ng = min(32, A - g0);
+      const int a0 = g0 * step;
+      ck.mark(kPhDecide);
+      unsigned live = (ng == 32 ? kFull : (1u << ng) - 1u) & ~bump_group(s, p, X, np, a0, step, ng, lane, wk);
+      ck.mark(kPhBump);
+      nfeas += __popc(live);
+      while (live) {
+        const bool mine = (live >> lane) & 1u;
+        const int rank = __popc(live & ((1u << lane) - 1u));
+        const unsigned take = __ballot_sync(kFull, mine && rank < B);
+        if (mine && rank < B) s.lidx[rank] = static_cast<uint8_t>(lane);
+        const int nb = __popc(take);
+        live &= ~take;
+        __syncwarp();
+        query_slots(s, p, X, n, nf, nb, a0, step, lane, wk);
+        __syncwarp();
+        ck.mark(kPhQuery);
+        double score = -kInfinity;
+        if (lane < nb) {
+          double sum = pre;
+          const double* vc = s.v + lane * n;
+#pragma unroll kFoldUnroll
+          for (int i = first; i < n; ++i) sum = dadd(sum, vc[i]);
+          score = __ddiv_rn(static_cast<double>(n), sum);
+          wk.add(kTerms, n);
+          wk.add(kEvals, 1);
+        }
+        __syncwarp();
+        ck.mark(kPhFold);
+        int c;
+        const double v = batch_max(score, 0u, nb, lane, c);
+        if (c >= 0 && v > best) {
+          best = v;
+          best_a = a0 + s.lidx[c] * step;
+        }
+        __syncwarp();
+      }
+    }
+    evals = 1 + nfeas;
+    checks = A;
+    return;
+  }
   if (!refined) {
     // optimize_fragment_flat (kernel.hpp:125-143).
     const int A = 360 / step;
