@@ -37,10 +37,10 @@ namespace gdb200 {
 namespace {
 
 // CTA shape: W chains (warps) per CTA, 24 / W CTAs per SM (the register
-// budget: 65536 / (24 * 32) = 85 registers).  8-chain CTAs for batches of
-// up to 6 candidates (r2k: c1 12.28 vs 12.36 ms with 12, c2 flex 58.6 vs
-// 59.1), 4-chain CTAs for 8-candidate batches, whose larger v rows fit
-// better.
+// budget: 65536 / (24 * 32) = 85 registers).  12-chain CTAs for batches of
+// up to 6 candidates (r3e, after the live-only query batches: c1 11.55 vs
+// 11.65 ms with 8; r2k had 8 ahead of 12), 4-chain CTAs for 8-candidate
+// batches, whose larger v rows fit better (c2 52.4 vs 52.8 ms with 8).
 #ifndef GD_FLEX_RESIDENT
 #define GD_FLEX_RESIDENT 24  // warps per SM the register budget targets
 #endif
@@ -86,7 +86,8 @@ constexpr int kFoldUnroll = GD_FOLD_UNROLL;
 #define GD_PHASE_CLOCKS 0    // 1: per-phase clock64 attribution (gd_phase_clocks)
 #endif
 #ifndef GD_FLEX_WARPS6
-#define GD_FLEX_WARPS6 8    // chains per CTA for batches of up to 6 candidates
+#define GD_FLEX_WARPS6 12    // chains per CTA for batches of up to 6 candidates (r3e: c1 flex
+                             // 11.55 ms vs 11.65 at 8, 12.44 at 4)
 #endif
 #ifndef GD_FLEX_WARPS8
 #define GD_FLEX_WARPS8 4     // chains per CTA for 8-candidate batches
@@ -1266,8 +1267,10 @@ int flex_batch(const DockParams& p) {
   if (GD_FLEX_BATCH) return GD_FLEX_BATCH;
   const int c = std::max(1, 360 / p.hp - 1);
   if (c <= 8) return c <= 4 ? 4 : c <= 6 ? 6 : 8;  // one batch
-  // Several batches: at most 6 candidates each (r2h, one lookup per lane:
-  // c2's 35 candidates 59.1 ms in 6-batches vs 60.8 in 8-batches).
+  // Many candidates (flat searches batch only the live ones since r3e): 8
+  // (c2's 35: flex 52.4 ms vs 54.2 at 6).  A few more than 8: at most 6
+  // each (c1's 11: 11.65 ms vs 12.41 at 8).
+  if (c > 16) return 8;
   const int batches = (c + 5) / 6;
   return (c + batches - 1) / batches <= 4 ? 4 : 6;
 }
