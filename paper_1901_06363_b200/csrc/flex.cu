@@ -1014,6 +1014,42 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     vout[0] = b0 ? 0 : 1;
     out[0] = b0 ? 0.0 : cur;
   }
+#if GD_FLAT_LIVE
+  // As the flat searches: bump checks 32 angles at a time, then only the
+  // live angles queried and folded, B at a time.
+  for (int g0 = 1; g0 < 360; g0 += 32) {
+    const int ng = min(32, 360 - g0);
+    const unsigned bumped = bump_group(s, p, st.X, st.np, g0, 1, ng, lane, wk);
+    if (lane < ng && ((bumped >> lane) & 1u)) {
+      vout[g0 + lane] = 0;
+      out[g0 + lane] = 0.0;
+    }
+    unsigned live = (ng == 32 ? kFull : (1u << ng) - 1u) & ~bumped;
+    while (live) {
+      const bool mine = (live >> lane) & 1u;
+      const int rank = __popc(live & ((1u << lane) - 1u));
+      const unsigned take = __ballot_sync(kFull, mine && rank < B);
+      if (mine && rank < B) s.lidx[rank] = static_cast<uint8_t>(lane);
+      const int nb = __popc(take);
+      live &= ~take;
+      __syncwarp();
+      query_slots(s, p, st.X, n, st.nf, nb, g0, 1, lane, wk);
+      __syncwarp();
+      if (lane < nb) {
+        double sum = st.pre;
+        const double* vc = s.v + lane * n;
+#pragma unroll kFoldUnroll
+        for (int i = st.first; i < n; ++i) sum = dadd(sum, vc[i]);
+        const int a = g0 + s.lidx[lane];
+        out[a] = __ddiv_rn(static_cast<double>(n), sum);
+        vout[a] = 1;
+        wk.add(kTerms, n);
+        wk.add(kEvals, 1);
+      }
+      __syncwarp();
+    }
+  }
+#else
   for (int kb = 0; kb < 359; kb += B) {
     const int nb = min(B, 359 - kb);
     const int a0 = 1 + kb;
@@ -1027,6 +1063,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       out[a0 + lane] = ok ? sc : 0.0;
     }
   }
+#endif
   publish_warp(wk, p.counters, 8, lane);
 }
 
