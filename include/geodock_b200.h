@@ -145,6 +145,18 @@ typedef struct {
   int64_t list_bytes;
 } gd_index_level;
 int gd_pocket_index_stats(const gd_ctx* ctx, gd_index_level out[2]);
+/* Record format of the staged pocket's index: 1 = coded (the pocket's
+ * distinct coordinate values fit a 128-entry table, e.g. lattice pockets:
+ * 32-byte records with four candidates inline as table indices), 0 = fp64
+ * records; GD_ERR_NO_POCKET without a pocket.  Both are exact; the choice
+ * is made per pocket by gd_set_pocket (GD_INDEX_COMPACT=0 forces fp64). */
+int gd_pocket_index_format(const gd_ctx* ctx);
+/* Record format of the staged pocket's index: 1 = coded (the pocket's
+ * distinct coordinate values fit a 128-entry table, e.g. lattice pockets:
+ * 32-byte records with four candidates inline as table indices), 0 = fp64
+ * records; GD_ERR_NO_POCKET without a pocket.  Both are exact; the choice
+ * is made per pocket by gd_set_pocket (GD_INDEX_COMPACT=0 forces fp64). */
+int gd_pocket_index_format(const gd_ctx* ctx);
 
 /* ---- batch docking (the hot path) --------------------------------------- */
 /* Host buffers in, host buffers out: validate + preprocess (Ligand ctor,

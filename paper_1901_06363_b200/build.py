@@ -21,7 +21,9 @@ BUILD = PKG / "_build"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 HOST_SRCS = ["capi.cpp", "prep.cpp", "orient.cpp", "synth.cpp", "analysis.cpp", "planner.cpp"]
-CUDA_SRCS = ["rigid.cu", "flex.cu", "pocket_index.cu", "prep.cu"]
+# flex_cp.cu / rigid_cp.cu compile flex.cu / rigid.cu again for the compact
+# voxel-record format (kernels.h).
+CUDA_SRCS = ["rigid.cu", "flex.cu", "rigid_cp.cu", "flex_cp.cu", "pocket_index.cu", "prep.cu"]
 HEADERS = ["kernels.h", "device_common.cuh", "prep.hpp", "orient.hpp"]
 
 
@@ -51,7 +53,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     objs = []
     for src in CUDA_SRCS:
         obj = BUILD / (src + ".o")
-        if force or _stale(obj, [CSRC / src] + hdrs):
+        deps = [CSRC / src] + hdrs + ([CSRC / src.replace("_cp", "")] if "_cp" in src else [])
+        if force or _stale(obj, deps):
             _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
                   *os.environ.get("GD_NVCC_EXTRA", "").split(), *DEFS,
                   "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *inc,

@@ -174,7 +174,7 @@ struct PocketSlot {
   uint64_t last_use = 0;
   int32_t P = 0;
   double centre[3] = {0, 0, 0};
-  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels];
+  DevBuf pts, vox_off[kGridLevels], vox_pts[kGridLevels], tab;
   VoxelGrid grid[kGridLevels] = {};
   int64_t n_cand = 0;
   int32_t max_cand = 0;
@@ -203,7 +203,7 @@ struct gd_ctx {
   int64_t n_cand = 0;
   int32_t max_cand = 0;
   PocketView view{};
-  DevBuf tiles, vox_counts, vox_doff, vox_keep, vox_scan;
+  DevBuf tiles, vox_counts, vox_doff, vox_keep, vox_scan, vox_codes;
 
   DevBuf cos_t, sin_t;
   int orient_step = -1;
@@ -489,6 +489,50 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
       tbox[6 * t + 3 + k] = fh;
     }
   }
+  // Coded index records when the pocket's distinct coordinate values fit a
+  // small table (lattice pockets; kernels.h): the table (x values, then y,
+  // then z, each ascending) and each point's three indices into it.
+  // GD_INDEX_COMPACT=0 forces the fp64 records (read per call).
+  bool compact = env_double("GD_INDEX_COMPACT", 1) != 0;
+  std::vector<double> tab;
+  std::vector<uint16_t> codes;
+  if (compact) {
+    int base[3];
+    std::vector<double> axis[3];
+    for (int k = 0; k < 3 && compact; ++k) {
+      axis[k].resize(n);
+      for (int32_t j = 0; j < n; ++j) axis[k][j] = padded[4 * j + k];
+      std::sort(axis[k].begin(), axis[k].end());
+      axis[k].erase(std::unique(axis[k].begin(), axis[k].end(),
+                                [](double a, double b) { return std::memcmp(&a, &b, sizeof a) == 0; }),
+                    axis[k].end());
+      base[k] = static_cast<int>(tab.size());
+      tab.insert(tab.end(), axis[k].begin(), axis[k].end());
+      compact = tab.size() <= static_cast<size_t>(kCodedTab);
+    }
+    if (compact) {
+      codes.resize(3 * static_cast<size_t>(n));
+      for (int32_t j = 0; j < n; ++j)
+        for (int k = 0; k < 3; ++k) {
+          const double x = padded[4 * j + k];
+          const size_t at = std::lower_bound(axis[k].begin(), axis[k].end(), x) - axis[k].begin();
+          codes[3 * j + k] = static_cast<uint16_t>(8 * (base[k] + at));  // byte offset
+        }
+    }
+  }
+  std::vector<uint16_t> head;  // coded list head: points 4.. of the pocket in blocks of 5
+  if (compact) {
+    const int32_t rest = std::max(n - kCodedInline, 0);
+    head.assign(16 * static_cast<size_t>((rest + kCodedBlock - 1) / kCodedBlock), 0);
+    for (int32_t b = 0; b < rest; ++b)
+      for (int k = 0; k < 3; ++k)
+        head[16 * (b / kCodedBlock) + 3 * (b % kCodedBlock) + k] = codes[3 * (kCodedInline + b) + k];
+    GD_CUDA(ctx, slot->tab.ensure(sizeof(double) * tab.size()));
+    GD_CUDA(ctx, cudaMemcpy(slot->tab.ptr, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+    GD_CUDA(ctx, ctx->vox_codes.ensure(sizeof(uint16_t) * codes.size()));
+    GD_CUDA(ctx, cudaMemcpy(ctx->vox_codes.ptr, codes.data(), sizeof(uint16_t) * codes.size(),
+                            cudaMemcpyHostToDevice));
+  }
   GD_CUDA(ctx, ctx->tiles.ensure(tbox.size() * sizeof(float)));
   GD_CUDA(ctx, cudaMemcpy(ctx->tiles.ptr, tbox.data(), tbox.size() * sizeof(float),
                           cudaMemcpyHostToDevice));
@@ -500,6 +544,9 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
   v.pts = slot->pts.as<double>();
   v.P = n;
   v.use_index = 1;
+  v.compact = compact ? 1 : 0;
+  v.tab = compact ? slot->tab.as<double>() : nullptr;
+  v.ntab = compact ? static_cast<int32_t>(tab.size()) : 0;
   slot->n_cand = 0;
   slot->max_cand = 0;
   // Edges/margins from A/B on config 1 (profiles/r1_voxel_ab.md, DESIGN
@@ -523,7 +570,8 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
         total *= dims[k];
       }
       if (total <= kMaxVoxels) {
-        g = VoxelGrid{lo[0] - margin, lo[1] - margin, lo[2] - margin, h, dims[0], dims[1], dims[2]};
+        g = VoxelGrid{lo[0] - margin, lo[1] - margin, lo[2] - margin, h, dims[0], dims[1], dims[2],
+                      static_cast<int32_t>(env_double("GD_VOXEL_OVERFLOW", 1024))};
         break;
       }
       h *= 1.25;
@@ -540,15 +588,16 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
                                                              counts.as<int32_t>(),
                                                              ctx->tiles.as<float>(), n_tiles, keep,
                                                              ctx->stream)));
-    // List offsets (exclusive scan of max(count - kVoxInline, 0)) and the
-    // totals on the device; only the three totals come back.
+    // List offsets (exclusive scan of each voxel's 32-byte list units) and
+    // the totals on the device; only the three totals come back.
     DevBuf& doff = ctx->vox_doff;
     GD_CUDA(ctx, doff.ensure(sizeof(int32_t) * nv));
     GD_CUDA(ctx, ctx->vox_scan.ensure(static_cast<size_t>(list_offsets_scratch_bytes(nv)) + 64));
     long long* dtot = reinterpret_cast<long long*>(static_cast<unsigned char*>(ctx->vox_scan.ptr) +
                                                    list_offsets_scratch_bytes(nv));
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_list_offsets(counts.as<int32_t>(), nv, n, n,
-                                                              doff.as<int32_t>(), ctx->vox_scan.ptr,
+    GD_CUDA(ctx, static_cast<cudaError_t>(launch_list_offsets(counts.as<int32_t>(), nv, n,
+                                                              compact ? static_cast<long long>(head.size() / 16) : n,
+                                                              compact ? 1 : 0, doff.as<int32_t>(), ctx->vox_scan.ptr,
                                                               dtot, ctx->stream)));
     long long tot[3];
     GD_CUDA(ctx, cudaMemcpyAsync(tot, dtot, sizeof tot, cudaMemcpyDeviceToHost, ctx->stream));
@@ -556,20 +605,26 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     const int64_t listed = tot[0], total = tot[1];
     const int32_t mx = static_cast<int32_t>(tot[2]);
     if (listed > (1ll << 30)) return ctx->fail(GD_ERR_INVALID, "pocket: voxel index too large");
-    GD_CUDA(ctx, slot->vox_off[L].ensure(sizeof(double) * kRecDoubles * static_cast<size_t>(nv)));
+    const size_t rec_bytes = (compact ? 32 : sizeof(double) * kRecDoubles) * static_cast<size_t>(nv);
+    GD_CUDA(ctx, slot->vox_off[L].ensure(rec_bytes));
     GD_CUDA(ctx, slot->vox_pts[L].ensure(sizeof(double) * 4 * std::max<int64_t>(listed, 1)));
     // List head: the whole pocket, the list of every overflow voxel.
-    GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_pts[L].ptr, slot->pts.ptr, sizeof(double) * 4 * n,
-                                 cudaMemcpyDeviceToDevice, ctx->stream));
+    if (compact)
+      GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_pts[L].ptr, head.data(), sizeof(uint16_t) * head.size(),
+                                   cudaMemcpyHostToDevice, ctx->stream));
+    else
+      GD_CUDA(ctx, cudaMemcpyAsync(slot->vox_pts[L].ptr, slot->pts.ptr, sizeof(double) * 4 * n,
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
     GD_CUDA(ctx, static_cast<cudaError_t>(
                      launch_voxel_fill(slot->pts.as<double>(), n, g, doff.as<int32_t>(),
                                        slot->vox_off[L].as<double>(), slot->vox_pts[L].as<double>(),
                                        ctx->tiles.as<float>(), n_tiles, counts.as<int32_t>(),
-                                       keep, ctx->stream)));
+                                       keep, compact ? ctx->vox_codes.as<uint16_t>() : nullptr,
+                                       ctx->stream)));
     GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
     slot->grid[L] = g;
     slot->stats[L] = gd_index_level{{g.dim_x, g.dim_y, g.dim_z}, g.h, total,
-                                    static_cast<int64_t>(sizeof(double) * kRecDoubles) * nv,
+                                    static_cast<int64_t>(rec_bytes),
                                     static_cast<int64_t>(sizeof(double) * 4) * std::max<int64_t>(listed, 1)};
     slot->n_cand += total;
     slot->max_cand = std::max(slot->max_cand, mx);
@@ -583,10 +638,18 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     gl.dim_x = g.dim_x;
     gl.dim_y = g.dim_y;
     gl.dim_z = g.dim_z;
+    gl.fdim_x = g.dim_x;
+    gl.fdim_y = g.dim_y;
+    gl.fdim_z = g.dim_z;
   }
   slot->P = n;
   activate(*slot);
   return GD_OK;
+}
+
+extern "C" int gd_pocket_index_format(const gd_ctx* ctx) {
+  if (ctx == nullptr || ctx->P == 0) return GD_ERR_NO_POCKET;
+  return ctx->view.compact ? 1 : 0;
 }
 
 extern "C" int gd_pocket_index_stats(const gd_ctx* ctx, gd_index_level out[2]) {
@@ -975,11 +1038,12 @@ static int launch_range(gd_ctx* ctx, DockParams p, int c0, int c1, int max_n, cu
   if (p.top_best != nullptr)
     GD_CUDA(ctx, cudaMemsetAsync(p.top_best + c0, 0, sizeof(unsigned long long) * (c1 - c0), s));
   if (p.rigid) {
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_rigid_topk(p, s)));
+    GD_CUDA(ctx, static_cast<cudaError_t>(p.pocket.compact ? launch_rigid_topk_cp(p, s)
+                                                           : launch_rigid_topk(p, s)));
     ctx->timing.launches += 1;
   }
   if (e_mid) cudaEventRecord(e_mid, s);
-  GD_CUDA(ctx, static_cast<cudaError_t>(launch_flex(p, s)));
+  GD_CUDA(ctx, static_cast<cudaError_t>(p.pocket.compact ? launch_flex_cp(p, s) : launch_flex(p, s)));
   GD_CUDA(ctx, static_cast<cudaError_t>(launch_finalize(p, s)));
   ctx->timing.launches += 2;
   return GD_OK;
@@ -1467,7 +1531,8 @@ extern "C" int gd_optimize_fragment_batch(gd_ctx* ctx, const gd_ligand_batch* ba
   io.evaluations = ctx->st_evals.as<int64_t>();
   io.checks = ctx->st_checks.as<int64_t>();
   io.pose = ctx->o_pose.as<double>();
-  GD_CUDA(ctx, static_cast<cudaError_t>(launch_fragment_search(p, io, ctx->stream)));
+  GD_CUDA(ctx, static_cast<cudaError_t>(p.pocket.compact ? launch_fragment_search_cp(p, io, ctx->stream)
+                                                         : launch_fragment_search(p, io, ctx->stream)));
   if ((rc = fetch(ctx, best_angle, ctx->o_orient, sizeof(int32_t) * L))) return rc;
   if ((rc = fetch(ctx, best_score, ctx->st_final, sizeof(double) * L))) return rc;
   if ((rc = fetch(ctx, evaluations, ctx->st_evals, sizeof(int64_t) * L))) return rc;
@@ -1630,7 +1695,7 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores,
     ctx->counted = p.counters != nullptr;
     ctx->timing = gd_timing{};
     cudaEventRecord(ctx->ev[2], ctx->stream);
-    GD_CUDA(ctx, static_cast<cudaError_t>(launch_profiles(
+    GD_CUDA(ctx, static_cast<cudaError_t>((p.pocket.compact ? launch_profiles_cp : launch_profiles)(
                      p, ctx->prof_items.as<int32_t>(), static_cast<int>(n_items),
                      ctx->prof_scores.as<double>(), ctx->prof_valid.as<uint8_t>(), ctx->stream)));
     cudaEventRecord(ctx->ev[3], ctx->stream);

@@ -13,6 +13,7 @@
 
 #include <climits>
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.h"
 
@@ -118,16 +119,85 @@ __device__ __noinline__ double min_dist_sq_brute(const double* pts, int P, doubl
 // reference's PocketIndex makes the same exactness argument,
 // geometry.hpp:45-46).  Fine level first, then the coarse far-field level;
 // queries beyond both fall back to the full scan.
+//
+// Two record formats (kernels.h), both in 32-byte units:
+//   fp64  {int32 start, int32 count, x0, y0, z0}, list entries (x, y, z, pad);
+//   coded {u32 start, u32 count, 4 inline candidates}, list blocks of 5
+//         candidates; a candidate is three 16-bit indices into the pocket's
+//         table of distinct coordinate values (PocketView::tab), chosen when
+//         that table is small (lattice pockets).  The query reads the very
+//         same doubles from the table, so the minimum has the same bits;
+//         with four candidates inline almost no query needs a dependent
+//         list load.
+// Translation units compiled with GD_TU_COMPACT=1 (flex_cp, rigid_cp) read
+// the coded format; the launchers dispatch on PocketView::compact.
+#ifndef GD_TU_COMPACT
+#define GD_TU_COMPACT 0
+#endif
+constexpr bool kCompactTU = GD_TU_COMPACT != 0;
+#if GD_TU_COMPACT
+#define GD_API(name) name##_cp
+#else
+#define GD_API(name) name
+#endif
+
+template <bool NoAlloc = false>
+__device__ __forceinline__ void ld256w(const void* p, uint32_t (&w)[8]) {
+  if constexpr (NoAlloc)
+    asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+        : "l"(p));
+  else
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+        : "l"(p));
+}
+// 16-bit field K (compile-time) of a word array.
+template <int K, int N>
+__device__ __forceinline__ unsigned u16at(const uint32_t (&w)[N]) {
+  return (K & 1) ? (w[K >> 1] >> 16) : (w[K >> 1] & 0xffffu);
+}
+// The coded format's coordinate table, staged per CTA into shared memory
+// (stage_tab) by every kernel that queries a coded pocket: a candidate
+// coordinate is one shared load at [byte offset + table base].
+__shared__ __align__(16) double s_tab[kCodedTab];
+// A no-op in kernels compiled for the fp64 format (CP false: no table).
+template <bool CP>
+__device__ __forceinline__ void stage_tab(const PocketView& pk) {
+  if constexpr (CP) {
+    for (int i = threadIdx.x; i < pk.ntab; i += blockDim.x) s_tab[i] = pk.tab[i];
+    __syncthreads();
+  }
+}
+__device__ __forceinline__ double tab_at(unsigned off) {
+  return *reinterpret_cast<const double*>(reinterpret_cast<const unsigned char*>(s_tab) + off);
+}
+// distance_sq to coded candidate C of a word array (fields 3C..3C+2).
+template <int C, int N>
+__device__ __forceinline__ double coded_d2(const double*, const uint32_t (&w)[N], double x, double y,
+                                           double z) {
+  return dist_sq(x, y, z, tab_at(u16at<3 * C>(w)), tab_at(u16at<3 * C + 1>(w)), tab_at(u16at<3 * C + 2>(w)));
+}
+
 // Voxel lookup: the record of the first grid level containing q (one or
 // two independent 256-bit loads); lst == nullptr means the full-scan
 // fallback.
 struct Loc {
   const double* lst;  // further candidates (start already applied)
   int count;          // candidates in the voxel (>= 1)
-  double x0, y0, z0;  // the inline candidates (the second repeats the first
-  double x1, y1, z1;  // when count == 1; unused when kVoxInline == 1)
+  double x0, y0, z0;  // the inline candidates (the second only with
+  double x1, y1, z1;  // kVoxInline == 2; it repeats the first when count == 1)
 };
-__device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, double z) {
+struct LocC {
+  const double* lst;  // list blocks (start already applied)
+  int count;          // candidates in the voxel (>= 1)
+  uint32_t w[6];      // the inline candidates' table indices
+};
+template <bool CP>
+using LocT = typename std::conditional<CP, LocC, Loc>::type;
+
+template <bool CP = kCompactTU>
+__device__ __forceinline__ LocT<CP> locate(const PocketView& pk, double x, double y, double z) {
   if (pk.use_index) {
 #pragma unroll
     for (int L = 0; L < kGridLevels; ++L) {
@@ -135,47 +205,87 @@ __device__ __forceinline__ Loc locate(const PocketView& pk, double x, double y, 
       const double fx = (x - g.lo_x) * g.inv_h;
       const double fy = (y - g.lo_y) * g.inv_h;
       const double fz = (z - g.lo_z) * g.inv_h;
-      if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.dim_x && fy < g.dim_y && fz < g.dim_z) {
+      if (fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.fdim_x && fy < g.fdim_y && fz < g.fdim_z) {
         const int v = (static_cast<int>(fx) * g.dim_y + static_cast<int>(fy)) * g.dim_z +
                       static_cast<int>(fz);
-        const double* r = g.rec + kRecDoubles * static_cast<size_t>(v);
-        double hdr, pad;
-        Loc l;
-        ld256<GD_REC_NA>(r, hdr, l.x0, l.y0, l.z0);
-        if constexpr (kVoxInline == 2) ld256<GD_REC_NA>(r + 4, l.x1, l.y1, l.z1, pad);
-        const long long h = __double_as_longlong(hdr);
-        l.count = static_cast<int>(h >> 32);
-        l.lst = g.lst + 4 * static_cast<size_t>(static_cast<unsigned>(h & 0xffffffffll));
-        return l;
+        if constexpr (CP) {
+          uint32_t w[8];
+          ld256w<GD_REC_NA>(g.rec + 4 * static_cast<size_t>(v), w);
+          LocC l;
+          l.count = static_cast<int>(w[1]);
+          l.lst = g.lst + 4 * static_cast<size_t>(w[0]);
+#pragma unroll
+          for (int k = 0; k < 6; ++k) l.w[k] = w[2 + k];
+          return l;
+        } else {
+          const double* r = g.rec + kRecDoubles * static_cast<size_t>(v);
+          double hdr, pad;
+          Loc l;
+          ld256<GD_REC_NA>(r, hdr, l.x0, l.y0, l.z0);
+          if constexpr (kVoxInline == 2) ld256<GD_REC_NA>(r + 4, l.x1, l.y1, l.z1, pad);
+          const long long h = __double_as_longlong(hdr);
+          l.count = static_cast<int>(h >> 32);
+          l.lst = g.lst + 4 * static_cast<size_t>(static_cast<unsigned>(h & 0xffffffffll));
+          return l;
+        }
       }
     }
   }
-  return Loc{nullptr, 0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  LocT<CP> l{};
+  l.lst = nullptr;
+  return l;
 }
 
-// min over the inline candidates; the list scan covers count - kVoxInline.
-__device__ __forceinline__ double inline_min(const Loc& a, double x, double y, double z) {
+// min over the inline candidates; the list scan covers the rest.
+__device__ __forceinline__ double inline_min(const PocketView&, const Loc& a, double x, double y, double z) {
   double m = dist_sq(x, y, z, a.x0, a.y0, a.z0);
   if constexpr (kVoxInline == 2) m = fmin(m, dist_sq(x, y, z, a.x1, a.y1, a.z1));
   return m;
 }
+__device__ __forceinline__ double inline_min(const PocketView& pk, const LocC& a, double x, double y,
+                                             double z) {
+  double m = coded_d2<0>(pk.tab, a.w, x, y, z);
+  if (a.count > 1) m = fmin(m, coded_d2<1>(pk.tab, a.w, x, y, z));
+  if (a.count > 2) m = fmin(m, coded_d2<2>(pk.tab, a.w, x, y, z));
+  if (a.count > 3) m = fmin(m, coded_d2<3>(pk.tab, a.w, x, y, z));
+  return m;
+}
+// List loads of a located voxel (0 on the full-scan fallback).
 __device__ __forceinline__ int listed(const Loc& a) { return a.lst ? a.count - kVoxInline : 0; }
+__device__ __forceinline__ int listed(const LocC& a) {
+  return a.lst ? (max(a.count - kCodedInline, 0) + kCodedBlock - 1) / kCodedBlock : 0;
+}
+// Folds list load k of a located voxel into m.
+__device__ __forceinline__ void list_min(const PocketView&, const Loc& a, int k, double x, double y,
+                                         double z, double& m) {
+  const P3 p = ldp<GD_LST_NA>(a.lst, k);
+  m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
+}
+__device__ __forceinline__ void list_min(const PocketView& pk, const LocC& a, int k, double x, double y,
+                                         double z, double& m) {
+  uint32_t w[8];
+  ld256w<GD_LST_NA>(a.lst + 4 * static_cast<size_t>(k), w);
+  const int left = a.count - kCodedInline - kCodedBlock * k;  // >= 1
+  m = fmin(m, coded_d2<0>(pk.tab, w, x, y, z));
+  if (left > 1) m = fmin(m, coded_d2<1>(pk.tab, w, x, y, z));
+  if (left > 2) m = fmin(m, coded_d2<2>(pk.tab, w, x, y, z));
+  if (left > 3) m = fmin(m, coded_d2<3>(pk.tab, w, x, y, z));
+  if (left > 4) m = fmin(m, coded_d2<4>(pk.tab, w, x, y, z));
+}
 
-template <bool On>
+template <bool On, bool CP = kCompactTU>
 __device__ __forceinline__ double min_dist_sq(const PocketView& pk, double x, double y, double z,
                                               Work<On>& w) {
   w.add(kQuery, 1);
-  const Loc a = locate(pk, x, y, z);
+  const auto a = locate<CP>(pk, x, y, z);
   if (a.lst == nullptr) {
     w.add(kPairs, pk.P);
     return min_dist_sq_brute(pk.pts, pk.P, x, y, z);
   }
   w.add(kPairs, a.count);
-  double m = inline_min(a, x, y, z);
-  for (int k = 0; k < a.count - kVoxInline; ++k) {
-    const P3 p = ldp<GD_LST_NA>(a.lst, k);
-    m = fmin(m, dist_sq(x, y, z, p.x, p.y, p.z));
-  }
+  double m = inline_min(pk, a, x, y, z);
+  const int nl = listed(a);
+  for (int k = 0; k < nl; ++k) list_min(pk, a, k, x, y, z, m);
   return m;
 }
 
@@ -186,26 +296,20 @@ __device__ __forceinline__ void min_dist_sq2(const PocketView& pk, double x0, do
                                              double x1, double y1, double z1, double& m0,
                                              double& m1, Work<On>& w) {
   w.add(kQuery, 2);
-  const Loc a = locate(pk, x0, y0, z0);
-  const Loc b = locate(pk, x1, y1, z1);
+  const auto a = locate(pk, x0, y0, z0);
+  const auto b = locate(pk, x1, y1, z1);
   const int na = listed(a), nb = listed(b);
   w.add(kPairs, (a.lst ? a.count : 0) + (b.lst ? b.count : 0));
-  m0 = inline_min(a, x0, y0, z0);
-  m1 = inline_min(b, x1, y1, z1);
+  m0 = inline_min(pk, a, x0, y0, z0);
+  m1 = inline_min(pk, b, x1, y1, z1);
 #if GD_WHATIF_NOLIST
   const int nmax = 0;  // timing experiment only: wrong minima
 #else
   const int nmax = max(na, nb);
 #endif
   for (int k = 0; k < nmax; ++k) {
-    if (k < na) {
-      const P3 p = ldp<GD_LST_NA>(a.lst, k);
-      m0 = fmin(m0, dist_sq(x0, y0, z0, p.x, p.y, p.z));
-    }
-    if (k < nb) {
-      const P3 p = ldp<GD_LST_NA>(b.lst, k);
-      m1 = fmin(m1, dist_sq(x1, y1, z1, p.x, p.y, p.z));
-    }
+    if (k < na) list_min(pk, a, k, x0, y0, z0, m0);
+    if (k < nb) list_min(pk, b, k, x1, y1, z1, m1);
   }
   if (a.lst == nullptr) {
     w.add(kPairs, pk.P);
@@ -223,24 +327,20 @@ template <int M, bool On>
 __device__ __forceinline__ void min_dist_sqM(const PocketView& pk, const double* x, const double* y,
                                              const double* z, double* m, Work<On>& w) {
   w.add(kQuery, M);
-  Loc a[M];
+  LocT<kCompactTU> a[M];
 #pragma unroll
   for (int r = 0; r < M; ++r) a[r] = locate(pk, x[r], y[r], z[r]);
   int nmax = 0;
 #pragma unroll
   for (int r = 0; r < M; ++r) {
-    m[r] = inline_min(a[r], x[r], y[r], z[r]);
+    m[r] = inline_min(pk, a[r], x[r], y[r], z[r]);
     nmax = max(nmax, listed(a[r]));
     if (a[r].lst) w.add(kPairs, a[r].count);
   }
   for (int k = 0; k < nmax; ++k) {
 #pragma unroll
-    for (int r = 0; r < M; ++r) {
-      if (k < listed(a[r])) {
-        const P3 p = ldp<GD_LST_NA>(a[r].lst, k);
-        m[r] = fmin(m[r], dist_sq(x[r], y[r], z[r], p.x, p.y, p.z));
-      }
-    }
+    for (int r = 0; r < M; ++r)
+      if (k < listed(a[r])) list_min(pk, a[r], k, x[r], y[r], z[r], m[r]);
   }
 #pragma unroll
   for (int r = 0; r < M; ++r) {

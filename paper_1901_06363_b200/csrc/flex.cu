@@ -798,6 +798,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     flex_chain_kernel(DockParams p) {
   static_assert(B >= 1 && B <= 8, "batch_max reduces over an 8-lane butterfly");
   extern __shared__ __align__(16) unsigned char smem[];
+  stage_tab<kCompactTU>(p.pocket);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = p.k_slots;
   const long long item = static_cast<long long>(blockIdx.x) * kWarps + warp;
@@ -957,6 +958,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     profile_kernel(DockParams p, const int32_t* items, int n_items, double* scores, uint8_t* valid) {
   static_assert(B >= 1 && B <= 8, "batch_max reduces over an 8-lane butterfly");
   extern __shared__ __align__(16) unsigned char smem[];
+  stage_tab<kCompactTU>(p.pocket);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = blockIdx.x * kWarps + warp;
   if (item >= n_items) return;
@@ -1082,6 +1084,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
     fragment_search_kernel(DockParams p, FragmentIO io) {
   static_assert(B >= 1 && B <= 8, "batch_max reduces over an 8-lane butterfly");
   extern __shared__ __align__(16) unsigned char smem[];
+  stage_tab<kCompactTU>(p.pocket);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int l = blockIdx.x * kWarps + warp;
   if (l >= p.n_lig) return;
@@ -1312,12 +1315,14 @@ int flex_batch(const DockParams& p) {
   return (c + batches - 1) / batches <= 4 ? 4 : 6;
 }
 
+// Dynamic shared memory a CTA may opt into (the coded format's kernels also
+// hold the static coordinate table).
 int max_smem_optin() {
   static int v = [] {
     int dev = 0, bytes = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&bytes, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    return bytes;
+    return bytes - (kCompactTU ? static_cast<int>(sizeof(double)) * kCodedTab : 0);
   }();
   return v;
 }
@@ -1379,7 +1384,7 @@ int launch_profiles_b(const DockParams& p, const int32_t* items, int n_items, do
 
 }  // namespace
 
-int launch_flex(const DockParams& p, void* stream) {
+int GD_API(launch_flex)(const DockParams& p, void* stream) {
   const long long chains = static_cast<long long>(p.n_lig) * p.k_slots;
   if (chains == 0) return cudaSuccess;
   const auto s = static_cast<cudaStream_t>(stream);
@@ -1390,8 +1395,8 @@ int launch_flex(const DockParams& p, void* stream) {
   }
 }
 
-int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
-                    uint8_t* valid, void* stream) {
+int GD_API(launch_profiles)(const DockParams& p, const int32_t* items, int n_items, double* scores,
+                            uint8_t* valid, void* stream) {
   if (n_items == 0) return cudaSuccess;
 #ifndef GD_PROFILE_BATCH
 #define GD_PROFILE_BATCH 8
@@ -1412,7 +1417,7 @@ int launch_fragment_search_bw(const DockParams& p, const FragmentIO& io, cudaStr
   return cudaGetLastError();
 }
 
-int launch_fragment_search(const DockParams& p, const FragmentIO& io, void* stream) {
+int GD_API(launch_fragment_search)(const DockParams& p, const FragmentIO& io, void* stream) {
   if (p.n_lig == 0) return cudaSuccess;
   const auto s = static_cast<cudaStream_t>(stream);
   if (flex_smem_bytes<8, 4>(p) <= static_cast<size_t>(max_smem_optin()))
@@ -1420,6 +1425,7 @@ int launch_fragment_search(const DockParams& p, const FragmentIO& io, void* stre
   return launch_fragment_search_bw<8, 1>(p, io, s);
 }
 
+#if !GD_TU_COMPACT  // format-independent launchers: defined once
 int launch_fragment_rotate(const DockParams& p, const double* cs, const double* sn,
                            const uint8_t* is_zero, double* out, void* stream) {
   if (p.n_lig == 0) return cudaSuccess;
@@ -1440,5 +1446,6 @@ int launch_finalize(const DockParams& p, void* stream) {
   finalize_kernel<<<p.n_lig, 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
   return cudaGetLastError();
 }
+#endif
 
 }  // namespace gdb200

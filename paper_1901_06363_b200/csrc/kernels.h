@@ -32,6 +32,17 @@ struct LigMeta {
 constexpr int kVoxInline = GD_VOX_INLINE;
 static_assert(kVoxInline == 1 || kVoxInline == 2, "1 or 2 inline candidates");
 constexpr int kRecDoubles = kVoxInline == 1 ? 4 : 8;
+// Coded format, chosen per pocket when its distinct coordinate values are
+// few (lattice pockets: a table of at most kCodedTab doubles): a candidate
+// is three 16-bit indices into that table (PocketView::tab); record {u32
+// start, u32 count, 4 candidates} (32 B; entries past count are unused),
+// list blocks of 5 candidates (32 B).  Each index is stored pre-scaled to
+// a byte offset (8 x index).  `start` counts 32-byte units in both formats.
+// Exact: the query reads the pocket's own doubles from the table.
+constexpr int kCodedTab = 128;    // table capacity (1 KB, staged in shared memory: larger tables
+                                  // would cost the 4-chain CTAs their sixth slot per SM)
+constexpr int kCodedInline = 4;  // candidates in a coded record
+constexpr int kCodedBlock = 5;   // candidates per coded list block
 struct GridLevel {
   const double* rec;       // [nvox*kRecDoubles] voxel records
   const double* lst;       // [sum max(count-kVoxInline,0) * 4] further candidates, voxel-major
@@ -39,6 +50,7 @@ struct GridLevel {
   double inv_h;            // 1 / voxel edge
   int32_t dim_x, dim_y, dim_z;
   int32_t pad;
+  double fdim_x, fdim_y, fdim_z;  // the dims as doubles (no conversion per query)
 };
 
 constexpr int kGridLevels = 2;  // fine (near field) + coarse (far field)
@@ -50,6 +62,9 @@ struct PocketView {
   const double* pts;       // [P*4] x,y,z,pad (32-B records)
   int32_t P;
   int32_t use_index;       // 0 = brute force only
+  int32_t compact;         // 1: coded voxel records (see below), tab set
+  const double* tab;       // coded: the distinct coordinate values (x's, y's, z's)
+  int32_t ntab;            // coded: table entries (<= kCodedTab)
   GridLevel lv[kGridLevels];
 };
 
@@ -150,6 +165,13 @@ int launch_fragment_rotate(const DockParams& p, const double* cs, const double* 
 int launch_fragment_bumps(const DockParams& p, uint8_t* feasible, void* stream);
 // E7 final ordering + poses scored, one CTA per ligand.
 int launch_finalize(const DockParams& p, void* stream);
+// The same launchers compiled for the compact index format (GD_TU_COMPACT=1:
+// flex_cp.cu, rigid_cp.cu); callers dispatch on PocketView::compact.
+int launch_rigid_topk_cp(const DockParams& p, void* stream);
+int launch_flex_cp(const DockParams& p, void* stream);
+int launch_profiles_cp(const DockParams& p, const int32_t* items, int n_items, double* scores,
+                       uint8_t* valid, void* stream);
+int launch_fragment_search_cp(const DockParams& p, const FragmentIO& io, void* stream);
 int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int n_poses,
                        double* out, void* stream);
 
@@ -183,6 +205,8 @@ int launch_prep(const PrepParams& q, void* stream);
 struct VoxelGrid {
   double lo_x, lo_y, lo_z, h;
   int32_t dim_x, dim_y, dim_z;
+  int32_t overflow = 1024;  // more survivors than this: the voxel lists the whole pocket
+                            // (<= 1024; lowered only by tests, GD_VOXEL_OVERFLOW)
 };
 // counts[v] = candidates of voxel v (>= 1), or -1 when more than 1,024
 // survive (the voxel then scans the whole pocket, held once at the head of
@@ -197,13 +221,15 @@ int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, c
                        int nt, int32_t* keep, void* stream);
 int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
                       double* lst, const float* tbox, int nt, const int32_t* counts,
-                      const int32_t* keep, void* stream);
-// offsets[v] = base + exclusive prefix of max(counts - kVoxInline, 0) over
-// voxels (the first `base` = P list records hold the whole pocket for
-// overflow voxels); totals[3] (device) = {listed entries incl. base,
+                      const int32_t* keep, const uint16_t* codes, void* stream);
+// codes (nullable) [P][3]: the coded format's table indices of each point.
+// offsets[v] = base + exclusive prefix of the voxels' list units (32 B:
+// max(counts - kVoxInline, 0) fp64 entries, or ceil(max(counts - 4, 0) / 5)
+// coded blocks) over voxels (the first `base` units hold the whole pocket
+// for overflow voxels); totals[3] (device) = {list units incl. base,
 // candidates, max count}; `scratch` holds list_offsets_scratch_bytes(nv).
 int list_offsets_scratch_bytes(int nv);
-int launch_list_offsets(const int32_t* counts, int nv, int P, long long base, int32_t* offsets,
-                        void* scratch, long long* totals, void* stream);
+int launch_list_offsets(const int32_t* counts, int nv, int P, long long base, int compact,
+                        int32_t* offsets, void* scratch, long long* totals, void* stream);
 
 }  // namespace gdb200

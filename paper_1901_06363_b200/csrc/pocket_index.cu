@@ -9,15 +9,17 @@ namespace {
 // --------------------------------------------------------------------------
 // overlap_score for arbitrary poses: one thread per pose.
 // --------------------------------------------------------------------------
+template <bool CP>
 __global__ void score_poses_kernel(PocketView pk, const double* xyz, int n_atoms, int n_poses,
                                    double* out) {
+  stage_tab<CP>(pk);
   const int pose = blockIdx.x * blockDim.x + threadIdx.x;
   if (pose >= n_poses) return;
   const double* q = xyz + static_cast<size_t>(3) * n_atoms * pose;
   Work<false> wk;
   double sum = 0.0;
   for (int i = 0; i < n_atoms; ++i)
-    sum = dadd(sum, fmax(kMinDistanceSq, min_dist_sq(pk, q[3 * i], q[3 * i + 1], q[3 * i + 2], wk)));
+    sum = dadd(sum, fmax(kMinDistanceSq, min_dist_sq<false, CP>(pk, q[3 * i], q[3 * i + 1], q[3 * i + 2], wk)));
   out[pose] = __ddiv_rn(static_cast<double>(n_atoms), sum);
 }
 
@@ -128,7 +130,7 @@ __device__ int voxel_list(const double* pts, int P, const VoxelGrid& g, int v, b
       if (nx * nx + ny * ny + nz * nz > lim) continue;
       const P3 Q = ldp(pts, t0 + i);
       if (dominates(C, Q, bl, bh)) continue;
-      if (k >= kVoxMaxCand) {
+      if (k >= min(g.overflow, kVoxMaxCand)) {
         over = true;
         break;
       }
@@ -316,7 +318,7 @@ __device__ int voxel_list_culled(const double* pts, int P, const VoxelGrid& g, i
         const int j = __float_as_int(q.w);
         const P3 Q = ldp(pts, j);
         if (dominates(C, Q, bl, bh)) continue;
-        if (k >= kVoxMaxCand) {
+        if (k >= min(g.overflow, kVoxMaxCand)) {
           over = true;
           break;
         }
@@ -373,7 +375,8 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double*
                                                                    double* rec, double* lst,
                                                                    const float* tbox, int nt,
                                                                    const int32_t* counts,
-                                                                   const int32_t* keep) {
+                                                                   const int32_t* keep,
+                                                                   const uint16_t* codes) {
   __shared__ float4 tile[kTile];
   __shared__ BrickScratch sc;
   int cand[kVoxMaxCand];
@@ -404,6 +407,28 @@ __global__ void __launch_bounds__(kBuildThreads) voxel_fill_kernel(const double*
   // 0 inline} and costs no list memory.
   const int len = k < 0 ? P : k;  // >= 1: the nearest point always survives
   const int start = k < 0 ? 1 : offsets[v];
+  if (codes != nullptr) {
+    // Coded: {start, count, 4 candidates} and list blocks of 5 past the
+    // inline ones.  Overflow voxels: the head holds points 4.. of the whole
+    // pocket in blocks of 5 from unit 0, the inline ones are points 0..3.
+    auto pt = [&](int a) { return k < 0 ? a : cand[a]; };
+    uint32_t* r = reinterpret_cast<uint32_t*>(rec + 4 * static_cast<size_t>(v));
+    r[0] = static_cast<uint32_t>(k < 0 ? 0 : start);
+    r[1] = static_cast<uint32_t>(len);
+    uint16_t* e = reinterpret_cast<uint16_t*>(r + 2);
+    for (int q = 0; q < kCodedInline; ++q) {
+      const int j = pt(min(q, len - 1));
+      for (int c = 0; c < 3; ++c) e[3 * q + c] = codes[3 * j + c];
+    }
+    if (k < 0) return;
+    uint16_t* out = reinterpret_cast<uint16_t*>(lst + 4 * static_cast<size_t>(start));
+    for (int a = kCodedInline; a < len; ++a) {
+      const int b = a - kCodedInline;
+      uint16_t* blk = out + 16 * (b / kCodedBlock) + 3 * (b % kCodedBlock);
+      for (int c = 0; c < 3; ++c) blk[c] = codes[3 * pt(a) + c];
+    }
+    return;
+  }
   double* r = rec + kRecDoubles * static_cast<size_t>(v);
   reinterpret_cast<int2*>(r)[0] = make_int2(start, len);
   for (int q = 0; q < kVoxInline; ++q) {
@@ -438,9 +463,15 @@ __device__ __forceinline__ long long block_sum_ll(long long x, long long* red) {
   return t;
 }
 
+// 32-byte list units of a voxel with `raw` candidates (overflow voxels,
+// raw < 0, share the head: none of their own).
+__device__ __forceinline__ int list_units(int raw, int compact) {
+  return compact ? (max(raw - kCodedInline, 0) + kCodedBlock - 1) / kCodedBlock : max(raw - kVoxInline, 0);
+}
+
 __global__ void __launch_bounds__(kScanBlock) list_block_sums(const int32_t* counts, int nv, int P,
-                                                              long long* bsum, long long* bcand,
-                                                              int* bmax) {
+                                                              int compact, long long* bsum,
+                                                              long long* bcand, int* bmax) {
   __shared__ long long red[kScanBlock / 32];
   __shared__ int mx;
   const int v = blockIdx.x * kScanBlock + threadIdx.x;
@@ -449,7 +480,7 @@ __global__ void __launch_bounds__(kScanBlock) list_block_sums(const int32_t* cou
   if (threadIdx.x == 0) mx = 0;
   __syncthreads();
   atomicMax(&mx, c);
-  const long long l = block_sum_ll(max(raw - kVoxInline, 0), red);
+  const long long l = block_sum_ll(list_units(raw, compact), red);
   const long long t = block_sum_ll(c, red);
   if (threadIdx.x == 0) {
     bsum[blockIdx.x] = l;
@@ -498,11 +529,11 @@ __global__ void __launch_bounds__(kScanBlock) list_scan_sums(long long* bsum, co
   }
 }
 
-__global__ void __launch_bounds__(kScanBlock) list_apply(const int32_t* counts, int nv,
+__global__ void __launch_bounds__(kScanBlock) list_apply(const int32_t* counts, int nv, int compact,
                                                          const long long* bsum, int32_t* offsets) {
   __shared__ long long part[kScanBlock];
   const int v = blockIdx.x * kScanBlock + threadIdx.x;
-  const long long x = v < nv ? max(counts[v] - kVoxInline, 0) : 0;
+  const long long x = v < nv ? list_units(counts[v], compact) : 0;
   part[threadIdx.x] = x;
   __syncthreads();
   for (int o = 1; o < kScanBlock; o <<= 1) {
@@ -598,8 +629,13 @@ int launch_score_poses(const PocketView& pk, const double* xyz, int n_atoms, int
                        double* out, void* stream) {
   if (n_poses <= 0) return cudaSuccess;
   const int bt = 128;
-  score_poses_kernel<<<(n_poses + bt - 1) / bt, bt, 0, static_cast<cudaStream_t>(stream)>>>(
-      pk, xyz, n_atoms, n_poses, out);
+  const unsigned blocks = (n_poses + bt - 1) / bt;
+  if (pk.compact)
+    score_poses_kernel<true><<<blocks, bt, 0, static_cast<cudaStream_t>(stream)>>>(pk, xyz, n_atoms,
+                                                                                 n_poses, out);
+  else
+    score_poses_kernel<false><<<blocks, bt, 0, static_cast<cudaStream_t>(stream)>>>(pk, xyz, n_atoms,
+                                                                                  n_poses, out);
   return cudaGetLastError();
 }
 
@@ -622,10 +658,10 @@ int launch_voxel_count(const double* pts, int P, VoxelGrid g, int32_t* counts, c
 
 int launch_voxel_fill(const double* pts, int P, VoxelGrid g, const int32_t* offsets, double* rec,
                       double* lst, const float* tbox, int nt, const int32_t* counts,
-                      const int32_t* keep, void* stream) {
+                      const int32_t* keep, const uint16_t* codes, void* stream) {
   if (nt > kMaxTiles) nt = 0;
   voxel_fill_kernel<<<build_blocks(g, nt), kBuildThreads, 0, static_cast<cudaStream_t>(stream)>>>(
-      pts, P, g, offsets, rec, lst, tbox, nt, counts, keep);
+      pts, P, g, offsets, rec, lst, tbox, nt, counts, keep, codes);
   return cudaGetLastError();
 }
 
@@ -634,16 +670,16 @@ int list_offsets_scratch_bytes(int nv) {
   return 3 * 8 * nb + 64;
 }
 
-int launch_list_offsets(const int32_t* counts, int nv, int P, long long base, int32_t* offsets,
-                        void* scratch, long long* totals, void* stream) {
+int launch_list_offsets(const int32_t* counts, int nv, int P, long long base, int compact,
+                        int32_t* offsets, void* scratch, long long* totals, void* stream) {
   const int nb = (nv + kScanBlock - 1) / kScanBlock;
   auto* bsum = static_cast<long long*>(scratch);
   long long* bcand = bsum + nb;
   int* bmax = reinterpret_cast<int*>(bcand + nb);
   const cudaStream_t st = static_cast<cudaStream_t>(stream);
-  list_block_sums<<<nb, kScanBlock, 0, st>>>(counts, nv, P, bsum, bcand, bmax);
+  list_block_sums<<<nb, kScanBlock, 0, st>>>(counts, nv, P, compact, bsum, bcand, bmax);
   list_scan_sums<<<1, kScanBlock, 0, st>>>(bsum, bcand, bmax, nb, base, totals);
-  list_apply<<<nb, kScanBlock, 0, st>>>(counts, nv, bsum, offsets);
+  list_apply<<<nb, kScanBlock, 0, st>>>(counts, nv, compact, bsum, offsets);
   return cudaGetLastError();
 }
 

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_top32_kernel(DockPara
     if (threadIdx.x == 0) p.k_eff[l] = 0;
     return;
   }
+  stage_tab<kCompactTU>(p.pocket);
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = m.n;
   double* vx = reinterpret_cast<double*>(smem);
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_topk_kernel(DockParam
     if (threadIdx.x == 0) p.k_eff[l] = 0;
     return;
   }
+  stage_tab<kCompactTU>(p.pocket);
   const int n = m.n;
   const int No = p.n_orient;
   const int K = min(p.top_k, No);
@@ -321,7 +323,7 @@ int launch(const DockParams& p, cudaStream_t stream) {
 
 }  // namespace
 
-int launch_rigid_topk(const DockParams& p, void* stream) {
+int GD_API(launch_rigid_topk)(const DockParams& p, void* stream) {
   const auto s = static_cast<cudaStream_t>(stream);
   return p.counters ? launch<true>(p, s) : launch<false>(p, s);
 }
