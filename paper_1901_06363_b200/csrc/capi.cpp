@@ -527,8 +527,12 @@ extern "C" int gd_set_pocket(gd_ctx* ctx, const double* xyz, int32_t n) {
     for (int32_t b = 0; b < rest; ++b)
       for (int k = 0; k < 3; ++k)
         head[16 * (b / kCodedBlock) + 3 * (b % kCodedBlock) + k] = codes[3 * (kCodedInline + b) + k];
-    GD_CUDA(ctx, slot->tab.ensure(sizeof(double) * tab.size()));
-    GD_CUDA(ctx, cudaMemcpy(slot->tab.ptr, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice));
+    // The kernels stage the table with one fixed-size bulk copy (stage_tab):
+    // the device copy is always kCodedTab doubles, zero-padded.
+    std::vector<double> full(tab);
+    full.resize(kCodedTab, 0.0);
+    GD_CUDA(ctx, slot->tab.ensure(sizeof(double) * full.size()));
+    GD_CUDA(ctx, cudaMemcpy(slot->tab.ptr, full.data(), sizeof(double) * full.size(), cudaMemcpyHostToDevice));
     GD_CUDA(ctx, ctx->vox_codes.ensure(sizeof(uint16_t) * codes.size()));
     GD_CUDA(ctx, cudaMemcpy(ctx->vox_codes.ptr, codes.data(), sizeof(uint16_t) * codes.size(),
                             cudaMemcpyHostToDevice));

@@ -162,11 +162,44 @@ __device__ __forceinline__ unsigned u16at(const uint32_t (&w)[N]) {
 // coordinate is one shared load at [byte offset + table base].
 __shared__ __align__(16) double s_tab[kCodedTab];
 // A no-op in kernels compiled for the fp64 format (CP false: no table).
+// The copy is one TMA bulk transfer (cp.async.bulk, SASS UBLKCP) of the whole
+// zero-padded table, issued by thread 0 and awaited by every thread on an
+// mbarrier, so no thread spends load/store instructions on it.
+// GD_TAB_TMA=0 restores the cooperative copy (A/B).
+#ifndef GD_TAB_TMA
+#define GD_TAB_TMA 1
+#endif
 template <bool CP>
 __device__ __forceinline__ void stage_tab(const PocketView& pk) {
   if constexpr (CP) {
+#if GD_TAB_TMA
+    __shared__ __align__(8) unsigned long long s_tab_bar;
+    const unsigned bar = static_cast<unsigned>(__cvta_generic_to_shared(&s_tab_bar));
+    constexpr unsigned kBytes = sizeof(double) * kCodedTab;
+    static_assert(kBytes % 16 == 0, "bulk copies move multiples of 16 bytes");
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(kBytes)
+                   : "memory");
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              static_cast<unsigned>(__cvta_generic_to_shared(s_tab))),
+          "l"(__cvta_generic_to_global(pk.tab)), "r"(kBytes), "r"(bar)
+          : "memory");
+    }
+    __syncthreads();  // the initialised barrier is visible to every waiter
+    unsigned done = 0;
+    while (!done)
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+#else
     for (int i = threadIdx.x; i < pk.ntab; i += blockDim.x) s_tab[i] = pk.tab[i];
     __syncthreads();
+#endif
   }
 }
 __device__ __forceinline__ double tab_at(unsigned off) {

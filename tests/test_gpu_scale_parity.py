@@ -131,3 +131,32 @@ def test_hollow_shell_pocket_overflow_voxels(docker):
     from oracle import oracle_py as O
     want = np.array([O.overlap_score(q, shell) for q in poses[:64]])
     assert np.array_equal(a[:64], want)
+
+
+def test_fixed_point_replay_many_restarts(docker):
+    """Chains with several restarts stop searching once every fragment has
+    kept angle 0 in a row and replay the remaining steps' counts
+    (flex_chain_kernel, kReplay).  Eight restarts make most steps replays;
+    the zig-zag ligand has more than 32 fragments, so its chains run every
+    step; scores, poses and both CandidateEvaluator counters must still
+    equal the reference's, which searches every step."""
+    from paper_1901_06363_b200 import LigandBatch
+    from gd_test_helpers import Lig
+    from test_gpu_prep import _zigzag
+    w = W.config(1)
+    pocket = w.pocket()
+    c = pocket.mean(axis=0)
+    base = w.ligands(range(12))
+    long = Lig(_zigzag(40), [(i, i + 1, True) for i in range(39)], radius=0.9)  # 37 rotamers
+    parts = [(base.xyz[base.atom_offsets[l]:base.atom_offsets[l + 1]],
+              base.radii[base.atom_offsets[l]:base.atom_offsets[l + 1]],
+              base.bonds[base.bond_offsets[l]:base.bond_offsets[l + 1]],
+              base.rotatable[base.bond_offsets[l]:base.bond_offsets[l + 1]]) for l in range(12)]
+    parts.append((long.xyz + c - long.xyz.mean(axis=0), long.radii, long.bonds, long.rot))
+    batch = LigandBatch.from_parts(parts)
+    docker.set_pocket(pocket)
+    for knobs in (Knobs.baseline(45, 30, 8, 6), Knobs(20, 60, 0.3, 5, True, 45, 4)):
+        got = docker.dock(batch, knobs, keep_poses=True)
+        assert (got.status == 0).all()
+        want = _cpu(batch, pocket, knobs)
+        assert_same_result(got, want, ctx=f"replay {knobs}: ")
