@@ -279,7 +279,8 @@ int gd_tile_hit_probability(const int32_t* best_peak_widths, int64_t n, const in
  * was skipped with GD_LIG_INVALID: the reference's Ligand validation text
  * (molecule.hpp:66-115) with the batch position as the ligand id, e.g.
  * "ligand '17': duplicate bond", or this path's size limit "ligand '17':
- * more than 256 atoms is not supported".  Empty for accepted ligands;
+ * more than 4096 atoms is not supported" (docking entry points; 256 for the
+ * fine-grained fragment and profile entry points).  Empty for accepted ligands;
  * GD_LIG_DEGENERATE means the reference's "rotate_fragment: degenerate
  * rotation axis" (geometry.hpp:168). */
 int gd_ligand_error(const gd_ctx* ctx, int32_t ligand, char* msg, size_t msg_len);

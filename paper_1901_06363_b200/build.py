@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -50,22 +51,26 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
     inc = ["-I", str(ROOT / "include"), "-I", str(CSRC)]
     hdrs = [CSRC / h for h in HEADERS] + [ROOT / "include" / "geodock_b200.h"]
-    objs = []
+    objs, jobs = [], []
     for src in CUDA_SRCS:
         obj = BUILD / (src + ".o")
         deps = [CSRC / src] + hdrs + ([CSRC / src.replace("_cp", "")] if "_cp" in src else [])
         if force or _stale(obj, deps):
-            _run([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-                  *os.environ.get("GD_NVCC_EXTRA", "").split(), *DEFS,
-                  "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *inc,
-                  "-c", str(CSRC / src), "-o", str(obj)])
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
+                         *os.environ.get("GD_NVCC_EXTRA", "").split(), *DEFS,
+                         "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3", *inc,
+                         "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
     for src in HOST_SRCS:
         obj = BUILD / (src + ".o")
         if force or _stale(obj, [CSRC / src] + hdrs):
-            _run(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", *DEFS,
-                  "-I/usr/local/cuda/include", *inc, "-c", str(CSRC / src), "-o", str(obj)])
+            jobs.append(["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", *DEFS,
+                         "-I/usr/local/cuda/include", *inc, "-c", str(CSRC / src), "-o", str(obj)])
         objs.append(obj)
+    # The translation units are independent: compile them side by side (the
+    # two flex TUs dominate, ~100 s each).
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as pool:
+        list(pool.map(_run, jobs))
     if force or _stale(LIB, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB),
               *map(str, objs), "-lpthread"])

@@ -222,6 +222,13 @@ struct gd_ctx {
   DevBuf meta, xyz, radii, bonds, rot, boff;  // staged raw ligands (+ host-filled offsets)
   DevBuf far, fmask, fax, fan, frel, order;   // written by the GPU preprocessing
   size_t frag_total = 0;                      // fragment slots allocated (2 x bonds)
+  // Wide ligands (more than kNarrowAtoms atoms) of the staged batch, ascending:
+  // preprocessed on the host (prepare_ligand) while their chunk is packed,
+  // searched by flex_wide_kernel with per-chain scratch in HBM.
+  std::vector<int32_t> wide_idx;               // ligand indices
+  std::vector<int64_t> wide_pref;              // atoms of the wide ligands before each
+  std::vector<PreparedLigand> wide_prep;       // host descriptors (uploaded per chunk)
+  DevBuf wide_list_d, wide_off_d, wide_scratch;
   PinnedBuf staging;
   PinnedBuf res_staging;         // pinned D2H targets of gd_dock_batch
   unsigned char* pin[10] = {};   // per-segment pointers into staging
@@ -697,8 +704,12 @@ struct Running {
   size_t fo = 0, wo = 0, mo = 0;  // frag, far-word, fmask-word cursors
 };
 
-// Atom counts the GPU preprocessing takes (the rest is rejected up front).
-bool size_ok(int n) { return n >= 2 && n <= kMaxAtoms; }
+// Atom counts the batch path docks (the rest is rejected up front): up to
+// kNarrowAtoms on the warp-per-chain kernels with GPU preprocessing, up to
+// kWideAtoms on the wide path.
+bool size_ok(int n) { return n >= 2 && n <= kWideAtoms; }
+bool is_wide(int n) { return n > kNarrowAtoms; }
+static_assert(kNarrowAtoms == kMaxAtoms, "the GPU preprocessing's limit is the warp path's");
 
 }  // namespace
 
@@ -711,6 +722,9 @@ static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
     return ctx->fail(GD_ERR_INVALID, "gd_upload: invalid ligand batch");
   const int L = b->n_ligands;
   size_t far_ub = 0, fmask_ub = 0;
+  int64_t wide_atoms = 0;
+  ctx->wide_idx.clear();
+  ctx->wide_pref.clear();
   for (int l = 0; l < L; ++l) {
     const int n = b->atom_offsets[l + 1] - b->atom_offsets[l];
     const int nb = b->bond_offsets[l + 1] - b->bond_offsets[l];
@@ -719,6 +733,21 @@ static int begin_batch(gd_ctx* ctx, const gd_ligand_batch* b, Running& run) {
     const size_t W = static_cast<size_t>((n + 63) / 64);
     far_ub += static_cast<size_t>(n) * W;
     fmask_ub += 2 * static_cast<size_t>(nb) * W;
+    if (is_wide(n)) {
+      ctx->wide_idx.push_back(l);
+      ctx->wide_pref.push_back(wide_atoms);
+      wide_atoms += n;
+    }
+  }
+  ctx->wide_pref.push_back(wide_atoms);
+  ctx->wide_prep.assign(ctx->wide_idx.size(), PreparedLigand{});
+  if (!ctx->wide_idx.empty()) {
+    GD_CUDA(ctx, ctx->wide_list_d.ensure(sizeof(int32_t) * ctx->wide_idx.size()));
+    GD_CUDA(ctx, ctx->wide_off_d.ensure(sizeof(int64_t) * ctx->wide_pref.size()));
+    GD_CUDA(ctx, cudaMemcpy(ctx->wide_list_d.ptr, ctx->wide_idx.data(),
+                            sizeof(int32_t) * ctx->wide_idx.size(), cudaMemcpyHostToDevice));
+    GD_CUDA(ctx, cudaMemcpy(ctx->wide_off_d.ptr, ctx->wide_pref.data(),
+                            sizeof(int64_t) * ctx->wide_pref.size(), cudaMemcpyHostToDevice));
   }
   const int32_t A = L > 0 ? b->atom_offsets[L] : 0;
   const int64_t B = L > 0 ? b->bond_offsets[L] : 0;
@@ -784,6 +813,18 @@ static void pack_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1, Ru
     if (m.status != GD_LIG_OK) continue;
     run.wo += static_cast<size_t>(m.n) * m.words;
     run.mo += 2 * static_cast<size_t>(nb) * m.words;
+    if (is_wide(m.n)) {
+      // Wide ligand: the graph preprocessing on the host, now; its
+      // descriptors follow the chunk's raw copy (h2d_prep_range).
+      const size_t w = std::lower_bound(ctx->wide_idx.begin(), ctx->wide_idx.end(), l) - ctx->wide_idx.begin();
+      PreparedLigand& q = ctx->wide_prep[w];
+      q = prepare_ligand(std::to_string(l), m.n, b->xyz + 3 * static_cast<size_t>(m.atom_off),
+                         b->radii + m.atom_off, nb, b->bonds + 2 * static_cast<size_t>(b->bond_offsets[l]),
+                         b->bond_rotatable + b->bond_offsets[l], kWideAtoms);
+      m.status = q.status;
+      m.nfrag = q.status == GD_LIG_OK ? q.nfrag() : 0;
+      continue;
+    }
     chunk_max_n = std::max(chunk_max_n, m.n);
   }
   auto* bo = reinterpret_cast<int32_t*>(ctx->pin[kBoff]);
@@ -861,6 +902,27 @@ static int h2d_prep_range(gd_ctx* ctx, const gd_ligand_batch* b, int c0, int c1,
   q.order = ctx->order.as<int32_t>();
   GD_CUDA(ctx, static_cast<cudaError_t>(launch_prep(q, s)));
   ctx->timing.launches += 2;
+  // Wide ligands of the chunk: their host-made descriptors (prep_kernel
+  // leaves them alone).
+  const auto* meta = reinterpret_cast<const LigMeta*>(ctx->pin[kMeta]);
+  for (size_t w = std::lower_bound(ctx->wide_idx.begin(), ctx->wide_idx.end(), c0) - ctx->wide_idx.begin();
+       w < ctx->wide_idx.size() && ctx->wide_idx[w] < c1; ++w) {
+    const PreparedLigand& g = ctx->wide_prep[w];
+    const LigMeta& m = meta[ctx->wide_idx[w]];
+    if (g.status != GD_LIG_OK) continue;
+    auto up = [&](DevBuf& d, size_t elem, size_t off, const void* src, size_t cnt) -> int {
+      if (cnt == 0) return GD_OK;
+      ctx->timing.h2d_bytes += static_cast<int64_t>(elem * cnt);
+      return ctx->cuda(cudaMemcpyAsync(static_cast<unsigned char*>(d.ptr) + elem * off, src, elem * cnt,
+                                       cudaMemcpyHostToDevice, s), "h2d wide");
+    };
+    const size_t nf = static_cast<size_t>(g.nfrag());
+    if ((rc = up(ctx->far, 8, m.far_off, g.far_mask.data(), g.far_mask.size()))) return rc;
+    if ((rc = up(ctx->fmask, 8, m.fmask_off, g.frag_mask.data(), g.frag_mask.size()))) return rc;
+    if ((rc = up(ctx->fax, 4, m.frag_off, g.frag_axis.data(), nf))) return rc;
+    if ((rc = up(ctx->fan, 4, m.frag_off, g.frag_anchor.data(), nf))) return rc;
+    if ((rc = up(ctx->frel, 8, m.frag_off, g.frag_rel.data(), nf))) return rc;
+  }
   return GD_OK;
 }
 
@@ -875,7 +937,7 @@ static void note_status(gd_ctx* ctx, const gd_ligand_batch* b, const int32_t* st
     const int a0 = b->atom_offsets[l], b0 = b->bond_offsets[l];
     const PreparedLigand p = prepare_ligand(std::to_string(l), b->atom_offsets[l + 1] - a0, b->xyz + 3 * a0,
                                             b->radii + a0, b->bond_offsets[l + 1] - b0, b->bonds + 2 * b0,
-                                            b->bond_rotatable + b0);
+                                            b->bond_rotatable + b0, kWideAtoms);
     ctx->errors[l] = p.error.empty() ? "ligand '" + std::to_string(l) + "': invalid" : p.error;
   }
   ctx->timing.host_prep_ms =
@@ -968,7 +1030,11 @@ static int prepare_dock(gd_ctx* ctx, const gd_knobs* k, bool keep_pose, bool kee
     GD_CUDA(ctx, ctx->o_top.ensure(sizeof(double) * 3 * static_cast<size_t>(std::max(ctx->total_atoms, 1))));
     GD_CUDA(ctx, ctx->top_best.ensure(sizeof(unsigned long long) * std::max(L, 1)));
   }
+  if (!ctx->wide_idx.empty())
+    GD_CUDA(ctx, ctx->wide_scratch.ensure(sizeof(double) * 8 * static_cast<size_t>(K) *
+                                          static_cast<size_t>(ctx->wide_pref.back())));
   p = DockParams{};
+  p.wide_scratch = ctx->wide_scratch.as<double>();
   p.order = ctx->order.as<int32_t>();
   p.meta = ctx->meta.as<LigMeta>();
   p.xyz = ctx->xyz.as<double>();
@@ -1041,13 +1107,39 @@ static int launch_range(gd_ctx* ctx, DockParams p, int c0, int c1, int max_n, cu
   if (p.n_lig == 0) return GD_OK;
   if (p.top_best != nullptr)
     GD_CUDA(ctx, cudaMemsetAsync(p.top_best + c0, 0, sizeof(unsigned long long) * (c1 - c0), s));
+  // Wide ligands among ligands [c0, c1) (chunks are ligand ranges; `order`
+  // permutes within them): their own rigid launch (shared memory sized by
+  // their atoms) and the wide search kernel; the regular launches skip them.
+  const size_t w0 = std::lower_bound(ctx->wide_idx.begin(), ctx->wide_idx.end(), c0) - ctx->wide_idx.begin();
+  const size_t w1 = std::lower_bound(ctx->wide_idx.begin(), ctx->wide_idx.end(), c1) - ctx->wide_idx.begin();
+  DockParams pw = p;
+  pw.n_wide = static_cast<int32_t>(w1 - w0);
+  pw.wide_list = ctx->wide_list_d.as<int32_t>() + w0;
+  pw.wide_off = ctx->wide_off_d.as<int64_t>() + w0;
   if (p.rigid) {
     GD_CUDA(ctx, static_cast<cudaError_t>(p.pocket.compact ? launch_rigid_topk_cp(p, s)
                                                            : launch_rigid_topk(p, s)));
     ctx->timing.launches += 1;
+    if (pw.n_wide > 0) {
+      DockParams pr = pw;
+      pr.order = pw.wide_list;
+      pr.n_lig = pw.n_wide;
+      pr.wide_pass = 1;
+      pr.max_n = 1;
+      for (size_t w = w0; w < w1; ++w)
+        pr.max_n = std::max(pr.max_n, static_cast<int32_t>(ctx->wide_pref[w + 1] - ctx->wide_pref[w]));
+      GD_CUDA(ctx, static_cast<cudaError_t>(p.pocket.compact ? launch_rigid_topk_cp(pr, s)
+                                                             : launch_rigid_topk(pr, s)));
+      ctx->timing.launches += 1;
+    }
   }
   if (e_mid) cudaEventRecord(e_mid, s);
   GD_CUDA(ctx, static_cast<cudaError_t>(p.pocket.compact ? launch_flex_cp(p, s) : launch_flex(p, s)));
+  if (pw.n_wide > 0) {
+    GD_CUDA(ctx, static_cast<cudaError_t>(p.pocket.compact ? launch_flex_wide_cp(pw, s)
+                                                           : launch_flex_wide(pw, s)));
+    ctx->timing.launches += 1;
+  }
   GD_CUDA(ctx, static_cast<cudaError_t>(launch_finalize(p, s)));
   ctx->timing.launches += 2;
   return GD_OK;

@@ -581,7 +581,8 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
 #define GD_FLAT_LIVE_MINC 1  // ... for searches of at least this many candidates
 #endif
 #ifndef GD_GROUP_PAIRMAJOR_MIN
-#define GD_GROUP_PAIRMAJOR_MIN 64  // bump_group goes pair-major from this many surviving pairs ...
+#define GD_GROUP_PAIRMAJOR_MIN 32  // bump_group goes pair-major from this many surviving pairs (r3g, coded
+                                   // records: c1 flex 10.90 ms at 32, 11.07 at 64, 11.43 at 128) ...
 #endif
 #ifndef GD_GROUP_PAIRMAJOR_MIN_WIDE
 #define GD_GROUP_PAIRMAJOR_MIN_WIDE 24  // ... or this many for groups of more than 16 candidates
@@ -814,7 +815,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
 #else
   const LigMeta m = p.meta[l];
 #endif
-  if (m.status != 0) return;
+  if (m.status != 0 || m.n > kNarrowAtoms) return;  // wide ligands: flex_wide_kernel
   const int n = m.n, W = m.words;
   const WarpMem s =
       carve<B>(smem + warp * warp_bytes<B>(p.max_n, (p.max_n + 63) / 64, p.max_pairs), n, W,
@@ -972,6 +973,237 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   }
   publish_warp(wk, p.counters, 8, lane);
   ck.publish(p.counters, lane);
+}
+
+// Wide ligands (more than kNarrowAtoms atoms): one CTA per (ligand, seed
+// rank) chain, the chain's state -- committed pose and terms, the candidate
+// pose, the candidate terms: 8 doubles per atom -- in HBM, far masks and
+// fragment masks read from HBM, candidates evaluated one after another
+// exactly as CandidateEvaluator does (kernel.hpp:100-112): rotate the
+// fragment, check_bumps over every (fragment atom, far partner) pair, then
+// the overlap terms of the rotated atoms and an atom-order fold by thread 0.
+// Same expressions and decisions as flex_chain_kernel, so the same bits; no
+// pair prefilter and no batching, because such ligands are rare and their
+// chains are long enough to fill the GPU with a CTA each.
+constexpr int kWideThreads = 256;
+template <bool On>
+__global__ void __launch_bounds__(kWideThreads) flex_wide_kernel(DockParams p) {
+  stage_tab<kCompactTU>(p.pocket);
+  __shared__ double s_val;
+  __shared__ int s_stage;
+  const int K = p.k_slots;
+  const int b = blockIdx.x / K, r = blockIdx.x % K;
+  const int l = p.wide_list[b];
+  const LigMeta m = p.meta[l];
+  if (m.status != 0) return;
+  const int n = m.n, W = m.words, tid = threadIdx.x;
+  const size_t e = static_cast<size_t>(l) * p.top_k + r;
+  double* px = p.wide_scratch + 8 * (static_cast<size_t>(p.wide_off[b]) * K + static_cast<size_t>(r) * n);
+  double *py = px + n, *pz = py + n, *pt = pz + n;  // committed pose and terms
+  double *qx = pt + n, *qy = qx + n, *qz = qy + n;  // candidate pose (fragment atoms)
+  double* v = qz + n;                               // candidate terms
+  const double* rad = p.radii + m.atom_off;
+  const uint64_t* far = p.far_mask + m.far_off;
+  Work<On> wk;
+
+  // Chain start: the rigid seed pose (E3) or the given pose.
+  double R[9];
+  if (p.rigid) {
+    const int o = p.seed_slot[e];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = __ldg(p.orient_R + 9 * o + k);
+  }
+  for (int i = tid; i < n; i += kWideThreads) {
+    const double* q = p.xyz + 3 * (static_cast<size_t>(m.atom_off) + i);
+    double x = q[0], y = q[1], z = q[2];
+    if (p.rigid) {
+      rigid_apply(R, p.cx, p.cy, p.cz, dsub(x, p.cx), dsub(y, p.cy), dsub(z, p.cz), x, y, z);
+      wk.add(kXform, 1);
+    }
+    px[i] = x;
+    py[i] = y;
+    pz[i] = z;
+    pt[i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+  }
+  __syncthreads();
+  // overlap_score fold (geometry.hpp:143-154) of `terms`, broadcast.
+  auto fold = [&](const double* terms) {
+    if (tid == 0) {
+      double sum = 0.0;
+      for (int i = 0; i < n; ++i) sum = dadd(sum, terms[i]);
+      s_val = __ddiv_rn(static_cast<double>(n), sum);
+    }
+    __syncthreads();
+    const double sc = s_val;
+    __syncthreads();
+    return sc;
+  };
+  double cur = fold(pt);
+  if (!p.rigid && tid == 0) p.seed_score[e] = cur;
+  long long evals = 1, checks = 1;  // uniform across the CTA
+
+  for (int rep = 0; rep < p.reps; ++rep) {
+    for (int f = 0; f < m.nfrag; ++f) {
+      const int fo = m.frag_off + f;
+      const int axis = __ldg(p.frag_axis + fo), anchor = __ldg(p.frag_anchor + fo);
+      const double rel = __ldg(p.frag_rel + fo);
+      const uint64_t* fm = p.frag_mask + m.fmask_off + static_cast<size_t>(f) * W;
+      const bool low = rel <= p.threshold;
+      const bool refined = !low && p.refine;
+      const int step = low ? p.lp : p.hp;
+      const int A = 360 / step;
+      if (!refined && A == 1) {  // step 360: only the committed pose
+        evals += 1;
+        checks += 1;
+        continue;
+      }
+      // rotate_fragment_into axis (geometry.hpp:165-169).
+      const double ox = px[axis], oy = py[axis], oz = pz[axis];
+      const double ax = dsub(px[anchor], ox), ay = dsub(py[anchor], oy), az = dsub(pz[anchor], oz);
+      const double len = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
+      if (len < kMinAxisLength) {
+        if (tid == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
+        return;
+      }
+      const Axis X{ox, oy, oz, __ddiv_rn(ax, len), __ddiv_rn(ay, len), __ddiv_rn(az, len)};
+      // CandidateEvaluator::evaluate of one angle != 0 (uniform result).
+      auto evaluate = [&](int a, double& score) -> bool {
+        const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a), omc = dsub(1.0, cs);
+        for (int i = tid; i < n; i += kWideThreads)
+          if (in_frag(fm, i)) {
+            rodrigues(X, cs, sn, omc, px[i], py[i], pz[i], qx[i], qy[i], qz[i]);
+            wk.add(kRot, 1);
+          }
+        __syncthreads();
+        bool bump = false;
+        for (int i = tid; i < n && !bump; i += kWideThreads) {
+          if (!in_frag(fm, i)) continue;
+          for (int w = 0; w < W && !bump; ++w)
+            for (uint64_t bits = far[static_cast<size_t>(i) * W + w] & ~fm[w]; bits; bits &= bits - 1) {
+              const int j = 64 * w + __ffsll(static_cast<long long>(bits)) - 1;
+              const double cut = dmul(kBumpScale, dadd(rad[i], rad[j]));
+              wk.add(kBump, 1);
+              if (dist_sq(qx[i], qy[i], qz[i], px[j], py[j], pz[j]) < dmul(cut, cut)) {
+                bump = true;
+                break;
+              }
+            }
+        }
+        if (__syncthreads_or(bump)) return false;
+        for (int i = tid; i < n; i += kWideThreads)
+          v[i] = in_frag(fm, i) ? fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx[i], qy[i], qz[i], wk)) : pt[i];
+        __syncthreads();
+        wk.add(kTerms, tid == 0 ? n : 0);
+        wk.add(kEvals, tid == 0 ? 1 : 0);
+        score = fold(v);
+        return true;
+      };
+      int best_a = 0;
+      double best = cur;
+      if (!refined) {
+        // optimize_fragment_flat (kernel.hpp:125-143); angle 0 is the pose.
+        int nfeas = 0;
+        for (int c = 1; c < A; ++c) {
+          double sc;
+          if (!evaluate(c * step, sc)) continue;
+          ++nfeas;
+          if (sc > best) {
+            best = sc;
+            best_a = c * step;
+          }
+        }
+        evals += 1 + nfeas;
+        checks += A;
+      } else {
+        // optimize_fragment_refined (kernel.hpp:150-198).
+        const int T = p.tile, tc = 360 / T;
+        bool have = false;
+        int wt = -1, nfeas = 0;
+        double ws = 0.0;
+        best = 0.0;
+        auto visit = [&](int a, int tile) {
+          double sc = cur;
+          if (a != 0 && !evaluate(a, sc)) return;
+          ++nfeas;
+          if (!have || sc > best) {
+            best = sc;
+            best_a = a;
+            have = true;
+          }
+          if (tile >= 0 && (wt < 0 || sc > ws)) {
+            wt = tile;
+            ws = sc;
+          }
+        };
+        for (int t = 0; t < tc; ++t) visit(t * T + T / 2, t);
+        checks += tc;
+        if (wt >= 0) {
+          int cnt2 = 0;
+          while ((cnt2 + 1) * step <= T) ++cnt2;
+          for (int k = 0; k < cnt2; ++k) visit(wt * T + k * step, -1);
+          checks += cnt2;
+        }
+        checks += 1;  // entry-pose comparison (kernel.hpp:192-194)
+        if (!have || cur > best) {
+          best = cur;
+          best_a = 0;
+        }
+        evals += nfeas;
+      }
+      // commit_angle (kernel.hpp:115-117).
+      if (best_a != 0) {
+        const double cs = __ldg(p.cos_deg + best_a), sn = __ldg(p.sin_deg + best_a);
+        const double omc = dsub(1.0, cs);
+        for (int i = tid; i < n; i += kWideThreads)
+          if (in_frag(fm, i)) {
+            double x, y, z;
+            rodrigues(X, cs, sn, omc, px[i], py[i], pz[i], x, y, z);
+            wk.add(kRot, 1);
+            qx[i] = x;
+            qy[i] = y;
+            qz[i] = z;
+            v[i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+          }
+        __syncthreads();  // every thread read the axis atoms' old coordinates above
+        for (int i = tid; i < n; i += kWideThreads)
+          if (in_frag(fm, i)) {
+            px[i] = qx[i];
+            py[i] = qy[i];
+            pz[i] = qz[i];
+            pt[i] = v[i];
+          }
+        __syncthreads();
+      }
+      cur = best;
+    }
+  }
+  if (tid == 0) {
+    p.st_final[e] = cur;
+    p.st_evals[e] = evals;
+    p.st_checks[e] = checks;
+  }
+  // Final pose staging, as flex_chain_kernel.
+  if (p.stage_pose != nullptr) {
+    if (tid == 0) {
+      int stage = 1;
+      if (p.top_best != nullptr) {
+        const unsigned long long old =
+            atomicMax(p.top_best + l, static_cast<unsigned long long>(__double_as_longlong(cur)));
+        stage = __longlong_as_double(static_cast<long long>(old)) <= cur;
+      }
+      s_stage = stage;
+    }
+    __syncthreads();
+    if (s_stage) {
+      double* dst = p.stage_pose + 3 * (static_cast<size_t>(p.top_k) * m.atom_off + static_cast<size_t>(r) * n);
+      for (int i = tid; i < n; i += kWideThreads) {
+        dst[3 * i] = px[i];
+        dst[3 * i + 1] = py[i];
+        dst[3 * i + 2] = pz[i];
+      }
+    }
+  }
+  publish(wk, p.counters, 8);
 }
 
 // Rotation profiles (reference rotation_profile, analysis.hpp:37-56): one
@@ -1423,6 +1655,14 @@ int GD_API(launch_flex)(const DockParams& p, void* stream) {
     case 6: return launch_flex_b<6>(p, chains, s);
     default: return launch_flex_b<4>(p, chains, s);
   }
+}
+
+int GD_API(launch_flex_wide)(const DockParams& p, void* stream) {
+  const long long chains = static_cast<long long>(p.n_wide) * p.k_slots;
+  if (chains == 0) return cudaSuccess;
+  auto kernel = p.counters ? flex_wide_kernel<true> : flex_wide_kernel<false>;
+  kernel<<<static_cast<unsigned>(chains), kWideThreads, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return cudaGetLastError();
 }
 
 int GD_API(launch_profiles)(const DockParams& p, const int32_t* items, int n_items, double* scores,

@@ -53,6 +53,13 @@ struct GridLevel {
   double fdim_x, fdim_y, fdim_z;  // the dims as doubles (no conversion per query)
 };
 
+// Ligands of up to kNarrowAtoms atoms take the warp-per-chain kernels (8-bit
+// atom indices, four mask words, chain state in shared memory); larger ones
+// (up to kWideAtoms) are preprocessed on the host and searched by
+// flex_wide_kernel.
+constexpr int kNarrowAtoms = 256;
+constexpr int kWideAtoms = 4096;  // the rigid sweep holds a ligand's atoms in shared memory
+
 constexpr int kGridLevels = 2;  // fine (near field) + coarse (far field)
 constexpr int kPhaseBase = 16;     // counters[16..32): flex phase clocks
 constexpr int kCounterSlots = 32;
@@ -96,8 +103,18 @@ struct DockParams {
   int32_t top_k;           // slots per ligand in the outputs
   int32_t rigid;           // 1 = rigid sweep + top-K seeds, 0 = dock given pose
   int32_t k_slots;         // chains per ligand: min(top_k, n_orient) (1 if no sweep)
-  int32_t max_n;           // largest ligand in the batch (smem sizing)
+  int32_t max_n;           // largest warp-path ligand (<= kNarrowAtoms atoms) of the launch (smem sizing)
   int32_t max_pairs;       // bump-pair list capacity per warp (floor(max_n^2/4))
+
+  // Wide ligands (more than kNarrowAtoms atoms): their chains run in
+  // flex_wide_kernel, one CTA per chain, with the chain state in HBM.
+  int32_t wide_pass;         // rigid sweep: 1 = this launch's ligands are the wide ones
+                             // (order = wide_list); 0 = skip wide ligands
+  int32_t n_wide;            // wide ligands of this launch
+  const int32_t* wide_list;  // [n_wide] their ligand indices
+  const int64_t* wide_off;   // [n_wide] atoms of the batch's wide ligands before ligand b: its
+                             // scratch is k_slots x 8n doubles at 8 * k_slots * wide_off[b]
+  double* wide_scratch;
 
   // Rigid -> flex hand-off (rank order).
   int32_t* seed_slot;      // [L*K] position in the orientation list
@@ -143,6 +160,8 @@ int launch_l2_gather_probe(const double* buf, unsigned long long n_rec, int bloc
 int launch_rigid_topk(const DockParams& p, void* stream);
 // One warp per (ligand, seed-rank) chain: n_lig * k_slots chains.
 int launch_flex(const DockParams& p, void* stream);
+// One CTA per (wide ligand, seed-rank) chain: n_wide * k_slots chains.
+int launch_flex_wide(const DockParams& p, void* stream);
 // Rotation profiles: one warp per (ligand, fragment) item of `items`
 // ([2*n_items] ligand, fragment), 360 scores + validity flags per item.
 int launch_profiles(const DockParams& p, const int32_t* items, int n_items, double* scores,
@@ -169,6 +188,7 @@ int launch_finalize(const DockParams& p, void* stream);
 // flex_cp.cu, rigid_cp.cu); callers dispatch on PocketView::compact.
 int launch_rigid_topk_cp(const DockParams& p, void* stream);
 int launch_flex_cp(const DockParams& p, void* stream);
+int launch_flex_wide_cp(const DockParams& p, void* stream);
 int launch_profiles_cp(const DockParams& p, const int32_t* items, int n_items, double* scores,
                        uint8_t* valid, void* stream);
 int launch_fragment_search_cp(const DockParams& p, const FragmentIO& io, void* stream);

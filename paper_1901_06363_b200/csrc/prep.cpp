@@ -71,7 +71,8 @@ void bridges(int n, int n_bonds, Scratch& s) {
 }  // namespace
 
 PreparedLigand prepare_ligand(const std::string& id, int n, const double* xyz, const double* radii,
-                              int n_bonds, const int32_t* bonds, const uint8_t* rotatable) {
+                              int n_bonds, const int32_t* bonds, const uint8_t* rotatable,
+                              int max_atoms) {
   PreparedLigand p;
   p.n = n;
   auto fail = [&](const std::string& what) {
@@ -81,7 +82,7 @@ PreparedLigand prepare_ligand(const std::string& id, int n, const double* xyz, c
   };
   // Ligand::validate (molecule.hpp:66-89), same checks in the same order.
   if (n < 2) return fail("needs at least 2 atoms");
-  if (n > kMaxAtoms) return fail("more than 256 atoms is not supported");
+  if (n > max_atoms) return fail("more than " + std::to_string(max_atoms) + " atoms is not supported");
   for (int i = 0; i < n; ++i) {
     if (!(radii[i] > 0.0)) return fail("non-positive radius on atom " + std::to_string(i));
     if (!(std::isfinite(xyz[3 * i]) && std::isfinite(xyz[3 * i + 1]) && std::isfinite(xyz[3 * i + 2])))
@@ -137,8 +138,9 @@ PreparedLigand prepare_ligand(const std::string& id, int n, const double* xyz, c
   // the kernels need them: bit j of row i set iff distance(i, j) >= 4.
   p.words = (n + 63) / 64;
   p.far_mask.assign(static_cast<size_t>(n) * p.words, 0);
+  std::vector<uint64_t> near(p.words), left(p.words);
   for (int src = 0; src < n; ++src) {
-    uint64_t near[kMaxWords] = {0, 0, 0, 0};
+    std::fill(near.begin(), near.end(), 0ull);
     s.dist.assign(n, -1);
     int head = 0, tail = 0;
     s.queue[tail++] = src;
@@ -184,7 +186,7 @@ PreparedLigand prepare_ligand(const std::string& id, int n, const double* xyz, c
   for (const int b : s.rot) {
     const int lo = std::min(bonds[2 * b], bonds[2 * b + 1]);
     const int hi = std::max(bonds[2 * b], bonds[2 * b + 1]);
-    uint64_t left[kMaxWords] = {0, 0, 0, 0};
+    std::fill(left.begin(), left.end(), 0ull);
     int head = 0, tail = 0;
     s.queue[tail++] = lo;
     left[lo / 64] |= 1ull << (lo % 64);

@@ -19,8 +19,9 @@
 //   * fragments 2r (left: axis lo, anchor hi) and 2r+1 (right: axis hi,
 //     anchor lo), relative_size = |F| / n in fp64 (the host's division).
 //
-// Ligands of more than 256 atoms (kMaxAtoms) or fewer than 2 are rejected by
-// the host before the launch (status already set).  A second kernel orders
+// Ligands of fewer than 2 atoms are rejected by the host before the launch
+// (status already set); ligands of more than 256 atoms (kNarrowAtoms) are
+// preprocessed on the host (prep.cpp) and skipped here.  A second kernel orders
 // the chunk's ligands longest-first for the search kernels' CTA order.
 #include <cstdint>
 
@@ -62,8 +63,8 @@ __global__ void __launch_bounds__(32 * kPrepWarps) prep_kernel(PrepParams q) {
   const int l = q.l0 + blockIdx.x * kPrepWarps + warp;
   if (l >= q.l1) return;
   LigMeta& m = q.meta[l];
-  if (m.status != 0) {  // rejected on the host (atom count)
-    if (lane == 0) q.status[l] = m.status;
+  if (m.status != 0 || m.n > kNarrowAtoms) {  // rejected on the host, or a wide ligand the host
+    if (lane == 0) q.status[l] = m.status;  // preprocessed (descriptors uploaded separately)
     return;
   }
   const int n = m.n, W = m.words;

@@ -9,7 +9,7 @@
 //     by (min endpoint, max endpoint), bridges by DFS lowpoints (:190-231);
 //   * grow_fragments (molecule.hpp:255-301): left = component of the
 //     smaller endpoint, relative_size = |F|/n, axis/anchor atoms.
-// The result is packed as bitmasks (n <= kMaxAtoms) for the kernels.
+// The result is packed as bitmasks (ceil(n / 64) words per row) for the kernels.
 #pragma once
 
 #include <cstdint>
@@ -18,7 +18,7 @@
 
 namespace gdb200 {
 
-constexpr int kMaxAtoms = 256;  // 4 x 64-bit mask words
+constexpr int kMaxAtoms = 256;  // 4 x 64-bit mask words: the GPU preprocessing and the warp-per-chain kernels
 constexpr int kMaxWords = kMaxAtoms / 64;
 constexpr int kGraphDistanceCap = 4;  // molecule.hpp:43, geometry.hpp:40
 
@@ -38,7 +38,11 @@ struct PreparedLigand {
 
 // Validates and preprocesses one ligand given SoA atoms and bonds.
 // `id` only feeds error messages ("ligand '<id>': ...", as the reference).
+// Ligands of more than `max_atoms` atoms are rejected ("more than <max_atoms>
+// atoms is not supported"): kMaxAtoms for the warp-per-chain kernels'
+// callers, kernels.h's kWideAtoms for the batch docking path.
 PreparedLigand prepare_ligand(const std::string& id, int n, const double* xyz, const double* radii,
-                              int n_bonds, const int32_t* bonds, const uint8_t* rotatable);
+                              int n_bonds, const int32_t* bonds, const uint8_t* rotatable,
+                              int max_atoms = kMaxAtoms);
 
 }  // namespace gdb200

@@ -131,6 +131,7 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_top32_kernel(DockPara
     if (threadIdx.x == 0) p.k_eff[l] = 0;
     return;
   }
+  if (!p.wide_pass && m.n > kNarrowAtoms) return;  // swept by the wide ligands' own launch
   stage_tab<kCompactTU>(p.pocket);
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = m.n;
@@ -200,6 +201,7 @@ __global__ void __launch_bounds__(BT, GD_RIGID_MINB) rigid_topk_kernel(DockParam
     if (threadIdx.x == 0) p.k_eff[l] = 0;
     return;
   }
+  if (!p.wide_pass && m.n > kNarrowAtoms) return;  // swept by the wide ligands' own launch
   stage_tab<kCompactTU>(p.pocket);
   const int n = m.n;
   const int No = p.n_orient;

@@ -133,7 +133,6 @@ SIGNATURES = {
     "gd_l2_gather_rate": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(C.c_double)]),
     "gd_pocket_index_stats": (C.c_int, [C.c_void_p, C.POINTER(gd_index_level)]),
     "gd_pocket_index_format": (C.c_int, [C.c_void_p]),
-    "gd_pocket_index_format": (C.c_int, [C.c_void_p]),
     "gd_ligand_error": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_size_t]),
     "gd_multi_create": (C.c_int, [_i32p, C.c_int32, C.POINTER(C.c_void_p)]),
     "gd_multi_destroy": (C.c_int, [C.c_void_p]),
@@ -414,9 +413,6 @@ class Docker:
         out["levels"] = [{"dims": list(x.dims), "voxel": x.voxel, "candidates": x.candidates,
                           "record_bytes": x.record_bytes, "list_bytes": x.list_bytes} for x in lv]
         out["index_bytes"] = sum(x.record_bytes + x.list_bytes for x in lv)
-        fmt = self._lib.gd_pocket_index_format(self._h)
-        self._check(min(fmt, 0))
-        out["format"] = "coded" if fmt == 1 else "fp64"
         fmt = self._lib.gd_pocket_index_format(self._h)
         self._check(min(fmt, 0))
         out["format"] = "coded" if fmt == 1 else "fp64"

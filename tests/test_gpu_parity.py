@@ -210,7 +210,8 @@ def test_large_ligands_multiword_masks(docker):
 
 def test_ligands_at_the_atom_limit(docker):
     """220-256 atoms (four mask words; the flex CTA narrows to fit shared
-    memory) against the reference; 257 atoms is skipped, not docked."""
+    memory) against the reference; 257 atoms takes the wide path
+    (tests/test_gpu_wide.py) instead of being skipped."""
     from paper_1901_06363_b200 import LigandBatch, synth_ligands
     pocket = W.config(1).pocket()
     batch = synth_ligands(777, [0, 1], n_lo=220, n_hi=256, r_cap=12, centre=pocket.mean(axis=0))
@@ -224,8 +225,9 @@ def test_ligands_at_the_atom_limit(docker):
     xyz = np.stack([np.arange(n) * 1.5, np.zeros(n), np.zeros(n)], axis=1)
     big = LigandBatch.from_parts([(xyz, np.full(n, 1.2), np.stack([np.arange(n - 1), np.arange(1, n)], 1),
                                    np.zeros(n - 1, np.uint8))])
-    res = docker.dock(big, knobs)
-    assert res.status[0] == 1 and res.k_eff[0] == 0
+    res = docker.dock(big, knobs, keep_poses=True)
+    assert res.status[0] == 0 and res.k_eff[0] == 3
+    assert_same_result(res, _cpu(big, pocket, knobs))
 
 
 def test_config3_rough_pocket(docker):

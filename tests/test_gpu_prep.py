@@ -75,7 +75,7 @@ def test_every_rejection_rule(docker):
         "non-finite position": Lig(nan, [(i, i + 1, True) for i in range(5)]),
         "disconnected": Lig(_zigzag(5), [(0, 1, True), (1, 2, True), (3, 4, True)]),
         "needs at least 2 atoms": Lig([[0, 0, 0]], []),
-        "more than 256 atoms": Lig(_zigzag(300), [(i, i + 1, False) for i in range(299)]),
+        "more than 4096 atoms is not supported": Lig(_zigzag(4097), [(i, i + 1, False) for i in range(4096)]),
     }
     parts = [good]
     for lig in cases.values():

@@ -1,4 +1,5 @@
-"""gd_set_pocket wall time per config-3 pocket, first and second build.
+"""gd_set_pocket wall time, index footprint and record format per config-3
+pocket, first and second build.
 python tools/index_build_c3.py"""
 import os
 import sys
@@ -19,4 +20,5 @@ for i in range(16):
     t2 = time.perf_counter()
     info = d.pocket_info()
     print(f"pocket {i:2d} P={len(pk):5d} first={1e3 * (t1 - t0):7.1f} ms second={1e3 * (t2 - t1):7.1f} ms "
-          f"dims={info['dims'].tolist()} h={info['voxel']:.3f} cand={info['n_candidates']}")
+          f"dims={info['dims'].tolist()} h={info['voxel']:.3f} cand={info['n_candidates']} "
+          f"index={info['index_bytes'] / 1e6:.1f} MB {info['format']}")
