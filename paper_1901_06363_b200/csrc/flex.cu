@@ -103,10 +103,17 @@ constexpr int warps_for() {
 constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+// Row stride (doubles) of the candidate-term table v: odd, so the fold's
+// lanes -- one per candidate, all at the same atom -- hit distinct banks
+// (stride n put candidates 0, 2, 4 of an n = 40 ligand on the same ones).
+#ifndef GD_V_PAD
+#define GD_V_PAD 1
+#endif
+__host__ __device__ __forceinline__ int vrow(int n) { return GD_V_PAD ? (n | 1) : n; }
 
 template <int B>
 __host__ __device__ __forceinline__ size_t warp_bytes(int n, int W, int max_pairs) {
-  return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * B * n) +
+  return a16(8ull * n) + a16(8ull * n * W) + 4 * a16(8ull * n) + a16(8ull * B * vrow(n)) +
          a16(2ull * max_pairs) + a16(n) + a16(32) + a16(16) + a16(sizeof(Axis)) + a16(8);
 }
 
@@ -116,10 +123,63 @@ struct __align__(16) PT {
   double x, y, z, t;
 };
 
+// The chain's pose table in shared memory.  Lanes mostly read consecutive
+// atoms, and 32-byte records read with 128-bit loads put atoms i and i + 4
+// on the same banks (a quarter warp's eight 16-byte chunks must fall in the
+// eight distinct 16-byte bank groups): ncu counted 45-65% excess wavefronts
+// on these loads with the shared-memory pipe at 50% of its peak.
+// GD_PT_LAYOUT 1 swaps the (x, y) and (z, t) halves of every second group
+// of four atoms, so eight consecutive atoms cover all eight bank groups;
+// 2 keeps x, y, z and t in four arrays (64-bit loads, an unused t is never
+// loaded); 0 is the plain record array.
+#ifndef GD_PT_LAYOUT
+#define GD_PT_LAYOUT 1
+#endif
+struct Pose {
+  double* b;
+  int n;
+  __device__ __forceinline__ PT get(int i) const {
+#if GD_PT_LAYOUT == 2
+    return PT{b[i], b[n + i], b[2 * n + i], b[3 * n + i]};
+#elif GD_PT_LAYOUT == 1
+    const double2* c = reinterpret_cast<const double2*>(b);
+    const int h = (i >> 2) & 1;
+    const double2 xy = c[2 * i + h], zt = c[2 * i + 1 - h];
+    return PT{xy.x, xy.y, zt.x, zt.y};
+#else
+    return reinterpret_cast<const PT*>(b)[i];
+#endif
+  }
+  __device__ __forceinline__ double t(int i) const {
+#if GD_PT_LAYOUT == 2
+    return b[3 * n + i];
+#elif GD_PT_LAYOUT == 1
+    return b[4 * i + 3 - 2 * ((i >> 2) & 1)];
+#else
+    return b[4 * i + 3];
+#endif
+  }
+  __device__ __forceinline__ void set(int i, const PT& v) const {
+#if GD_PT_LAYOUT == 2
+    b[i] = v.x;
+    b[n + i] = v.y;
+    b[2 * n + i] = v.z;
+    b[3 * n + i] = v.t;
+#elif GD_PT_LAYOUT == 1
+    double2* c = reinterpret_cast<double2*>(b);
+    const int h = (i >> 2) & 1;
+    c[2 * i + h] = make_double2(v.x, v.y);
+    c[2 * i + 1 - h] = make_double2(v.z, v.t);
+#else
+    reinterpret_cast<PT*>(b)[i] = v;
+#endif
+  }
+};
+
 struct WarpMem {
   double* radius;        // [n]
   uint64_t* far;         // [n*W]  bit j of row i: capped graph distance >= 4
-  PT* pt;                // [n]    committed pose + terms of the chain
+  Pose pt;               // [n]    committed pose + terms of the chain
   double* v;             // [B*n] candidate terms of fragment atoms
   uint16_t* pairs;       // [max_pairs] surviving bump pairs: F-slot | j << 8
   uint8_t* fidx;         // [n] fragment atoms, ascending
@@ -140,8 +200,8 @@ __device__ WarpMem carve(unsigned char* base, int n, int W, int max_pairs) {
   };
   s.radius = reinterpret_cast<double*>(take(8ull * n));
   s.far = reinterpret_cast<uint64_t*>(take(8ull * n * W));
-  s.pt = reinterpret_cast<PT*>(take(32ull * n));
-  s.v = reinterpret_cast<double*>(take(8ull * B * n));
+  s.pt = Pose{reinterpret_cast<double*>(take(32ull * n)), n};
+  s.v = reinterpret_cast<double*>(take(8ull * B * vrow(n)));
   s.pairs = reinterpret_cast<uint16_t*>(take(2ull * max_pairs));
   s.fidx = reinterpret_cast<uint8_t*>(take(n));
   s.fm = reinterpret_cast<uint64_t*>(take(32));
@@ -207,7 +267,7 @@ __device__ __forceinline__ void bump_item(const WarpMem& s, const DockParams& p,
   const int a = a0 + c * da;
   const double cs = __ldg(p.cos_deg + a), sn = __ldg(p.sin_deg + a);
   double qx, qy, qz;
-  const PT ai = s.pt[i], aj = s.pt[j];
+  const PT ai = s.pt.get(i), aj = s.pt.get(j);
   rodrigues(X, cs, sn, dsub(1.0, cs), ai.x, ai.y, ai.z, qx, qy, qz);
   wk.add(kRot, 1);
   wk.add(kBump, 1);
@@ -244,10 +304,10 @@ __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& 
     const int ac = a0 + c * da;
     const double cs = __ldg(p.cos_deg + ac), sn = __ldg(p.sin_deg + ac);
     double x, y, z;
-    const PT q = s.pt[i];
+    const PT q = s.pt.get(i);
     rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
     wk.add(kRot, 1);
-    s.v[c * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+    s.v[c * vrow(n) + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
   }
   return;
 #endif
@@ -259,10 +319,10 @@ __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& 
     const int ac = a0 + c * da;
     const double cs = __ldg(p.cos_deg + ac), sn = __ldg(p.sin_deg + ac);
     double x, y, z;
-    const PT q = s.pt[i];
+    const PT q = s.pt.get(i);
     rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
     wk.add(kRot, 1);
-    s.v[c * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+    s.v[c * vrow(n) + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
   }
   return;
 #endif
@@ -277,13 +337,13 @@ __device__ __forceinline__ void query_phase(const WarpMem& s, const DockParams& 
     const double cs0 = __ldg(p.cos_deg + a0c), sn0 = __ldg(p.sin_deg + a0c);
     const double cs1 = __ldg(p.cos_deg + a1c), sn1 = __ldg(p.sin_deg + a1c);
     double x0, y0, z0, x1, y1, z1, m0, m1;
-    const PT q0 = s.pt[i0], q1 = s.pt[i1];
+    const PT q0 = s.pt.get(i0), q1 = s.pt.get(i1);
     rodrigues(X, cs0, sn0, dsub(1.0, cs0), q0.x, q0.y, q0.z, x0, y0, z0);
     rodrigues(X, cs1, sn1, dsub(1.0, cs1), q1.x, q1.y, q1.z, x1, y1, z1);
     wk.add(kRot, 2);
     min_dist_sq2(p.pocket, x0, y0, z0, x1, y1, z1, m0, m1, wk);
-    if (l0) s.v[c0 * n + i0] = fmax(kMinDistanceSq, m0);
-    if (l1) s.v[c1 * n + i1] = fmax(kMinDistanceSq, m1);
+    if (l0) s.v[c0 * vrow(n) + i0] = fmax(kMinDistanceSq, m0);
+    if (l1) s.v[c1 * vrow(n) + i1] = fmax(kMinDistanceSq, m1);
   }
 }
 
@@ -318,8 +378,8 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
       if (act) {
         const int pr = s.pairs[t];
         const int i = pr & 0xff, j = pr >> 8;
-        const PT ai = s.pt[i];
-        aj = s.pt[j];
+        const PT ai = s.pt.get(i);
+        aj = s.pt.get(j);
         r = arm_of(X, ai.x, ai.y, ai.z);
         const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
         cut2 = dmul(cut, cut);
@@ -353,7 +413,7 @@ __device__ void eval_batch(const WarpMem& s, const DockParams& p, const Axis& X,
   double score = cur;
   if (lane < nb && ((live >> lane) & 1u)) {
     double sum = pre;
-    const double* vc = s.v + lane * n;
+    const double* vc = s.v + lane * vrow(n);
 #pragma unroll kFoldUnroll
     for (int i = first; i < n; ++i) sum = dadd(sum, vc[i]);
     score = __ddiv_rn(static_cast<double>(n), sum);
@@ -417,7 +477,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   const int n = m.n, W = m.words;
   if (lane < W) s.fm[lane] = fm_word;  // loaded by the caller with the descriptors
   // rotate_fragment_into axis (geometry.hpp:165-169), identical in every lane.
-  const PT pa = s.pt[axis], pb = s.pt[anchor];
+  const PT pa = s.pt.get(axis), pb = s.pt.get(anchor);
   const double ox = pa.x, oy = pa.y, oz = pa.z;
   const double ax = dsub(pb.x, ox), ay = dsub(pb.y, oy), az = dsub(pb.z, oz);
   const double len = __dsqrt_rn(dadd(dadd(dmul(ax, ax), dmul(ay, ay)), dmul(az, az)));
@@ -440,7 +500,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   double pre = 0.0;
   if (lane == 0) {
 #pragma unroll 4
-    for (int i = 0; i < first; ++i) pre = dadd(pre, s.pt[i].t);
+    for (int i = 0; i < first; ++i) pre = dadd(pre, s.pt.t(i));
   }
   pre = __shfl_sync(kFull, pre, 0);
   ck.mark(kPhSetup);
@@ -468,7 +528,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
     float* rad2 = axc + n;
     float* rf = rad2 + n;
     for (int i = lane; i < n; i += 32) {
-      const PT q = s.pt[i];
+      const PT q = s.pt.get(i);
       const double vx = q.x - ox, vy = q.y - oy, vz = q.z - oz;
       const double a = X.kx * vx + X.ky * vy + X.kz * vz;
       axc[i] = static_cast<float>(a);
@@ -560,9 +620,9 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
   // pre-fill them into each candidate slot so the fold is a plain sum.
   for (int i = lane; i < n; i += 32)
     if (!in_frag(s.fm, i)) {
-      const double t = s.pt[i].t;
+      const double t = s.pt.t(i);
 #pragma unroll
-      for (int c = 0; c < B; ++c) s.v[c * n + i] = t;
+      for (int c = 0; c < B; ++c) s.v[c * vrow(n) + i] = t;
     }
   __syncwarp();
   ck.mark(kPhPrefill);
@@ -611,8 +671,8 @@ __device__ __forceinline__ unsigned bump_group(const WarpMem& s, const DockParam
       if (act) {
         const int pr = s.pairs[t];
         const int i = pr & 0xff, j = pr >> 8;
-        const PT ai = s.pt[i];
-        aj = s.pt[j];
+        const PT ai = s.pt.get(i);
+        aj = s.pt.get(j);
         r = arm_of(X, ai.x, ai.y, ai.z);
         const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
         cut2 = dmul(cut, cut);
@@ -649,10 +709,10 @@ __device__ __forceinline__ void query_slots(const WarpMem& s, const DockParams& 
     const int ac = a0 + s.lidx[k] * da;
     const double cs = __ldg(p.cos_deg + ac), sn = __ldg(p.sin_deg + ac);
     double x, y, z;
-    const PT q = s.pt[i];
+    const PT q = s.pt.get(i);
     rodrigues(X, cs, sn, dsub(1.0, cs), q.x, q.y, q.z, x, y, z);
     wk.add(kRot, 1);
-    s.v[k * n + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
+    s.v[k * vrow(n) + i] = fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk));
   }
 }
 
@@ -699,7 +759,7 @@ __device__ __forceinline__ void search_fragment(const WarpMem& s, const DockPara
         double score = -kInfinity;
         if (lane < nb) {
           double sum = pre;
-          const double* vc = s.v + lane * n;
+          const double* vc = s.v + lane * vrow(n);
 #pragma unroll kFoldUnroll
           for (int i = first; i < n; ++i) sum = dadd(sum, vc[i]);
           score = __ddiv_rn(static_cast<double>(n), sum);
@@ -840,14 +900,14 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       rigid_apply(R, p.cx, p.cy, p.cz, dsub(x, p.cx), dsub(y, p.cy), dsub(z, p.cz), x, y, z);
       wk.add(kXform, 1);
     }
-    s.pt[i] = PT{x, y, z, fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk))};
+    s.pt.set(i, PT{x, y, z, fmax(kMinDistanceSq, min_dist_sq(p.pocket, x, y, z, wk))});
   }
   __syncwarp();
   // match_probes_shape prologue (kernel.hpp:215-218).
   double cur = 0.0;
   if (lane == 0) {
     double sum = 0.0;
-    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt[i].t);
+    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt.t(i));
     cur = __ddiv_rn(static_cast<double>(n), sum);
   }
   cur = __shfl_sync(kFull, cur, 0);
@@ -935,10 +995,10 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
         for (int sl = lane; sl < nf; sl += 32) {
           const int i = s.fidx[sl];
           double qx, qy, qz;
-          const PT q = s.pt[i];
+          const PT q = s.pt.get(i);
           rodrigues(X, cs, sn, omc, q.x, q.y, q.z, qx, qy, qz);
           wk.add(kRot, 1);
-          s.pt[i] = PT{qx, qy, qz, fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx, qy, qz, wk))};
+          s.pt.set(i, PT{qx, qy, qz, fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx, qy, qz, wk))});
         }
       }
       __syncwarp();
@@ -965,7 +1025,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   if (stage) {
     double* dst = p.stage_pose + 3 * (static_cast<size_t>(p.top_k) * m.atom_off + static_cast<size_t>(r) * n);
     for (int i = lane; i < n; i += 32) {
-      const PT q = s.pt[i];
+      const PT q = s.pt.get(i);
       dst[3 * i] = q.x;
       dst[3 * i + 1] = q.y;
       dst[3 * i + 2] = q.z;
@@ -1237,13 +1297,13 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   for (int i = lane; i < n * W; i += 32) s.far[i] = __ldg(p.far_mask + m.far_off + i);
   for (int i = lane; i < n; i += 32) {
     const double* q = p.xyz + 3 * (m.atom_off + i);
-    s.pt[i] = PT{q[0], q[1], q[2], fmax(kMinDistanceSq, min_dist_sq(p.pocket, q[0], q[1], q[2], wk))};
+    s.pt.set(i, PT{q[0], q[1], q[2], fmax(kMinDistanceSq, min_dist_sq(p.pocket, q[0], q[1], q[2], wk))});
   }
   __syncwarp();
   double cur = 0.0;
   if (lane == 0) {
     double sum = 0.0;
-    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt[i].t);
+    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt.t(i));
     cur = __ddiv_rn(static_cast<double>(n), sum);
   }
   cur = __shfl_sync(kFull, cur, 0);
@@ -1266,7 +1326,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   for (int t = lane; t < st.np; t += 32) {
     const int pr = s.pairs[t];
     const int i = pr & 0xff, j = pr >> 8;
-    const PT ai = s.pt[i], aj = s.pt[j];
+    const PT ai = s.pt.get(i), aj = s.pt.get(j);
     const double cut = dmul(kBumpScale, dadd(s.radius[i], s.radius[j]));
     wk.add(kBump, 1);
     if (dist_sq(ai.x, ai.y, ai.z, aj.x, aj.y, aj.z) < dmul(cut, cut)) b0 = true;
@@ -1299,7 +1359,7 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       __syncwarp();
       if (lane < nb) {
         double sum = st.pre;
-        const double* vc = s.v + lane * n;
+        const double* vc = s.v + lane * vrow(n);
 #pragma unroll kFoldUnroll
         for (int i = st.first; i < n; ++i) sum = dadd(sum, vc[i]);
         const int a = g0 + s.lidx[lane];
@@ -1360,13 +1420,13 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
   for (int i = lane; i < n * W; i += 32) s.far[i] = __ldg(p.far_mask + m.far_off + i);
   for (int i = lane; i < n; i += 32) {
     const double* q = p.xyz + 3 * (m.atom_off + i);
-    s.pt[i] = PT{q[0], q[1], q[2], fmax(kMinDistanceSq, min_dist_sq(p.pocket, q[0], q[1], q[2], wk))};
+    s.pt.set(i, PT{q[0], q[1], q[2], fmax(kMinDistanceSq, min_dist_sq(p.pocket, q[0], q[1], q[2], wk))});
   }
   __syncwarp();
   double cur = 0.0;
   if (lane == 0) {
     double sum = 0.0;
-    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt[i].t);
+    for (int i = 0; i < n; ++i) sum = dadd(sum, s.pt.t(i));
     cur = __ddiv_rn(static_cast<double>(n), sum);
   }
   cur = __shfl_sync(kFull, cur, 0);
@@ -1392,16 +1452,16 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       const double omc = dsub(1.0, cs);
       for (int sl = lane; sl < st.nf; sl += 32) {
         const int i = s.fidx[sl];
-        const PT q = s.pt[i];
+        const PT q = s.pt.get(i);
         double qx, qy, qz;
         rodrigues(st.X, cs, sn, omc, q.x, q.y, q.z, qx, qy, qz);
-        s.pt[i] = PT{qx, qy, qz, 0.0};
+        s.pt.set(i, PT{qx, qy, qz, 0.0});
       }
     }
     __syncwarp();
   }
   for (int i = lane; i < n; i += 32) {
-    const PT q = s.pt[i];
+    const PT q = s.pt.get(i);
     double* d = io.pose + 3 * (static_cast<size_t>(m.atom_off) + i);
     d[0] = q.x;
     d[1] = q.y;
