@@ -89,6 +89,9 @@ constexpr int kFoldUnroll = GD_FOLD_UNROLL;
 #define GD_FIXED_POINT 1     // chains with several restarts replay the counts of steps past
                              // their fixed point instead of searching again
 #endif
+#ifndef GD_COMMIT_REUSE
+#define GD_COMMIT_REUSE 1    // commits take the winner's terms from v when its batch was the search's last
+#endif
 #ifndef GD_FLEX_WARPS6
 #define GD_FLEX_WARPS6 12    // chains per CTA for batches of up to 6 candidates (r3e: c1 flex
                              // 11.55 ms vs 11.65 at 8, 12.44 at 4)
@@ -103,11 +106,13 @@ constexpr int warps_for() {
 constexpr unsigned kFull = 0xffffffffu;
 
 __host__ __device__ __forceinline__ size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
-// Row stride (doubles) of the candidate-term table v: odd, so the fold's
-// lanes -- one per candidate, all at the same atom -- hit distinct banks
-// (stride n put candidates 0, 2, 4 of an n = 40 ligand on the same ones).
+// Row stride (doubles) of the candidate-term table v.  GD_V_PAD=1 makes it
+// odd, so the fold's lanes -- one per candidate, all at the same atom -- hit
+// distinct banks (stride n puts candidates 0, 2, 4 of an n = 40 ligand on
+// the same ones); measured neutral (c1 flex 11.03 vs 11.06 ms, and 11.06 vs
+// 10.95 on top of the SoA pose table), so rows stay unpadded.
 #ifndef GD_V_PAD
-#define GD_V_PAD 1
+#define GD_V_PAD 0
 #endif
 __host__ __device__ __forceinline__ int vrow(int n) { return GD_V_PAD ? (n | 1) : n; }
 
@@ -127,13 +132,15 @@ struct __align__(16) PT {
 // atoms, and 32-byte records read with 128-bit loads put atoms i and i + 4
 // on the same banks (a quarter warp's eight 16-byte chunks must fall in the
 // eight distinct 16-byte bank groups): ncu counted 45-65% excess wavefronts
-// on these loads with the shared-memory pipe at 50% of its peak.
-// GD_PT_LAYOUT 1 swaps the (x, y) and (z, t) halves of every second group
-// of four atoms, so eight consecutive atoms cover all eight bank groups;
-// 2 keeps x, y, z and t in four arrays (64-bit loads, an unused t is never
-// loaded); 0 is the plain record array.
+// on these loads with the shared-memory pipe at 50% of its peak (r3f).
+// GD_PT_LAYOUT 2 keeps x, y, z and t in four arrays (64-bit loads,
+// conflict-free for consecutive atoms, an unused t is never loaded): c1 flex
+// 11.06 -> 10.95 ms, c2 39.3 -> 38.6 (r3h).  1 swaps the (x, y) and (z, t)
+// halves of every second group of four atoms so eight consecutive atoms
+// cover all eight bank groups (11.15 ms: the address arithmetic costs more
+// than the conflicts); 0 is the plain record array.
 #ifndef GD_PT_LAYOUT
-#define GD_PT_LAYOUT 1
+#define GD_PT_LAYOUT 2
 #endif
 struct Pose {
   double* b;
@@ -727,9 +734,10 @@ __device__ __forceinline__ void search_fragment(const WarpMem& s, const DockPara
                                                 int n, int nf, int np, int first, double pre,
                                                 double cur, double entry, int step, bool refined,
                                                 int lane, int& best_a, double& best, int& evals,
-                                                int& checks, Work<On>& wk, CK& ck) {
+                                                int& checks, int& win_row, Work<On>& wk, CK& ck) {
   best_a = 0;
   best = cur;
+  win_row = -1;  // row of v still holding the winner's terms (flat searches, GD_COMMIT_REUSE)
   if (!refined && GD_FLAT_LIVE && 360 / step - 1 >= GD_FLAT_LIVE_MINC) {
     // optimize_fragment_flat (kernel.hpp:125-143): candidates c*step,
     // c = 1..A-1, bump-checked 32 at a time, then the live ones queried and
@@ -770,9 +778,11 @@ __device__ __forceinline__ void search_fragment(const WarpMem& s, const DockPara
         ck.mark(kPhFold);
         int c;
         const double v = batch_max(score, 0u, nb, lane, c);
+        win_row = -1;  // this batch overwrote the rows of every earlier one
         if (c >= 0 && v > best) {
           best = v;
           best_a = a0 + s.lidx[c] * step;
+          win_row = c;
         }
         __syncwarp();
       }
@@ -978,9 +988,9 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
 
       int best_a = 0;
       double best = cur;
-      int evals = 0, checks = 0;
+      int evals = 0, checks = 0, win_row = -1;
       search_fragment<On, B>(s, p, X, n, nf, np, first, pre, cur, cur, step, refined, lane, best_a,
-                             best, evals, checks, wk, ck);
+                             best, evals, checks, win_row, wk, ck);
       tally(evals, checks);
       if (kReplay) {
         if (lane == f) hist = (static_cast<unsigned>(evals) << 16) | static_cast<unsigned>(checks);
@@ -998,7 +1008,13 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
           const PT q = s.pt.get(i);
           rodrigues(X, cs, sn, omc, q.x, q.y, q.z, qx, qy, qz);
           wk.add(kRot, 1);
-          s.pt.set(i, PT{qx, qy, qz, fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx, qy, qz, wk))});
+          // The winner's terms are still in its row of v when it was scored
+          // in the search's last batch: the same rotation, the same query,
+          // so the same bits -- no second lookup.
+          const double t = (GD_COMMIT_REUSE && win_row >= 0)
+                               ? s.v[win_row * vrow(n) + i]
+                               : fmax(kMinDistanceSq, min_dist_sq(p.pocket, qx, qy, qz, wk));
+          s.pt.set(i, PT{qx, qy, qz, t});
         }
       }
       __syncwarp();
@@ -1445,8 +1461,9 @@ __global__ void __launch_bounds__(kWarps * 32, GD_FLEX_RESIDENT / kWarps)
       if (lane == 0) p.status[l] = 3;  // "rotate_fragment: degenerate rotation axis"
       return;
     }
+    int win_row = -1;
     search_fragment<On, B>(s, p, st.X, n, st.nf, st.np, st.first, st.pre, cur, entry, step, refined,
-                           lane, best_a, best, evals, checks, wk, ck);
+                           lane, best_a, best, evals, checks, win_row, wk, ck);
     if (best_a != 0) {  // commit_angle: rotate the fragment by the winning angle
       const double cs = __ldg(p.cos_deg + best_a), sn = __ldg(p.sin_deg + best_a);
       const double omc = dsub(1.0, cs);
