@@ -248,7 +248,9 @@ int gd_ligand_graph(int32_t n_atoms, const double* xyz, const double* radii, int
  * the per-ligand fragment prefix (skipped ligands have none);
  * relative_size[f] (nullable) Fragment::relative_size; status[L] (nullable)
  * GD_LIG_* per ligand (GD_LIG_DEGENERATE: a fragment's axis is degenerate,
- * its profile is all-invalid).  `capacity` is in fragments; twice the
+ * its profile is all-invalid; a ligand of more than 256 atoms is reported
+ * GD_LIG_INVALID with no fragments -- the docking entry points take such
+ * ligands, this warp-per-fragment kernel does not).  `capacity` is in fragments; twice the
  * number of rotatable bonds always suffices.  flags: GD_FLAG_BRUTE_FORCE,
  * GD_FLAG_COUNT_WORK (work lands in gd_work_counters' flex slots); the
  * kernel time goes to gd_last_timing's flex_ms. */

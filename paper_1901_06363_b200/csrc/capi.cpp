@@ -1744,8 +1744,17 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores,
   }
   std::vector<int32_t> items;
   frag_offsets[0] = 0;
+  std::vector<int> wide_skipped;
   for (int l = 0; l < L; ++l) {
-    const int nf = ctx->status_host[l] == 0 ? meta[l].nfrag : 0;
+    int nf = ctx->status_host[l] == 0 ? meta[l].nfrag : 0;
+    if (nf > 0 && is_wide(meta[l].n)) {
+      // The profile kernel is a warp-per-fragment kernel (8-bit atom
+      // indices): wide ligands are reported as skipped, not profiled.
+      nf = 0;
+      wide_skipped.push_back(l);
+      ctx->errors[l] = "ligand '" + std::to_string(l) + "': more than " + std::to_string(kNarrowAtoms) +
+                       " atoms is not supported by gd_rotation_profiles";
+    }
     for (int f = 0; f < nf; ++f) {
       items.push_back(l);
       items.push_back(f);
@@ -1808,6 +1817,8 @@ extern "C" int gd_rotation_profiles(gd_ctx* ctx, uint32_t flags, double* scores,
     GD_CUDA(ctx, cudaMemcpyAsync(status, ctx->o_status.ptr, sizeof(int32_t) * L,
                                  cudaMemcpyDeviceToHost, ctx->stream));
   GD_CUDA(ctx, cudaStreamSynchronize(ctx->stream));
+  if (status)
+    for (const int l : wide_skipped) status[l] = GD_LIG_INVALID;
   if (n_items > 0) {
     cudaEventElapsedTime(&ctx->timing.flex_ms, ctx->ev[2], ctx->ev[3]);
     cudaEventElapsedTime(&ctx->timing.total_ms, ctx->ev[2], ctx->ev[4]);

@@ -130,3 +130,20 @@ def test_wide_ligand_rejections(docker):
     assert_same_result(sub, want)
     for f in ("orientation", "final_score", "evaluations"):
         assert np.array_equal(getattr(got, f)[[0, 4]], getattr(sub, f))
+
+
+def test_rotation_profiles_skip_wide_ligands(docker):
+    """gd_rotation_profiles is a warp-per-fragment kernel: a wide ligand in
+    the staged batch is reported as skipped (status, message, no fragments)
+    and the other ligands' profiles are unaffected."""
+    pocket = W.config(1).pocket()
+    c = pocket.mean(axis=0)
+    small = _parts(W.config(1).ligands(range(3), c))
+    ch = Lig(_zigzag(300), [(i, i + 1, i % 11 == 4) for i in range(299)], radius=0.8)
+    wide = (ch.xyz + c - ch.xyz.mean(axis=0), ch.radii, ch.bonds, ch.rot)
+    docker.set_pocket(pocket)
+    mixed = docker.rotation_profiles(LigandBatch.from_parts([small[0], wide, small[1], small[2]]))
+    alone = docker.rotation_profiles(LigandBatch.from_parts(small))
+    assert mixed.status.tolist() == [0, 1, 0, 0]
+    assert mixed.frag_offsets[2] == mixed.frag_offsets[1]  # no fragments for the wide ligand
+    assert np.array_equal(mixed.scores, alone.scores) and np.array_equal(mixed.valid, alone.valid)

@@ -14,3 +14,4 @@ SKIP=0 KERNELS="prep_kernel" bash tools/prof.sh ${T}
 timeout 900 python tools/screen_c3.py > gpurun_out/c3_${T}_multi.json 2> gpurun_out/c3_${T}_multi.err
 timeout 900 python tools/screen_c3.py --ranks > gpurun_out/c3_${T}_ranks.json 2> gpurun_out/c3_${T}_ranks.err
 timeout 2400 python tools/knob_sweep.py --ligands 20000 --pockets 4 --full > gpurun_out/knob_sweep_full_${T}.json 2> gpurun_out/knob_sweep_full_${T}.err
+python tools/index_build_c3.py > gpurun_out/index_c3_${T}.txt 2>&1
