@@ -706,10 +706,39 @@ __device__ __forceinline__ unsigned bump_group(const WarpMem& s, const DockParam
 
 // Query phase over a batch of live candidates: slot k < nb is candidate
 // s.lidx[k] (angle a0 + lidx[k]*da); its terms land in row k of v.
+#ifndef GD_QUERY_PAIRS
+#define GD_QUERY_PAIRS 0     // 1: a lane serves one atom for two live slots (shared rotation arm,
+                             // two lookups in flight): exact, but c1 flex 13.05 vs 10.79 ms and c2
+                             // 52.4 vs 38.6 (r3i) -- two queries' state per lane and a scan as long
+                             // as the longer of the two candidate lists
+#endif
 template <bool On>
 __device__ __forceinline__ void query_slots(const WarpMem& s, const DockParams& p, const Axis& X, int n,
                                             int nf, int nb, int a0, int da, int lane, Work<On>& wk) {
   const float rnf = 1.0f / static_cast<float>(nf);
+#if GD_QUERY_PAIRS
+  if (nb >= 2) {
+    const int npair = (nb + 1) >> 1;
+    for (int t = lane; t < npair * nf; t += 32) {
+      const int j = qdiv(t, rnf);
+      const int i = s.fidx[t - j * nf];
+      const int k0 = 2 * j, k1 = min(2 * j + 1, nb - 1);
+      const int ac0 = a0 + s.lidx[k0] * da, ac1 = a0 + s.lidx[k1] * da;
+      const double cs0 = __ldg(p.cos_deg + ac0), sn0 = __ldg(p.sin_deg + ac0);
+      const double cs1 = __ldg(p.cos_deg + ac1), sn1 = __ldg(p.sin_deg + ac1);
+      const PT q = s.pt.get(i);
+      const Arm r = arm_of(X, q.x, q.y, q.z);
+      double x0, y0, z0, x1, y1, z1, m0, m1;
+      turn(X, r, cs0, sn0, dsub(1.0, cs0), x0, y0, z0);
+      turn(X, r, cs1, sn1, dsub(1.0, cs1), x1, y1, z1);
+      wk.add(kRot, k1 != k0 ? 2 : 1);
+      min_dist_sq2(p.pocket, x0, y0, z0, x1, y1, z1, m0, m1, wk);
+      s.v[k0 * vrow(n) + i] = fmax(kMinDistanceSq, m0);
+      if (k1 != k0) s.v[k1 * vrow(n) + i] = fmax(kMinDistanceSq, m1);
+    }
+    return;
+  }
+#endif
   for (int t = lane; t < nb * nf; t += 32) {
     const int k = qdiv(t, rnf);
     const int i = s.fidx[t - k * nf];
