@@ -1703,7 +1703,8 @@ extern "C" int gd_ligand_graph(int32_t n_atoms, const double* xyz, const double*
   if (n_atoms < 0 || n_bonds < 0 || (n_atoms > 0 && (!xyz || !radii)) ||
       (n_bonds > 0 && (!bonds || !rotatable)) || !n_rotamers)
     return GD_LIG_INVALID;
-  const PreparedLigand p = prepare_ligand("L", n_atoms, xyz, radii, n_bonds, bonds, rotatable);
+  // The graph itself has no size limit (host code); the docking path's is kWideAtoms.
+  const PreparedLigand p = prepare_ligand("L", n_atoms, xyz, radii, n_bonds, bonds, rotatable, kWideAtoms);
   if (msg && msg_len) {
     std::strncpy(msg, p.error.c_str(), msg_len - 1);
     msg[msg_len - 1] = 0;

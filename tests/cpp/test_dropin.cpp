@@ -225,6 +225,26 @@ int main() {
     CHECK(a.score == overlap_score(a.final_pose, pocket));
     CHECK(a.score >= overlap_score(make_initial_pose(lig), pocket));
   });
+  run("match_probes_shape: a 300-atom ligand docks (the reference has no size limit)", [] {
+    // 300 atoms take the wide path (flex_wide_kernel): committed pose,
+    // never regressing, deterministic, feasible under the bump oracle.
+    const Ligand lig = synth(424242, 0, 300, 300, 10);
+    const Pocket pocket = synth_pocket(10, 8, 6, 0.795);
+    const KnobConfig cfg{60, 90, 0.0, 1, false};
+    const Pose initial = make_initial_pose(lig);
+    const auto a = match_probes_shape(lig, pocket, initial, cfg);
+    const auto b = match_probes_shape(lig, pocket, initial, cfg);
+    CHECK(a.final_pose.positions.size() == 300);
+    CHECK(a.score == b.score);
+    CHECK(a.final_pose.positions == b.final_pose.positions);
+    CHECK(a.score == overlap_score(a.final_pose, pocket));
+    CHECK(a.score >= overlap_score(initial, pocket));
+    CHECK(a.feasibility_checks == 1 + static_cast<long>(2 * find_rotamers(lig).size()) * (360 / 60));
+    for (const auto& rot : find_rotamers(lig)) {
+      const auto [left, right] = grow_fragments(lig, rot);
+      CHECK(bump_oracle(a.final_pose, lig, left) || !bump_oracle(initial, lig, left));
+    }
+  });
   run("match_probes_shape: pose/ligand size mismatch", [] {
     try {
       match_probes_shape(rig_ligand(), rig_pocket(), pose_of({{0, 0, 0}}), KnobConfig{});
