@@ -275,13 +275,33 @@ __device__ __forceinline__ double inline_min(const PocketView&, const Loc& a, do
   if constexpr (kVoxInline == 2) m = fmin(m, dist_sq(x, y, z, a.x1, a.y1, a.z1));
   return m;
 }
+// Unused inline slots of a coded record repeat its last candidate
+// (voxel_fill_kernel), so slots can be evaluated two at a time without a
+// count test in between: a warp runs the second pair whenever any lane's
+// voxel holds more than two candidates (almost always), and two independent
+// distance chains overlap where four predicated ones ran back to back.
+// GD_CODED_PAIRED=0 restores one test per slot (A/B).
+#ifndef GD_CODED_PAIRED
+#define GD_CODED_PAIRED 1
+#endif
 __device__ __forceinline__ double inline_min(const PocketView& pk, const LocC& a, double x, double y,
                                              double z) {
+#if GD_CODED_PAIRED == 2
+  // All four slots, no count test at all.
+  return fmin(fmin(coded_d2<0>(pk.tab, a.w, x, y, z), coded_d2<1>(pk.tab, a.w, x, y, z)),
+              fmin(coded_d2<2>(pk.tab, a.w, x, y, z), coded_d2<3>(pk.tab, a.w, x, y, z)));
+#elif GD_CODED_PAIRED
+  double m = fmin(coded_d2<0>(pk.tab, a.w, x, y, z), coded_d2<1>(pk.tab, a.w, x, y, z));
+  if (a.count > 2)
+    m = fmin(m, fmin(coded_d2<2>(pk.tab, a.w, x, y, z), coded_d2<3>(pk.tab, a.w, x, y, z)));
+  return m;
+#else
   double m = coded_d2<0>(pk.tab, a.w, x, y, z);
   if (a.count > 1) m = fmin(m, coded_d2<1>(pk.tab, a.w, x, y, z));
   if (a.count > 2) m = fmin(m, coded_d2<2>(pk.tab, a.w, x, y, z));
   if (a.count > 3) m = fmin(m, coded_d2<3>(pk.tab, a.w, x, y, z));
   return m;
+#endif
 }
 // List loads of a located voxel (0 on the full-scan fallback).
 __device__ __forceinline__ int listed(const Loc& a) { return a.lst ? a.count - kVoxInline : 0; }

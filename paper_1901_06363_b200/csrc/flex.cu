@@ -89,6 +89,9 @@ constexpr int kFoldUnroll = GD_FOLD_UNROLL;
 #define GD_FIXED_POINT 1     // chains with several restarts replay the counts of steps past
                              // their fixed point instead of searching again
 #endif
+#ifndef GD_PREF_PACK
+#define GD_PREF_PACK 1       // prefilter: per-atom (axial, radial^2, radius) as one float4 record
+#endif
 #ifndef GD_COMMIT_REUSE
 #define GD_COMMIT_REUSE 1    // commits take the winner's terms from v when its batch was the search's last
 #endif
@@ -531,6 +534,30 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
       s.pairs[t] = static_cast<uint16_t>((pr >> 8) | ((pr & 0xffu) << 8));
     }
   } else {
+#if GD_PREF_PACK
+    // One 16-byte record per atom (axial coordinate, squared axis distance,
+    // radius): a pair test is two 128-bit shared loads instead of six 32-bit.
+    float4* pa = reinterpret_cast<float4*>(s.v);
+    float* rf = reinterpret_cast<float*>(pa + n) - n;  // pref follows the records (rf + n below)
+    for (int i = lane; i < n; i += 32) {
+      const PT q = s.pt.get(i);
+      const double vx = q.x - ox, vy = q.y - oy, vz = q.z - oz;
+      const double a = X.kx * vx + X.ky * vy + X.kz * vz;
+      pa[i] = make_float4(static_cast<float>(a),
+                          static_cast<float>(fmax(0.0, vx * vx + vy * vy + vz * vz - a * a)),
+                          static_cast<float>(s.radius[i]), 0.0f);
+    }
+    __syncwarp();
+    auto test = [&](int i, int j) {
+      const float4 ai = pa[i], aj = pa[j];
+      const float h = aj.x - ai.x;
+      const float s2 = aj.y, r2 = ai.y;
+      const float cut = 0.8f * (ai.z + aj.z);
+      const float C = __fmaf_rn(cut * cut, 1.0001f, 1e-2f);
+      const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
+      return !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
+    };
+#else
     float* axc = reinterpret_cast<float*>(s.v);
     float* rad2 = axc + n;
     float* rf = rad2 + n;
@@ -551,6 +578,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
       const float Lq = (s2 + r2) + __fmaf_rn(h, h, -C);
       return !(Lq > 0.0f && Lq * Lq > 4.00004f * s2 * r2);
     };
+#endif
     {
       // Flattened over the actual partner pairs: per-slot partner counts and
       // a warp prefix sum give each slot its range of pair indices; slot
@@ -559,7 +587,7 @@ __device__ __forceinline__ bool setup_step(const WarpMem& s, const DockParams& p
       // the warp tests and compacts them in place (writes never pass the
       // chunk being read).
       int* pref = reinterpret_cast<int*>(rf + n);
-      GD_BOUND(12 * n + 4 * nf <= 8 * B * n);  // per-atom floats + pref fit the v scratch
+      GD_BOUND((GD_PREF_PACK ? 16 : 12) * n + 4 * nf <= 8 * B * n);  // per-atom floats + pref fit the v scratch
       int total = 0;
       for (int b = 0; b < nf; b += 32) {
         const int sl = b + lane;
