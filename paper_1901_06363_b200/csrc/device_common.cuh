@@ -229,8 +229,44 @@ struct LocC {
 template <bool CP>
 using LocT = typename std::conditional<CP, LocC, Loc>::type;
 
+// GD_LOCATE_FLAT=1 (coded format, two levels): both levels' voxels are
+// computed up front and the record comes from ONE load -- the fine level's if
+// the query is inside it, else the coarse level's -- instead of a second,
+// divergent lookup (with its own L2 round trip) for the lanes outside the
+// fine grid.
+#ifndef GD_LOCATE_FLAT
+#define GD_LOCATE_FLAT 1
+#endif
 template <bool CP = kCompactTU>
 __device__ __forceinline__ LocT<CP> locate(const PocketView& pk, double x, double y, double z) {
+#if GD_LOCATE_FLAT
+  if constexpr (CP && kGridLevels == 2) {
+    if (pk.use_index) {
+      const GridLevel& g0 = pk.lv[0];
+      const GridLevel& g1 = pk.lv[1];
+      const double fx = (x - g0.lo_x) * g0.inv_h, fy = (y - g0.lo_y) * g0.inv_h, fz = (z - g0.lo_z) * g0.inv_h;
+      const double cx = (x - g1.lo_x) * g1.inv_h, cy = (y - g1.lo_y) * g1.inv_h, cz = (z - g1.lo_z) * g1.inv_h;
+      const bool in0 = fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g0.fdim_x && fy < g0.fdim_y && fz < g0.fdim_z;
+      const bool in1 = cx >= 0.0 && cy >= 0.0 && cz >= 0.0 && cx < g1.fdim_x && cy < g1.fdim_y && cz < g1.fdim_z;
+      if (in0 || in1) {
+        const int v0 = (static_cast<int>(fx) * g0.dim_y + static_cast<int>(fy)) * g0.dim_z + static_cast<int>(fz);
+        const int v1 = (static_cast<int>(cx) * g1.dim_y + static_cast<int>(cy)) * g1.dim_z + static_cast<int>(cz);
+        const double* rec = in0 ? g0.rec + 4 * static_cast<size_t>(v0) : g1.rec + 4 * static_cast<size_t>(v1);
+        uint32_t w[8];
+        ld256w<GD_REC_NA>(rec, w);
+        LocC l;
+        l.count = static_cast<int>(w[1]);
+        l.lst = (in0 ? g0.lst : g1.lst) + 4 * static_cast<size_t>(w[0]);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) l.w[k] = w[2 + k];
+        return l;
+      }
+    }
+    LocC l{};
+    l.lst = nullptr;
+    return l;
+  }
+#endif
   if (pk.use_index) {
 #pragma unroll
     for (int L = 0; L < kGridLevels; ++L) {
@@ -280,7 +316,9 @@ __device__ __forceinline__ double inline_min(const PocketView&, const Loc& a, do
 // count test in between: a warp runs the second pair whenever any lane's
 // voxel holds more than two candidates (almost always), and two independent
 // distance chains overlap where four predicated ones ran back to back.
-// GD_CODED_PAIRED=0 restores one test per slot (A/B).
+// GD_CODED_PAIRED=0 restores one test per slot (r3j, same box: c1 flex
+// 11.09 -> 10.82 ms, rigid 2.585 -> 2.550); 2 evaluates all four slots with
+// no test (flex 10.52 vs 10.57, but rigid 2.68 vs 2.55: not adopted).
 #ifndef GD_CODED_PAIRED
 #define GD_CODED_PAIRED 1
 #endif

@@ -90,7 +90,9 @@ constexpr int kFoldUnroll = GD_FOLD_UNROLL;
                              // their fixed point instead of searching again
 #endif
 #ifndef GD_PREF_PACK
-#define GD_PREF_PACK 1       // prefilter: per-atom (axial, radial^2, radius) as one float4 record
+#define GD_PREF_PACK 0       // 1: prefilter's per-atom (axial, radial^2, radius) as one float4 record
+                             // (two 128-bit loads per pair test instead of six 32-bit): slower,
+                             // c1 flex 10.82 vs 10.57 ms, c2 38.7 vs 37.7 (r3j)
 #endif
 #ifndef GD_COMMIT_REUSE
 #define GD_COMMIT_REUSE 1    // commits take the winner's terms from v when its batch was the search's last
