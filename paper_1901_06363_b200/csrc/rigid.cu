@@ -10,6 +10,14 @@
 // winners (scores beating the current K-th) are merged by rank.
 #include <algorithm>
 
+// The rigid sweep keeps the two-step voxel lookup: its atoms sit around the
+// pocket centre, mostly inside the fine level, and at 40 registers the
+// branch-free form's extra arithmetic costs more than the rare second lookup
+// (r3j: c1 rigid 2.68 vs 2.55 ms, c2 18.1 vs 17.0; the fragment search gains
+// 3% from it, see device_common.cuh).
+#ifndef GD_LOCATE_FLAT
+#define GD_LOCATE_FLAT 0
+#endif
 #include "device_common.cuh"
 
 namespace gdb200 {
