@@ -3,7 +3,7 @@
 //
 // flex_chain_kernel: one WARP per (ligand, seed rank) chain, i.e. one
 // match_probes_shape call (reference kernel.hpp:205-248).  Chains are
-// independent, so warps never wait for each other: a CTA is just four
+// independent, so warps never wait for each other: a CTA is just 4 to 12
 // chains (usually of the same ligand, in longest-ligand-first order) with
 // private shared-memory state.  Within a chain the greedy dependency
 // (rep -> rotamer -> left/right fragment, kernel.hpp:225-242) is sequential;
