@@ -31,6 +31,14 @@
 #include <cassert>
 #include <cstdlib>
 
+// Inline-slot evaluation in this translation unit (device_common.cuh,
+// GD_CODED_PAIRED): 1 = two slots at a time; 2 = all four with no count test.
+#ifndef GD_FLEX_SLOTS
+#define GD_FLEX_SLOTS 1
+#endif
+#ifndef GD_CODED_PAIRED
+#define GD_CODED_PAIRED GD_FLEX_SLOTS
+#endif
 #include "device_common.cuh"
 
 namespace gdb200 {
